@@ -1,0 +1,590 @@
+// extern "C" boundary of libscc_b200.so (include/scc_b200.h).
+//
+// Maps the reference's exception taxonomy (errors.hpp:9-55) onto status codes,
+// validates arguments the way kernel.cpp:14-25,32-35,100-103,142-146 do, keeps
+// the per-device plan tables, and dispatches to the kernel families.
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstring>
+#include <exception>
+#include <mutex>
+#include <string>
+
+#include "scc_b200.h"
+#include "scc_kernels.hpp"
+#include "scc_plan.hpp"
+
+struct scc_plan : scc::Plan {};
+
+namespace scc {
+
+namespace {
+
+thread_local std::string g_err;
+std::atomic<uint64_t> g_launches{0};
+
+[[noreturn]] void fail(scc_status_t code, std::string msg) { throw Error{code, std::move(msg)}; }
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) {
+    fail(SCC_ERR_CUDA, std::string(what) + ": " + cudaGetErrorName(e) + " (" +
+                           cudaGetErrorString(e) + ")");
+  }
+}
+
+template <class F>
+scc_status_t guard(F&& f) {
+  try {
+    f();
+    g_err.clear();
+    return SCC_OK;
+  } catch (const Error& e) {
+    g_err = e.msg;
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_err = "host allocation failed";
+    return SCC_ERR_INTERNAL;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return SCC_ERR_INTERNAL;
+  }
+}
+
+// One-time check that the current device is a B200-class sm_100 part: the
+// fat binary only carries sm_100a code, so anything else must fail loudly.
+int current_device() {
+  int dev = -1;
+  cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+  static std::mutex mu;
+  static int checked[64] = {0};  // 0 unknown, 1 ok, 2 bad
+  std::lock_guard<std::mutex> lk(mu);
+  if (dev >= 0 && dev < 64 && checked[dev] == 0) {
+    cudaDeviceProp prop{};
+    cuda_check(cudaGetDeviceProperties(&prop, dev), "cudaGetDeviceProperties");
+    checked[dev] = (prop.major == 10 && prop.minor == 0) ? 1 : 2;
+  }
+  if (dev < 0 || dev >= 64 || checked[dev] != 1) {
+    fail(SCC_ERR_CUDA, "libscc_b200 carries sm_100a code only; current device is not sm_100");
+  }
+  return dev;
+}
+
+const DeviceTables& tables(Plan& p) {
+  const int dev = current_device();
+  std::lock_guard<std::mutex> lk(p.dev_mu);
+  for (const DeviceTables& t : p.dev) {
+    if (t.device == dev) return t;
+  }
+  // Pack every table into one int32 buffer.
+  std::vector<int32_t> h;
+  auto put = [&](const std::vector<int32_t>& v) {
+    const size_t off = h.size();
+    h.insert(h.end(), v.begin(), v.end());
+    while (h.size() % 4) h.push_back(0);  // 16-byte alignment of every table
+    return off;
+  };
+  auto arcs = [](const std::vector<Arc>& v) {
+    std::vector<int32_t> o;
+    for (const Arc& a : v) {
+      o.push_back(a.start);
+      o.push_back(a.len);
+    }
+    return o;
+  };
+  const size_t o_fr = put(p.fwd.rows), o_fb = put(arcs(p.fwd.blocks)), o_fg = put(p.fwd.groups);
+  const size_t o_br = put(p.bwd.rows), o_bb = put(arcs(p.bwd.blocks)), o_bg = put(p.bwd.groups);
+  const size_t o_pm = put(p.perm), o_ip = put(p.inv_perm);
+  DeviceTables t;
+  t.device = dev;
+  cuda_check(cudaMalloc(&t.base, h.size() * sizeof(int32_t)), "cudaMalloc(plan tables)");
+  cuda_check(cudaMemcpy(t.base, h.data(), h.size() * sizeof(int32_t), cudaMemcpyHostToDevice),
+             "cudaMemcpy(plan tables)");
+  const int32_t* b = static_cast<const int32_t*>(t.base);
+  t.fwd_rows = b + o_fr;
+  t.fwd_blocks = b + o_fb;
+  t.fwd_groups = b + o_fg;
+  t.bwd_rows = b + o_br;
+  t.bwd_blocks = b + o_bb;
+  t.bwd_groups = b + o_bg;
+  t.perm = b + o_pm;
+  t.inv_perm = b + o_ip;
+  p.dev.push_back(t);
+  return p.dev.back();
+}
+
+void check_extents(int64_t n, int64_t h, int64_t w) {
+  // Tensor4 requires every extent >= 1 (tensor.cpp:11-18).
+  if (n < 1 || h < 1 || w < 1) {
+    fail(SCC_ERR_SHAPE, "tensor extents must all be >= 1, got n=" + std::to_string(n) +
+                            " h=" + std::to_string(h) + " w=" + std::to_string(w));
+  }
+}
+
+void check_ptr(const void* p, const char* name) {
+  if (p == nullptr) fail(SCC_ERR_ARGUMENT, std::string(name) + " is null");
+}
+
+// check_weights (kernel.cpp:14-25): bias present exactly when has_bias.
+void check_bias(const Plan& p, const void* bias, const char* name) {
+  if (p.cfg.has_bias && bias == nullptr) {
+    fail(SCC_ERR_SHAPE, std::string(name) + " array has 0 entries, config needs " +
+                            std::to_string(p.cfg.c_out));
+  }
+  if (!p.cfg.has_bias && bias != nullptr) {
+    fail(SCC_ERR_SHAPE, std::string(name) + " given but config has no bias");
+  }
+}
+
+int32_t choose_path(const Plan& p, int64_t /*n*/, int64_t /*h*/, int64_t /*w*/) {
+  if (p.path != SCC_PATH_AUTO) return p.path;
+  return SCC_PATH_CUDA_CORE;
+}
+
+BandLaunch band_args(const Plan& p, const DeviceTables& t, bool bwd, int64_t n, int64_t plane,
+                     const float* in, float* out, const float* weight, const float* bias) {
+  const BandSide& side = bwd ? p.bwd : p.fwd;
+  BandLaunch a{};
+  a.in = in;
+  a.out = out;
+  a.weight = weight;
+  a.bias = bias;
+  a.rows = bwd ? t.bwd_rows : t.fwd_rows;
+  a.ring_map = bwd ? t.perm : nullptr;
+  a.blocks = bwd ? t.bwd_blocks : t.fwd_blocks;
+  a.groups = bwd ? t.bwd_groups : t.fwd_groups;
+  a.ngrp = side.ngrp();
+  a.ring = side.ring;
+  a.c_in_t = static_cast<int32_t>(bwd ? p.cfg.c_out : p.cfg.c_in);
+  a.c_out_t = static_cast<int32_t>(bwd ? p.cfg.c_in : p.cfg.c_out);
+  a.c_in = static_cast<int32_t>(p.cfg.c_in);
+  a.gw = static_cast<int32_t>(p.cfg.group_width);
+  a.shift = p.cfg.shift;
+  a.n = n;
+  a.plane = plane;
+  a.backward_data = bwd;
+  return a;
+}
+
+WeightLaunch weight_args(const Plan& p, const DeviceTables& t, int64_t n, int64_t plane,
+                         const float* dy, const float* x, float* dw, float* db, void* ws) {
+  WeightLaunch a{};
+  a.dy = dy;
+  a.x = x;
+  a.dweight = dw;
+  a.dbias = db;
+  a.partial = static_cast<float*>(ws);
+  a.rows = t.fwd_rows;
+  a.blocks = t.fwd_blocks;
+  a.inv_perm = t.inv_perm;
+  a.nblk = p.fwd.nblk();
+  a.max_block_len = p.fwd.max_block_len;
+  a.c_in = static_cast<int32_t>(p.cfg.c_in);
+  a.c_out = static_cast<int32_t>(p.cfg.c_out);
+  a.gw = static_cast<int32_t>(p.cfg.group_width);
+  a.shift = p.cfg.shift;
+  a.n = n;
+  a.plane = plane;
+  return a;
+}
+
+size_t weight_ws_bytes(const Plan& p, int64_t n, int64_t plane) {
+  return weight_cc_workspace_bytes(p.fwd.nblk(), p.fwd.max_block_len, n, plane);
+}
+
+void do_forward(Plan& p, int64_t n, int64_t h, int64_t w, const float* x, const float* wt,
+                const float* b, float* y, cudaStream_t s) {
+  check_extents(n, h, w);
+  check_ptr(x, "x");
+  check_ptr(wt, "weight");
+  check_ptr(y, "y");
+  check_bias(p, b, "bias");
+  const DeviceTables& t = tables(p);
+  (void)choose_path(p, n, h, w);
+  cuda_check(launch_band_cc(band_args(p, t, false, n, h * w, x, y, wt, b), s), "forward launch");
+}
+
+void do_backward_data(Plan& p, int64_t n, int64_t h, int64_t w, const float* dy, const float* wt,
+                      float* dx, cudaStream_t s) {
+  check_extents(n, h, w);
+  check_ptr(dy, "dy");
+  check_ptr(wt, "weight");
+  check_ptr(dx, "dx");
+  const DeviceTables& t = tables(p);
+  cuda_check(launch_band_cc(band_args(p, t, true, n, h * w, dy, dx, wt, nullptr), s),
+             "backward-data launch");
+}
+
+void do_backward_weight(Plan& p, int64_t n, int64_t h, int64_t w, const float* dy, const float* x,
+                        float* dw, float* db, void* ws, size_t ws_bytes, cudaStream_t s) {
+  check_extents(n, h, w);
+  check_ptr(dy, "dy");
+  check_ptr(x, "x");
+  check_ptr(dw, "dweight");
+  check_bias(p, db, "dbias");
+  const size_t need = weight_ws_bytes(p, n, h * w);
+  if (ws_bytes < need || (need > 0 && ws == nullptr)) {
+    fail(SCC_ERR_ARGUMENT, "workspace too small: need " + std::to_string(need) + " bytes");
+  }
+  const DeviceTables& t = tables(p);
+  cuda_check(launch_weight_cc(weight_args(p, t, n, h * w, dy, x, dw, db, ws), ws_bytes, s),
+             "backward-weight launch");
+}
+
+// Host-buffer staging ------------------------------------------------------
+
+struct Staged {
+  float *x, *w, *b, *dy, *y, *dx, *dw, *db;
+  void* ws;
+  size_t ws_bytes;
+  cudaStream_t s;
+};
+
+Staged stage(Plan& p, int64_t n, int64_t h, int64_t wd) {
+  const int dev = current_device();
+  const scc_config_t& c = p.cfg;
+  const size_t nx = static_cast<size_t>(n * c.c_in * h * wd);
+  const size_t ny = static_cast<size_t>(n * c.c_out * h * wd);
+  const size_t nw = static_cast<size_t>(c.c_out * c.group_width);
+  const size_t nb = static_cast<size_t>(c.c_out);
+  const size_t wsb = weight_ws_bytes(p, n, h * wd);
+  auto al = [](size_t bytes) { return (bytes + 255) & ~size_t(255); };
+  const size_t total = al(nx * 4) * 2 + al(ny * 4) * 2 + al(nw * 4) * 2 + al(nb * 4) * 2 + al(wsb);
+  HostStaging* st = nullptr;
+  for (HostStaging& e : p.staging) {
+    if (e.device == dev) st = &e;
+  }
+  if (st == nullptr) {
+    p.staging.push_back(HostStaging{});
+    st = &p.staging.back();
+    st->device = dev;
+    cudaStream_t s;
+    cuda_check(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "cudaStreamCreate");
+    st->stream = s;
+  }
+  if (st->bytes < total) {
+    if (st->buf) cuda_check(cudaFree(st->buf), "cudaFree(staging)");
+    st->buf = nullptr;
+    cuda_check(cudaMalloc(&st->buf, total), "cudaMalloc(staging)");
+    st->bytes = total;
+  }
+  char* q = static_cast<char*>(st->buf);
+  Staged g{};
+  auto take = [&](size_t bytes) {
+    char* r = q;
+    q += al(bytes);
+    return r;
+  };
+  g.x = reinterpret_cast<float*>(take(nx * 4));
+  g.dx = reinterpret_cast<float*>(take(nx * 4));
+  g.y = reinterpret_cast<float*>(take(ny * 4));
+  g.dy = reinterpret_cast<float*>(take(ny * 4));
+  g.w = reinterpret_cast<float*>(take(nw * 4));
+  g.dw = reinterpret_cast<float*>(take(nw * 4));
+  g.b = reinterpret_cast<float*>(take(nb * 4));
+  g.db = reinterpret_cast<float*>(take(nb * 4));
+  g.ws = take(wsb);
+  g.ws_bytes = wsb;
+  g.s = static_cast<cudaStream_t>(st->stream);
+  return g;
+}
+
+void h2d(void* d, const void* h, size_t bytes, cudaStream_t s) {
+  cuda_check(cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, s), "cudaMemcpyAsync H2D");
+}
+void d2h(void* h, const void* d, size_t bytes, cudaStream_t s) {
+  cuda_check(cudaMemcpyAsync(h, d, bytes, cudaMemcpyDeviceToHost, s), "cudaMemcpyAsync D2H");
+}
+
+}  // namespace
+
+void note_launches(uint64_t k) { g_launches.fetch_add(k, std::memory_order_relaxed); }
+
+}  // namespace scc
+
+using scc::guard;
+
+extern "C" {
+
+const char* scc_last_error(void) { return scc::g_err.c_str(); }
+int scc_abi_version(void) { return SCC_B200_ABI_VERSION; }
+uint64_t scc_launch_count(void) { return scc::g_launches.load(); }
+
+scc_status_t scc_overlap_parse(const char* text, int32_t* kind, double* ratio, int64_t* count) {
+  return guard([&] {
+    scc::check_ptr(kind, "kind");
+    scc::check_ptr(ratio, "ratio");
+    scc::check_ptr(count, "count");
+    scc::parse_overlap(text, kind, ratio, count);
+  });
+}
+
+scc_status_t scc_overlap_resolve(int32_t kind, double ratio, int64_t count, int64_t gw,
+                                 int64_t* channels) {
+  return guard([&] {
+    scc::check_ptr(channels, "channels");
+    *channels = scc::resolve_overlap(kind, ratio, count, gw);
+  });
+}
+
+scc_status_t scc_plan_create(int64_t c_in, int64_t c_out, int64_t cg, int32_t kind, double ratio,
+                             int64_t count, int32_t has_bias, scc_plan_t** plan) {
+  return guard([&] {
+    scc::check_ptr(plan, "plan");
+    *plan = nullptr;
+    auto* p = new scc_plan;
+    try {
+      scc::build_plan(*p, c_in, c_out, cg, kind, ratio, count, has_bias);
+    } catch (...) {
+      delete p;
+      throw;
+    }
+    *plan = p;
+  });
+}
+
+scc_status_t scc_plan_destroy(scc_plan_t* plan) {
+  return guard([&] {
+    if (plan == nullptr) return;
+    int prev = -1;
+    cudaGetDevice(&prev);
+    for (const scc::DeviceTables& t : plan->dev) {
+      cudaSetDevice(t.device);
+      cudaFree(t.base);
+    }
+    for (const scc::HostStaging& s : plan->staging) {
+      cudaSetDevice(s.device);
+      if (s.buf) cudaFree(s.buf);
+      if (s.stream) cudaStreamDestroy(static_cast<cudaStream_t>(s.stream));
+    }
+    if (prev >= 0) cudaSetDevice(prev);
+    delete plan;
+  });
+}
+
+scc_status_t scc_plan_config(const scc_plan_t* plan, scc_config_t* out) {
+  return guard([&] {
+    scc::check_ptr(plan, "plan");
+    scc::check_ptr(out, "out");
+    *out = plan->cfg;
+  });
+}
+
+scc_status_t scc_plan_cycle_starts(const scc_plan_t* plan, int64_t* starts, int64_t capacity,
+                                   int64_t* count) {
+  return guard([&] {
+    scc::check_ptr(plan, "plan");
+    scc::check_ptr(count, "count");
+    const auto& cs = plan->cycle_starts;
+    *count = static_cast<int64_t>(cs.size());
+    for (int64_t i = 0; i < capacity && i < static_cast<int64_t>(cs.size()); ++i) starts[i] = cs[i];
+  });
+}
+
+scc_status_t scc_plan_window_of(const scc_plan_t* plan, int64_t oc, int64_t* start,
+                                int64_t* length) {
+  return guard([&] {
+    scc::check_ptr(plan, "plan");
+    // window_of (cycle.cpp:23-26) throws IndexError for oc < 0 and wraps the
+    // cycle for oc >= c_out.
+    if (oc < 0) scc::fail(SCC_ERR_INDEX, "output channel must be >= 0, got " + std::to_string(oc));
+    const auto& cs = plan->cycle_starts;
+    if (start) *start = cs[static_cast<size_t>(oc % static_cast<int64_t>(cs.size()))];
+    if (length) *length = plan->cfg.group_width;
+  });
+}
+
+scc_status_t scc_plan_covering_filters(const scc_plan_t* plan, int64_t ic, int64_t* filters,
+                                       int64_t capacity, int64_t* count) {
+  return guard([&] {
+    scc::check_ptr(plan, "plan");
+    scc::check_ptr(count, "count");
+    const scc_config_t& c = plan->cfg;
+    if (ic < 0 || ic >= c.c_in) {
+      scc::fail(SCC_ERR_INDEX, "input channel " + std::to_string(ic) + " out of range [0, " +
+                                   std::to_string(c.c_in) + ")");
+    }
+    int64_t k = 0;
+    for (int64_t oc = 0; oc < c.c_out; ++oc) {
+      if (plan->slot_of(oc, ic) >= 0) {
+        if (filters && k < capacity) filters[k] = oc;
+        ++k;
+      }
+    }
+    *count = k;
+  });
+}
+
+scc_status_t scc_forward_macs(const scc_plan_t* plan, int64_t n, int64_t h, int64_t w,
+                              uint64_t* macs) {
+  return guard([&] {
+    scc::check_ptr(plan, "plan");
+    scc::check_ptr(macs, "macs");
+    scc::check_extents(n, h, w);
+    *macs = static_cast<uint64_t>(n * plan->cfg.c_out * h * w * plan->cfg.group_width);
+  });
+}
+
+scc_status_t scc_plan_set_path(scc_plan_t* plan, int32_t path) {
+  return guard([&] {
+    scc::check_ptr(plan, "plan");
+    if (path != SCC_PATH_AUTO && path != SCC_PATH_CUDA_CORE && path != SCC_PATH_TENSOR) {
+      scc::fail(SCC_ERR_ARGUMENT, "unknown path " + std::to_string(path));
+    }
+    if (path == SCC_PATH_TENSOR) {
+      scc::fail(SCC_ERR_ARGUMENT, "tensor-core path not available in this build");
+    }
+    plan->path = path;
+  });
+}
+
+scc_status_t scc_plan_get_path(const scc_plan_t* plan, int64_t n, int64_t h, int64_t w,
+                               int32_t* path) {
+  return guard([&] {
+    scc::check_ptr(plan, "plan");
+    scc::check_ptr(path, "path");
+    *path = scc::choose_path(*plan, n, h, w);
+  });
+}
+
+scc_status_t scc_forward_f32(const scc_plan_t* plan, int64_t n, int64_t h, int64_t w,
+                             const float* x, const float* weight, const float* bias, float* y,
+                             void* stream) {
+  return guard([&] {
+    scc::check_ptr(plan, "plan");
+    scc::do_forward(*const_cast<scc_plan_t*>(plan), n, h, w, x, weight, bias, y,
+                    static_cast<cudaStream_t>(stream));
+  });
+}
+
+scc_status_t scc_backward_data_f32(const scc_plan_t* plan, int64_t n, int64_t h, int64_t w,
+                                   const float* dy, const float* weight, float* dx, void* stream) {
+  return guard([&] {
+    scc::check_ptr(plan, "plan");
+    scc::do_backward_data(*const_cast<scc_plan_t*>(plan), n, h, w, dy, weight, dx,
+                          static_cast<cudaStream_t>(stream));
+  });
+}
+
+scc_status_t scc_backward_weight_workspace_size(const scc_plan_t* plan, int64_t n, int64_t h,
+                                                int64_t w, size_t* bytes) {
+  return guard([&] {
+    scc::check_ptr(plan, "plan");
+    scc::check_ptr(bytes, "bytes");
+    scc::check_extents(n, h, w);
+    *bytes = scc::weight_ws_bytes(*plan, n, h * w);
+  });
+}
+
+scc_status_t scc_backward_weight_f32(const scc_plan_t* plan, int64_t n, int64_t h, int64_t w,
+                                     const float* dy, const float* x, float* dweight,
+                                     float* dbias, void* workspace, size_t workspace_bytes,
+                                     void* stream) {
+  return guard([&] {
+    scc::check_ptr(plan, "plan");
+    scc::do_backward_weight(*const_cast<scc_plan_t*>(plan), n, h, w, dy, x, dweight, dbias,
+                            workspace, workspace_bytes, static_cast<cudaStream_t>(stream));
+  });
+}
+
+scc_status_t scc_backward_f32(const scc_plan_t* plan, int64_t n, int64_t h, int64_t w,
+                              const float* dy, const float* x, const float* weight, float* dx,
+                              float* dweight, float* dbias, void* workspace,
+                              size_t workspace_bytes, void* stream) {
+  return guard([&] {
+    scc::check_ptr(plan, "plan");
+    auto& p = *const_cast<scc_plan_t*>(plan);
+    const auto s = static_cast<cudaStream_t>(stream);
+    scc::do_backward_data(p, n, h, w, dy, weight, dx, s);
+    scc::do_backward_weight(p, n, h, w, dy, x, dweight, dbias, workspace, workspace_bytes, s);
+  });
+}
+
+scc_status_t scc_forward_host_f32(scc_plan_t* plan, int64_t n, int64_t h, int64_t w,
+                                  const float* x, const float* weight, const float* bias,
+                                  float* y) {
+  return guard([&] {
+    scc::check_ptr(plan, "plan");
+    scc::check_extents(n, h, w);
+    scc::check_ptr(x, "x");
+    scc::check_ptr(weight, "weight");
+    scc::check_ptr(y, "y");
+    scc::check_bias(*plan, bias, "bias");
+    std::lock_guard<std::mutex> lk(plan->host_mu);
+    const scc_config_t& c = plan->cfg;
+    scc::Staged g = scc::stage(*plan, n, h, w);
+    const size_t nx = n * c.c_in * h * w * 4, ny = n * c.c_out * h * w * 4;
+    scc::h2d(g.x, x, nx, g.s);
+    scc::h2d(g.w, weight, c.c_out * c.group_width * 4, g.s);
+    if (bias) scc::h2d(g.b, bias, c.c_out * 4, g.s);
+    scc::do_forward(*plan, n, h, w, g.x, g.w, bias ? g.b : nullptr, g.y, g.s);
+    scc::d2h(y, g.y, ny, g.s);
+    scc::cuda_check(cudaStreamSynchronize(g.s), "cudaStreamSynchronize");
+  });
+}
+
+scc_status_t scc_backward_host_f32(scc_plan_t* plan, int64_t n, int64_t h, int64_t w,
+                                   const float* dy, const float* x, const float* weight,
+                                   float* dx, float* dweight, float* dbias) {
+  return guard([&] {
+    scc::check_ptr(plan, "plan");
+    scc::check_extents(n, h, w);
+    scc::check_ptr(dy, "dy");
+    scc::check_ptr(x, "x");
+    scc::check_ptr(weight, "weight");
+    scc::check_ptr(dx, "dx");
+    scc::check_ptr(dweight, "dweight");
+    scc::check_bias(*plan, dbias, "dbias");
+    std::lock_guard<std::mutex> lk(plan->host_mu);
+    const scc_config_t& c = plan->cfg;
+    scc::Staged g = scc::stage(*plan, n, h, w);
+    const size_t nx = n * c.c_in * h * w * 4, ny = n * c.c_out * h * w * 4;
+    scc::h2d(g.dy, dy, ny, g.s);
+    scc::h2d(g.x, x, nx, g.s);
+    scc::h2d(g.w, weight, c.c_out * c.group_width * 4, g.s);
+    scc::do_backward_data(*plan, n, h, w, g.dy, g.w, g.dx, g.s);
+    scc::do_backward_weight(*plan, n, h, w, g.dy, g.x, g.dw, dbias ? g.db : nullptr, g.ws,
+                            g.ws_bytes, g.s);
+    scc::d2h(dx, g.dx, nx, g.s);
+    scc::d2h(dweight, g.dw, c.c_out * c.group_width * 4, g.s);
+    if (dbias) scc::d2h(dbias, g.db, c.c_out * 4, g.s);
+    scc::cuda_check(cudaStreamSynchronize(g.s), "cudaStreamSynchronize");
+  });
+}
+
+scc_status_t scc_fwd_bwd_host_f32(scc_plan_t* plan, int64_t n, int64_t h, int64_t w,
+                                  const float* x, const float* weight, const float* bias,
+                                  const float* dy, float* y, float* dx, float* dweight,
+                                  float* dbias) {
+  return guard([&] {
+    scc::check_ptr(plan, "plan");
+    scc::check_extents(n, h, w);
+    for (const void* p : {static_cast<const void*>(x), static_cast<const void*>(weight),
+                          static_cast<const void*>(dy), static_cast<const void*>(y),
+                          static_cast<const void*>(dx), static_cast<const void*>(dweight)}) {
+      scc::check_ptr(p, "buffer");
+    }
+    scc::check_bias(*plan, bias, "bias");
+    scc::check_bias(*plan, dbias, "dbias");
+    std::lock_guard<std::mutex> lk(plan->host_mu);
+    const scc_config_t& c = plan->cfg;
+    scc::Staged g = scc::stage(*plan, n, h, w);
+    const size_t nx = n * c.c_in * h * w * 4, ny = n * c.c_out * h * w * 4;
+    const size_t nw = c.c_out * c.group_width * 4;
+    scc::h2d(g.x, x, nx, g.s);
+    scc::h2d(g.w, weight, nw, g.s);
+    if (bias) scc::h2d(g.b, bias, c.c_out * 4, g.s);
+    scc::h2d(g.dy, dy, ny, g.s);
+    scc::do_forward(*plan, n, h, w, g.x, g.w, bias ? g.b : nullptr, g.y, g.s);
+    scc::do_backward_data(*plan, n, h, w, g.dy, g.w, g.dx, g.s);
+    scc::do_backward_weight(*plan, n, h, w, g.dy, g.x, g.dw, dbias ? g.db : nullptr, g.ws,
+                            g.ws_bytes, g.s);
+    scc::d2h(y, g.y, ny, g.s);
+    scc::d2h(dx, g.dx, nx, g.s);
+    scc::d2h(dweight, g.dw, nw, g.s);
+    if (dbias) scc::d2h(dbias, g.db, c.c_out * 4, g.s);
+    scc::cuda_check(cudaStreamSynchronize(g.s), "cudaStreamSynchronize");
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,400 @@
+// CUDA-core (fp32 FFMA) family of the SCC operator, sm_100a.
+//
+// band_cc_kernel  — forward (kernel.cpp:29-69) AND input-centric backward-data
+//                   (kernel.cpp:98-138).  Both are the same "banded channel
+//                   mix": every output row (a filter, or an input channel)
+//                   reduces a cyclic arc of the other side's channels.  A CTA
+//                   owns 128 pixels and a group of 8 row-blocks (8 rows each,
+//                   one per warp); it stages the group's arc of input rows in
+//                   shared memory chunk by chunk, so each input row is read
+//                   once per group and reused by every filter whose window
+//                   covers it (the paper's channel-cyclic reuse).  Writes are
+//                   disjoint per output element: no atomics anywhere.
+// weight_cc_kernel — backward-weight (kernel.cpp:140-181): per row-block and
+//                   arc tile, outer products over pixel tiles staged in smem,
+//                   fixed-order reduction across lanes, then a fixed-order
+//                   reduction across pixel splits in weight_finalize_kernel.
+//                   Deterministic: bitwise identical from run to run.
+#include <algorithm>
+
+#include "scc_kernels.hpp"
+#include "scc_plan.hpp"
+
+namespace scc {
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int KC = 32;   // ring positions per staged chunk
+constexpr int TQ = 128;  // pixels per CTA in the band kernel (32 lanes x 4)
+
+__device__ __forceinline__ int wrap(int v, int n) { return v >= n ? v - n : v; }
+
+// w[oc][(ic - start(oc)) mod c_in] inside the window, else 0.
+__device__ __forceinline__ float band_weight(const BandLaunch& a, int oc, int ic) {
+  const int st = static_cast<int>((static_cast<long long>(oc) * a.shift) % a.c_in);
+  int s = ic - st;
+  if (s < 0) s += a.c_in;
+  return s < a.gw ? __ldg(a.weight + static_cast<long long>(oc) * a.gw + s) : 0.f;
+}
+
+template <bool VEC>
+__device__ __forceinline__ float4 load4(const float* __restrict__ base, int64_t c_t,
+                                        int ch, int64_t plane, int64_t q, int64_t qend) {
+  float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (VEC) {
+    if (q < qend) {
+      const int64_t n = q / plane, p = q - n * plane;
+      v = __ldg(reinterpret_cast<const float4*>(base + (n * c_t + ch) * plane + p));
+    }
+  } else {
+    float e[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int64_t qi = q + i;
+      e[i] = 0.f;
+      if (qi < qend) {
+        const int64_t n = qi / plane, p = qi - n * plane;
+        e[i] = __ldg(base + (n * c_t + ch) * plane + p);
+      }
+    }
+    v = make_float4(e[0], e[1], e[2], e[3]);
+  }
+  return v;
+}
+
+template <bool VEC>
+__device__ __forceinline__ void store4(float* __restrict__ base, int64_t c_t, int ch,
+                                       int64_t plane, int64_t q, int64_t qend, float4 v) {
+  if (VEC) {
+    if (q < qend) {
+      const int64_t n = q / plane, p = q - n * plane;
+      *reinterpret_cast<float4*>(base + (n * c_t + ch) * plane + p) = v;
+    }
+  } else {
+    const float e[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int64_t qi = q + i;
+      if (qi < qend) {
+        const int64_t n = qi / plane, p = qi - n * plane;
+        base[(n * c_t + ch) * plane + p] = e[i];
+      }
+    }
+  }
+}
+
+template <bool VEC>
+__global__ void __launch_bounds__(kThreads) band_cc_kernel(const BandLaunch a) {
+  __shared__ __align__(16) float xs[KC][TQ];
+  __shared__ __align__(16) float ws[kBlocksPerGroup][KC][kRowsPerBlock];
+
+  const int g = static_cast<int>(blockIdx.x % a.ngrp);
+  const int64_t q0 = static_cast<int64_t>(blockIdx.x / a.ngrp) * TQ;
+  const int first = a.groups[4 * g + 0];
+  const int nb = a.groups[4 * g + 1];
+  const int gstart = a.groups[4 * g + 2];
+  const int glen = a.groups[4 * g + 3];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t qend = a.n * a.plane;
+
+  const bool active = warp < nb;
+  int boff = 0, blen = 0;
+  int orow[kRowsPerBlock];
+  float4 acc[kRowsPerBlock];
+  if (active) {
+    const int blk = first + warp;
+    blen = a.blocks[2 * blk + 1];
+    boff = a.blocks[2 * blk] - gstart;
+    if (boff < 0) boff += a.ring;
+#pragma unroll
+    for (int j = 0; j < kRowsPerBlock; ++j) {
+      orow[j] = a.rows[blk * kRowsPerBlock + j];
+      const float b = (a.bias != nullptr && orow[j] >= 0) ? __ldg(a.bias + orow[j]) : 0.f;
+      acc[j] = make_float4(b, b, b, b);
+    }
+  }
+  // The block's arc in group coordinates: [boff, boff+blen), which can wrap
+  // past glen only when the group arc is the whole ring.
+  const int i1_lo = boff, i1_hi = min(boff + blen, glen);
+  const int i2_hi = max(0, boff + blen - glen);
+
+  for (int c0 = 0; c0 < glen; c0 += KC) {
+    const int kc = min(KC, glen - c0);
+    for (int idx = threadIdx.x; idx < KC * (TQ / 4); idx += kThreads) {
+      const int r = idx / (TQ / 4), c4 = idx - r * (TQ / 4);
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (r < kc) {
+        const int pos = wrap(gstart + c0 + r, a.ring);
+        const int ch = a.ring_map ? __ldg(a.ring_map + pos) : pos;
+        v = load4<VEC>(a.in, a.c_in_t, ch, a.plane, q0 + c4 * 4, qend);
+      }
+      *reinterpret_cast<float4*>(&xs[r][c4 * 4]) = v;
+    }
+    for (int idx = threadIdx.x; idx < nb * KC * kRowsPerBlock; idx += kThreads) {
+      const int wb = idx / (KC * kRowsPerBlock);
+      const int rem = idx - wb * (KC * kRowsPerBlock);
+      const int r = rem / kRowsPerBlock, j = rem - r * kRowsPerBlock;
+      float v = 0.f;
+      if (r < kc) {
+        const int blk = first + wb;
+        int off = a.blocks[2 * blk] - gstart;
+        if (off < 0) off += a.ring;
+        int u = c0 + r - off;
+        if (u < 0) u += a.ring;
+        const int row = a.rows[blk * kRowsPerBlock + j];
+        if (u < a.blocks[2 * blk + 1] && row >= 0) {
+          const int pos = wrap(gstart + c0 + r, a.ring);
+          v = a.backward_data ? band_weight(a, __ldg(a.ring_map + pos), row)
+                              : band_weight(a, row, pos);
+        }
+      }
+      ws[wb][r][j] = v;
+    }
+    __syncthreads();
+    if (active) {
+      // Two sub-ranges of this chunk that lie inside the block arc.
+      const int ra0 = max(i1_lo - c0, 0), ra1 = min(i1_hi - c0, kc);
+      const int rb0 = 0, rb1 = min(i2_hi - c0, kc);
+#pragma unroll 1
+      for (int pass = 0; pass < 2; ++pass) {
+        const int r0 = pass == 0 ? ra0 : rb0;
+        const int r1 = pass == 0 ? ra1 : rb1;
+#pragma unroll 4
+        for (int r = r0; r < r1; ++r) {
+          const float4 xv = *reinterpret_cast<const float4*>(&xs[r][lane * 4]);
+          const float4 w0 = *reinterpret_cast<const float4*>(&ws[warp][r][0]);
+          const float4 w1 = *reinterpret_cast<const float4*>(&ws[warp][r][4]);
+          const float wv[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+#pragma unroll
+          for (int j = 0; j < kRowsPerBlock; ++j) {
+            acc[j].x = fmaf(wv[j], xv.x, acc[j].x);
+            acc[j].y = fmaf(wv[j], xv.y, acc[j].y);
+            acc[j].z = fmaf(wv[j], xv.z, acc[j].z);
+            acc[j].w = fmaf(wv[j], xv.w, acc[j].w);
+          }
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (active) {
+#pragma unroll
+    for (int j = 0; j < kRowsPerBlock; ++j) {
+      if (orow[j] >= 0) store4<VEC>(a.out, a.c_out_t, orow[j], a.plane, q0 + lane * 4, qend, acc[j]);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// backward-weight
+
+struct WeightGrid {
+  int kt_size;      // 32 or 64 arc positions per CTA
+  int nkt;          // arc tiles per block
+  int splits;       // pixel splits (reduced in finalize)
+  int64_t qchunk;   // pixels per split (multiple of the pixel tile)
+  int64_t blk_stride;   // floats per block in one split's partial slab
+  int64_t split_stride; // floats per split
+};
+
+WeightGrid weight_grid(int32_t nblk, int32_t max_block_len, int64_t n, int64_t plane) {
+  WeightGrid g{};
+  g.kt_size = max_block_len <= 32 ? 32 : 64;
+  g.nkt = std::max(1, (max_block_len + g.kt_size - 1) / g.kt_size);
+  const int tqw = (kThreads / (g.kt_size / 4)) * 4;
+  const int64_t q = n * plane;
+  const int64_t tiles = std::max<int64_t>(1, (q + tqw - 1) / tqw);
+  const int64_t want = (148 * 6 + static_cast<int64_t>(nblk) * g.nkt - 1) /
+                       (static_cast<int64_t>(nblk) * g.nkt);
+  g.splits = static_cast<int>(std::clamp<int64_t>(want, 1, std::max<int64_t>(1, tiles / 2)));
+  const int64_t tiles_per = (tiles + g.splits - 1) / g.splits;
+  g.qchunk = tiles_per * tqw;
+  g.splits = static_cast<int>((q + g.qchunk - 1) / g.qchunk);
+  if (g.splits < 1) g.splits = 1;
+  g.blk_stride = static_cast<int64_t>(g.nkt) * g.kt_size * kRowsPerBlock + kRowsPerBlock;
+  g.split_stride = g.blk_stride * nblk;
+  return g;
+}
+
+template <int KT, bool VEC>
+__global__ void __launch_bounds__(kThreads) weight_cc_kernel(const WeightLaunch a, WeightGrid gr) {
+  constexpr int NKG = KT / 4;          // arc-position groups (4 positions each, strided)
+  constexpr int NQL = kThreads / NKG;  // pixel lanes
+  constexpr int TQW = NQL * 4;         // pixels per staged tile
+  constexpr int XS = TQW + 4;          // padded row stride (bank-conflict free)
+  constexpr int kStage = kRowsPerBlock * TQW + KT * XS;
+  constexpr int kRed = NQL * kRowsPerBlock * KT;
+  constexpr int kSmem = (kStage > kRed ? kStage : kRed) + NQL * kRowsPerBlock;
+  __shared__ __align__(16) float smem[kSmem];
+  float* gs = smem;                       // [8][TQW]
+  float* xs = smem + kRowsPerBlock * TQW; // [KT][XS]
+  float* red = smem;                      // [NQL][8][KT] (after the main loop)
+  float* bred = smem + (kStage > kRed ? kStage : kRed);  // [NQL][8]
+
+  const int blk = static_cast<int>(blockIdx.x % a.nblk);
+  const int rest = static_cast<int>(blockIdx.x / a.nblk);
+  const int kt = rest % gr.nkt;
+  const int split = rest / gr.nkt;
+  const int bstart = a.blocks[2 * blk], blen = a.blocks[2 * blk + 1];
+  const int k0 = kt * KT;
+  if (k0 >= blen && kt > 0) return;  // uniform across the CTA
+  const int tid = threadIdx.x;
+  const int kg = tid % NKG, ql = tid / NKG;
+  const int64_t qend_all = a.n * a.plane;
+  const int64_t qs = static_cast<int64_t>(split) * gr.qchunk;
+  const int64_t qe = min(qend_all, qs + gr.qchunk);
+  const bool bias_lane = (a.dbias != nullptr) && kt == 0 && kg == 0;
+
+  int rows[kRowsPerBlock];
+#pragma unroll
+  for (int j = 0; j < kRowsPerBlock; ++j) rows[j] = a.rows[blk * kRowsPerBlock + j];
+
+  float acc[kRowsPerBlock][4];
+  float bacc[kRowsPerBlock];
+#pragma unroll
+  for (int j = 0; j < kRowsPerBlock; ++j) {
+    bacc[j] = 0.f;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) acc[j][i] = 0.f;
+  }
+
+  for (int64_t q0 = qs; q0 < qe; q0 += TQW) {
+    for (int idx = tid; idx < kRowsPerBlock * (TQW / 4); idx += kThreads) {
+      const int j = idx / (TQW / 4), c4 = idx - j * (TQW / 4);
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (a.rows[blk * kRowsPerBlock + j] >= 0)
+        v = load4<VEC>(a.dy, a.c_out, a.rows[blk * kRowsPerBlock + j], a.plane, q0 + c4 * 4, qe);
+      *reinterpret_cast<float4*>(gs + j * TQW + c4 * 4) = v;
+    }
+    for (int idx = tid; idx < KT * (TQW / 4); idx += kThreads) {
+      const int r = idx / (TQW / 4), c4 = idx - r * (TQW / 4);
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (k0 + r < blen) {
+        const int ch = wrap(bstart + k0 + r, a.c_in);
+        v = load4<VEC>(a.x, a.c_in, ch, a.plane, q0 + c4 * 4, qe);
+      }
+      *reinterpret_cast<float4*>(xs + r * XS + c4 * 4) = v;
+    }
+    __syncthreads();
+    float4 xv[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) xv[i] = *reinterpret_cast<const float4*>(xs + (kg + NKG * i) * XS + ql * 4);
+#pragma unroll
+    for (int j = 0; j < kRowsPerBlock; ++j) {
+      const float4 g4 = *reinterpret_cast<const float4*>(gs + j * TQW + ql * 4);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        float t = acc[j][i];
+        t = fmaf(g4.x, xv[i].x, t);
+        t = fmaf(g4.y, xv[i].y, t);
+        t = fmaf(g4.z, xv[i].z, t);
+        t = fmaf(g4.w, xv[i].w, t);
+        acc[j][i] = t;
+      }
+      if (bias_lane) bacc[j] += ((g4.x + g4.y) + g4.z) + g4.w;
+    }
+    __syncthreads();
+  }
+
+  // Fixed-order reduction across the pixel lanes.
+#pragma unroll
+  for (int j = 0; j < kRowsPerBlock; ++j) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) red[(ql * kRowsPerBlock + j) * KT + kg + NKG * i] = acc[j][i];
+  }
+  if (kt == 0 && kg == 0) {
+#pragma unroll
+    for (int j = 0; j < kRowsPerBlock; ++j) bred[ql * kRowsPerBlock + j] = bacc[j];
+  }
+  __syncthreads();
+  float* part = a.partial + split * gr.split_stride + blk * gr.blk_stride;
+  for (int o = tid; o < kRowsPerBlock * KT; o += kThreads) {
+    const int j = o / KT, k = o - j * KT;
+    float s = 0.f;
+#pragma unroll 4
+    for (int l = 0; l < NQL; ++l) s += red[(l * kRowsPerBlock + j) * KT + k];
+    part[(k0 + k) * kRowsPerBlock + j] = s;
+  }
+  if (kt == 0 && tid < kRowsPerBlock) {
+    float s = 0.f;
+    for (int l = 0; l < NQL; ++l) s += bred[l * kRowsPerBlock + tid];
+    part[gr.nkt * KT * kRowsPerBlock + tid] = s;
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) weight_finalize_kernel(const WeightLaunch a, WeightGrid gr) {
+  const int64_t nw = static_cast<int64_t>(a.c_out) * a.gw;
+  const int64_t total = nw + (a.dbias != nullptr ? a.c_out : 0);
+  for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
+       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    if (idx < nw) {
+      const int oc = static_cast<int>(idx / a.gw);
+      const int slot = static_cast<int>(idx - static_cast<int64_t>(oc) * a.gw);
+      const int pos = a.inv_perm[oc];
+      const int blk = pos / kRowsPerBlock, j = pos - blk * kRowsPerBlock;
+      const int st = static_cast<int>((static_cast<long long>(oc) * a.shift) % a.c_in);
+      int k = st + slot - a.blocks[2 * blk];
+      k %= a.c_in;
+      if (k < 0) k += a.c_in;
+      const float* p = a.partial + blk * gr.blk_stride + k * kRowsPerBlock + j;
+      float s = 0.f;
+      for (int sp = 0; sp < gr.splits; ++sp) s += p[sp * gr.split_stride];
+      a.dweight[idx] = s;
+    } else {
+      const int oc = static_cast<int>(idx - nw);
+      const int pos = a.inv_perm[oc];
+      const int blk = pos / kRowsPerBlock, j = pos - blk * kRowsPerBlock;
+      const float* p = a.partial + blk * gr.blk_stride + gr.nkt * gr.kt_size * kRowsPerBlock + j;
+      float s = 0.f;
+      for (int sp = 0; sp < gr.splits; ++sp) s += p[sp * gr.split_stride];
+      a.dbias[oc] = s;
+    }
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_band_cc(const BandLaunch& a, cudaStream_t s) {
+  const int64_t q = a.n * a.plane;
+  const int64_t tiles = (q + TQ - 1) / TQ;
+  const int64_t grid = tiles * a.ngrp;
+  if (grid <= 0) return cudaSuccess;
+  if (grid > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
+  if (a.plane % 4 == 0) {
+    band_cc_kernel<true><<<static_cast<unsigned>(grid), kThreads, 0, s>>>(a);
+  } else {
+    band_cc_kernel<false><<<static_cast<unsigned>(grid), kThreads, 0, s>>>(a);
+  }
+  note_launches(1);
+  return cudaGetLastError();
+}
+
+size_t weight_cc_workspace_bytes(int32_t nblk, int32_t max_block_len, int64_t n,
+                                 int64_t plane) {
+  const WeightGrid g = weight_grid(nblk, max_block_len, n, plane);
+  return static_cast<size_t>(g.split_stride) * g.splits * sizeof(float);
+}
+
+cudaError_t launch_weight_cc(const WeightLaunch& a, size_t ws_bytes, cudaStream_t s) {
+  const WeightGrid g = weight_grid(a.nblk, a.max_block_len, a.n, a.plane);
+  if (static_cast<size_t>(g.split_stride) * g.splits * sizeof(float) > ws_bytes)
+    return cudaErrorInvalidValue;
+  const int64_t grid = static_cast<int64_t>(a.nblk) * g.nkt * g.splits;
+  const bool vec = a.plane % 4 == 0;
+  if (g.kt_size == 32) {
+    if (vec) weight_cc_kernel<32, true><<<static_cast<unsigned>(grid), kThreads, 0, s>>>(a, g);
+    else weight_cc_kernel<32, false><<<static_cast<unsigned>(grid), kThreads, 0, s>>>(a, g);
+  } else {
+    if (vec) weight_cc_kernel<64, true><<<static_cast<unsigned>(grid), kThreads, 0, s>>>(a, g);
+    else weight_cc_kernel<64, false><<<static_cast<unsigned>(grid), kThreads, 0, s>>>(a, g);
+  }
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  const int64_t total = static_cast<int64_t>(a.c_out) * a.gw + (a.dbias ? a.c_out : 0);
+  const int fgrid = static_cast<int>(std::min<int64_t>((total + kThreads - 1) / kThreads, 148 * 8));
+  weight_finalize_kernel<<<fgrid, kThreads, 0, s>>>(a, g);
+  note_launches(2);
+  return cudaGetLastError();
+}
+
+}  // namespace scc

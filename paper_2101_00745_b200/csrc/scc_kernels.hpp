@@ -1,0 +1,55 @@
+// Launch interface of the SCC device kernels (CUDA-core and tcgen05 families).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+
+namespace scc {
+
+// Geometry + tables one band launch needs (all device pointers).
+struct BandLaunch {
+  const float* in;          // [N][c_in_t][P]  (x for forward, dy for backward-data)
+  float* out;               // [N][c_out_t][P]
+  const float* weight;      // [c_out*gw], window-relative
+  const float* bias;        // [c_out] or nullptr (forward only)
+  const int32_t* rows;      // [nblk*8] output channel per row, -1 = pad
+  const int32_t* ring_map;  // ring position -> input channel, nullptr = identity
+  const int32_t* blocks;    // [nblk][2] arc on the ring
+  const int32_t* groups;    // [ngrp][4]
+  int32_t ngrp;
+  int32_t ring;
+  int32_t c_in_t, c_out_t;  // channel counts of in / out tensors
+  int32_t c_in, gw;         // operator geometry (weight lookup)
+  int64_t shift;
+  int64_t n, plane;         // batch, H*W
+  bool backward_data;       // weight lookup orientation
+};
+
+struct WeightLaunch {
+  const float* dy;          // [N][c_out][P]
+  const float* x;           // [N][c_in][P]
+  float* dweight;           // [c_out*gw]
+  float* dbias;             // [c_out] or nullptr
+  float* partial;           // workspace
+  const int32_t* rows;      // forward rows (sorted filters), [nblk*8]
+  const int32_t* blocks;    // forward block arcs
+  const int32_t* inv_perm;  // oc -> sorted position
+  int32_t nblk;
+  int32_t max_block_len;
+  int32_t c_in, c_out, gw;
+  int64_t shift;
+  int64_t n, plane;
+};
+
+// Counter of kernels launched by this library (scc_launch_count()).
+void note_launches(uint64_t k);
+
+// CUDA-core family -----------------------------------------------------------
+cudaError_t launch_band_cc(const BandLaunch& a, cudaStream_t s);
+size_t weight_cc_workspace_bytes(int32_t nblk, int32_t max_block_len, int64_t n,
+                                 int64_t plane);
+cudaError_t launch_weight_cc(const WeightLaunch& a, size_t ws_bytes, cudaStream_t s);
+
+}  // namespace scc

@@ -1,0 +1,242 @@
+// Host plan construction (see scc_plan.hpp).
+#include "scc_plan.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <numeric>
+#include <stdexcept>
+
+namespace scc {
+
+namespace {
+
+[[noreturn]] void fail(scc_status_t code, std::string msg) {
+  throw Error{code, std::move(msg)};
+}
+
+// The cycle walk of compute_channel_cycle (cycle.cpp:9-21): starts 0, +shift
+// mod c_in, stop at the first repeat or after c_out windows.
+std::vector<int64_t> walk_cycle(int64_t c_in, int64_t c_out, int64_t shift) {
+  std::vector<int64_t> starts;
+  std::vector<char> seen(static_cast<size_t>(c_in), 0);
+  int64_t s = 0;
+  while (static_cast<int64_t>(starts.size()) < c_out && !seen[static_cast<size_t>(s)]) {
+    seen[static_cast<size_t>(s)] = 1;
+    starts.push_back(s);
+    s = (s + shift) % c_in;
+  }
+  return starts;
+}
+
+void build_groups(BandSide& side) {
+  side.groups.clear();
+  const int nb = side.nblk();
+  for (int b0 = 0; b0 < nb; b0 += kBlocksPerGroup) {
+    const int cnt = std::min(kBlocksPerGroup, nb - b0);
+    std::vector<Arc> parts(side.blocks.begin() + b0, side.blocks.begin() + b0 + cnt);
+    const Arc a = cover_arcs(parts, side.ring);
+    side.groups.insert(side.groups.end(), {b0, cnt, a.start, a.len});
+  }
+  side.max_block_len = 0;
+  for (const Arc& a : side.blocks) side.max_block_len = std::max(side.max_block_len, a.len);
+}
+
+}  // namespace
+
+Arc cover_arcs(const std::vector<Arc>& parts, int32_t n) {
+  Arc best{0, 0};
+  bool any = false;
+  int64_t best_len = INT64_MAX;
+  for (const Arc& cand : parts) {
+    if (cand.len <= 0) continue;
+    any = true;
+    if (cand.len >= n) return Arc{0, n};
+    int64_t need = 0;
+    for (const Arc& a : parts) {
+      if (a.len <= 0) continue;
+      const int64_t off = ((static_cast<int64_t>(a.start) - cand.start) % n + n) % n;
+      need = std::max<int64_t>(need, off + a.len);
+    }
+    if (need < best_len) {
+      best_len = need;
+      best = Arc{cand.start, static_cast<int32_t>(std::min<int64_t>(need, n))};
+    }
+  }
+  if (!any) return Arc{0, 0};
+  if (best.len >= n) best = Arc{0, n};
+  return best;
+}
+
+int64_t resolve_overlap(int32_t kind, double ratio, int64_t count, int64_t gw) {
+  if (kind == SCC_OVERLAP_RATIO) {
+    if (!(ratio >= 0.0 && ratio <= 1.0)) {
+      fail(SCC_ERR_CONFIG, "overlap fraction " + std::to_string(ratio) + " outside [0, 1]");
+    }
+    // std::llround: halves round away from zero (config.cpp:45); Python's
+    // round() would not (gw=5, co=50% -> 3 here, 2 under banker's rounding).
+    return std::llround(ratio * static_cast<double>(gw));
+  }
+  if (kind != SCC_OVERLAP_CHANNELS) fail(SCC_ERR_ARGUMENT, "unknown overlap kind");
+  if (count < 0 || count > gw) {
+    fail(SCC_ERR_CONFIG, "overlap of " + std::to_string(count) + " channels outside [0, " +
+                             std::to_string(gw) + "] for window width " + std::to_string(gw));
+  }
+  return count;
+}
+
+void parse_overlap(const char* text, int32_t* kind, double* ratio, int64_t* count) {
+  if (text == nullptr) fail(SCC_ERR_ARGUMENT, "null overlap text");
+  const std::string t(text);
+  if (t.empty()) fail(SCC_ERR_ARGUMENT, "empty overlap value");
+  try {
+    size_t used = 0;
+    if (t.back() == '%') {
+      const std::string num = t.substr(0, t.size() - 1);
+      const double pct = std::stod(num, &used);
+      if (used != num.size()) fail(SCC_ERR_ARGUMENT, "bad overlap '" + t + "'");
+      *kind = SCC_OVERLAP_RATIO;
+      *ratio = pct / 100.0;
+      *count = 0;
+      return;
+    }
+    if (t.find_first_of(".eE") != std::string::npos) {
+      const double r = std::stod(t, &used);
+      if (used != t.size()) fail(SCC_ERR_ARGUMENT, "bad overlap '" + t + "'");
+      *kind = SCC_OVERLAP_RATIO;
+      *ratio = r;
+      *count = 0;
+      return;
+    }
+    const long long c = std::stoll(t, &used);
+    if (used != t.size()) fail(SCC_ERR_ARGUMENT, "bad overlap '" + t + "'");
+    *kind = SCC_OVERLAP_CHANNELS;
+    *ratio = 0.0;
+    *count = c;
+  } catch (const std::invalid_argument&) {
+    fail(SCC_ERR_ARGUMENT, "bad overlap '" + t + "'");
+  } catch (const std::out_of_range&) {
+    fail(SCC_ERR_ARGUMENT, "overlap '" + t + "' out of numeric range");
+  }
+}
+
+void build_plan(Plan& p, int64_t c_in, int64_t c_out, int64_t cg, int32_t kind,
+                double ratio, int64_t count, int32_t has_bias) {
+  // scc_config_new (config.cpp:62-83).
+  if (c_in < 1) fail(SCC_ERR_CONFIG, "c_in must be >= 1, got " + std::to_string(c_in));
+  if (c_out < 1) fail(SCC_ERR_CONFIG, "c_out must be >= 1, got " + std::to_string(c_out));
+  if (cg < 1 || cg > c_in) {
+    fail(SCC_ERR_CONFIG, "cg must be in [1, c_in=" + std::to_string(c_in) + "], got " +
+                             std::to_string(cg));
+  }
+  if (c_in % cg != 0) {
+    fail(SCC_ERR_CONFIG,
+         "cg=" + std::to_string(cg) + " does not divide c_in=" + std::to_string(c_in));
+  }
+  if (c_in > (1 << 24) || c_out > (1 << 24)) {
+    fail(SCC_ERR_CONFIG, "channel counts above 2^24 are not supported by the device tables");
+  }
+  scc_config_t& c = p.cfg;
+  c.c_in = c_in;
+  c.c_out = c_out;
+  c.cg = cg;
+  c.group_width = c_in / cg;
+  c.overlap_channels = resolve_overlap(kind, ratio, count, c.group_width);
+  c.shift = c.group_width - c.overlap_channels;
+  c.has_bias = has_bias ? 1 : 0;
+  c.fully_overlapped = (c.shift == 0 && cg > 1) ? 1 : 0;
+  p.cycle_starts = walk_cycle(c_in, c_out, c.shift);
+  c.cyclic_dist = static_cast<int64_t>(p.cycle_starts.size());
+
+  // The closed form the device uses must agree with the cycle lookup.
+  for (int64_t oc = 0; oc < c_out; ++oc) {
+    if (p.cycle_starts[static_cast<size_t>(oc % c.cyclic_dist)] != p.start_of(oc)) {
+      fail(SCC_ERR_INTERNAL, "window-start closed form disagrees with the cycle walk");
+    }
+  }
+
+  // Cycle-sorted order of the filters: by window start, then oc.
+  p.perm.resize(static_cast<size_t>(c_out));
+  std::iota(p.perm.begin(), p.perm.end(), 0);
+  std::stable_sort(p.perm.begin(), p.perm.end(), [&](int32_t a, int32_t b) {
+    return p.start_of(a) < p.start_of(b);
+  });
+  p.inv_perm.resize(static_cast<size_t>(c_out));
+  for (int64_t i = 0; i < c_out; ++i) p.inv_perm[static_cast<size_t>(p.perm[i])] = static_cast<int32_t>(i);
+
+  const int32_t gw = static_cast<int32_t>(c.group_width);
+
+  // Forward: rows = filters in sorted order, ring = input channels.
+  {
+    BandSide& f = p.fwd;
+    f.ring = static_cast<int32_t>(c_in);
+    f.ring_map.clear();
+    const int nb = static_cast<int>((c_out + kRowsPerBlock - 1) / kRowsPerBlock);
+    f.rows.assign(static_cast<size_t>(nb) * kRowsPerBlock, -1);
+    f.blocks.resize(static_cast<size_t>(nb));
+    for (int b = 0; b < nb; ++b) {
+      std::vector<Arc> parts;
+      for (int j = 0; j < kRowsPerBlock; ++j) {
+        const int64_t i = static_cast<int64_t>(b) * kRowsPerBlock + j;
+        if (i >= c_out) break;
+        const int32_t oc = p.perm[static_cast<size_t>(i)];
+        f.rows[static_cast<size_t>(i)] = oc;
+        parts.push_back(Arc{static_cast<int32_t>(p.start_of(oc)), gw});
+      }
+      f.blocks[static_cast<size_t>(b)] = cover_arcs(parts, f.ring);
+    }
+    build_groups(f);
+  }
+
+  // Backward-data: rows = input channels, ring = filters in sorted order.
+  // The filters covering ic are those with start in (ic-gw, ic] (cyclic), a
+  // contiguous run of the sorted order (verified below against the direct
+  // membership test of ChannelWindow::contains, cycle.hpp:18-20).
+  {
+    BandSide& d = p.bwd;
+    d.ring = static_cast<int32_t>(c_out);
+    d.ring_map = p.perm;
+    const int nb = static_cast<int>((c_in + kRowsPerBlock - 1) / kRowsPerBlock);
+    d.rows.assign(static_cast<size_t>(nb) * kRowsPerBlock, -1);
+    d.blocks.resize(static_cast<size_t>(nb));
+    std::vector<int32_t> covered;
+    for (int b = 0; b < nb; ++b) {
+      std::vector<Arc> parts;
+      for (int j = 0; j < kRowsPerBlock; ++j) {
+        const int64_t ic = static_cast<int64_t>(b) * kRowsPerBlock + j;
+        if (ic >= c_in) break;
+        d.rows[static_cast<size_t>(ic)] = static_cast<int32_t>(ic);
+        covered.clear();
+        for (int64_t i = 0; i < c_out; ++i) {
+          if (p.slot_of(p.perm[static_cast<size_t>(i)], ic) >= 0) covered.push_back(static_cast<int32_t>(i));
+        }
+        if (covered.empty()) continue;
+        // Find the arc: the covered positions are contiguous modulo c_out.
+        const int32_t n = static_cast<int32_t>(c_out);
+        int32_t first = covered.front();
+        if (static_cast<int64_t>(covered.size()) < n && covered.front() == 0 &&
+            covered.back() == n - 1) {
+          // Wrapping run: starts after the first gap.
+          for (size_t k = 1; k < covered.size(); ++k) {
+            if (covered[k] != covered[k - 1] + 1) {
+              first = covered[k];
+              break;
+            }
+          }
+        }
+        const Arc a{first, static_cast<int32_t>(covered.size())};
+        for (int32_t k = 0; k < a.len; ++k) {
+          const int32_t pos = (a.start + k) % n;
+          if (p.slot_of(p.perm[static_cast<size_t>(pos)], ic) < 0) {
+            fail(SCC_ERR_INTERNAL, "covering filters are not contiguous in cycle order");
+          }
+        }
+        parts.push_back(a);
+      }
+      d.blocks[static_cast<size_t>(b)] = cover_arcs(parts, d.ring);
+    }
+    build_groups(d);
+  }
+}
+
+}  // namespace scc

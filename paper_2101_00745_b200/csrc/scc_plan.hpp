@@ -1,0 +1,111 @@
+// Host-side plan for the B200 SCC operator.
+//
+// Replaces the reference's per-call geometry work (config.cpp:62-83,
+// cycle.cpp:9-40, the pull table of kernel.cpp:109-118) with tables built once
+// per layer configuration and uploaded once per device:
+//   * the window start of every filter, start(oc) = (oc*shift) mod c_in, which
+//     equals windows[oc mod cyclic_dist] of compute_channel_cycle
+//     (cycle_test.cpp:104-106, asserted in build());
+//   * a "cycle-sorted" permutation of the output channels (by window start,
+//     then oc), under which every input channel's covering filters form one
+//     contiguous arc (the inverse map covering_filters walks, cycle.cpp:28-40);
+//   * band tiles: runs of kRowsPerBlock consecutive output rows (forward) or
+//     input rows (backward-data) together with the smallest cyclic arc of the
+//     other side's channels that feeds them.  The CUDA kernels iterate over
+//     exactly that arc, so no kernel ever touches channels outside the band.
+#pragma once
+
+#include <cstdint>
+#include <deque>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "scc_b200.h"
+
+namespace scc {
+
+constexpr int kRowsPerBlock = 8;    // output rows owned by one warp
+constexpr int kBlocksPerGroup = 8;  // warps (blocks) per CTA in the band kernels
+
+// Thrown inside the library and mapped to scc_status_t at the C boundary.
+struct Error {
+  scc_status_t code;
+  std::string msg;
+};
+
+// A cyclic arc [start, start+len) over a ring of `ring` positions.
+struct Arc {
+  int32_t start = 0;
+  int32_t len = 0;
+};
+
+// Smallest arc covering every (non-empty) arc of `parts` on a ring of size n.
+Arc cover_arcs(const std::vector<Arc>& parts, int32_t n);
+
+// Band tiling of one operator direction.
+struct BandSide {
+  int32_t ring = 0;                  // positions on the reduction ring
+  std::vector<int32_t> ring_map;     // ring position -> channel (empty = identity)
+  std::vector<int32_t> rows;         // nblk*8 output channels (-1 = padding)
+  std::vector<Arc> blocks;           // per block: arc on the ring
+  std::vector<int32_t> groups;       // per group: first_blk, nblk, arc.start, arc.len
+  int32_t max_block_len = 0;
+  int nblk() const { return static_cast<int>(blocks.size()); }
+  int ngrp() const { return static_cast<int>(groups.size() / 4); }
+};
+
+// Device copy of the tables (one per CUDA device).
+struct DeviceTables {
+  int device = -1;
+  void* base = nullptr;  // single allocation
+  const int32_t* fwd_rows = nullptr;
+  const int32_t* fwd_blocks = nullptr;  // [nblk][2]
+  const int32_t* fwd_groups = nullptr;  // [ngrp][4]
+  const int32_t* bwd_rows = nullptr;
+  const int32_t* bwd_blocks = nullptr;
+  const int32_t* bwd_groups = nullptr;
+  const int32_t* perm = nullptr;      // sorted position -> oc
+  const int32_t* inv_perm = nullptr;  // oc -> sorted position
+};
+
+// Device staging for the host-buffer entry points.
+struct HostStaging {
+  int device = -1;
+  void* buf = nullptr;
+  size_t bytes = 0;
+  void* stream = nullptr;  // cudaStream_t
+};
+
+struct Plan {
+  scc_config_t cfg{};
+  std::vector<int64_t> cycle_starts;  // compute_channel_cycle order
+  std::vector<int32_t> perm, inv_perm;
+  BandSide fwd, bwd;
+  int32_t path = SCC_PATH_AUTO;
+
+  std::mutex dev_mu;
+  std::deque<DeviceTables> dev;  // deque: references stay valid
+  std::mutex host_mu;
+  std::deque<HostStaging> staging;
+
+  int64_t start_of(int64_t oc) const { return (oc * cfg.shift) % cfg.c_in; }
+  // Forward-band weight of output channel oc on input channel ic (0 outside
+  // the window); slot index into the [oc][k] weight array, or -1.
+  int64_t slot_of(int64_t oc, int64_t ic) const {
+    const int64_t s = ((ic - start_of(oc)) % cfg.c_in + cfg.c_in) % cfg.c_in;
+    return s < cfg.group_width ? oc * cfg.group_width + s : -1;
+  }
+};
+
+// Validates like scc_config_new and builds every table (throws Error).
+void build_plan(Plan& p, int64_t c_in, int64_t c_out, int64_t cg, int32_t kind,
+                double ratio, int64_t count, int32_t has_bias);
+
+// Overlap::resolve semantics (config.cpp:39-53).
+int64_t resolve_overlap(int32_t kind, double ratio, int64_t count, int64_t gw);
+
+// Overlap::parse semantics (config.cpp:15-37).
+void parse_overlap(const char* text, int32_t* kind, double* ratio, int64_t* count);
+
+}  // namespace scc

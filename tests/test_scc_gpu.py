@@ -1,0 +1,369 @@
+"""GPU parity: the sm_100a kernels (through the C ABI) against the CPU oracle.
+
+Bars (BASELINE.json north_star): forward norm-relative error <= 1e-5, dx/dW/db
+<= 1e-4 (max|d| / max|ref|, the reference's own metric, gradcheck.cpp:199-216);
+the window/channel index mapping bit-exact (integer-valued inputs, for which
+fp32 arithmetic is exact).  Every kernel family the build offers is tested.
+"""
+import glob
+import os
+
+import numpy as np
+import pytest
+
+from conftest import norm_rel
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+FWD_TOL = 1e-5
+GRAD_TOL = 1e-4
+GOLDEN = sorted(glob.glob(os.path.join(os.path.dirname(__file__), "golden", "probe_*.npz")))
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    torch.cuda.set_device(0)
+
+
+def _paths():
+    import paper_2101_00745_b200 as scc
+    from paper_2101_00745_b200 import _lib
+    out = [_lib.SCC_PATH_CUDA_CORE]
+    cfg = scc.scc_config_new(8, 8, 2, "50%", True)
+    try:
+        cfg.set_path(_lib.SCC_PATH_TENSOR)
+        out.append(_lib.SCC_PATH_TENSOR)
+    except scc.ArgumentError:
+        pass
+    return out
+
+
+PATHS = _paths() if torch.cuda.is_available() else [1]
+PATH_IDS = {1: "cuda_core", 2: "tensor"}
+
+
+def make_cfg(ci, co, cg, ov, hb, path):
+    import paper_2101_00745_b200 as scc
+    cfg = scc.scc_config_new(ci, co, cg, ov if isinstance(ov, str) else scc.Overlap.channels(ov), hb)
+    cfg.set_path(path)
+    return cfg
+
+
+def run_gpu(cfg, x, w, b, dy):
+    import paper_2101_00745_b200 as scc
+    d = "cuda"
+    xt = torch.from_numpy(np.ascontiguousarray(x, np.float32)).to(d)
+    wts = scc.SccWeights(torch.from_numpy(np.ascontiguousarray(w, np.float32)).to(d),
+                         None if b is None else torch.from_numpy(np.ascontiguousarray(b, np.float32)).to(d))
+    gt = torch.from_numpy(np.ascontiguousarray(dy, np.float32)).to(d)
+    y = scc.scc_forward(xt, wts, cfg)
+    dx = scc.scc_backward_input(gt, wts, cfg)
+    p = scc.scc_backward_params(gt, xt, cfg)
+    g = scc.scc_backward(gt, xt, wts, cfg)
+    torch.cuda.synchronize()
+    out = dict(y=y.cpu().numpy(), dx=dx.cpu().numpy(), dw=p.grad_weight.cpu().numpy(),
+               db=None if p.grad_bias is None else p.grad_bias.cpu().numpy(),
+               dx2=g.grad_input.cpu().numpy(), dw2=g.params.grad_weight.cpu().numpy(),
+               db2=None if g.params.grad_bias is None else g.params.grad_bias.cpu().numpy())
+    return out
+
+
+def oracle_cfg(port, cfg):
+    return port.config(cfg.c_in, cfg.c_out, cfg.cg, ("channels", cfg.overlap_channels),
+                       cfg.has_bias)
+
+
+def check_against_oracle(port, cfg, x, w, b, dy, exact=False):
+    o = oracle_cfg(port, cfg)
+    got = run_gpu(cfg, x, w, b, dy)
+    y = port.forward(o, x, w, b)
+    dx = port.backward_input(o, dy, w)
+    dw, db = port.backward_params(o, dy, x)
+    pairs = [("y", got["y"], y, FWD_TOL), ("dx", got["dx"], dx, GRAD_TOL),
+             ("dw", got["dw"], dw, GRAD_TOL), ("dx2", got["dx2"], dx, GRAD_TOL),
+             ("dw2", got["dw2"], dw, GRAD_TOL)]
+    if cfg.has_bias:
+        pairs += [("db", got["db"], db, GRAD_TOL), ("db2", got["db2"], db, GRAD_TOL)]
+    for name, g, r, tol in pairs:
+        assert g.shape == np.asarray(r).reshape(g.shape).shape
+        r = np.asarray(r).reshape(g.shape)
+        if exact:
+            assert np.array_equal(g.astype(np.float64), r), f"{name} not bit-exact"
+        else:
+            e = norm_rel(g, r)
+            assert e <= tol, f"{name}: norm-relative error {e:.3g} > {tol}"
+    # fused and separate backward agree bitwise
+    assert np.array_equal(got["dx"], got["dx2"]) and np.array_equal(got["dw"], got["dw2"])
+    return got
+
+
+def rand_problem(rng, ci, co, gw, n, h, w, hb, integer=False):
+    if integer:
+        x = rng.integers(-3, 4, (n, ci, h, w)).astype(np.float32)
+        wt = rng.integers(-2, 3, co * gw).astype(np.float32)
+        b = rng.integers(-4, 5, co).astype(np.float32) if hb else None
+        dy = rng.integers(-3, 4, (n, co, h, w)).astype(np.float32)
+    else:
+        x = rng.standard_normal((n, ci, h, w)).astype(np.float32)
+        bound = np.sqrt(1.0 / gw)
+        wt = rng.uniform(-bound, bound, co * gw).astype(np.float32)
+        b = rng.uniform(-0.5, 0.5, co).astype(np.float32) if hb else None
+        dy = rng.standard_normal((n, co, h, w)).astype(np.float32)
+    return x, wt, b, dy
+
+
+# --- known-answer tests (kernel_test.cpp) -----------------------------------
+
+@pytest.mark.parametrize("path", PATHS, ids=lambda p: PATH_IDS[p])
+def test_kat_worked_examples(path):
+    import paper_2101_00745_b200 as scc
+    cfg = make_cfg(4, 4, 2, 1, False, path)
+    x = torch.tensor([1.0, 2.0, 3.0, 4.0], device="cuda").view(1, 4, 1, 1)
+    wts = scc.scc_weights_filled(cfg, 1.0)
+    assert scc.scc_forward(x, wts, cfg).flatten().tolist() == [3.0, 5.0, 7.0, 5.0]
+    ones = torch.ones(1, 4, 1, 1, device="cuda")
+    assert scc.scc_backward_input(ones, wts, cfg).flatten().tolist() == [2.0] * 4
+    dw = scc.scc_backward_params(ones, x, cfg).grad_weight.tolist()
+    assert dw[0:2] == [1.0, 2.0] and dw[6:8] == [4.0, 1.0]
+    cfgb = make_cfg(4, 4, 2, 1, True, path)
+    p = scc.scc_backward_params(torch.ones(1, 4, 2, 2, device="cuda"),
+                                torch.full((1, 4, 2, 2), 0.5, device="cuda"), cfgb)
+    assert p.grad_bias.tolist() == [4.0] * 4
+
+
+@pytest.mark.parametrize("path", PATHS, ids=lambda p: PATH_IDS[p])
+def test_bias_only_and_zero_cotangent(path):
+    import paper_2101_00745_b200 as scc
+    cfg = make_cfg(6, 6, 3, 0, True, path)
+    wts = scc.scc_weights_filled(cfg, 0.0)
+    wts.bias.copy_(torch.arange(6.0))
+    x = torch.randn(2, 6, 3, 2, device="cuda")
+    y = scc.scc_forward(x, wts, cfg)
+    for oc in range(6):
+        assert torch.all(y[:, oc] == oc)
+    cfg = make_cfg(8, 8, 4, 1, True, path)
+    wts = scc.scc_weights_init(cfg)
+    g = scc.scc_backward(torch.zeros(2, 8, 3, 3, device="cuda"), torch.randn(2, 8, 3, 3, device="cuda"),
+                         wts, cfg)
+    assert torch.all(g.grad_input == 0) and torch.all(g.params.grad_weight == 0)
+    assert torch.all(g.params.grad_bias == 0)
+
+
+@pytest.mark.parametrize("path", PATHS, ids=lambda p: PATH_IDS[p])
+def test_shape_errors(path):  # kernel_test.cpp:243-253
+    import paper_2101_00745_b200 as scc
+    cfg = make_cfg(4, 4, 2, 1, True, path)
+    wts = scc.scc_weights_init(cfg)
+    with pytest.raises(scc.ShapeError):
+        scc.scc_forward(torch.randn(1, 6, 2, 2, device="cuda"), wts, cfg)
+    ok = torch.randn(1, 4, 2, 2, device="cuda")
+    bad = torch.randn(1, 5, 2, 2, device="cuda")
+    with pytest.raises(scc.ShapeError):
+        scc.scc_backward_input(bad, wts, cfg)
+    with pytest.raises(scc.ShapeError):
+        scc.scc_backward_params(bad, ok, cfg)
+    with pytest.raises(scc.ShapeError):
+        scc.scc_forward(ok, scc.SccWeights(wts.weight[:-1], wts.bias), cfg)
+
+
+# --- golden fixtures (from the compiled reference) ----------------------------
+
+@pytest.mark.parametrize("path", PATHS, ids=lambda p: PATH_IDS[p])
+@pytest.mark.parametrize("fixture", GOLDEN, ids=lambda p: os.path.basename(p)[:-4])
+def test_golden(path, fixture):
+    g = np.load(fixture)
+    ci, co, cg, hb, n, h, w = (int(v) for v in g["geometry"])
+    cfg = make_cfg(ci, co, cg, int(g["cfg"][0]), bool(hb), path)
+    got = run_gpu(cfg, g["x"], g["w"], g["b"] if hb else None, g["dy"])
+    assert norm_rel(got["y"], g["y"]) <= FWD_TOL
+    assert norm_rel(got["dx"], g["dx"]) <= GRAD_TOL
+    assert norm_rel(got["dw"], g["dw"]) <= GRAD_TOL
+    if hb:
+        assert norm_rel(got["db"], g["db"]) <= GRAD_TOL
+
+
+# --- bit-exact index mapping --------------------------------------------------
+
+@pytest.mark.parametrize("path", PATHS, ids=lambda p: PATH_IDS[p])
+def test_index_mapping_bit_exact(port, path):
+    """Integer-valued data: every product and partial sum is exact in fp32,
+    so any mis-mapped window slot or covering filter shows up as a mismatch."""
+    rng = np.random.default_rng(11)
+    geoms = [(4, 4, 2, 1), (6, 4, 2, 1), (8, 5, 4, 1), (12, 12, 3, 2), (16, 24, 4, 2),
+             (64, 128, 2, 16), (24, 24, 3, 0), (16, 16, 2, 8), (32, 40, 1, 16), (20, 7, 5, 3),
+             (96, 96, 3, 31), (128, 72, 8, 5), (256, 256, 4, 48)]
+    for ci, co, cg, ov in geoms:
+        gw = ci // cg
+        for (n, h, w) in ((2, 5, 5), (3, 4, 8), (1, 7, 7)):
+            cfg = make_cfg(ci, co, cg, ov, True, path)
+            x, wt, b, dy = rand_problem(rng, ci, co, gw, n, h, w, True, integer=True)
+            check_against_oracle(port, cfg, x, wt, b, dy, exact=True)
+
+
+# --- random geometries (acceptance.cpp:147-163 style) ----------------------------
+
+@pytest.mark.parametrize("path", PATHS, ids=lambda p: PATH_IDS[p])
+def test_random_geometries(port, path):
+    rng = np.random.default_rng(2024)
+    for trial in range(50):
+        ci = int(rng.integers(1, 33)) * 2
+        divs = [d for d in range(1, ci + 1) if ci % d == 0]
+        cg = int(rng.choice(divs))
+        gw = ci // cg
+        ov = int(rng.integers(0, gw + 1))
+        co = int(rng.integers(1, 3 * ci + 1))
+        hb = bool(rng.integers(0, 2))
+        n = int(rng.integers(1, 5))
+        h, w = int(rng.integers(1, 12)), int(rng.integers(1, 12))
+        cfg = make_cfg(ci, co, cg, ov, hb, path)
+        x, wt, b, dy = rand_problem(rng, ci, co, gw, n, h, w, hb)
+        check_against_oracle(port, cfg, x, wt, b, dy)
+
+
+@pytest.mark.parametrize("path", PATHS, ids=lambda p: PATH_IDS[p])
+def test_config1_full_size(port, path):
+    """BASELINE config 1 at full size: N=32, 64->128, 32x32, cg=2, co=50%."""
+    rng = np.random.default_rng(0)
+    cfg = make_cfg(64, 128, 2, "50%", True, path)
+    x, wt, b, dy = rand_problem(rng, 64, 128, 32, 32, 32, 32, True)
+    check_against_oracle(port, cfg, x, wt, b, dy)
+
+
+@pytest.mark.parametrize("path", PATHS, ids=lambda p: PATH_IDS[p])
+def test_ragged_and_edge_shapes(port, path):
+    rng = np.random.default_rng(5)
+    cases = [
+        (64, 128, 2, "50%", 3, 7, 7),     # P=49: not a multiple of 4
+        (256, 256, 2, "50%", 2, 1, 1),    # P=1
+        (64, 60, 2, "25%", 2, 6, 6),      # c_out not a multiple of 8
+        (60, 64, 3, "75%", 2, 5, 3),      # c_in not a multiple of 8
+        (512, 512, 2, "50%", 1, 4, 4),    # wide window gw=256
+        (1024, 1024, 2, "75%", 1, 2, 2),  # gw=512
+        (32, 3, 1, "50%", 2, 9, 9),       # tiny c_out, cg=1
+        (8, 5, 4, "1", 4, 11, 11),        # uncovered input channels (dx must be 0)
+    ]
+    for ci, co, cg, ov, n, h, w in cases:
+        cfg = make_cfg(ci, co, cg, ov, True, path)
+        x, wt, b, dy = rand_problem(rng, ci, co, cfg.group_width, n, h, w, True)
+        got = check_against_oracle(port, cfg, x, wt, b, dy)
+        if (ci, co) == (8, 5):
+            assert np.all(got["dx"][:, 6:] == 0)
+
+
+# --- full-size sweep shapes: size-independent properties ---------------------------
+
+SWEEP = [(c, cg, co, hw) for c in (256, 512, 1024) for cg in (2, 4, 8)
+         for co in ("25%", "50%", "75%") for hw in (56, 14)]
+
+
+@pytest.mark.parametrize("path", PATHS, ids=lambda p: PATH_IDS[p])
+@pytest.mark.parametrize("shape", SWEEP[::5], ids=lambda s: f"C{s[0]}_cg{s[1]}_co{s[2][:-1]}_{s[3]}")
+def test_sweep_full_size_properties(port, path, shape):
+    """N=32 sweep shapes: (1) sample 0 of the batch equals the oracle run on
+    that sample alone (per-sample independence of fwd / bwd-data);
+    (2) adjoint identity <dy, Wx> = <W^T dy, x>; (3) dW of the batch equals
+    the sum of the dW of its two halves (linearity over samples); (4) repeat
+    runs are bitwise identical."""
+    import paper_2101_00745_b200 as scc
+    c, cg, co, hw = shape
+    n = 32
+    cfg = make_cfg(c, c, cg, co, True, path)
+    gen = torch.Generator(device="cuda").manual_seed(0)
+    x = torch.randn(n, c, hw, hw, device="cuda", generator=gen)
+    dy = torch.randn(n, c, hw, hw, device="cuda", generator=gen)
+    wts = scc.scc_weights_init(cfg)
+    wts.bias.uniform_(-0.5, 0.5)
+    y = scc.scc_forward(x, wts, cfg)
+    g = scc.scc_backward(dy, x, wts, cfg)
+    # (4) determinism
+    y2 = scc.scc_forward(x, wts, cfg)
+    g2 = scc.scc_backward(dy, x, wts, cfg)
+    assert torch.equal(y, y2) and torch.equal(g.grad_input, g2.grad_input)
+    assert torch.equal(g.params.grad_weight, g2.params.grad_weight)
+    # (1) sample 0 vs oracle
+    o = oracle_cfg(port, cfg)
+    x0, dy0 = x[:1].cpu().numpy(), dy[:1].cpu().numpy()
+    wn, bn = wts.weight.cpu().numpy(), wts.bias.cpu().numpy()
+    assert norm_rel(y[:1].cpu().numpy(), port.forward(o, x0, wn, bn)) <= FWD_TOL
+    assert norm_rel(g.grad_input[:1].cpu().numpy(), port.backward_input(o, dy0, wn)) <= GRAD_TOL
+    # (2) adjoint identity in fp64 over the whole batch
+    lhs = torch.sum(dy.double() * (y.double() - wts.bias.double().view(1, -1, 1, 1))).item()
+    rhs = torch.sum(g.grad_input.double() * x.double()).item()
+    assert abs(lhs - rhs) <= 1e-4 * max(abs(lhs), abs(rhs), 1.0) + 1e-3
+    # (3) linearity of dW over the batch
+    pa = scc.scc_backward_params(dy[: n // 2].contiguous(), x[: n // 2].contiguous(), cfg)
+    pb = scc.scc_backward_params(dy[n // 2:].contiguous(), x[n // 2:].contiguous(), cfg)
+    full = g.params.grad_weight.double()
+    halves = pa.grad_weight.double() + pb.grad_weight.double()
+    assert (full - halves).abs().max().item() <= 1e-4 * full.abs().max().item()
+    dbs = pa.grad_bias.double() + pb.grad_bias.double()
+    assert (g.params.grad_bias.double() - dbs).abs().max().item() <= \
+        1e-4 * g.params.grad_bias.double().abs().max().item()
+    # dW of sample 0 against the oracle
+    p0 = scc.scc_backward_params(dy[:1].contiguous(), x[:1].contiguous(), cfg)
+    dw0, db0 = port.backward_params(o, dy0, x0)
+    assert norm_rel(p0.grad_weight.cpu().numpy(), dw0) <= GRAD_TOL
+    assert norm_rel(p0.grad_bias.cpu().numpy(), db0) <= GRAD_TOL
+
+
+# --- autograd layer ---------------------------------------------------------------
+
+def test_scc2d_autograd_matches_dense_conv():
+    """SCC2d forward/backward against a plain fp64 PyTorch dense 1x1 conv with
+    the band-densified weight (oracles.hpp:118-132 scc_to_dense_rows)."""
+    import paper_2101_00745_b200 as scc
+    torch.manual_seed(0)
+    layer = scc.SCC2d(48, 80, 4, "50%").cuda()
+    with torch.no_grad():
+        layer.bias.uniform_(-0.5, 0.5)
+    x = torch.randn(4, 48, 9, 9, device="cuda", requires_grad=True)
+    y = layer(x)
+    gy = torch.randn_like(y)
+    y.backward(gy)
+    cfg = layer.cfg
+    dense = torch.zeros(80, 48, dtype=torch.float64)
+    wcpu = layer.weight.detach().double().cpu()
+    for oc in range(80):
+        st = (oc * cfg.shift) % 48
+        for k in range(cfg.group_width):
+            dense[oc, (st + k) % 48] = wcpu[oc, k]
+    dense.requires_grad_(True)
+    xd = x.detach().double().cpu().requires_grad_(True)
+    bd = layer.bias.detach().double().cpu().requires_grad_(True)
+    yd = torch.nn.functional.conv2d(xd, dense.view(80, 48, 1, 1), bd)
+    yd.backward(gy.double().cpu())
+    assert norm_rel(y.detach().cpu().numpy(), yd.detach().numpy()) <= FWD_TOL
+    assert norm_rel(x.grad.cpu().numpy(), xd.grad.numpy()) <= GRAD_TOL
+    gd = torch.stack([torch.stack([dense.grad[oc, ((oc * cfg.shift) % 48 + k) % 48]
+                                   for k in range(cfg.group_width)]) for oc in range(80)])
+    assert norm_rel(layer.weight.grad.cpu().numpy(), gd.numpy()) <= GRAD_TOL
+    assert norm_rel(layer.bias.grad.cpu().numpy(), bd.grad.numpy()) <= GRAD_TOL
+
+
+def test_host_buffer_entry_points(port):
+    """The host-buffer C entry points (what a host caller of proj/core binds)."""
+    import ctypes as C
+    import paper_2101_00745_b200 as scc
+    from paper_2101_00745_b200 import _lib
+    rng = np.random.default_rng(3)
+    cfg = scc.scc_config_new(64, 128, 2, "50%", True)
+    x, wt, b, dy = rand_problem(rng, 64, 128, 32, 4, 8, 8, True)
+    y = np.empty((4, 128, 8, 8), np.float32)
+    dx = np.empty_like(x)
+    dw = np.empty_like(wt)
+    db = np.empty_like(b)
+    p = lambda a: a.ctypes.data_as(C.c_void_p)  # noqa: E731
+    _lib.check(_lib.lib().scc_fwd_bwd_host_f32(cfg.handle, 4, 8, 8, p(x), p(wt), p(b), p(dy), p(y),
+                                               p(dx), p(dw), p(db)))
+    o = oracle_cfg(port, cfg)
+    assert norm_rel(y, port.forward(o, x, wt, b)) <= FWD_TOL
+    assert norm_rel(dx, port.backward_input(o, dy, wt)) <= GRAD_TOL
+    rdw, rdb = port.backward_params(o, dy, x)
+    assert norm_rel(dw, rdw) <= GRAD_TOL and norm_rel(db, rdb) <= GRAD_TOL
+    y2 = np.empty_like(y)
+    _lib.check(_lib.lib().scc_forward_host_f32(cfg.handle, 4, 8, 8, p(x), p(wt), p(b), p(y2)))
+    assert np.array_equal(y, y2)
