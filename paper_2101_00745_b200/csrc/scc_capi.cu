@@ -94,7 +94,7 @@ const DeviceTables& tables(Plan& p) {
   };
   const size_t o_fr = put(p.fwd.rows), o_fb = put(arcs(p.fwd.blocks)), o_fg = put(p.fwd.groups);
   const size_t o_br = put(p.bwd.rows), o_bb = put(arcs(p.bwd.blocks)), o_bg = put(p.bwd.groups);
-  const size_t o_pm = put(p.perm), o_ip = put(p.inv_perm);
+  const size_t o_pm = put(p.perm), o_ip = put(p.inv_perm), o_st = put(p.starts);
   DeviceTables t;
   t.device = dev;
   cuda_check(cudaMalloc(&t.base, h.size() * sizeof(int32_t)), "cudaMalloc(plan tables)");
@@ -109,6 +109,7 @@ const DeviceTables& tables(Plan& p) {
   t.bwd_groups = b + o_bg;
   t.perm = b + o_pm;
   t.inv_perm = b + o_ip;
+  t.starts = b + o_st;
   p.dev.push_back(t);
   return p.dev.back();
 }
@@ -151,6 +152,7 @@ BandLaunch band_args(const Plan& p, const DeviceTables& t, bool bwd, int64_t n, 
   a.bias = bias;
   a.rows = bwd ? t.bwd_rows : t.fwd_rows;
   a.ring_map = bwd ? t.perm : nullptr;
+  a.starts = t.starts;
   a.blocks = bwd ? t.bwd_blocks : t.fwd_blocks;
   a.groups = bwd ? t.bwd_groups : t.fwd_groups;
   a.ngrp = side.ngrp();
@@ -177,6 +179,7 @@ WeightLaunch weight_args(const Plan& p, const DeviceTables& t, int64_t n, int64_
   a.rows = t.fwd_rows;
   a.blocks = t.fwd_blocks;
   a.inv_perm = t.inv_perm;
+  a.starts = t.starts;
   a.nblk = p.fwd.nblk();
   a.max_block_len = p.fwd.max_block_len;
   a.c_in = static_cast<int32_t>(p.cfg.c_in);

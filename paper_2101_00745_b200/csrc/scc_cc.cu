@@ -31,56 +31,29 @@ __device__ __forceinline__ int wrap(int v, int n) { return v >= n ? v - n : v; }
 
 // w[oc][(ic - start(oc)) mod c_in] inside the window, else 0.
 __device__ __forceinline__ float band_weight(const BandLaunch& a, int oc, int ic) {
-  const int st = static_cast<int>((static_cast<long long>(oc) * a.shift) % a.c_in);
-  int s = ic - st;
+  int s = ic - __ldg(a.starts + oc);
   if (s < 0) s += a.c_in;
-  return s < a.gw ? __ldg(a.weight + static_cast<long long>(oc) * a.gw + s) : 0.f;
+  return s < a.gw ? __ldg(a.weight + static_cast<int64_t>(oc) * a.gw + s) : 0.f;
 }
 
-template <bool VEC>
-__device__ __forceinline__ float4 load4(const float* __restrict__ base, int64_t c_t,
-                                        int ch, int64_t plane, int64_t q, int64_t qend) {
-  float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-  if (VEC) {
-    if (q < qend) {
-      const int64_t n = q / plane, p = q - n * plane;
-      v = __ldg(reinterpret_cast<const float4*>(base + (n * c_t + ch) * plane + p));
-    }
+// Pixel q -> (sample n, in-plane p); 32-bit division when it fits.
+__device__ __forceinline__ void pix_np(int64_t q, int64_t plane, int64_t& n, int64_t& p) {
+  if (q < 0x7fffffffLL && plane < 0x7fffffffLL) {
+    const uint32_t qq = static_cast<uint32_t>(q), pl = static_cast<uint32_t>(plane);
+    const uint32_t nn = qq / pl;
+    n = nn;
+    p = qq - nn * pl;
   } else {
-    float e[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int64_t qi = q + i;
-      e[i] = 0.f;
-      if (qi < qend) {
-        const int64_t n = qi / plane, p = qi - n * plane;
-        e[i] = __ldg(base + (n * c_t + ch) * plane + p);
-      }
-    }
-    v = make_float4(e[0], e[1], e[2], e[3]);
+    n = q / plane;
+    p = q - n * plane;
   }
-  return v;
 }
 
-template <bool VEC>
-__device__ __forceinline__ void store4(float* __restrict__ base, int64_t c_t, int ch,
-                                       int64_t plane, int64_t q, int64_t qend, float4 v) {
-  if (VEC) {
-    if (q < qend) {
-      const int64_t n = q / plane, p = q - n * plane;
-      *reinterpret_cast<float4*>(base + (n * c_t + ch) * plane + p) = v;
-    }
-  } else {
-    const float e[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int64_t qi = q + i;
-      if (qi < qend) {
-        const int64_t n = qi / plane, p = qi - n * plane;
-        base[(n * c_t + ch) * plane + p] = e[i];
-      }
-    }
-  }
+// Pixel q -> element offset of (n, channel 0, p) in an [N][C][P] tensor.
+__device__ __forceinline__ int64_t pix_offset(int64_t q, int64_t plane, int64_t c_t) {
+  int64_t n, p;
+  pix_np(q, plane, n, p);
+  return n * c_t * plane + p;
 }
 
 template <bool VEC>
@@ -118,37 +91,61 @@ __global__ void __launch_bounds__(kThreads) band_cc_kernel(const BandLaunch a) {
   const int i1_lo = boff, i1_hi = min(boff + blen, glen);
   const int i2_hi = max(0, boff + blen - glen);
 
+  // Staging role of this thread: pixel column c4 (fixed), rows warp+8k.
+  const int c4 = threadIdx.x & (TQ / 4 - 1);
+  const int64_t qv = q0 + c4 * 4;
+  int64_t poff[4];
+  bool pval[4];
+  if (VEC) {
+    pval[0] = qv < qend;
+    poff[0] = pval[0] ? pix_offset(qv, a.plane, a.c_in_t) : 0;
+  } else {
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      pval[e] = qv + e < qend;
+      poff[e] = pval[e] ? pix_offset(qv + e, a.plane, a.c_in_t) : 0;
+    }
+  }
+  // Weight-staging role: (r, j) fixed, one entry per block of the group.
+  const int wr = threadIdx.x >> 3, wj = threadIdx.x & 7;
+
   for (int c0 = 0; c0 < glen; c0 += KC) {
     const int kc = min(KC, glen - c0);
-    for (int idx = threadIdx.x; idx < KC * (TQ / 4); idx += kThreads) {
-      const int r = idx / (TQ / 4), c4 = idx - r * (TQ / 4);
+#pragma unroll
+    for (int k = 0; k < KC / (kThreads / (TQ / 4)); ++k) {
+      const int r = (threadIdx.x >> 5) + k * (kThreads / (TQ / 4));
       float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
       if (r < kc) {
         const int pos = wrap(gstart + c0 + r, a.ring);
         const int ch = a.ring_map ? __ldg(a.ring_map + pos) : pos;
-        v = load4<VEC>(a.in, a.c_in_t, ch, a.plane, q0 + c4 * 4, qend);
+        const float* src = a.in + static_cast<int64_t>(ch) * a.plane;
+        if (VEC) {
+          if (pval[0]) v = __ldg(reinterpret_cast<const float4*>(src + poff[0]));
+        } else {
+          v.x = pval[0] ? __ldg(src + poff[0]) : 0.f;
+          v.y = pval[1] ? __ldg(src + poff[1]) : 0.f;
+          v.z = pval[2] ? __ldg(src + poff[2]) : 0.f;
+          v.w = pval[3] ? __ldg(src + poff[3]) : 0.f;
+        }
       }
       *reinterpret_cast<float4*>(&xs[r][c4 * 4]) = v;
     }
-    for (int idx = threadIdx.x; idx < nb * KC * kRowsPerBlock; idx += kThreads) {
-      const int wb = idx / (KC * kRowsPerBlock);
-      const int rem = idx - wb * (KC * kRowsPerBlock);
-      const int r = rem / kRowsPerBlock, j = rem - r * kRowsPerBlock;
+    for (int wb = 0; wb < nb; ++wb) {
       float v = 0.f;
-      if (r < kc) {
+      if (wr < kc) {
         const int blk = first + wb;
         int off = a.blocks[2 * blk] - gstart;
         if (off < 0) off += a.ring;
-        int u = c0 + r - off;
+        int u = c0 + wr - off;
         if (u < 0) u += a.ring;
-        const int row = a.rows[blk * kRowsPerBlock + j];
+        const int row = a.rows[blk * kRowsPerBlock + wj];
         if (u < a.blocks[2 * blk + 1] && row >= 0) {
-          const int pos = wrap(gstart + c0 + r, a.ring);
+          const int pos = wrap(gstart + c0 + wr, a.ring);
           v = a.backward_data ? band_weight(a, __ldg(a.ring_map + pos), row)
                               : band_weight(a, row, pos);
         }
       }
-      ws[wb][r][j] = v;
+      ws[wb][wr][wj] = v;
     }
     __syncthreads();
     if (active) {
@@ -178,9 +175,31 @@ __global__ void __launch_bounds__(kThreads) band_cc_kernel(const BandLaunch a) {
     __syncthreads();
   }
   if (active) {
+    const int64_t qo = q0 + lane * 4;
+    int64_t ooff[4];
+    bool oval[4];
+    if (VEC) {
+      oval[0] = qo < qend;
+      ooff[0] = oval[0] ? pix_offset(qo, a.plane, a.c_out_t) : 0;
+    } else {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        oval[e] = qo + e < qend;
+        ooff[e] = oval[e] ? pix_offset(qo + e, a.plane, a.c_out_t) : 0;
+      }
+    }
 #pragma unroll
     for (int j = 0; j < kRowsPerBlock; ++j) {
-      if (orow[j] >= 0) store4<VEC>(a.out, a.c_out_t, orow[j], a.plane, q0 + lane * 4, qend, acc[j]);
+      if (orow[j] < 0) continue;
+      float* dst = a.out + static_cast<int64_t>(orow[j]) * a.plane;
+      if (VEC) {
+        if (oval[0]) *reinterpret_cast<float4*>(dst + ooff[0]) = acc[j];
+      } else {
+        if (oval[0]) dst[ooff[0]] = acc[j].x;
+        if (oval[1]) dst[ooff[1]] = acc[j].y;
+        if (oval[2]) dst[ooff[2]] = acc[j].z;
+        if (oval[3]) dst[ooff[3]] = acc[j].w;
+      }
     }
   }
 }
@@ -258,22 +277,64 @@ __global__ void __launch_bounds__(kThreads) weight_cc_kernel(const WeightLaunch 
     for (int i = 0; i < 4; ++i) acc[j][i] = 0.f;
   }
 
+  // Staging role: pixel column sc4 (fixed per thread), rows (tid / (TQW/4)) + step*k.
+  constexpr int kCols = TQW / 4;
+  constexpr int kRowStep = kThreads / kCols;
+  const int sc4 = tid % kCols;
+  const int srow = tid / kCols;
   for (int64_t q0 = qs; q0 < qe; q0 += TQW) {
-    for (int idx = tid; idx < kRowsPerBlock * (TQW / 4); idx += kThreads) {
-      const int j = idx / (TQW / 4), c4 = idx - j * (TQW / 4);
-      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (a.rows[blk * kRowsPerBlock + j] >= 0)
-        v = load4<VEC>(a.dy, a.c_out, a.rows[blk * kRowsPerBlock + j], a.plane, q0 + c4 * 4, qe);
-      *reinterpret_cast<float4*>(gs + j * TQW + c4 * 4) = v;
+    const int64_t qv = q0 + sc4 * 4;
+    int64_t offx[4], offg[4];
+    bool val[4];
+    if (VEC) {
+      val[0] = qv < qe;
+      if (val[0]) {
+        int64_t n, p;
+        pix_np(qv, a.plane, n, p);
+        offx[0] = n * a.c_in * a.plane + p;
+        offg[0] = n * a.c_out * a.plane + p;
+      } else {
+        offx[0] = offg[0] = 0;
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        val[e] = qv + e < qe;
+        offx[e] = val[e] ? pix_offset(qv + e, a.plane, a.c_in) : 0;
+        offg[e] = val[e] ? pix_offset(qv + e, a.plane, a.c_out) : 0;
+      }
     }
-    for (int idx = tid; idx < KT * (TQW / 4); idx += kThreads) {
-      const int r = idx / (TQW / 4), c4 = idx - r * (TQW / 4);
+    for (int j = srow; j < kRowsPerBlock; j += kRowStep) {
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (rows[j] >= 0) {
+        const float* src = a.dy + static_cast<int64_t>(rows[j]) * a.plane;
+        if (VEC) {
+          if (val[0]) v = __ldg(reinterpret_cast<const float4*>(src + offg[0]));
+        } else {
+          v.x = val[0] ? __ldg(src + offg[0]) : 0.f;
+          v.y = val[1] ? __ldg(src + offg[1]) : 0.f;
+          v.z = val[2] ? __ldg(src + offg[2]) : 0.f;
+          v.w = val[3] ? __ldg(src + offg[3]) : 0.f;
+        }
+      }
+      *reinterpret_cast<float4*>(gs + j * TQW + sc4 * 4) = v;
+    }
+#pragma unroll
+    for (int r = srow; r < KT; r += kRowStep) {
       float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
       if (k0 + r < blen) {
         const int ch = wrap(bstart + k0 + r, a.c_in);
-        v = load4<VEC>(a.x, a.c_in, ch, a.plane, q0 + c4 * 4, qe);
+        const float* src = a.x + static_cast<int64_t>(ch) * a.plane;
+        if (VEC) {
+          if (val[0]) v = __ldg(reinterpret_cast<const float4*>(src + offx[0]));
+        } else {
+          v.x = val[0] ? __ldg(src + offx[0]) : 0.f;
+          v.y = val[1] ? __ldg(src + offx[1]) : 0.f;
+          v.z = val[2] ? __ldg(src + offx[2]) : 0.f;
+          v.w = val[3] ? __ldg(src + offx[3]) : 0.f;
+        }
       }
-      *reinterpret_cast<float4*>(xs + r * XS + c4 * 4) = v;
+      *reinterpret_cast<float4*>(xs + r * XS + sc4 * 4) = v;
     }
     __syncthreads();
     float4 xv[4];
@@ -332,10 +393,9 @@ __global__ void __launch_bounds__(kThreads) weight_finalize_kernel(const WeightL
       const int slot = static_cast<int>(idx - static_cast<int64_t>(oc) * a.gw);
       const int pos = a.inv_perm[oc];
       const int blk = pos / kRowsPerBlock, j = pos - blk * kRowsPerBlock;
-      const int st = static_cast<int>((static_cast<long long>(oc) * a.shift) % a.c_in);
-      int k = st + slot - a.blocks[2 * blk];
-      k %= a.c_in;
+      int k = a.starts[oc] + slot - a.blocks[2 * blk];
       if (k < 0) k += a.c_in;
+      if (k >= a.c_in) k -= a.c_in;
       const float* p = a.partial + blk * gr.blk_stride + k * kRowsPerBlock + j;
       float s = 0.f;
       for (int sp = 0; sp < gr.splits; ++sp) s += p[sp * gr.split_stride];

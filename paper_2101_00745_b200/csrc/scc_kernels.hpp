@@ -16,6 +16,7 @@ struct BandLaunch {
   const float* bias;        // [c_out] or nullptr (forward only)
   const int32_t* rows;      // [nblk*8] output channel per row, -1 = pad
   const int32_t* ring_map;  // ring position -> input channel, nullptr = identity
+  const int32_t* starts;    // oc -> window start
   const int32_t* blocks;    // [nblk][2] arc on the ring
   const int32_t* groups;    // [ngrp][4]
   int32_t ngrp;
@@ -36,6 +37,7 @@ struct WeightLaunch {
   const int32_t* rows;      // forward rows (sorted filters), [nblk*8]
   const int32_t* blocks;    // forward block arcs
   const int32_t* inv_perm;  // oc -> sorted position
+  const int32_t* starts;    // oc -> window start
   int32_t nblk;
   int32_t max_block_len;
   int32_t c_in, c_out, gw;

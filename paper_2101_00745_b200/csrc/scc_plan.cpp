@@ -155,6 +155,9 @@ void build_plan(Plan& p, int64_t c_in, int64_t c_out, int64_t cg, int32_t kind,
     }
   }
 
+  p.starts.resize(static_cast<size_t>(c_out));
+  for (int64_t oc = 0; oc < c_out; ++oc) p.starts[static_cast<size_t>(oc)] = static_cast<int32_t>(p.start_of(oc));
+
   // Cycle-sorted order of the filters: by window start, then oc.
   p.perm.resize(static_cast<size_t>(c_out));
   std::iota(p.perm.begin(), p.perm.end(), 0);

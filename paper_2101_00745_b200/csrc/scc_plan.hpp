@@ -67,6 +67,7 @@ struct DeviceTables {
   const int32_t* bwd_groups = nullptr;
   const int32_t* perm = nullptr;      // sorted position -> oc
   const int32_t* inv_perm = nullptr;  // oc -> sorted position
+  const int32_t* starts = nullptr;    // oc -> window start
 };
 
 // Device staging for the host-buffer entry points.
@@ -80,7 +81,7 @@ struct HostStaging {
 struct Plan {
   scc_config_t cfg{};
   std::vector<int64_t> cycle_starts;  // compute_channel_cycle order
-  std::vector<int32_t> perm, inv_perm;
+  std::vector<int32_t> perm, inv_perm, starts;
   BandSide fwd, bwd;
   int32_t path = SCC_PATH_AUTO;
 
