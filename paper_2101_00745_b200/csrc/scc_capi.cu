@@ -95,6 +95,11 @@ const DeviceTables& tables(Plan& p) {
   const size_t o_fr = put(p.fwd.rows), o_fb = put(arcs(p.fwd.blocks)), o_fg = put(p.fwd.groups);
   const size_t o_br = put(p.bwd.rows), o_bb = put(arcs(p.bwd.blocks)), o_bg = put(p.bwd.groups);
   const size_t o_pm = put(p.perm), o_ip = put(p.inv_perm), o_st = put(p.starts);
+  const size_t o_tf[4] = {put(p.tc_fwd.rt_info), put(p.tc_fwd.rows), put(p.tc_fwd.class_d),
+                          put(p.tc_fwd.chunk_base)};
+  const size_t o_tb[4] = {put(p.tc_bwd.rt_info), put(p.tc_bwd.rows), put(p.tc_bwd.class_d),
+                          put(p.tc_bwd.chunk_base)};
+  if (h.empty()) h.push_back(0);
   DeviceTables t;
   t.device = dev;
   cuda_check(cudaMalloc(&t.base, h.size() * sizeof(int32_t)), "cudaMalloc(plan tables)");
@@ -110,6 +115,16 @@ const DeviceTables& tables(Plan& p) {
   t.perm = b + o_pm;
   t.inv_perm = b + o_ip;
   t.starts = b + o_st;
+  for (int k = 0; k < 2; ++k) {
+    TcDeviceTables& d = k == 0 ? t.tc_fwd : t.tc_bwd;
+    const size_t* o = k == 0 ? o_tf : o_tb;
+    d.rt_info = b + o[0];
+    d.rows = b + o[1];
+    d.class_d = b + o[2];
+    d.chunk_base = b + o[3];
+    d.starts = t.starts;
+    d.perm = t.perm;
+  }
   p.dev.push_back(t);
   return p.dev.back();
 }
@@ -137,9 +152,31 @@ void check_bias(const Plan& p, const void* bias, const char* name) {
   }
 }
 
-int32_t choose_path(const Plan& p, int64_t /*n*/, int64_t /*h*/, int64_t /*w*/) {
-  if (p.path != SCC_PATH_AUTO) return p.path;
+// Kernel family for one direction (0 forward, 1 backward-data).  A forced
+// tensor path falls back to CUDA cores for directions the band GEMM cannot
+// express (ring not a multiple of 8, plane not a multiple of 4, ...).
+int32_t choose_path(const Plan& p, int64_t /*n*/, int64_t h, int64_t w, int dir = 0) {
+  const TcBandPlan& tp = dir == 0 ? p.tc_fwd : p.tc_bwd;
+  const bool tc_ok = tc_band_supported(tp, h * w);
+  if (p.path == SCC_PATH_CUDA_CORE) return SCC_PATH_CUDA_CORE;
+  if (p.path == SCC_PATH_TENSOR) return tc_ok ? SCC_PATH_TENSOR : SCC_PATH_CUDA_CORE;
   return SCC_PATH_CUDA_CORE;
+}
+
+TcBandCall tc_call(const Plan& p, bool bwd, int64_t n, int64_t plane, const float* in, float* out,
+                   const float* weight, const float* bias) {
+  TcBandCall c{};
+  c.in = in;
+  c.out = out;
+  c.weight = weight;
+  c.bias = bias;
+  c.n = n;
+  c.plane = plane;
+  c.c_in = static_cast<int32_t>(p.cfg.c_in);
+  c.gw = static_cast<int32_t>(p.cfg.group_width);
+  c.c_out_t = static_cast<int32_t>(bwd ? p.cfg.c_in : p.cfg.c_out);
+  c.backward_data = bwd;
+  return c;
 }
 
 BandLaunch band_args(const Plan& p, const DeviceTables& t, bool bwd, int64_t n, int64_t plane,
@@ -203,7 +240,11 @@ void do_forward(Plan& p, int64_t n, int64_t h, int64_t w, const float* x, const 
   check_ptr(y, "y");
   check_bias(p, b, "bias");
   const DeviceTables& t = tables(p);
-  (void)choose_path(p, n, h, w);
+  if (choose_path(p, n, h, w, 0) == SCC_PATH_TENSOR) {
+    cuda_check(launch_band_tc(p.tc_fwd, t.tc_fwd, tc_call(p, false, n, h * w, x, y, wt, b), s),
+               "forward (tensor) launch");
+    return;
+  }
   cuda_check(launch_band_cc(band_args(p, t, false, n, h * w, x, y, wt, b), s), "forward launch");
 }
 
@@ -214,6 +255,12 @@ void do_backward_data(Plan& p, int64_t n, int64_t h, int64_t w, const float* dy,
   check_ptr(wt, "weight");
   check_ptr(dx, "dx");
   const DeviceTables& t = tables(p);
+  if (choose_path(p, n, h, w, 1) == SCC_PATH_TENSOR) {
+    cuda_check(launch_band_tc(p.tc_bwd, t.tc_bwd, tc_call(p, true, n, h * w, dy, dx, wt, nullptr),
+                              s),
+               "backward-data (tensor) launch");
+    return;
+  }
   cuda_check(launch_band_cc(band_args(p, t, true, n, h * w, dy, dx, wt, nullptr), s),
              "backward-data launch");
 }
@@ -434,8 +481,9 @@ scc_status_t scc_plan_set_path(scc_plan_t* plan, int32_t path) {
     if (path != SCC_PATH_AUTO && path != SCC_PATH_CUDA_CORE && path != SCC_PATH_TENSOR) {
       scc::fail(SCC_ERR_ARGUMENT, "unknown path " + std::to_string(path));
     }
-    if (path == SCC_PATH_TENSOR) {
-      scc::fail(SCC_ERR_ARGUMENT, "tensor-core path not available in this build");
+    if (path == SCC_PATH_TENSOR && !plan->tc_fwd.ok && !plan->tc_bwd.ok) {
+      scc::fail(SCC_ERR_ARGUMENT, "tensor-core path cannot express this geometry: " +
+                                      plan->tc_fwd.why);
     }
     plan->path = path;
   });

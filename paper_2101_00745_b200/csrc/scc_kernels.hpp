@@ -45,6 +45,21 @@ struct WeightLaunch {
   int64_t n, plane;
 };
 
+struct TcBandPlan;
+struct TcDeviceTables;
+
+// One tensor-core band call (forward or backward-data).
+struct TcBandCall {
+  const float* in;      // x (forward) / dy (backward-data)
+  float* out;           // y / dx
+  const float* weight;
+  const float* bias;    // forward only
+  int64_t n, plane;
+  int32_t c_in, gw;     // operator geometry
+  int32_t c_out_t;      // channels of the output tensor
+  bool backward_data;
+};
+
 // Counter of kernels launched by this library (scc_launch_count()).
 void note_launches(uint64_t k);
 
@@ -53,5 +68,10 @@ cudaError_t launch_band_cc(const BandLaunch& a, cudaStream_t s);
 size_t weight_cc_workspace_bytes(int32_t nblk, int32_t max_block_len, int64_t n,
                                  int64_t plane);
 cudaError_t launch_weight_cc(const WeightLaunch& a, size_t ws_bytes, cudaStream_t s);
+
+// Tensor-core family -----------------------------------------------------------
+bool tc_band_supported(const TcBandPlan& tp, int64_t plane);
+cudaError_t launch_band_tc(const TcBandPlan& tp, const TcDeviceTables& dt, const TcBandCall& call,
+                           cudaStream_t s);
 
 }  // namespace scc

@@ -120,6 +120,91 @@ void parse_overlap(const char* text, int32_t* kind, double* ratio, int64_t* coun
   }
 }
 
+void build_tc_side(const Plan& p, bool bwd, TcBandPlan& tp) {
+  const scc_config_t& c = p.cfg;
+  tp = TcBandPlan{};
+  const int32_t rows_total = static_cast<int32_t>(bwd ? c.c_in : c.c_out);
+  tp.ring = static_cast<int32_t>(bwd ? c.c_out : c.c_in);
+  if (tp.ring % 8 != 0) {
+    tp.why = "ring length not a multiple of 8";
+    return;
+  }
+  if (bwd) {
+    const int32_t D = static_cast<int32_t>(c.cyclic_dist);
+    if (c.c_out % D != 0 || (c.c_out / D) % 8 != 0) {
+      tp.why = "filters per window class not a multiple of 8";
+      return;
+    }
+    tp.cls = static_cast<int32_t>(c.c_out / D);
+    tp.n_class = D;
+    tp.rows_per_sample_3d = tp.cls;
+    for (int32_t cl = 0; cl < D; ++cl) {
+      const int32_t d = p.perm[static_cast<size_t>(cl) * tp.cls];
+      if (d >= D) {
+        tp.why = "cycle classes are not residues mod cyclic_dist";
+        return;
+      }
+      for (int32_t j = 0; j < tp.cls; ++j) {
+        if (p.perm[static_cast<size_t>(cl) * tp.cls + j] != d + D * j) {
+          tp.why = "cycle class layout mismatch";
+          return;
+        }
+      }
+      tp.class_d.push_back(d);
+    }
+  } else {
+    tp.cls = static_cast<int32_t>(c.c_in);
+    tp.n_class = 1;
+    tp.rows_per_sample_3d = static_cast<int32_t>(c.c_in);
+    tp.class_d = {0};
+  }
+  // Row-tile width: fewest padded rows, ties to the wider tile.
+  int32_t best = 0;
+  int64_t best_pad = INT64_MAX;
+  for (int32_t nt : {256, 128, 64}) {
+    const int64_t tiles = (rows_total + nt - 1) / nt;
+    const int64_t pad = tiles * nt;
+    if (pad < best_pad) {
+      best_pad = pad;
+      best = nt;
+    }
+  }
+  tp.nt = best;
+  tp.n_rt = (rows_total + tp.nt - 1) / tp.nt;
+  tp.rows.assign(static_cast<size_t>(tp.n_rt) * tp.nt, -1);
+  tp.chunk_base.assign(1, 0);
+  const int32_t gw = static_cast<int32_t>(c.group_width);
+  for (int32_t rt = 0; rt < tp.n_rt; ++rt) {
+    std::vector<Arc> arcs;
+    for (int32_t r = 0; r < tp.nt; ++r) {
+      const int32_t i = rt * tp.nt + r;
+      if (i >= rows_total) break;
+      if (bwd) {
+        tp.rows[static_cast<size_t>(i)] = i;
+        arcs.push_back(p.ic_arcs[static_cast<size_t>(i)]);
+      } else {
+        const int32_t oc = p.perm[static_cast<size_t>(i)];
+        tp.rows[static_cast<size_t>(i)] = oc;
+        arcs.push_back(Arc{static_cast<int32_t>(p.start_of(oc)), gw});
+      }
+    }
+    const Arc cov = cover_arcs(arcs, tp.ring);
+    int32_t start8 = (cov.start / 8) * 8;
+    int32_t nk8 = (cov.start + cov.len - start8 + 7) / 8;
+    if (nk8 < 1) nk8 = 1;  // uncovered rows still get written (as zeros)
+    if (nk8 * 8 >= tp.ring) {
+      start8 = 0;
+      nk8 = tp.ring / 8;
+    }
+    const int32_t chunks = (nk8 + 3) / 4;
+    tp.rt_info.insert(tp.rt_info.end(),
+                      {start8, nk8, tp.chunk_base.back() * 2 * tp.nt * 32, chunks});
+    tp.chunk_base.push_back(tp.chunk_base.back() + chunks);
+  }
+  tp.total_chunks = tp.chunk_base.back();
+  tp.ok = true;
+}
+
 void build_plan(Plan& p, int64_t c_in, int64_t c_out, int64_t cg, int32_t kind,
                 double ratio, int64_t count, int32_t has_bias) {
   // scc_config_new (config.cpp:62-83).
@@ -203,6 +288,7 @@ void build_plan(Plan& p, int64_t c_in, int64_t c_out, int64_t cg, int32_t kind,
     d.rows.assign(static_cast<size_t>(nb) * kRowsPerBlock, -1);
     d.blocks.resize(static_cast<size_t>(nb));
     std::vector<int32_t> covered;
+    p.ic_arcs.assign(static_cast<size_t>(c_in), Arc{0, 0});
     for (int b = 0; b < nb; ++b) {
       std::vector<Arc> parts;
       for (int j = 0; j < kRowsPerBlock; ++j) {
@@ -228,6 +314,7 @@ void build_plan(Plan& p, int64_t c_in, int64_t c_out, int64_t cg, int32_t kind,
           }
         }
         const Arc a{first, static_cast<int32_t>(covered.size())};
+        p.ic_arcs[static_cast<size_t>(ic)] = a;
         for (int32_t k = 0; k < a.len; ++k) {
           const int32_t pos = (a.start + k) % n;
           if (p.slot_of(p.perm[static_cast<size_t>(pos)], ic) < 0) {
@@ -240,6 +327,8 @@ void build_plan(Plan& p, int64_t c_in, int64_t c_out, int64_t cg, int32_t kind,
     }
     build_groups(d);
   }
+  build_tc_side(p, false, p.tc_fwd);
+  build_tc_side(p, true, p.tc_bwd);
 }
 
 }  // namespace scc

@@ -55,6 +55,31 @@ struct BandSide {
   int ngrp() const { return static_cast<int>(groups.size() / 4); }
 };
 
+// Tensor-core band tiling of one direction (see scc_tc.cu): row tiles of nt
+// output rows, each with an 8-aligned arc of the ring in 8-position k-steps.
+struct TcBandPlan {
+  bool ok = false;
+  std::string why;                  // reason when !ok
+  int32_t nt = 0, n_rt = 0, ring = 0;
+  int32_t cls = 0;                  // ring positions per class (TMA dim 2 run)
+  int32_t n_class = 1;              // TMA dim 1 extent (D for backward-data)
+  int32_t rows_per_sample_3d = 0;   // TMA dim-2 rows per sample
+  int32_t total_chunks = 0;
+  std::vector<int32_t> rt_info;     // per row tile: start8, nk8, panel offset (floats), chunks
+  std::vector<int32_t> rows;        // n_rt * nt
+  std::vector<int32_t> class_d;     // class -> d coordinate
+  std::vector<int32_t> chunk_base;  // n_rt + 1 prefix sums of chunks
+};
+
+struct TcDeviceTables {
+  const int32_t* rt_info = nullptr;
+  const int32_t* rows = nullptr;
+  const int32_t* class_d = nullptr;
+  const int32_t* chunk_base = nullptr;
+  const int32_t* starts = nullptr;
+  const int32_t* perm = nullptr;
+};
+
 // Device copy of the tables (one per CUDA device).
 struct DeviceTables {
   int device = -1;
@@ -68,6 +93,7 @@ struct DeviceTables {
   const int32_t* perm = nullptr;      // sorted position -> oc
   const int32_t* inv_perm = nullptr;  // oc -> sorted position
   const int32_t* starts = nullptr;    // oc -> window start
+  TcDeviceTables tc_fwd, tc_bwd;
 };
 
 // Device staging for the host-buffer entry points.
@@ -83,6 +109,8 @@ struct Plan {
   std::vector<int64_t> cycle_starts;  // compute_channel_cycle order
   std::vector<int32_t> perm, inv_perm, starts;
   BandSide fwd, bwd;
+  std::vector<Arc> ic_arcs;          // covering arc of each input channel (sorted order)
+  TcBandPlan tc_fwd, tc_bwd;
   int32_t path = SCC_PATH_AUTO;
 
   std::mutex dev_mu;

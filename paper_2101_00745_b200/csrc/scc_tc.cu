@@ -1,0 +1,429 @@
+// Tensor-core (tcgen05, 3xTF32) family of the SCC operator, sm_100a.
+//
+// tc_band_kernel — forward (kernel.cpp:29-69) and input-centric backward-data
+// (kernel.cpp:98-138) as one banded GEMM per 128-pixel tile:
+//     D[p, r] = sum_{k in arc(r-tile)} A[p, k] * B[k, r]
+//   forward:       A = x rows (ring = input channels),      B = W band^T
+//   backward-data: A = dy rows (ring = filters, cycle-sorted), B = W band
+// M = 128 pixels (TMEM lanes), N = NT rows (TMEM columns), K = the row tile's
+// arc of the ring in 8-row steps.  Activations arrive by TMA (SWIZZLE_128B,
+// MN-major); the band weights arrive pre-split (hi/lo) and pre-swizzled
+// (K-major) by a bulk copy.  fp32 accuracy from three tf32 MMAs per step:
+//     A_hi*B_hi + A_lo*B_hi + A_hi*B_lo,  A_hi = A with the low 13 bits dropped
+// (the tensor core reads raw fp32 operands that way; tests/test_tc_probe.py).
+//
+// Warp roles (persistent CTA, one per SM):
+//   warp 0      TMA / bulk-copy producer
+//   warp 1      TMEM allocator + MMA issuer (one elected lane)
+//   warps 2..5  converters: A_lo = A - A_hi in shared memory
+//   warps 6..9  epilogue: TMEM -> registers -> coalesced NCHW stores (+ bias)
+// Accumulators are double-buffered in TMEM so the epilogue of tile i overlaps
+// the MMAs of tile i+1.  Every output element is written exactly once.
+#include <algorithm>
+#include <cstdio>
+
+#include "scc_kernels.hpp"
+#include "scc_plan.hpp"
+#include "sm100.cuh"
+#include "tmap.hpp"
+
+namespace scc {
+namespace {
+
+using namespace sm100;
+
+constexpr int kTcThreads = 320;
+constexpr int KC = 32;          // ring positions per pipeline stage (4 k-steps of 8)
+constexpr int TM = 128;         // pixels per tile
+constexpr int kABytes = TM * KC * 4;  // 16 KB per A buffer
+
+template <int NT>
+struct TcCfg {
+  static constexpr int kBBytes = 2 * NT * KC * 4;  // hi + lo image
+  static constexpr int kStageBytes = 2 * kABytes + kBBytes;
+  static constexpr int kStages = (NT >= 256) ? 2 : 3;
+  static constexpr int kTmemCols = (2 * NT <= 32) ? 32 : (2 * NT <= 64) ? 64 : (2 * NT <= 128) ? 128 : (2 * NT <= 256) ? 256 : 512;
+  static constexpr int kSmem = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+};
+
+struct TcBandArgs {
+  const float* panel;        // B images: per row tile, per chunk: hi[NT][32], lo[NT][32] (swizzled)
+  const int32_t* rt_info;    // per row tile: start8 (ring pos), nk8, panel offset (floats), pad
+  const int32_t* rows;       // [n_rt * NT] output channel per tile row, -1 = none
+  const int32_t* class_d;    // ring class -> TMA coordinate d
+  const float* bias;         // forward only
+  float* out;
+  int32_t n_rt;              // row tiles
+  int32_t ring;              // ring length (c_in fwd / c_out bwd)
+  int32_t cls;               // ring positions per class (c_in fwd / c_out/D bwd)
+  int32_t c_out_t;           // channels of the output tensor
+  int32_t rows_per_sample_3d;  // TMA dim-2 rows per sample (c_in fwd / c_out/D bwd)
+  int32_t ptiles;            // pixel tiles per sample
+  int64_t plane;
+  int64_t n;
+};
+
+__device__ __forceinline__ void advance(int& stage, uint32_t& phase, int stages) {
+  if (++stage == stages) {
+    stage = 0;
+    phase ^= 1u;
+  }
+}
+
+template <int NT>
+__global__ void __launch_bounds__(kTcThreads, 1)
+    tc_band_kernel(const __grid_constant__ CUtensorMap tmap, const TcBandArgs a) {
+  using C = TcCfg<NT>;
+  constexpr int S = C::kStages;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S * C::kStageBytes);
+  uint64_t* full = bars;            // [S] TMA + bulk bytes landed
+  uint64_t* conv = bars + S;        // [S] A_lo written
+  uint64_t* empty = bars + 2 * S;   // [S] MMAs done with the stage
+  uint64_t* tfull = bars + 3 * S;   // [2] accumulator ready
+  uint64_t* tempty = bars + 3 * S + 2;  // [2] accumulator drained
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * S + 4);
+
+  auto a_hi = [&](int s) { return smem + s * C::kStageBytes; };
+  auto a_lo = [&](int s) { return smem + s * C::kStageBytes + kABytes; };
+  auto b_img = [&](int s) { return smem + s * C::kStageBytes + 2 * kABytes; };
+
+  const uint32_t warp = warp_id();
+  const int lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&conv[s], 128);
+      mbar_init(&empty[s], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 128);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 0 && lane == 0) prefetch_tmap(&tmap);
+  if (warp == 1) tmem_alloc<C::kTmemCols>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  const int64_t total = a.n * a.ptiles * a.n_rt;
+
+  if (warp == 0) {
+    // ---------------- producer ----------------
+    // Activations do not depend on the preceding panel-build kernel; the
+    // panel does (programmatic dependent launch): wait only before the first
+    // panel copy.
+    if (elect_one()) {
+      bool dep_synced = false;
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int64_t t = blockIdx.x; t < total; t += gridDim.x) {
+        const int rt = static_cast<int>(t % a.n_rt);
+        const int64_t pt = t / a.n_rt;
+        const int64_t n = pt / a.ptiles;
+        const int p0 = static_cast<int>(pt - n * a.ptiles) * TM;
+        const int start8 = a.rt_info[4 * rt], nk8 = a.rt_info[4 * rt + 1];
+        const float* panel = a.panel + a.rt_info[4 * rt + 2];
+        const int nch = (nk8 + 3) / 4;
+        for (int c = 0; c < nch; ++c) {
+          mbar_wait(&empty[stage], phase ^ 1u);
+          const int steps = min(4, nk8 - 4 * c);
+          mbar_expect_tx(&full[stage], steps * 4 * 1024 + C::kBBytes);
+          for (int st = 0; st < steps; ++st) {
+            int pos = start8 + 8 * (4 * c + st);
+            while (pos >= a.ring) pos -= a.ring;
+            const int cl = pos / a.cls, j = pos - cl * a.cls;
+            const int d = __ldg(a.class_d + cl);
+            const int row = static_cast<int>(n) * a.rows_per_sample_3d + j;
+#pragma unroll
+            for (int cb = 0; cb < 4; ++cb) {
+              tma_load_3d(a_hi(stage) + cb * kABytes / 4 + st * 1024, &tmap, &full[stage],
+                          p0 + 32 * cb, d, row);
+            }
+          }
+          if (!dep_synced) {
+            cudaGridDependencySynchronize();
+            dep_synced = true;
+          }
+          bulk_load(b_img(stage), panel + static_cast<int64_t>(c) * (C::kBBytes / 4),
+                    C::kBBytes, &full[stage]);
+          advance(stage, phase, S);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer ----------------
+    constexpr uint32_t idesc = idesc_tf32(TM, NT, 1, 0);
+    int stage = 0;
+    uint32_t phase = 0;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int64_t t = blockIdx.x; t < total; t += gridDim.x) {
+      const int rt = static_cast<int>(t % a.n_rt);
+      const int nk8 = a.rt_info[4 * rt + 1];
+      const int nch = (nk8 + 3) / 4;
+      mbar_wait(&tempty[acc], acc_phase ^ 1u);
+      tc_fence_after();
+      const uint32_t d_tmem = tmem + acc * NT;
+      for (int c = 0; c < nch; ++c) {
+        mbar_wait(&conv[stage], phase);
+        tc_fence_after();
+        const int steps = min(4, nk8 - 4 * c);
+        if (elect_one()) {
+          const uint32_t ah = smem_u32(a_hi(stage)), al = smem_u32(a_lo(stage));
+          const uint32_t bh = smem_u32(b_img(stage)), bl = bh + NT * KC * 4;
+          for (int st = 0; st < steps; ++st) {
+            const uint64_t dah = desc_sw128(ah + st * 1024, kABytes / 4, 1024);
+            const uint64_t dal = desc_sw128(al + st * 1024, kABytes / 4, 1024);
+            const uint64_t dbh = desc_sw128(bh + st * 32, 16, 1024);
+            const uint64_t dbl = desc_sw128(bl + st * 32, 16, 1024);
+            mma_tf32(d_tmem, dah, dbh, idesc, (c | st) != 0);
+            mma_tf32(d_tmem, dal, dbh, idesc, 1);
+            mma_tf32(d_tmem, dah, dbl, idesc, 1);
+          }
+          mma_commit(&empty[stage]);
+          if (c == nch - 1) mma_commit(&tfull[acc]);
+        }
+        __syncwarp();
+        advance(stage, phase, S);
+      }
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1u;
+      }
+    }
+  } else if (warp < 6) {
+    // ---------------- converters ----------------
+    const int ct = threadIdx.x - 64;  // 0..127
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int64_t t = blockIdx.x; t < total; t += gridDim.x) {
+      const int rt = static_cast<int>(t % a.n_rt);
+      const int nk8 = a.rt_info[4 * rt + 1];
+      const int nch = (nk8 + 3) / 4;
+      for (int c = 0; c < nch; ++c) {
+        mbar_wait(&full[stage], phase);
+        const int steps = min(4, nk8 - 4 * c);
+        // Each k-step of each column block is a 1 KB slab (8 rows x 128 B).
+        const float4* src = reinterpret_cast<const float4*>(a_hi(stage));
+        float4* dst = reinterpret_cast<float4*>(a_lo(stage));
+        for (int cb = 0; cb < 4; ++cb) {
+          for (int i = ct; i < steps * 64; i += 128) {
+            const int idx = cb * (kABytes / 64) + i;  // float4 index
+            const float4 v = src[idx];
+            float4 lo;
+            lo.x = v.x - tf32_hi(v.x);
+            lo.y = v.y - tf32_hi(v.y);
+            lo.z = v.z - tf32_hi(v.z);
+            lo.w = v.w - tf32_hi(v.w);
+            dst[idx] = lo;
+          }
+        }
+        fence_proxy_async_smem();
+        mbar_arrive(&conv[stage]);
+        advance(stage, phase, S);
+      }
+    }
+  } else {
+    // ---------------- epilogue ----------------
+    const int quarter = warp & 3;  // TMEM lane quarter this warp may access
+    const int prow = quarter * 32 + lane;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int64_t t = blockIdx.x; t < total; t += gridDim.x) {
+      const int rt = static_cast<int>(t % a.n_rt);
+      const int64_t pt = t / a.n_rt;
+      const int64_t n = pt / a.ptiles;
+      const int64_t p = static_cast<int64_t>(pt - n * a.ptiles) * TM + prow;
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const bool pv = p < a.plane;
+      float* obase = a.out + n * a.c_out_t * a.plane + p;
+      const int32_t* rows = a.rows + rt * NT;
+#pragma unroll 1
+      for (int c0 = 0; c0 < NT; c0 += 16) {
+        float v[16];
+        tmem_ld16(tmem + acc * NT + c0 + (static_cast<uint32_t>(quarter * 32) << 16), v);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const int row = __ldg(rows + c0 + j);
+          if (row >= 0 && pv) {
+            const float b = a.bias ? __ldg(a.bias + row) : 0.f;
+            obase[static_cast<int64_t>(row) * a.plane] = v[j] + b;
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty[acc]);
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1u;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc<C::kTmemCols>(tmem);
+}
+
+// Band weight panel: per row tile and chunk, hi and lo images of the K-major
+// SWIZZLE_128B layout the MMA reads ([NT rows][32 k], 8-row groups of 1 KB).
+struct PanelArgs {
+  const float* weight;
+  const int32_t* rt_info;
+  const int32_t* rows;     // output row channel per tile row (-1 none)
+  const int32_t* starts;   // oc -> window start
+  const int32_t* ring_map; // bwd: ring pos -> oc; fwd: nullptr
+  float* panel;
+  int32_t n_rt, ring, c_in, gw;
+  int32_t backward_data;
+  int64_t total;           // number of (rt, chunk, row, k) entries
+  const int32_t* chunk_base;  // prefix sum of chunks per row tile (entries / (NT*32))
+};
+
+template <int NT>
+__global__ void __launch_bounds__(256) tc_panel_kernel(const PanelArgs a) {
+  for (int64_t e = blockIdx.x * 256ll + threadIdx.x; e < a.total; e += gridDim.x * 256ll) {
+    const int k = static_cast<int>(e & 31);
+    const int r = static_cast<int>((e >> 5) % NT);
+    const int64_t gc = e / (32 * NT);  // global chunk index
+    int rt = 0;
+    while (rt + 1 < a.n_rt && a.chunk_base[rt + 1] <= gc) ++rt;
+    const int c = static_cast<int>(gc - a.chunk_base[rt]);
+    const int start8 = a.rt_info[4 * rt], nk8 = a.rt_info[4 * rt + 1];
+    const int kk = 32 * c + k;
+    float v = 0.f;
+    const int row = a.rows[rt * NT + r];
+    if (kk < 8 * nk8 && row >= 0) {
+      int pos = start8 + kk;
+      while (pos >= a.ring) pos -= a.ring;
+      const int oc = a.backward_data ? a.ring_map[pos] : row;
+      const int ic = a.backward_data ? row : pos;
+      int s = ic - a.starts[oc];
+      if (s < 0) s += a.c_in;
+      if (s < a.gw) v = a.weight[static_cast<int64_t>(oc) * a.gw + s];
+    }
+    const float hi = tf32_hi(v);
+    float* img = a.panel + gc * (2 * NT * 32);
+    const int off = (r >> 3) * 256 + (r & 7) * 32 + (((k >> 2) ^ (r & 7)) << 2) + (k & 3);
+    img[off] = hi;
+    img[NT * 32 + off] = v - hi;
+  }
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// host side
+
+bool tc_band_supported(const TcBandPlan& tp, int64_t plane) {
+  return tp.ok && plane % 4 == 0 && plane >= 4;
+}
+
+template <int NT>
+static cudaError_t launch_tc_nt(const TcBandPlan& tp, const TcDeviceTables& dt,
+                                const TcBandCall& call, cudaStream_t s) {
+  using C = TcCfg<NT>;
+  // --- panel ---
+  const int64_t entries = static_cast<int64_t>(tp.total_chunks) * NT * 32;
+  float* panel = nullptr;
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&panel),
+                                  static_cast<size_t>(entries) * 2 * sizeof(float), s);
+  if (e != cudaSuccess) return e;
+  PanelArgs pa{};
+  pa.weight = call.weight;
+  pa.rt_info = dt.rt_info;
+  pa.rows = dt.rows;
+  pa.starts = dt.starts;
+  pa.ring_map = call.backward_data ? dt.perm : nullptr;
+  pa.panel = panel;
+  pa.n_rt = tp.n_rt;
+  pa.ring = tp.ring;
+  pa.c_in = call.c_in;
+  pa.gw = call.gw;
+  pa.backward_data = call.backward_data ? 1 : 0;
+  pa.total = entries;
+  pa.chunk_base = dt.chunk_base;
+  const int pgrid = static_cast<int>(std::min<int64_t>((entries + 255) / 256, 148 * 8));
+  tc_panel_kernel<NT><<<pgrid, 256, 0, s>>>(pa);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+
+  // --- activations tensor map: {P, D, N * rows_per_sample} fp32, SW128, box {32, 1, 8}
+  CUtensorMap tm;
+  const uint64_t dims[3] = {static_cast<uint64_t>(call.plane), static_cast<uint64_t>(tp.n_class),
+                            static_cast<uint64_t>(call.n) * tp.rows_per_sample_3d};
+  const uint64_t strides[2] = {static_cast<uint64_t>(call.plane) * 4,
+                               static_cast<uint64_t>(call.plane) * 4 * tp.n_class};
+  const uint32_t box[3] = {32, 1, 8};
+  if (!encode_f32_sw128(&tm, call.in, 3, dims, strides, box)) return cudaErrorInvalidValue;
+
+  TcBandArgs ka{};
+  ka.panel = panel;
+  ka.rt_info = dt.rt_info;
+  ka.rows = dt.rows;
+  ka.class_d = dt.class_d;
+  ka.bias = call.bias;
+  ka.out = call.out;
+  ka.n_rt = tp.n_rt;
+  ka.ring = tp.ring;
+  ka.cls = tp.cls;
+  ka.c_out_t = call.c_out_t;
+  ka.rows_per_sample_3d = tp.rows_per_sample_3d;
+  ka.ptiles = static_cast<int32_t>((call.plane + TM - 1) / TM);
+  ka.plane = call.plane;
+  ka.n = call.n;
+  const int64_t tiles = call.n * ka.ptiles * tp.n_rt;
+  int nsm = 148;
+  {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  }
+  {
+    static bool attr_set[64] = {false};  // per device, per template instance
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64 || !attr_set[dev]) {
+      e = cudaFuncSetAttribute(tc_band_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               C::kSmem);
+      if (e != cudaSuccess) return e;
+      if (dev >= 0 && dev < 64) attr_set[dev] = true;
+    }
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>(std::min<int64_t>(tiles, nsm)));
+  cfg.blockDim = dim3(kTcThreads);
+  cfg.dynamicSmemBytes = C::kSmem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  e = cudaLaunchKernelEx(&cfg, tc_band_kernel<NT>, tm, ka);
+  if (e != cudaSuccess) return e;
+  note_launches(2);
+  return cudaFreeAsync(panel, s);
+}
+
+cudaError_t launch_band_tc(const TcBandPlan& tp, const TcDeviceTables& dt, const TcBandCall& call,
+                           cudaStream_t s) {
+  switch (tp.nt) {
+    case 64:
+      return launch_tc_nt<64>(tp, dt, call, s);
+    case 128:
+      return launch_tc_nt<128>(tp, dt, call, s);
+    case 256:
+      return launch_tc_nt<256>(tp, dt, call, s);
+    default:
+      return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace scc
