@@ -161,7 +161,7 @@ void build_tc_side(const Plan& p, bool bwd, TcBandPlan& tp) {
   // Row-tile width: fewest padded rows, ties to the wider tile.
   int32_t best = 0;
   int64_t best_pad = INT64_MAX;
-  for (int32_t nt : {256, 128, 64}) {
+  for (int32_t nt : {128, 64}) {
     const int64_t tiles = (rows_total + nt - 1) / nt;
     const int64_t pad = tiles * nt;
     if (pad < best_pad) {

@@ -6,16 +6,21 @@
 //   forward:       A = x rows (ring = input channels),      B = W band^T
 //   backward-data: A = dy rows (ring = filters, cycle-sorted), B = W band
 // M = 128 pixels (TMEM lanes), N = NT rows (TMEM columns), K = the row tile's
-// arc of the ring in 8-row steps.  Activations arrive by TMA (SWIZZLE_128B,
-// MN-major); the band weights arrive pre-split (hi/lo) and pre-swizzled
-// (K-major) by a bulk copy.  fp32 accuracy from three tf32 MMAs per step:
+// arc of the ring in 8-row steps.  Activations arrive by TMA; the band
+// weights arrive pre-split (hi/lo) and pre-swizzled (K-major SWIZZLE_128B) by
+// a bulk copy.  fp32 accuracy from three tf32 MMAs per step:
 //     A_hi*B_hi + A_lo*B_hi + A_hi*B_lo,  A_hi = A with the low 13 bits dropped
 // (the tensor core reads raw fp32 operands that way; tests/test_tc_probe.py).
+//
+// kind::tf32 only accepts K-major operands (an MN-major A silently yields
+// zeros; tests/cuda/tc_layout_probe.cu), and activations are pixel-contiguous,
+// so the converter warps transpose each staged [ring][pixel] tile into TMEM
+// ([pixel lane][ring column]) as hi/lo parts and the MMA runs in TS mode.
 //
 // Warp roles (persistent CTA, one per SM):
 //   warp 0      TMA / bulk-copy producer
 //   warp 1      TMEM allocator + MMA issuer (one elected lane)
-//   warps 2..5  converters: A_lo = A - A_hi in shared memory
+//   warps 2..5  converters: smem [k][p] -> TMEM A_hi, A_lo
 //   warps 6..9  epilogue: TMEM -> registers -> coalesced NCHW stores (+ bias)
 // Accumulators are double-buffered in TMEM so the epilogue of tile i overlaps
 // the MMAs of tile i+1.  Every output element is written exactly once.
@@ -39,16 +44,20 @@ constexpr int kABytes = TM * KC * 4;  // 16 KB per A buffer
 
 template <int NT>
 struct TcCfg {
-  static constexpr int kBBytes = 2 * NT * KC * 4;  // hi + lo image
-  static constexpr int kStageBytes = 2 * kABytes + kBBytes;
-  static constexpr int kStages = (NT >= 256) ? 2 : 3;
-  static constexpr int kTmemCols = (2 * NT <= 32) ? 32 : (2 * NT <= 64) ? 64 : (2 * NT <= 128) ? 128 : (2 * NT <= 256) ? 256 : 512;
+  static_assert(NT == 64 || NT == 128, "row tile must be 64 or 128");
+  static constexpr int kBBytes = 2 * NT * KC * 4;        // hi + lo weight image
+  static constexpr int kStageBytes = kABytes + kBBytes;  // raw activations + weights
+  static constexpr int kStages = 4;
+  static constexpr int kAccCols = NT;                    // per accumulator buffer
+  static constexpr int kACol0 = 2 * NT;                  // first TMEM column of A stages
+  static constexpr int kTmemCols = 512;
+  static_assert(kACol0 + kStages * 2 * KC <= kTmemCols, "TMEM budget");
   static constexpr int kSmem = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
 };
 
 struct TcBandArgs {
   const float* panel;        // B images: per row tile, per chunk: hi[NT][32], lo[NT][32] (swizzled)
-  const int32_t* rt_info;    // per row tile: start8 (ring pos), nk8, panel offset (floats), pad
+  const int32_t* rt_info;    // per row tile: start8 (ring pos), nk8, panel offset (floats), chunks
   const int32_t* rows;       // [n_rt * NT] output channel per tile row, -1 = none
   const int32_t* class_d;    // ring class -> TMA coordinate d
   const float* bias;         // forward only
@@ -79,16 +88,15 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S * C::kStageBytes);
-  uint64_t* full = bars;            // [S] TMA + bulk bytes landed
-  uint64_t* conv = bars + S;        // [S] A_lo written
-  uint64_t* empty = bars + 2 * S;   // [S] MMAs done with the stage
-  uint64_t* tfull = bars + 3 * S;   // [2] accumulator ready
+  uint64_t* full = bars;                // [S] TMA + bulk bytes landed
+  uint64_t* conv = bars + S;            // [S] A hi/lo written to TMEM
+  uint64_t* empty = bars + 2 * S;       // [S] MMAs done with the stage
+  uint64_t* tfull = bars + 3 * S;       // [2] accumulator ready
   uint64_t* tempty = bars + 3 * S + 2;  // [2] accumulator drained
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * S + 4);
 
-  auto a_hi = [&](int s) { return smem + s * C::kStageBytes; };
-  auto a_lo = [&](int s) { return smem + s * C::kStageBytes + kABytes; };
-  auto b_img = [&](int s) { return smem + s * C::kStageBytes + 2 * kABytes; };
+  auto a_raw = [&](int s) { return smem + s * C::kStageBytes; };
+  auto b_img = [&](int s) { return smem + s * C::kStageBytes + kABytes; };
 
   const uint32_t warp = warp_id();
   const int lane = threadIdx.x & 31;
@@ -142,7 +150,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             const int row = static_cast<int>(n) * a.rows_per_sample_3d + j;
 #pragma unroll
             for (int cb = 0; cb < 4; ++cb) {
-              tma_load_3d(a_hi(stage) + cb * kABytes / 4 + st * 1024, &tmap, &full[stage],
+              // [cb][32 ring rows][32 pixels], 128 B per ring row, no swizzle
+              tma_load_3d(a_raw(stage) + cb * (KC * 128) + st * 1024, &tmap, &full[stage],
                           p0 + 32 * cb, d, row);
             }
           }
@@ -157,8 +166,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       }
     }
   } else if (warp == 1) {
-    // ---------------- MMA issuer ----------------
-    constexpr uint32_t idesc = idesc_tf32(TM, NT, 1, 0);
+    // ---------------- MMA issuer (A from TMEM, B from SMEM) ----------------
+    constexpr uint32_t idesc = idesc_tf32(TM, NT, 0, 0);
     int stage = 0;
     uint32_t phase = 0;
     int acc = 0;
@@ -169,22 +178,21 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       const int nch = (nk8 + 3) / 4;
       mbar_wait(&tempty[acc], acc_phase ^ 1u);
       tc_fence_after();
-      const uint32_t d_tmem = tmem + acc * NT;
+      const uint32_t d_tmem = tmem + acc * C::kAccCols;
       for (int c = 0; c < nch; ++c) {
         mbar_wait(&conv[stage], phase);
         tc_fence_after();
         const int steps = min(4, nk8 - 4 * c);
         if (elect_one()) {
-          const uint32_t ah = smem_u32(a_hi(stage)), al = smem_u32(a_lo(stage));
+          const uint32_t a_hi = tmem + C::kACol0 + stage * 2 * KC;
+          const uint32_t a_lo = a_hi + KC;
           const uint32_t bh = smem_u32(b_img(stage)), bl = bh + NT * KC * 4;
           for (int st = 0; st < steps; ++st) {
-            const uint64_t dah = desc_sw128(ah + st * 1024, kABytes / 4, 1024);
-            const uint64_t dal = desc_sw128(al + st * 1024, kABytes / 4, 1024);
             const uint64_t dbh = desc_sw128(bh + st * 32, 16, 1024);
             const uint64_t dbl = desc_sw128(bl + st * 32, 16, 1024);
-            mma_tf32(d_tmem, dah, dbh, idesc, (c | st) != 0);
-            mma_tf32(d_tmem, dal, dbh, idesc, 1);
-            mma_tf32(d_tmem, dah, dbl, idesc, 1);
+            mma_tf32_ts(d_tmem, a_hi + 8 * st, dbh, idesc, (c | st) != 0);
+            mma_tf32_ts(d_tmem, a_lo + 8 * st, dbh, idesc, 1);
+            mma_tf32_ts(d_tmem, a_hi + 8 * st, dbl, idesc, 1);
           }
           mma_commit(&empty[stage]);
           if (c == nch - 1) mma_commit(&tfull[acc]);
@@ -198,8 +206,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       }
     }
   } else if (warp < 6) {
-    // ---------------- converters ----------------
-    const int ct = threadIdx.x - 64;  // 0..127
+    // ---------------- converters: smem [k][p] -> TMEM [p][k] hi / lo ----------------
+    const int q = warp & 3;  // TMEM lane quarter = pixel rows 32q..32q+31
+    const uint32_t lane_base = static_cast<uint32_t>(q * 32) << 16;
     int stage = 0;
     uint32_t phase = 0;
     for (int64_t t = blockIdx.x; t < total; t += gridDim.x) {
@@ -208,23 +217,20 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       const int nch = (nk8 + 3) / 4;
       for (int c = 0; c < nch; ++c) {
         mbar_wait(&full[stage], phase);
-        const int steps = min(4, nk8 - 4 * c);
-        // Each k-step of each column block is a 1 KB slab (8 rows x 128 B).
-        const float4* src = reinterpret_cast<const float4*>(a_hi(stage));
-        float4* dst = reinterpret_cast<float4*>(a_lo(stage));
-        for (int cb = 0; cb < 4; ++cb) {
-          for (int i = ct; i < steps * 64; i += 128) {
-            const int idx = cb * (kABytes / 64) + i;  // float4 index
-            const float4 v = src[idx];
-            float4 lo;
-            lo.x = v.x - tf32_hi(v.x);
-            lo.y = v.y - tf32_hi(v.y);
-            lo.z = v.z - tf32_hi(v.z);
-            lo.w = v.w - tf32_hi(v.w);
-            dst[idx] = lo;
-          }
+        const float* src = reinterpret_cast<const float*>(a_raw(stage)) + q * (KC * 32) + lane;
+        uint32_t hi[KC], lo[KC];
+#pragma unroll
+        for (int k = 0; k < KC; ++k) {
+          const float v = src[k * 32];
+          const float h = tf32_hi(v);
+          hi[k] = __float_as_uint(h);
+          lo[k] = __float_as_uint(v - h);
         }
-        fence_proxy_async_smem();
+        const uint32_t col = tmem + C::kACol0 + stage * 2 * KC + lane_base;
+        tmem_st32(col, hi);
+        tmem_st32(col + KC, lo);
+        tmem_st_wait();
+        tc_fence_before();
         mbar_arrive(&conv[stage]);
         advance(stage, phase, S);
       }
@@ -248,7 +254,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 #pragma unroll 1
       for (int c0 = 0; c0 < NT; c0 += 16) {
         float v[16];
-        tmem_ld16(tmem + acc * NT + c0 + (static_cast<uint32_t>(quarter * 32) << 16), v);
+        tmem_ld16(tmem + acc * C::kAccCols + c0 + (static_cast<uint32_t>(quarter * 32) << 16), v);
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
           const int row = __ldg(rows + c0 + j);
@@ -354,14 +360,15 @@ static cudaError_t launch_tc_nt(const TcBandPlan& tp, const TcDeviceTables& dt,
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
 
-  // --- activations tensor map: {P, D, N * rows_per_sample} fp32, SW128, box {32, 1, 8}
+  // --- activations tensor map: {P, D, N * rows_per_sample} fp32, no swizzle, box {32, 1, 8}
   CUtensorMap tm;
   const uint64_t dims[3] = {static_cast<uint64_t>(call.plane), static_cast<uint64_t>(tp.n_class),
                             static_cast<uint64_t>(call.n) * tp.rows_per_sample_3d};
   const uint64_t strides[2] = {static_cast<uint64_t>(call.plane) * 4,
                                static_cast<uint64_t>(call.plane) * 4 * tp.n_class};
   const uint32_t box[3] = {32, 1, 8};
-  if (!encode_f32_sw128(&tm, call.in, 3, dims, strides, box)) return cudaErrorInvalidValue;
+  if (!encode_f32(&tm, call.in, 3, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_NONE))
+    return cudaErrorInvalidValue;
 
   TcBandArgs ka{};
   ka.panel = panel;
@@ -419,8 +426,6 @@ cudaError_t launch_band_tc(const TcBandPlan& tp, const TcDeviceTables& dt, const
       return launch_tc_nt<64>(tp, dt, call, s);
     case 128:
       return launch_tc_nt<128>(tp, dt, call, s);
-    case 256:
-      return launch_tc_nt<256>(tp, dt, call, s);
     default:
       return cudaErrorInvalidValue;
   }

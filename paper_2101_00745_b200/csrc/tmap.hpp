@@ -31,9 +31,10 @@ inline EncodeTiledFn encode_fn() {
 }
 
 // fp32 tensor of `rank` dims (dims[0] innermost, contiguous), byte strides of
-// dims 1..rank-1, box extents, 128-byte swizzle, zero fill out of bounds.
-inline bool encode_f32_sw128(CUtensorMap* map, const void* base, int rank, const uint64_t* dims,
-                             const uint64_t* strides_bytes, const uint32_t* box) {
+// dims 1..rank-1, box extents, zero fill out of bounds.
+inline bool encode_f32(CUtensorMap* map, const void* base, int rank, const uint64_t* dims,
+                      const uint64_t* strides_bytes, const uint32_t* box,
+                      CUtensorMapSwizzle swizzle) {
   EncodeTiledFn fn = encode_fn();
   if (fn == nullptr) return false;
   cuuint32_t elem[5] = {1, 1, 1, 1, 1};
@@ -41,9 +42,14 @@ inline bool encode_f32_sw128(CUtensorMap* map, const void* base, int rank, const
                         const_cast<void*>(base), reinterpret_cast<const cuuint64_t*>(dims),
                         reinterpret_cast<const cuuint64_t*>(strides_bytes),
                         reinterpret_cast<const cuuint32_t*>(box), elem,
-                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle,
                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
+}
+
+inline bool encode_f32_sw128(CUtensorMap* map, const void* base, int rank, const uint64_t* dims,
+                             const uint64_t* strides_bytes, const uint32_t* box) {
+  return encode_f32(map, base, rank, dims, strides_bytes, box, CU_TENSOR_MAP_SWIZZLE_128B);
 }
 
 }  // namespace scc

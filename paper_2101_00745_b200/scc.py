@@ -116,8 +116,9 @@ class SccConfig:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h is not None and h.value and _lib._lib is not None:
-            _lib._lib.scc_plan_destroy(h)
+        L = getattr(_lib, "_lib", None) if _lib is not None else None
+        if h is not None and h.value and L is not None:
+            L.scc_plan_destroy(h)
             self._h = None
 
     def __repr__(self) -> str:
