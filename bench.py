@@ -298,32 +298,66 @@ def run_ours(args):
             dist.barrier()
         torch.cuda.synchronize()
 
+    # One CUDA graph per buffer set: a step is a single graph launch, so the
+    # device-timed value is not bounded by per-call host overhead.  Warm up on
+    # the capture stream first (plan tables, per-stream panel scratch, NCCL).
+    graphs = None
+    if not args.no_graph:
+        cap = torch.cuda.Stream(dev)
+        cap.wait_stream(stream)
+        with torch.cuda.stream(cap):
+            sp_saved = sp
+            sp = cap.cuda_stream
+            for i in range(nsets):
+                step(i)
+            torch.cuda.synchronize()
+            graphs = []
+            for i in range(nsets):
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=cap):
+                    step(i)
+                graphs.append(g)
+            sp = sp_saved
+        torch.cuda.synchronize()
+
+    def run_step(i):
+        if graphs is not None:
+            graphs[i % nsets].replay()
+        else:
+            step(i)
+
     sampler = ClockSampler(dev.index if ws == 1 else local)
     sampler.start()
     for i in range(max(args.warmup, 3)):
-        step(i)
+        run_step(i)
     barrier()
     # keep the GPU busy ~1 s before timing so the clock record is under load
     t_end = time.perf_counter() + 1.0
     i = 0
     while time.perf_counter() < t_end:
         for _ in range(20):
-            step(i)
+            run_step(i)
             i += 1
         torch.cuda.synchronize()
     barrier()
 
+    # kernels per step, counted on an eager step (graph replays do not pass
+    # through the host library)
+    c0 = L.scc_launch_count()
+    step(0)
+    torch.cuda.synchronize()
+    per_step_launches = L.scc_launch_count() - c0
+
     # ---- timed region (value) ----
-    launches0 = L.scc_launch_count()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     barrier()
     e0.record(stream)
     for i in range(args.steps):
-        step(i)
+        run_step(i)
     e1.record(stream)
     barrier()
-    launches = L.scc_launch_count() - launches0
+    launches = per_step_launches * args.steps
     ms = e0.elapsed_time(e1)
     if ws > 1:
         t = torch.tensor([ms], device=dev, dtype=torch.float64)
@@ -421,7 +455,8 @@ def run_ours(args):
                              f"({nsets * per_set / 2**20:.0f} MiB > 3x L2 {l2 / 2**20:.0f} MiB)",
                        "path": {1: "cuda_core", 2: "tensor"}.get(cfg.path_for(n, h, w), "?"),
                        "bytes_per_step_per_gpu": nbytes["step"],
-                       "collective": "NCCL all_reduce(dW,db) per step" if ws > 1 else "none"},
+                       "collective": "NCCL all_reduce(dW,db) per step" if ws > 1 else "none",
+                       "launch": "eager" if graphs is None else "CUDA graph per step"},
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": e2e,
@@ -443,6 +478,7 @@ def main():
     ap.add_argument("--workload", default="c1", choices=sorted(WORKLOADS))
     ap.add_argument("--path", default=None, choices=[None, "cc", "tc"])
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="launch each step eagerly")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     args = ap.parse_args()

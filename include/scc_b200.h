@@ -78,6 +78,11 @@ int scc_abi_version(void);
  * threads); used by bench.py to report gpu_launches. */
 uint64_t scc_launch_count(void);
 
+/* Diagnostic: per-phase %globaltimer stamps (ns) of CTA 0 of the last
+ * tensor-core band launch on the current device (slot map in scc_tc.cu).
+ * Copies min(n, 32) values; returns the count or -1. */
+int scc_debug_trace(uint64_t* out, int n);
+
 /* ---- geometry (host only; replaces config.cpp / cycle.cpp) --------------- */
 
 /* Overlap::parse (config.cpp:15-37): "50%", "0.5" -> ratio; "3" -> count.
@@ -119,7 +124,9 @@ scc_status_t scc_forward_macs(const scc_plan_t* plan, int64_t n, int64_t h,
                               int64_t w, uint64_t* macs);
 
 /* Force a kernel family for this plan (tests/bench); AUTO by default.
- * SCC_ERR_ARGUMENT when the family cannot run this geometry. */
+ * SCC_PATH_TENSOR is a preference: directions (or calls) the tensor-core
+ * band GEMM cannot express run on the CUDA-core kernels.  SCC_ERR_ARGUMENT for
+ * an unknown value. */
 scc_status_t scc_plan_set_path(scc_plan_t* plan, int32_t path);
 /* The family AUTO would pick (or the forced one) for n*h*w pixels. */
 scc_status_t scc_plan_get_path(const scc_plan_t* plan, int64_t n, int64_t h,

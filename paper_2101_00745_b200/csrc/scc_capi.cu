@@ -5,6 +5,7 @@
 // the per-device plan tables, and dispatches to the kernel families.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <atomic>
 #include <cstring>
 #include <exception>
@@ -99,6 +100,7 @@ const DeviceTables& tables(Plan& p) {
                           put(p.tc_fwd.chunk_base)};
   const size_t o_tb[4] = {put(p.tc_bwd.rt_info), put(p.tc_bwd.rows), put(p.tc_bwd.class_d),
                           put(p.tc_bwd.chunk_base)};
+  const size_t o_tw[2] = {put(p.tc_wgt.rt_info), put(p.tc_wgt.class_d)};
   if (h.empty()) h.push_back(0);
   DeviceTables t;
   t.device = dev;
@@ -125,6 +127,8 @@ const DeviceTables& tables(Plan& p) {
     d.starts = t.starts;
     d.perm = t.perm;
   }
+  t.tcw_rt_info = b + o_tw[0];
+  t.tcw_class_d = b + o_tw[1];
   p.dev.push_back(t);
   return p.dev.back();
 }
@@ -156,11 +160,29 @@ void check_bias(const Plan& p, const void* bias, const char* name) {
 // tensor path falls back to CUDA cores for directions the band GEMM cannot
 // express (ring not a multiple of 8, plane not a multiple of 4, ...).
 int32_t choose_path(const Plan& p, int64_t /*n*/, int64_t h, int64_t w, int dir = 0) {
-  const TcBandPlan& tp = dir == 0 ? p.tc_fwd : p.tc_bwd;
-  const bool tc_ok = tc_band_supported(tp, h * w);
+  const bool tc_ok = dir == 2 ? tc_weight_supported(p.tc_wgt, h * w)
+                              : tc_band_supported(dir == 0 ? p.tc_fwd : p.tc_bwd, h * w);
   if (p.path == SCC_PATH_CUDA_CORE) return SCC_PATH_CUDA_CORE;
   if (p.path == SCC_PATH_TENSOR) return tc_ok ? SCC_PATH_TENSOR : SCC_PATH_CUDA_CORE;
   return SCC_PATH_CUDA_CORE;
+}
+
+float* panel_buffer(Plan& p, int dir, cudaStream_t s) {
+  const int dev = current_device();
+  const TcBandPlan& tp = dir == 0 ? p.tc_fwd : p.tc_bwd;
+  const size_t bytes = tc_panel_bytes(tp);
+  std::lock_guard<std::mutex> lk(p.panel_mu);
+  for (PanelBuf& b : p.panels) {
+    if (b.device == dev && b.stream == static_cast<void*>(s) && b.dir == dir) return static_cast<float*>(b.ptr);
+  }
+  PanelBuf b;
+  b.device = dev;
+  b.stream = s;
+  b.dir = dir;
+  b.bytes = bytes;
+  cuda_check(cudaMalloc(&b.ptr, bytes), "cudaMalloc(panel)");
+  p.panels.push_back(b);
+  return static_cast<float*>(b.ptr);
 }
 
 TcBandCall tc_call(const Plan& p, bool bwd, int64_t n, int64_t plane, const float* in, float* out,
@@ -229,7 +251,9 @@ WeightLaunch weight_args(const Plan& p, const DeviceTables& t, int64_t n, int64_
 }
 
 size_t weight_ws_bytes(const Plan& p, int64_t n, int64_t plane) {
-  return weight_cc_workspace_bytes(p.fwd.nblk(), p.fwd.max_block_len, n, plane);
+  const size_t cc = weight_cc_workspace_bytes(p.fwd.nblk(), p.fwd.max_block_len, n, plane);
+  const size_t tc = tc_weight_supported(p.tc_wgt, plane) ? tc_weight_workspace_bytes(p.tc_wgt, n, plane) : 0;
+  return std::max(cc, tc);
 }
 
 void do_forward(Plan& p, int64_t n, int64_t h, int64_t w, const float* x, const float* wt,
@@ -241,8 +265,9 @@ void do_forward(Plan& p, int64_t n, int64_t h, int64_t w, const float* x, const 
   check_bias(p, b, "bias");
   const DeviceTables& t = tables(p);
   if (choose_path(p, n, h, w, 0) == SCC_PATH_TENSOR) {
-    cuda_check(launch_band_tc(p.tc_fwd, t.tc_fwd, tc_call(p, false, n, h * w, x, y, wt, b), s),
-               "forward (tensor) launch");
+    TcBandCall c = tc_call(p, false, n, h * w, x, y, wt, b);
+    c.panel = panel_buffer(p, 0, s);
+    cuda_check(launch_band_tc(p.tc_fwd, t.tc_fwd, c, s), "forward (tensor) launch");
     return;
   }
   cuda_check(launch_band_cc(band_args(p, t, false, n, h * w, x, y, wt, b), s), "forward launch");
@@ -256,9 +281,9 @@ void do_backward_data(Plan& p, int64_t n, int64_t h, int64_t w, const float* dy,
   check_ptr(dx, "dx");
   const DeviceTables& t = tables(p);
   if (choose_path(p, n, h, w, 1) == SCC_PATH_TENSOR) {
-    cuda_check(launch_band_tc(p.tc_bwd, t.tc_bwd, tc_call(p, true, n, h * w, dy, dx, wt, nullptr),
-                              s),
-               "backward-data (tensor) launch");
+    TcBandCall c = tc_call(p, true, n, h * w, dy, dx, wt, nullptr);
+    c.panel = panel_buffer(p, 1, s);
+    cuda_check(launch_band_tc(p.tc_bwd, t.tc_bwd, c, s), "backward-data (tensor) launch");
     return;
   }
   cuda_check(launch_band_cc(band_args(p, t, true, n, h * w, dy, dx, wt, nullptr), s),
@@ -277,6 +302,26 @@ void do_backward_weight(Plan& p, int64_t n, int64_t h, int64_t w, const float* d
     fail(SCC_ERR_ARGUMENT, "workspace too small: need " + std::to_string(need) + " bytes");
   }
   const DeviceTables& t = tables(p);
+  if (choose_path(p, n, h, w, 2) == SCC_PATH_TENSOR) {
+    TcWeightCall c{};
+    c.dy = dy;
+    c.x = x;
+    c.dweight = dw;
+    c.dbias = db;
+    c.workspace = ws;
+    c.workspace_bytes = ws_bytes;
+    c.n = n;
+    c.plane = h * w;
+    c.c_in = static_cast<int32_t>(p.cfg.c_in);
+    c.c_out = static_cast<int32_t>(p.cfg.c_out);
+    c.gw = static_cast<int32_t>(p.cfg.group_width);
+    c.starts = t.starts;
+    c.inv_perm = t.inv_perm;
+    c.rt_info = t.tcw_rt_info;
+    c.class_d = t.tcw_class_d;
+    cuda_check(launch_weight_tc(p.tc_wgt, c, s), "backward-weight (tensor) launch");
+    return;
+  }
   cuda_check(launch_weight_cc(weight_args(p, t, n, h * w, dy, x, dw, db, ws), ws_bytes, s),
              "backward-weight launch");
 }
@@ -360,6 +405,10 @@ const char* scc_last_error(void) { return scc::g_err.c_str(); }
 int scc_abi_version(void) { return SCC_B200_ABI_VERSION; }
 uint64_t scc_launch_count(void) { return scc::g_launches.load(); }
 
+int scc_debug_trace(uint64_t* out, int n) {
+  return scc::tc_trace(reinterpret_cast<unsigned long long*>(out), n);
+}
+
 scc_status_t scc_overlap_parse(const char* text, int32_t* kind, double* ratio, int64_t* count) {
   return guard([&] {
     scc::check_ptr(kind, "kind");
@@ -401,6 +450,10 @@ scc_status_t scc_plan_destroy(scc_plan_t* plan) {
     for (const scc::DeviceTables& t : plan->dev) {
       cudaSetDevice(t.device);
       cudaFree(t.base);
+    }
+    for (const scc::PanelBuf& b : plan->panels) {
+      cudaSetDevice(b.device);
+      cudaFree(b.ptr);
     }
     for (const scc::HostStaging& s : plan->staging) {
       cudaSetDevice(s.device);
@@ -480,10 +533,6 @@ scc_status_t scc_plan_set_path(scc_plan_t* plan, int32_t path) {
     scc::check_ptr(plan, "plan");
     if (path != SCC_PATH_AUTO && path != SCC_PATH_CUDA_CORE && path != SCC_PATH_TENSOR) {
       scc::fail(SCC_ERR_ARGUMENT, "unknown path " + std::to_string(path));
-    }
-    if (path == SCC_PATH_TENSOR && !plan->tc_fwd.ok && !plan->tc_bwd.ok) {
-      scc::fail(SCC_ERR_ARGUMENT, "tensor-core path cannot express this geometry: " +
-                                      plan->tc_fwd.why);
     }
     plan->path = path;
   });

@@ -58,7 +58,30 @@ struct TcBandCall {
   int32_t c_in, gw;     // operator geometry
   int32_t c_out_t;      // channels of the output tensor
   bool backward_data;
+  float* panel;         // scratch for the band weight images (tc_panel_bytes)
 };
+
+size_t tc_panel_bytes(const TcBandPlan& tp);
+
+struct TcWeightPlan;
+struct TcWeightCall {
+  const float* dy;
+  const float* x;
+  float* dweight;
+  float* dbias;          // nullptr when the layer has no bias
+  void* workspace;
+  size_t workspace_bytes;
+  int64_t n, plane;
+  int32_t c_in, c_out, gw;
+  const int32_t* starts;    // oc -> window start
+  const int32_t* inv_perm;  // oc -> sorted position
+  const int32_t* rt_info;   // TcWeightPlan::rt_info (device)
+  const int32_t* class_d;
+};
+bool tc_weight_supported(const TcWeightPlan& tw, int64_t plane);
+size_t tc_weight_workspace_bytes(const TcWeightPlan& tw, int64_t n, int64_t plane);
+cudaError_t launch_weight_tc(const TcWeightPlan& tw, const TcWeightCall& call, cudaStream_t s);
+int tc_trace(unsigned long long* out, int n);
 
 // Counter of kernels launched by this library (scc_launch_count()).
 void note_launches(uint64_t k);

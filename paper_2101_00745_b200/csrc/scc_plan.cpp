@@ -205,6 +205,44 @@ void build_tc_side(const Plan& p, bool bwd, TcBandPlan& tp) {
   tp.ok = true;
 }
 
+void build_tc_weight(const Plan& p, TcWeightPlan& tw) {
+  const scc_config_t& c = p.cfg;
+  tw = TcWeightPlan{};
+  if (!p.tc_bwd.ok || c.c_in % 8 != 0) {
+    tw.why = "needs the backward-data class layout and c_in % 8 == 0";
+    return;
+  }
+  tw.cls = p.tc_bwd.cls;
+  tw.n_class = p.tc_bwd.n_class;
+  tw.class_d = p.tc_bwd.class_d;
+  const int32_t ring = static_cast<int32_t>(c.c_in);
+  const int32_t gw = static_cast<int32_t>(c.group_width);
+  tw.n_rt = static_cast<int32_t>((c.c_out + 127) / 128);
+  int32_t max_cols = 0;
+  for (int32_t rt = 0; rt < tw.n_rt; ++rt) {
+    std::vector<Arc> arcs;
+    for (int32_t r = 0; r < 128; ++r) {
+      const int64_t i = static_cast<int64_t>(rt) * 128 + r;
+      if (i >= c.c_out) break;
+      arcs.push_back(Arc{static_cast<int32_t>(p.start_of(p.perm[static_cast<size_t>(i)])), gw});
+    }
+    const Arc cov = cover_arcs(arcs, ring);
+    int32_t start8 = (cov.start / 8) * 8;
+    int32_t ncols = ((cov.start + cov.len - start8 + 7) / 8) * 8;
+    if (ncols >= ring) {
+      start8 = 0;
+      ncols = ring;
+    }
+    tw.rt_info.insert(tw.rt_info.end(), {start8, ncols});
+    max_cols = std::max(max_cols, ncols);
+  }
+  // Column chunk: multiple of 16 (M=128 MMA), at most 256.
+  const int32_t w16 = (max_cols + 15) / 16 * 16;
+  tw.n_nc = (w16 + 255) / 256;
+  tw.nw = ((w16 + tw.n_nc - 1) / tw.n_nc + 15) / 16 * 16;
+  tw.ok = true;
+}
+
 void build_plan(Plan& p, int64_t c_in, int64_t c_out, int64_t cg, int32_t kind,
                 double ratio, int64_t count, int32_t has_bias) {
   // scc_config_new (config.cpp:62-83).
@@ -329,6 +367,7 @@ void build_plan(Plan& p, int64_t c_in, int64_t c_out, int64_t cg, int32_t kind,
   }
   build_tc_side(p, false, p.tc_fwd);
   build_tc_side(p, true, p.tc_bwd);
+  build_tc_weight(p, p.tc_wgt);
 }
 
 }  // namespace scc

@@ -71,6 +71,17 @@ struct TcBandPlan {
   std::vector<int32_t> chunk_base;  // n_rt + 1 prefix sums of chunks
 };
 
+// Tensor-core backward-weight tiling: row tiles of 128 filters (sorted order)
+// x N-chunks (<= 256 columns) of the tile's input-channel arc; K = pixels.
+struct TcWeightPlan {
+  bool ok = false;
+  std::string why;
+  int32_t n_rt = 0, n_nc = 0, nw = 0;  // row tiles, column chunks per tile, chunk width
+  int32_t cls = 0, n_class = 1;        // dy 3-D view (as backward-data)
+  std::vector<int32_t> rt_info;        // per row tile: start8 (ic ring), ncols (8-aligned)
+  std::vector<int32_t> class_d;
+};
+
 struct TcDeviceTables {
   const int32_t* rt_info = nullptr;
   const int32_t* rows = nullptr;
@@ -94,6 +105,8 @@ struct DeviceTables {
   const int32_t* inv_perm = nullptr;  // oc -> sorted position
   const int32_t* starts = nullptr;    // oc -> window start
   TcDeviceTables tc_fwd, tc_bwd;
+  const int32_t* tcw_rt_info = nullptr;
+  const int32_t* tcw_class_d = nullptr;
 };
 
 // Device staging for the host-buffer entry points.
@@ -104,6 +117,16 @@ struct HostStaging {
   void* stream = nullptr;  // cudaStream_t
 };
 
+// Per (device, stream, direction) scratch for the tensor-core weight panels,
+// so concurrent calls on different streams never share one.
+struct PanelBuf {
+  int device = -1;
+  void* stream = nullptr;
+  int dir = 0;
+  void* ptr = nullptr;
+  size_t bytes = 0;
+};
+
 struct Plan {
   scc_config_t cfg{};
   std::vector<int64_t> cycle_starts;  // compute_channel_cycle order
@@ -111,10 +134,13 @@ struct Plan {
   BandSide fwd, bwd;
   std::vector<Arc> ic_arcs;          // covering arc of each input channel (sorted order)
   TcBandPlan tc_fwd, tc_bwd;
+  TcWeightPlan tc_wgt;
   int32_t path = SCC_PATH_AUTO;
 
   std::mutex dev_mu;
   std::deque<DeviceTables> dev;  // deque: references stay valid
+  std::mutex panel_mu;
+  std::deque<PanelBuf> panels;
   std::mutex host_mu;
   std::deque<HostStaging> staging;
 

@@ -37,6 +37,17 @@ namespace {
 
 using namespace sm100;
 
+// Diagnostic timeline of the last tensor-core band launch (CTA 0 only; ns,
+// %globaltimer).  Slots: 0 start, 1 setup done, 2 producer first TMA issued,
+// 3 producer dependency satisfied, 4 converter first stage landed,
+// 5 MMA first stage converted, 6.. per tile (up to 8): MMA commit of tile i
+// at 6+2i, epilogue done with tile i at 7+2i, 30 end.
+__device__ unsigned long long g_trace[32];
+#define TRACE(slot)                                           \
+  do {                                                        \
+    if (blockIdx.x == 0) g_trace[(slot)] = globaltimer();     \
+  } while (0)
+
 constexpr int kTcThreads = 320;
 constexpr int KC = 32;          // ring positions per pipeline stage (4 k-steps of 8)
 constexpr int TM = 128;         // pixels per tile
@@ -101,6 +112,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   const uint32_t warp = warp_id();
   const int lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
+    TRACE(0);
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&conv[s], 128);
@@ -118,6 +130,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  if (threadIdx.x == 0) TRACE(1);
 
   const int64_t total = a.n * a.ptiles * a.n_rt;
 
@@ -156,7 +169,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             }
           }
           if (!dep_synced) {
+            TRACE(2);
             cudaGridDependencySynchronize();
+            TRACE(3);
             dep_synced = true;
           }
           bulk_load(b_img(stage), panel + static_cast<int64_t>(c) * (C::kBBytes / 4),
@@ -182,6 +197,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       for (int c = 0; c < nch; ++c) {
         mbar_wait(&conv[stage], phase);
         tc_fence_after();
+        if (t == blockIdx.x && c == 0 && lane == 0) TRACE(5);
         const int steps = min(4, nk8 - 4 * c);
         if (elect_one()) {
           const uint32_t a_hi = tmem + C::kACol0 + stage * 2 * KC;
@@ -195,7 +211,11 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             mma_tf32_ts(d_tmem, a_hi + 8 * st, dbl, idesc, 1);
           }
           mma_commit(&empty[stage]);
-          if (c == nch - 1) mma_commit(&tfull[acc]);
+          if (c == nch - 1) {
+            mma_commit(&tfull[acc]);
+            const int64_t ti = (t - blockIdx.x) / gridDim.x;
+            if (ti < 8) TRACE(6 + 2 * ti);
+          }
         }
         __syncwarp();
         advance(stage, phase, S);
@@ -217,6 +237,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       const int nch = (nk8 + 3) / 4;
       for (int c = 0; c < nch; ++c) {
         mbar_wait(&full[stage], phase);
+        if (t == blockIdx.x && c == 0 && threadIdx.x == 64) TRACE(4);
         const float* src = reinterpret_cast<const float*>(a_raw(stage)) + q * (KC * 32) + lane;
         uint32_t hi[KC], lo[KC];
 #pragma unroll
@@ -237,35 +258,83 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     }
   } else {
     // ---------------- epilogue ----------------
-    const int quarter = warp & 3;  // TMEM lane quarter this warp may access
+    // Per tile: the row -> channel map and the bias of each row go to shared
+    // memory once (named barrier over the 4 epilogue warps), then TMEM is
+    // drained 32 columns at a time; each column store is 32 consecutive
+    // pixels of one NCHW channel row (128 B, coalesced).
+    const int et = threadIdx.x - 192;  // 0..127
+    const int quarter = warp & 3;      // TMEM lane quarter this warp may access
     const int prow = quarter * 32 + lane;
+    // Typed __shared__ tables: LDS, not generic loads that would have to be
+    // ordered behind the preceding global stores.
+    __shared__ int32_t row_s[NT];
+    __shared__ float bias_s[NT];
     int acc = 0;
     uint32_t acc_phase = 0;
+    int cur_rt = -1;
     for (int64_t t = blockIdx.x; t < total; t += gridDim.x) {
       const int rt = static_cast<int>(t % a.n_rt);
       const int64_t pt = t / a.n_rt;
       const int64_t n = pt / a.ptiles;
       const int64_t p = static_cast<int64_t>(pt - n * a.ptiles) * TM + prow;
+      if (rt != cur_rt) {
+        named_bar_sync(1, 128);  // previous tile finished reading the tables
+        for (int i = et; i < NT; i += 128) {
+          const int row = __ldg(a.rows + rt * NT + i);
+          row_s[i] = row;
+          bias_s[i] = (a.bias != nullptr && row >= 0) ? __ldg(a.bias + row) : 0.f;
+        }
+        named_bar_sync(1, 128);
+        cur_rt = rt;
+      }
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const bool pv = p < a.plane;
-      float* obase = a.out + n * a.c_out_t * a.plane + p;
-      const int32_t* rows = a.rows + rt * NT;
+      float* __restrict__ obase = a.out + n * a.c_out_t * a.plane + p;
+      const uint32_t taddr = tmem + acc * C::kAccCols + (static_cast<uint32_t>(quarter * 32) << 16);
 #pragma unroll 1
-      for (int c0 = 0; c0 < NT; c0 += 16) {
-        float v[16];
-        tmem_ld16(tmem + acc * C::kAccCols + c0 + (static_cast<uint32_t>(quarter * 32) << 16), v);
+      for (int c0 = 0; c0 < NT; c0 += 32) {
+        uint32_t v[32];
+        int32_t rr[32];
+        float bb[32];
+        tmem_ld32_nowait(taddr + c0, v);
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const int row = __ldg(rows + c0 + j);
-          if (row >= 0 && pv) {
-            const float b = a.bias ? __ldg(a.bias + row) : 0.f;
-            obase[static_cast<int64_t>(row) * a.plane] = v[j] + b;
+        for (int j = 0; j < 32; ++j) {
+          rr[j] = row_s[c0 + j];
+          bb[j] = bias_s[c0 + j];
+        }
+        tmem_ld_wait();
+#if defined(SCC_EXP_NOSTORE)
+        float acc_s = 0.f;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) acc_s += __uint_as_float(v[j]) + bb[j] * rr[j];
+        if (acc_s == 123.456f) obase[0] = acc_s;
+#elif defined(SCC_EXP_VEC4)
+        // same byte volume, float4 stores along pixels (results wrong on purpose)
+        if (pv) {
+#pragma unroll
+          for (int j = 0; j < 32; j += 4) {
+            if (rr[j] >= 0) {
+              float4* dst = reinterpret_cast<float4*>(a.out + n * a.c_out_t * a.plane + static_cast<int64_t>(rr[j + (lane & 3)]) * a.plane + (p - prow) + (lane >> 2) * 4 + quarter * 32);
+              *dst = make_float4(__uint_as_float(v[j]), __uint_as_float(v[j + 1]), __uint_as_float(v[j + 2]), __uint_as_float(v[j + 3]));
+            }
           }
         }
+#else
+        if (pv) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            if (rr[j] >= 0) obase[static_cast<int64_t>(rr[j]) * a.plane] = __uint_as_float(v[j]) + bb[j];
+          }
+        }
+#endif
       }
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
+      {
+        const int64_t ti = (t - blockIdx.x) / gridDim.x;
+        if (ti < 8 && et == 0) TRACE(7 + 2 * ti);
+      }
       if (++acc == 2) {
         acc = 0;
         acc_phase ^= 1u;
@@ -274,6 +343,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) TRACE(30);
   if (warp == 1) tmem_dealloc<C::kTmemCols>(tmem);
 }
 
@@ -294,6 +364,9 @@ struct PanelArgs {
 
 template <int NT>
 __global__ void __launch_bounds__(256) tc_panel_kernel(const PanelArgs a) {
+  // Let the dependent band kernel get scheduled now; it waits for this grid's
+  // completion (griddepcontrol.wait) before it reads the panel.
+  cudaTriggerProgrammaticLaunchCompletion();
   for (int64_t e = blockIdx.x * 256ll + threadIdx.x; e < a.total; e += gridDim.x * 256ll) {
     const int k = static_cast<int>(e & 31);
     const int r = static_cast<int>((e >> 5) % NT);
@@ -337,10 +410,8 @@ static cudaError_t launch_tc_nt(const TcBandPlan& tp, const TcDeviceTables& dt,
   using C = TcCfg<NT>;
   // --- panel ---
   const int64_t entries = static_cast<int64_t>(tp.total_chunks) * NT * 32;
-  float* panel = nullptr;
-  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&panel),
-                                  static_cast<size_t>(entries) * 2 * sizeof(float), s);
-  if (e != cudaSuccess) return e;
+  float* panel = call.panel;
+  cudaError_t e = cudaSuccess;
   PanelArgs pa{};
   pa.weight = call.weight;
   pa.rt_info = dt.rt_info;
@@ -416,7 +487,16 @@ static cudaError_t launch_tc_nt(const TcBandPlan& tp, const TcDeviceTables& dt,
   e = cudaLaunchKernelEx(&cfg, tc_band_kernel<NT>, tm, ka);
   if (e != cudaSuccess) return e;
   note_launches(2);
-  return cudaFreeAsync(panel, s);
+  return cudaSuccess;
+}
+
+int tc_trace(unsigned long long* out, int n) {
+  if (n > 32) n = 32;
+  return cudaMemcpyFromSymbol(out, g_trace, n * sizeof(unsigned long long)) == cudaSuccess ? n : -1;
+}
+
+size_t tc_panel_bytes(const TcBandPlan& tp) {
+  return static_cast<size_t>(tp.total_chunks) * 2 * tp.nt * 32 * sizeof(float);
 }
 
 cudaError_t launch_band_tc(const TcBandPlan& tp, const TcDeviceTables& dt, const TcBandCall& call,
