@@ -79,8 +79,9 @@ int scc_abi_version(void);
 uint64_t scc_launch_count(void);
 
 /* Diagnostic: per-phase %globaltimer stamps (ns) of CTA 0 of the last
- * tensor-core band launch on the current device (slot map in scc_tc.cu).
- * Copies min(n, 32) values; returns the count or -1. */
+ * tensor-core band launch (slots 0..31, map in scc_tc.cu) and of the last
+ * backward-weight launch (slots 32..63, map in scc_tc_wgrad.cu) on the
+ * current device.  Copies min(n, 64) values; returns the count or -1. */
 int scc_debug_trace(uint64_t* out, int n);
 
 /* ---- geometry (host only; replaces config.cpp / cycle.cpp) --------------- */

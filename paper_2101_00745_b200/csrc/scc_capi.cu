@@ -96,10 +96,10 @@ const DeviceTables& tables(Plan& p) {
   const size_t o_fr = put(p.fwd.rows), o_fb = put(arcs(p.fwd.blocks)), o_fg = put(p.fwd.groups);
   const size_t o_br = put(p.bwd.rows), o_bb = put(arcs(p.bwd.blocks)), o_bg = put(p.bwd.groups);
   const size_t o_pm = put(p.perm), o_ip = put(p.inv_perm), o_st = put(p.starts);
-  const size_t o_tf[4] = {put(p.tc_fwd.rt_info), put(p.tc_fwd.rows), put(p.tc_fwd.class_d),
-                          put(p.tc_fwd.chunk_base)};
-  const size_t o_tb[4] = {put(p.tc_bwd.rt_info), put(p.tc_bwd.rows), put(p.tc_bwd.class_d),
-                          put(p.tc_bwd.chunk_base)};
+  const size_t o_tf[5] = {put(p.tc_fwd.rt_info), put(p.tc_fwd.rows), put(p.tc_fwd.class_d),
+                          put(p.tc_fwd.chunk_base), put(p.tc_fwd.out_class_d)};
+  const size_t o_tb[5] = {put(p.tc_bwd.rt_info), put(p.tc_bwd.rows), put(p.tc_bwd.class_d),
+                          put(p.tc_bwd.chunk_base), put(p.tc_bwd.out_class_d)};
   const size_t o_tw[2] = {put(p.tc_wgt.rt_info), put(p.tc_wgt.class_d)};
   if (h.empty()) h.push_back(0);
   DeviceTables t;
@@ -124,6 +124,7 @@ const DeviceTables& tables(Plan& p) {
     d.rows = b + o[1];
     d.class_d = b + o[2];
     d.chunk_base = b + o[3];
+    d.out_class_d = b + o[4];
     d.starts = t.starts;
     d.perm = t.perm;
   }
@@ -406,7 +407,16 @@ int scc_abi_version(void) { return SCC_B200_ABI_VERSION; }
 uint64_t scc_launch_count(void) { return scc::g_launches.load(); }
 
 int scc_debug_trace(uint64_t* out, int n) {
-  return scc::tc_trace(reinterpret_cast<unsigned long long*>(out), n);
+  // slots [0, 32): band kernel; [32, 64): backward-weight kernel
+  int k = scc::tc_trace(reinterpret_cast<unsigned long long*>(out), n < 32 ? n : 32);
+  if (k < 0 || n <= 32) return k;
+  const int m = scc::tc_wtrace(reinterpret_cast<unsigned long long*>(out) + 32, n < 64 ? n - 32 : 32);
+  if (m < 0) return -1;
+  if (n < 128) return 32 + m;
+  unsigned int hang[64];
+  if (scc::tc_hang(hang) < 0) return -1;
+  for (int i = 0; i < 64; ++i) out[64 + i] = hang[i];  // watchdog builds only
+  return 128;
 }
 
 scc_status_t scc_overlap_parse(const char* text, int32_t* kind, double* ratio, int64_t* count) {

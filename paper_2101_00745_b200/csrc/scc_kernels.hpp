@@ -82,6 +82,8 @@ bool tc_weight_supported(const TcWeightPlan& tw, int64_t plane);
 size_t tc_weight_workspace_bytes(const TcWeightPlan& tw, int64_t n, int64_t plane);
 cudaError_t launch_weight_tc(const TcWeightPlan& tw, const TcWeightCall& call, cudaStream_t s);
 int tc_trace(unsigned long long* out, int n);
+int tc_hang(unsigned int* out);
+int tc_wtrace(unsigned long long* out, int n);
 
 // Counter of kernels launched by this library (scc_launch_count()).
 void note_launches(uint64_t k);

@@ -158,6 +158,37 @@ void build_tc_side(const Plan& p, bool bwd, TcBandPlan& tp) {
     tp.rows_per_sample_3d = static_cast<int32_t>(c.c_in);
     tp.class_d = {0};
   }
+  // Activation box height: the largest of 32/16/8 rows that divides the ring
+  // and the class run, so a box never leaves one contiguous run of rows.
+  tp.rb = 8;
+  for (int32_t rb : {32, 16}) {
+    if (tp.ring % rb == 0 && tp.cls % rb == 0) {
+      tp.rb = rb;
+      break;
+    }
+  }
+  // Output view for TMA stores (32-row groups of the tile's rows).
+  if (bwd) {
+    tp.out_cls = static_cast<int32_t>(c.c_in);
+    tp.out_n_class = 1;
+    tp.out_class_d = {0};
+    tp.store_ok = c.c_in % 32 == 0;
+  } else {
+    const int32_t D = static_cast<int32_t>(c.cyclic_dist);
+    tp.store_ok = c.c_out % D == 0 && (c.c_out / D) % 32 == 0;
+    if (tp.store_ok) {
+      tp.out_cls = static_cast<int32_t>(c.c_out / D);
+      tp.out_n_class = D;
+      for (int32_t cl = 0; cl < D && tp.store_ok; ++cl) {
+        const int32_t d = p.perm[static_cast<size_t>(cl) * tp.out_cls];
+        for (int32_t j = 0; j < tp.out_cls; ++j) {
+          if (d >= D || p.perm[static_cast<size_t>(cl) * tp.out_cls + j] != d + D * j) tp.store_ok = false;
+        }
+        tp.out_class_d.push_back(d);
+      }
+    }
+    if (!tp.store_ok) tp.out_class_d.assign(1, 0);
+  }
   // Row-tile width: fewest padded rows, ties to the wider tile.
   int32_t best = 0;
   int64_t best_pad = INT64_MAX;
@@ -189,9 +220,11 @@ void build_tc_side(const Plan& p, bool bwd, TcBandPlan& tp) {
       }
     }
     const Arc cov = cover_arcs(arcs, tp.ring);
-    int32_t start8 = (cov.start / 8) * 8;
-    int32_t nk8 = (cov.start + cov.len - start8 + 7) / 8;
-    if (nk8 < 1) nk8 = 1;  // uncovered rows still get written (as zeros)
+    // Align the arc to the TMA box height so every box stays inside one ring
+    // class and never wraps.
+    int32_t start8 = (cov.start / tp.rb) * tp.rb;
+    int32_t nk8 = (cov.start + cov.len - start8 + tp.rb - 1) / tp.rb * (tp.rb / 8);
+    if (nk8 < tp.rb / 8) nk8 = tp.rb / 8;  // uncovered rows still get written (as zeros)
     if (nk8 * 8 >= tp.ring) {
       start8 = 0;
       nk8 = tp.ring / 8;
@@ -236,10 +269,24 @@ void build_tc_weight(const Plan& p, TcWeightPlan& tw) {
     tw.rt_info.insert(tw.rt_info.end(), {start8, ncols});
     max_cols = std::max(max_cols, ncols);
   }
-  // Column chunk: multiple of 16 (M=128 MMA), at most 256.
-  const int32_t w16 = (max_cols + 15) / 16 * 16;
-  tw.n_nc = (w16 + 255) / 256;
-  tw.nw = ((w16 + tw.n_nc - 1) / tw.n_nc + 15) / 16 * 16;
+  // Column chunk: multiple of 32 (four 8-row quarters, M=128 MMA), <= 256.
+  const int32_t w32 = (max_cols + 31) / 32 * 32;
+  tw.n_nc = (w32 + 255) / 256;
+  tw.nw = ((w32 + tw.n_nc - 1) / tw.n_nc + 31) / 32 * 32;
+  // dy boxes: each converter warp loads its 32 filter rows; one box when the
+  // 32 rows are one contiguous class run.
+  tw.rba = (tw.cls % 32 == 0) ? 32 : (tw.cls % 16 == 0 ? 16 : 8);
+  // x boxes: a warp loads nw/4 consecutive arc rows; a box must not wrap the
+  // ring, so its height divides the ring, every arc start and the quarter.
+  tw.rbb = 8;
+  for (int32_t rb : {64, 32, 16}) {
+    bool ok = (tw.nw / 4) % rb == 0 && ring % rb == 0;
+    for (int32_t rt = 0; rt < tw.n_rt && ok; ++rt) ok = tw.rt_info[2 * rt] % rb == 0;
+    if (ok) {
+      tw.rbb = rb;
+      break;
+    }
+  }
   tw.ok = true;
 }
 

@@ -65,6 +65,12 @@ struct TcBandPlan {
   int32_t n_class = 1;              // TMA dim 1 extent (D for backward-data)
   int32_t rows_per_sample_3d = 0;   // TMA dim-2 rows per sample
   int32_t total_chunks = 0;
+  int32_t rb = 8;                   // TMA box rows for the activations (8, 16 or 32)
+  // Output tensor view for TMA stores of 32-row groups (store_ok == false:
+  // the epilogue uses plain stores).
+  bool store_ok = false;
+  int32_t out_cls = 0, out_n_class = 1;
+  std::vector<int32_t> out_class_d;
   std::vector<int32_t> rt_info;     // per row tile: start8, nk8, panel offset (floats), chunks
   std::vector<int32_t> rows;        // n_rt * nt
   std::vector<int32_t> class_d;     // class -> d coordinate
@@ -78,6 +84,7 @@ struct TcWeightPlan {
   std::string why;
   int32_t n_rt = 0, n_nc = 0, nw = 0;  // row tiles, column chunks per tile, chunk width
   int32_t cls = 0, n_class = 1;        // dy 3-D view (as backward-data)
+  int32_t rba = 8, rbb = 8;            // TMA box rows for dy (per warp quarter) and x
   std::vector<int32_t> rt_info;        // per row tile: start8 (ic ring), ncols (8-aligned)
   std::vector<int32_t> class_d;
 };
@@ -89,6 +96,7 @@ struct TcDeviceTables {
   const int32_t* chunk_base = nullptr;
   const int32_t* starts = nullptr;
   const int32_t* perm = nullptr;
+  const int32_t* out_class_d = nullptr;
 };
 
 // Device copy of the tables (one per CUDA device).

@@ -58,12 +58,13 @@ struct TcCfg {
   static_assert(NT == 64 || NT == 128, "row tile must be 64 or 128");
   static constexpr int kBBytes = 2 * NT * KC * 4;        // hi + lo weight image
   static constexpr int kStageBytes = kABytes + kBBytes;  // raw activations + weights
-  static constexpr int kStages = 4;
+  static constexpr int kStages = 3;
   static constexpr int kAccCols = NT;                    // per accumulator buffer
   static constexpr int kACol0 = 2 * NT;                  // first TMEM column of A stages
   static constexpr int kTmemCols = 512;
   static_assert(kACol0 + kStages * 2 * KC <= kTmemCols, "TMEM budget");
-  static constexpr int kSmem = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int kStoreBytes = 4 * 2 * 32 * 32 * 4;  // 4 warps x 2 bufs x [32 rows][32 px]
+  static constexpr int kSmem = kStages * kStageBytes + kStoreBytes + 1024 /*align*/ + 512 /*barriers*/;
 };
 
 struct TcBandArgs {
@@ -71,13 +72,18 @@ struct TcBandArgs {
   const int32_t* rt_info;    // per row tile: start8 (ring pos), nk8, panel offset (floats), chunks
   const int32_t* rows;       // [n_rt * NT] output channel per tile row, -1 = none
   const int32_t* class_d;    // ring class -> TMA coordinate d
+  const int32_t* out_class_d;  // output view class -> d (TMA stores)
   const float* bias;         // forward only
   float* out;
   int32_t n_rt;              // row tiles
   int32_t ring;              // ring length (c_in fwd / c_out bwd)
   int32_t cls;               // ring positions per class (c_in fwd / c_out/D bwd)
+  int32_t rb;                // activation box rows
   int32_t c_out_t;           // channels of the output tensor
+  int32_t rows_total;        // valid tile rows (c_out fwd / c_in bwd)
   int32_t rows_per_sample_3d;  // TMA dim-2 rows per sample (c_in fwd / c_out/D bwd)
+  int32_t out_cls;           // output view rows per class
+  int32_t store_ok;          // TMA-store epilogue usable
   int32_t ptiles;            // pixel tiles per sample
   int64_t plane;
   int64_t n;
@@ -90,23 +96,42 @@ __device__ __forceinline__ void advance(int& stage, uint32_t& phase, int stages)
   }
 }
 
+// Tile t -> (row tile, sample, first pixel).
+struct TileCoord {
+  int rt;
+  int n;
+  int p0;
+};
+__device__ __forceinline__ TileCoord tile_coord(const TcBandArgs& a, int64_t t) {
+  TileCoord c;
+  c.rt = static_cast<int>(t % a.n_rt);
+  const int64_t pt = t / a.n_rt;
+  c.n = static_cast<int>(pt / a.ptiles);
+  c.p0 = static_cast<int>(pt - static_cast<int64_t>(c.n) * a.ptiles) * TM;
+  return c;
+}
+
 template <int NT>
 __global__ void __launch_bounds__(kTcThreads, 1)
-    tc_band_kernel(const __grid_constant__ CUtensorMap tmap, const TcBandArgs a) {
+    tc_band_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap tout,
+                   const TcBandArgs a) {
   using C = TcCfg<NT>;
   constexpr int S = C::kStages;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S * C::kStageBytes);
-  uint64_t* full = bars;                // [S] TMA + bulk bytes landed
-  uint64_t* conv = bars + S;            // [S] A hi/lo written to TMEM
-  uint64_t* empty = bars + 2 * S;       // [S] MMAs done with the stage
-  uint64_t* tfull = bars + 3 * S;       // [2] accumulator ready
-  uint64_t* tempty = bars + 3 * S + 2;  // [2] accumulator drained
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * S + 4);
+  uint8_t* store_buf = smem + S * C::kStageBytes;  // [warp 0..3][2][32 rows][32 px]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(store_buf + C::kStoreBytes);
+  uint64_t* full_a = bars;              // [S][4] activations of one pixel quarter landed
+  uint64_t* full_b = bars + 4 * S;      // [S] weight panel landed
+  uint64_t* conv = bars + 5 * S;        // [S] A hi/lo written to TMEM (4 warp arrivals)
+  uint64_t* empty = bars + 6 * S;       // [S] MMAs done with the stage
+  uint64_t* tfull = bars + 7 * S;       // [2] accumulator ready
+  uint64_t* tempty = bars + 7 * S + 2;  // [2] accumulator drained
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 7 * S + 4);
 
-  auto a_raw = [&](int s) { return smem + s * C::kStageBytes; };
+  // A raw stage: [quarter 0..3][KC ring rows][32 pixels] (4 KB per quarter).
+  auto a_raw = [&](int s, int q) { return smem + s * C::kStageBytes + q * (KC * 128); };
   auto b_img = [&](int s) { return smem + s * C::kStageBytes + kABytes; };
 
   const uint32_t warp = warp_id();
@@ -114,17 +139,21 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   if (threadIdx.x == 0) {
     TRACE(0);
     for (int s = 0; s < S; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&conv[s], 128);
+      for (int q = 0; q < 4; ++q) mbar_init(&full_a[4 * s + q], 1);
+      mbar_init(&full_b[s], 1);
+      mbar_init(&conv[s], 4);
       mbar_init(&empty[s], 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], 128);
+      mbar_init(&tempty[i], 4);
     }
     fence_mbar_init();
   }
-  if (warp == 0 && lane == 0) prefetch_tmap(&tmap);
+  if (warp == 2 && lane == 0) {
+    prefetch_tmap(&tmap);
+    prefetch_tmap(&tout);
+  }
   if (warp == 1) tmem_alloc<C::kTmemCols>(tmem_slot);
   tc_fence_before();
   __syncthreads();
@@ -135,47 +164,25 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   const int64_t total = a.n * a.ptiles * a.n_rt;
 
   if (warp == 0) {
-    // ---------------- producer ----------------
-    // Activations do not depend on the preceding panel-build kernel; the
-    // panel does (programmatic dependent launch): wait only before the first
-    // panel copy.
+    // ---------------- weight-panel producer (one bulk copy per stage) ----------------
     if (elect_one()) {
-      bool dep_synced = false;
+      // The panel comes from the preceding panel-build kernel (programmatic
+      // dependent launch): wait for it once.
+      TRACE(2);
+      cudaGridDependencySynchronize();
+      TRACE(3);
       int stage = 0;
       uint32_t phase = 0;
       for (int64_t t = blockIdx.x; t < total; t += gridDim.x) {
         const int rt = static_cast<int>(t % a.n_rt);
-        const int64_t pt = t / a.n_rt;
-        const int64_t n = pt / a.ptiles;
-        const int p0 = static_cast<int>(pt - n * a.ptiles) * TM;
-        const int start8 = a.rt_info[4 * rt], nk8 = a.rt_info[4 * rt + 1];
+        const int nk8 = a.rt_info[4 * rt + 1];
         const float* panel = a.panel + a.rt_info[4 * rt + 2];
         const int nch = (nk8 + 3) / 4;
         for (int c = 0; c < nch; ++c) {
-          mbar_wait(&empty[stage], phase ^ 1u);
-          const int steps = min(4, nk8 - 4 * c);
-          mbar_expect_tx(&full[stage], steps * 4 * 1024 + C::kBBytes);
-          for (int st = 0; st < steps; ++st) {
-            int pos = start8 + 8 * (4 * c + st);
-            while (pos >= a.ring) pos -= a.ring;
-            const int cl = pos / a.cls, j = pos - cl * a.cls;
-            const int d = __ldg(a.class_d + cl);
-            const int row = static_cast<int>(n) * a.rows_per_sample_3d + j;
-#pragma unroll
-            for (int cb = 0; cb < 4; ++cb) {
-              // [cb][32 ring rows][32 pixels], 128 B per ring row, no swizzle
-              tma_load_3d(a_raw(stage) + cb * (KC * 128) + st * 1024, &tmap, &full[stage],
-                          p0 + 32 * cb, d, row);
-            }
-          }
-          if (!dep_synced) {
-            TRACE(2);
-            cudaGridDependencySynchronize();
-            TRACE(3);
-            dep_synced = true;
-          }
-          bulk_load(b_img(stage), panel + static_cast<int64_t>(c) * (C::kBBytes / 4),
-                    C::kBBytes, &full[stage]);
+          mbar_wait_tag(&empty[stage], phase ^ 1u, 1);
+          mbar_expect_tx(&full_b[stage], C::kBBytes);
+          bulk_load(b_img(stage), panel + static_cast<int64_t>(c) * (C::kBBytes / 4), C::kBBytes,
+                    &full_b[stage]);
           advance(stage, phase, S);
         }
       }
@@ -191,11 +198,12 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       const int rt = static_cast<int>(t % a.n_rt);
       const int nk8 = a.rt_info[4 * rt + 1];
       const int nch = (nk8 + 3) / 4;
-      mbar_wait(&tempty[acc], acc_phase ^ 1u);
+      mbar_wait_tag(&tempty[acc], acc_phase ^ 1u, 2);
       tc_fence_after();
       const uint32_t d_tmem = tmem + acc * C::kAccCols;
       for (int c = 0; c < nch; ++c) {
-        mbar_wait(&conv[stage], phase);
+        mbar_wait_tag(&conv[stage], phase, 3);
+        mbar_wait_tag(&full_b[stage], phase, 4);
         tc_fence_after();
         if (t == blockIdx.x && c == 0 && lane == 0) TRACE(5);
         const int steps = min(4, nk8 - 4 * c);
@@ -226,9 +234,36 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       }
     }
   } else if (warp < 6) {
-    // ---------------- converters: smem [k][p] -> TMEM [p][k] hi / lo ----------------
-    const int q = warp & 3;  // TMEM lane quarter = pixel rows 32q..32q+31
+    // ---------------- activation loaders + converters ----------------
+    // Warp q owns pixels 32q..32q+31 of every tile == TMEM lanes 32q..32q+31:
+    // it loads its own [ring rows][32 px] boxes, then transposes them into
+    // TMEM as tf32 hi / lo columns.  Loads run S chunks ahead.
+    const int q = warp & 3;
     const uint32_t lane_base = static_cast<uint32_t>(q * 32) << 16;
+    // Chunk sequence of this CTA, for the look-ahead issue.
+    int64_t it_t = blockIdx.x;  // tile of the next chunk to issue
+    int it_c = 0;               // chunk within that tile
+    auto issue_next = [&](int s) {
+      if (it_t >= total) return;
+      const TileCoord tc = tile_coord(a, it_t);
+      const int start8 = a.rt_info[4 * tc.rt], nk8 = a.rt_info[4 * tc.rt + 1];
+      const int steps = min(4, nk8 - 4 * it_c);
+      if (lane == 0) {
+        mbar_expect_tx(&full_a[4 * s + q], steps * 8 * 128);
+        for (int r = 0; r < steps * 8; r += a.rb) {
+          int pos = start8 + 32 * it_c + r;
+          while (pos >= a.ring) pos -= a.ring;
+          const int cl = pos / a.cls, j = pos - cl * a.cls;
+          tma_load_3d(a_raw(s, q) + r * 128, &tmap, &full_a[4 * s + q], tc.p0 + 32 * q,
+                      __ldg(a.class_d + cl), tc.n * a.rows_per_sample_3d + j);
+        }
+      }
+      if (++it_c == (nk8 + 3) / 4) {
+        it_c = 0;
+        it_t += gridDim.x;
+      }
+    };
+    for (int s = 0; s < S; ++s) issue_next(s);
     int stage = 0;
     uint32_t phase = 0;
     for (int64_t t = blockIdx.x; t < total; t += gridDim.x) {
@@ -236,9 +271,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       const int nk8 = a.rt_info[4 * rt + 1];
       const int nch = (nk8 + 3) / 4;
       for (int c = 0; c < nch; ++c) {
-        mbar_wait(&full[stage], phase);
-        if (t == blockIdx.x && c == 0 && threadIdx.x == 64) TRACE(4);
-        const float* src = reinterpret_cast<const float*>(a_raw(stage)) + q * (KC * 32) + lane;
+        mbar_wait_tag(&full_a[4 * stage + q], phase, 5);
+        if (t == blockIdx.x && c == 0 && q == 0 && lane == 0) TRACE(4);
+        const float* src = reinterpret_cast<const float*>(a_raw(stage, q)) + lane;
         uint32_t hi[KC], lo[KC];
 #pragma unroll
         for (int k = 0; k < KC; ++k) {
@@ -247,38 +282,41 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           hi[k] = __float_as_uint(h);
           lo[k] = __float_as_uint(v - h);
         }
+        __syncwarp();
+        // smem slot consumed: refill it for the chunk S ahead.
+        issue_next(stage);
+        // TMEM stage is free once the MMAs of the chunk S back are done.
+        mbar_wait_tag(&empty[stage], phase ^ 1u, 6);
+        tc_fence_after();
         const uint32_t col = tmem + C::kACol0 + stage * 2 * KC + lane_base;
         tmem_st32(col, hi);
         tmem_st32(col + KC, lo);
         tmem_st_wait();
         tc_fence_before();
-        mbar_arrive(&conv[stage]);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&conv[stage]);
         advance(stage, phase, S);
       }
     }
   } else {
     // ---------------- epilogue ----------------
-    // Per tile: the row -> channel map and the bias of each row go to shared
-    // memory once (named barrier over the 4 epilogue warps), then TMEM is
-    // drained 32 columns at a time; each column store is 32 consecutive
-    // pixels of one NCHW channel row (128 B, coalesced).
-    const int et = threadIdx.x - 192;  // 0..127
-    const int quarter = warp & 3;      // TMEM lane quarter this warp may access
-    const int prow = quarter * 32 + lane;
-    // Typed __shared__ tables: LDS, not generic loads that would have to be
-    // ordered behind the preceding global stores.
+    // Warp q drains TMEM lanes 32q..32q+31 (its pixel quarter) 32 columns at a
+    // time, adds the bias and either stages a [32 rows][32 px] block in smem
+    // for one TMA store, or (ragged rows / no contiguous output view) stores
+    // each channel row directly (128 B per warp store).
     __shared__ int32_t row_s[NT];
     __shared__ float bias_s[NT];
+    const int et = threadIdx.x - 192;  // 0..127
+    const int q = warp & 3;
     int acc = 0;
     uint32_t acc_phase = 0;
     int cur_rt = -1;
+    int sbuf = 0;
     for (int64_t t = blockIdx.x; t < total; t += gridDim.x) {
-      const int rt = static_cast<int>(t % a.n_rt);
-      const int64_t pt = t / a.n_rt;
-      const int64_t n = pt / a.ptiles;
-      const int64_t p = static_cast<int64_t>(pt - n * a.ptiles) * TM + prow;
+      const TileCoord tc = tile_coord(a, t);
+      const int rt = tc.rt;
       if (rt != cur_rt) {
-        named_bar_sync(1, 128);  // previous tile finished reading the tables
+        named_bar_sync(1, 128);
         for (int i = et; i < NT; i += 128) {
           const int row = __ldg(a.rows + rt * NT + i);
           row_s[i] = row;
@@ -287,50 +325,50 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         named_bar_sync(1, 128);
         cur_rt = rt;
       }
-      mbar_wait(&tfull[acc], acc_phase);
+      mbar_wait_tag(&tfull[acc], acc_phase, 7);
       tc_fence_after();
+      const int64_t p = tc.p0 + q * 32 + lane;
       const bool pv = p < a.plane;
-      float* __restrict__ obase = a.out + n * a.c_out_t * a.plane + p;
-      const uint32_t taddr = tmem + acc * C::kAccCols + (static_cast<uint32_t>(quarter * 32) << 16);
+      const uint32_t taddr = tmem + acc * C::kAccCols + (static_cast<uint32_t>(q * 32) << 16);
 #pragma unroll 1
       for (int c0 = 0; c0 < NT; c0 += 32) {
         uint32_t v[32];
-        int32_t rr[32];
-        float bb[32];
         tmem_ld32_nowait(taddr + c0, v);
+        float bb[32];
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          rr[j] = row_s[c0 + j];
-          bb[j] = bias_s[c0 + j];
-        }
+        for (int j = 0; j < 32; ++j) bb[j] = bias_s[c0 + j];
+        const int g0 = rt * NT + c0;  // first tile row of this group
+        const bool tma_group = a.store_ok && g0 + 32 <= a.rows_total;
         tmem_ld_wait();
-#if defined(SCC_EXP_NOSTORE)
-        float acc_s = 0.f;
+        if (tma_group) {
+          float* buf = reinterpret_cast<float*>(store_buf + (q * 2 + sbuf) * 4096);
+          if (lane == 0) bulk_wait_read<1>();  // this buffer's previous store has read it
+          __syncwarp();
 #pragma unroll
-        for (int j = 0; j < 32; ++j) acc_s += __uint_as_float(v[j]) + bb[j] * rr[j];
-        if (acc_s == 123.456f) obase[0] = acc_s;
-#elif defined(SCC_EXP_VEC4)
-        // same byte volume, float4 stores along pixels (results wrong on purpose)
-        if (pv) {
-#pragma unroll
-          for (int j = 0; j < 32; j += 4) {
-            if (rr[j] >= 0) {
-              float4* dst = reinterpret_cast<float4*>(a.out + n * a.c_out_t * a.plane + static_cast<int64_t>(rr[j + (lane & 3)]) * a.plane + (p - prow) + (lane >> 2) * 4 + quarter * 32);
-              *dst = make_float4(__uint_as_float(v[j]), __uint_as_float(v[j + 1]), __uint_as_float(v[j + 2]), __uint_as_float(v[j + 3]));
-            }
+          for (int j = 0; j < 32; ++j) buf[j * 32 + lane] = __uint_as_float(v[j]) + bb[j];
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            const int cl = g0 / a.out_cls, jj = g0 - cl * a.out_cls;
+            tma_store_3d(&tout, buf, tc.p0 + 32 * q, __ldg(a.out_class_d + cl),
+                         tc.n * a.out_cls + jj);
+            bulk_commit();
           }
-        }
-#else
-        if (pv) {
+          sbuf ^= 1;
+        } else if (pv) {
+          float* __restrict__ obase = a.out + static_cast<int64_t>(tc.n) * a.c_out_t * a.plane + p;
+          int32_t rr[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) rr[j] = row_s[c0 + j];
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
             if (rr[j] >= 0) obase[static_cast<int64_t>(rr[j]) * a.plane] = __uint_as_float(v[j]) + bb[j];
           }
         }
-#endif
       }
       tc_fence_before();
-      mbar_arrive(&tempty[acc]);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
       {
         const int64_t ti = (t - blockIdx.x) / gridDim.x;
         if (ti < 8 && et == 0) TRACE(7 + 2 * ti);
@@ -340,6 +378,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         acc_phase ^= 1u;
       }
     }
+    if (lane == 0) bulk_wait<0>();
   }
   tc_fence_before();
   __syncthreads();
@@ -431,27 +470,46 @@ static cudaError_t launch_tc_nt(const TcBandPlan& tp, const TcDeviceTables& dt,
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
 
-  // --- activations tensor map: {P, D, N * rows_per_sample} fp32, no swizzle, box {32, 1, 8}
-  CUtensorMap tm;
-  const uint64_t dims[3] = {static_cast<uint64_t>(call.plane), static_cast<uint64_t>(tp.n_class),
-                            static_cast<uint64_t>(call.n) * tp.rows_per_sample_3d};
-  const uint64_t strides[2] = {static_cast<uint64_t>(call.plane) * 4,
-                               static_cast<uint64_t>(call.plane) * 4 * tp.n_class};
-  const uint32_t box[3] = {32, 1, 8};
-  if (!encode_f32(&tm, call.in, 3, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_NONE))
-    return cudaErrorInvalidValue;
+  // --- activations: {P, D, N * rows_per_sample} fp32, no swizzle, box {32, 1, rb}
+  CUtensorMap tm, tout;
+  {
+    const uint64_t dims[3] = {static_cast<uint64_t>(call.plane), static_cast<uint64_t>(tp.n_class),
+                              static_cast<uint64_t>(call.n) * tp.rows_per_sample_3d};
+    const uint64_t strides[2] = {static_cast<uint64_t>(call.plane) * 4,
+                                 static_cast<uint64_t>(call.plane) * 4 * tp.n_class};
+    const uint32_t box[3] = {32, 1, static_cast<uint32_t>(tp.rb)};
+    if (!encode_f32(&tm, call.in, 3, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_NONE))
+      return cudaErrorInvalidValue;
+  }
+  // --- output view for TMA stores: {P, D_out, N * out_cls}, box {32, 1, 32}
+  {
+    const int32_t ocls = tp.store_ok ? tp.out_cls : call.c_out_t;
+    const int32_t ond = tp.store_ok ? tp.out_n_class : 1;
+    const uint64_t dims[3] = {static_cast<uint64_t>(call.plane), static_cast<uint64_t>(ond),
+                              static_cast<uint64_t>(call.n) * ocls};
+    const uint64_t strides[2] = {static_cast<uint64_t>(call.plane) * 4,
+                                 static_cast<uint64_t>(call.plane) * 4 * ond};
+    const uint32_t box[3] = {32, 1, 32};
+    if (!encode_f32(&tout, call.out, 3, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_NONE))
+      return cudaErrorInvalidValue;
+  }
 
   TcBandArgs ka{};
   ka.panel = panel;
   ka.rt_info = dt.rt_info;
   ka.rows = dt.rows;
   ka.class_d = dt.class_d;
+  ka.out_class_d = dt.out_class_d;
   ka.bias = call.bias;
   ka.out = call.out;
   ka.n_rt = tp.n_rt;
   ka.ring = tp.ring;
   ka.cls = tp.cls;
+  ka.rb = tp.rb;
   ka.c_out_t = call.c_out_t;
+  ka.rows_total = call.c_out_t;
+  ka.out_cls = tp.out_cls;
+  ka.store_ok = tp.store_ok && call.plane % 4 == 0;
   ka.rows_per_sample_3d = tp.rows_per_sample_3d;
   ka.ptiles = static_cast<int32_t>((call.plane + TM - 1) / TM);
   ka.plane = call.plane;
@@ -484,10 +542,19 @@ static cudaError_t launch_tc_nt(const TcBandPlan& tp, const TcDeviceTables& dt,
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  e = cudaLaunchKernelEx(&cfg, tc_band_kernel<NT>, tm, ka);
+  e = cudaLaunchKernelEx(&cfg, tc_band_kernel<NT>, tm, tout, ka);
   if (e != cudaSuccess) return e;
   note_launches(2);
   return cudaSuccess;
+}
+
+int tc_hang(unsigned int* out) {
+#if defined(SCC_WATCHDOG)
+  return cudaMemcpyFromSymbol(out, sm100::g_hang, 64 * sizeof(unsigned int)) == cudaSuccess ? 64 : -1;
+#else
+  (void)out;
+  return 0;
+#endif
 }
 
 int tc_trace(unsigned long long* out, int n) {

@@ -26,6 +26,15 @@ namespace {
 
 using namespace sm100;
 
+// Diagnostic timeline (CTA 0, ns): 0 start, 1 setup, 2+i refill of chunk
+// i issued (i<8), 10+i converter done with chunk i, 18+i MMA committed chunk
+// i, 26 epilogue done.
+__device__ unsigned long long g_wtrace[32];
+#define WTRACE(slot)                                            \
+  do {                                                          \
+    if (blockIdx.x == 0) g_wtrace[(slot)] = globaltimer();      \
+  } while (0)
+
 constexpr int kThreads = 320;
 constexpr int kPix = 32;             // pixels (K) per stage
 constexpr int kABytes = 128 * kPix * 4;  // 16 KB: 128 filter rows x 32 pixels
@@ -37,6 +46,7 @@ struct WArgs {
   float* part;             // [split][rt][nc][128][nw]
   float* pbias;            // [split][rt][128]
   int32_t n_rt, n_nc, nw, cls, c_in, c_out, stages;
+  int32_t rba, rbb;        // TMA box rows (dy per quarter, x)
   int32_t has_bias;
   int64_t pcs;             // pixel chunks per sample
   int64_t total_chunks, chunks_per_split;
@@ -59,11 +69,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int bbytes = a.nw * kPix * 4;
   const int stage_bytes = 2 * kABytes + 2 * bbytes;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S * stage_bytes);
-  uint64_t* full = bars;
-  uint64_t* conv = bars + kMaxStages;
-  uint64_t* empty = bars + 2 * kMaxStages;
-  uint64_t* tfull = bars + 3 * kMaxStages;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * kMaxStages + 1);
+  uint64_t* full = bars;                       // [kMaxStages][4] one per loader warp
+  uint64_t* conv = bars + 4 * kMaxStages;      // [kMaxStages] 4 warp arrivals
+  uint64_t* empty = bars + 5 * kMaxStages;     // [kMaxStages] MMA done with the stage
+  uint64_t* tfull = bars + 6 * kMaxStages;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 6 * kMaxStages + 1);
   auto a_hi = [&](int s) { return smem + s * stage_bytes; };
   auto a_lo = [&](int s) { return smem + s * stage_bytes + kABytes; };
   auto b_hi = [&](int s) { return smem + s * stage_bytes + 2 * kABytes; };
@@ -81,15 +91,16 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t warp = warp_id();
   const int lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
+    WTRACE(0);
     for (int s = 0; s < S; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&conv[s], 128);
+      for (int q = 0; q < 4; ++q) mbar_init(&full[4 * s + q], 1);
+      mbar_init(&conv[s], 4);
       mbar_init(&empty[s], 1);
     }
     mbar_init(tfull, 1);
     fence_mbar_init();
   }
-  if (warp == 0 && lane == 0) {
+  if (warp == 2 && lane == 0) {
     prefetch_tmap(&tdy);
     prefetch_tmap(&tx);
   }
@@ -98,45 +109,17 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  if (threadIdx.x == 0) WTRACE(1);
 
   if (warp == 0) {
-    // ---------------- producer ----------------
-    if (elect_one()) {
-      int stage = 0;
-      uint32_t phase = 0;
-      // Rows/columns that exist (padding rows are simply not loaded).
-      int a_boxes = 0, b_boxes = 0;
-      for (int g = 0; g < 16; ++g) a_boxes += (rt * 128 + 8 * g < a.c_out) ? 1 : 0;
-      for (int h = 0; h < a.nw / 8; ++h) b_boxes += (nc * a.nw + 8 * h < ncols) ? 1 : 0;
-      for (int64_t q = q_begin; q < q_end; ++q) {
-        const int n = static_cast<int>(q / a.pcs);
-        const int p0 = static_cast<int>(q - static_cast<int64_t>(n) * a.pcs) * kPix;
-        mbar_wait(&empty[stage], phase ^ 1u);
-        mbar_expect_tx(&full[stage], (a_boxes + b_boxes) * 1024);
-        for (int g = 0; g < 16; ++g) {
-          const int i0 = rt * 128 + 8 * g;
-          if (i0 >= a.c_out) break;
-          const int cl = i0 / a.cls, j = i0 - cl * a.cls;
-          tma_load_3d(a_hi(stage) + g * 1024, &tdy, &full[stage], p0, __ldg(a.class_d + cl),
-                      n * a.cls + j);
-        }
-        for (int h = 0; h < a.nw / 8; ++h) {
-          const int col = nc * a.nw + 8 * h;
-          if (col >= ncols) break;
-          int pos = start8 + col;
-          while (pos >= a.c_in) pos -= a.c_in;
-          tma_load_3d(b_hi(stage) + h * 1024, &tx, &full[stage], p0, 0, n * a.c_in + pos);
-        }
-        advance(stage, phase, S);
-      }
-    }
+    // (loads are issued by the four converter warps, see below)
   } else if (warp == 1) {
     // ---------------- MMA issuer ----------------
     const uint32_t idesc = idesc_tf32(128, a.nw, 0, 0);
     int stage = 0;
     uint32_t phase = 0;
     for (int c = 0; c < nchunks; ++c) {
-      mbar_wait(&conv[stage], phase);
+      mbar_wait_tag(&conv[stage], phase, 10);
       tc_fence_after();
       if (elect_one()) {
         const uint32_t ah = smem_u32(a_hi(stage)), al = smem_u32(a_lo(stage));
@@ -153,19 +136,53 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         mma_commit(&empty[stage]);
         if (c == nchunks - 1) mma_commit(tfull);
+        if (c < 8) WTRACE(18 + c);
       }
       __syncwarp();
       advance(stage, phase, S);
     }
   } else if (warp < 6) {
-    // ---------------- converters (+ bias row sums) ----------------
-    const int t = threadIdx.x - 64;  // 0..127 = filter row of the tile
+    // ---------------- loaders + converters (+ bias row sums) ----------------
+    // Warp q loads and converts filter rows 32q..32q+31 of the tile and x
+    // rows [q*nw/4, (q+1)*nw/4) of the column chunk: the TMA issue cost is
+    // spread over four warps and nobody waits for another warp's loads.
+    const int q = warp & 3;
+    const int t = q * 32 + lane;  // filter row of the tile owned by this thread
+    const int bq = a.nw / 4;      // x rows per warp
     float bsum = 0.f;
+    int a_rows = 0, b_rows = 0;
+    {
+      const int i0 = rt * 128 + 32 * q;
+      a_rows = min(32, max(0, a.c_out - i0));
+      const int r0 = nc * a.nw + q * bq;
+      b_rows = min(bq, max(0, ncols - r0));
+      a_rows = (a_rows + a.rba - 1) / a.rba * a.rba;  // boxes are issued whole
+      b_rows = (b_rows + a.rbb - 1) / a.rbb * a.rbb;
+    }
+    auto issue = [&](int s, int64_t qc) {
+      if (lane != 0) return;
+      const int n = static_cast<int>(qc / a.pcs);
+      const int p0 = static_cast<int>(qc - static_cast<int64_t>(n) * a.pcs) * kPix;
+      mbar_expect_tx(&full[4 * s + q], (a_rows + b_rows) * 128);
+      for (int r = 0; r < a_rows; r += a.rba) {
+        const int i0 = rt * 128 + 32 * q + r;
+        const int cl = i0 / a.cls, j = i0 - cl * a.cls;
+        tma_load_3d(a_hi(s) + (32 * q + r) * 128, &tdy, &full[4 * s + q], p0, __ldg(a.class_d + cl),
+                    n * a.cls + j);
+      }
+      for (int r = 0; r < b_rows; r += a.rbb) {
+        int pos = start8 + nc * a.nw + q * bq + r;
+        while (pos >= a.c_in) pos -= a.c_in;
+        tma_load_3d(b_hi(s) + (q * bq + r) * 128, &tx, &full[4 * s + q], p0, 0, n * a.c_in + pos);
+      }
+    };
+    for (int c = 0; c < min(S, nchunks); ++c) issue(c, q_begin + c);
     int stage = 0;
     uint32_t phase = 0;
-    const int bvec = a.nw * kPix / 4;  // float4 per B buffer
+    int prev_stage = 0;
+    uint32_t prev_phase = 0;
     for (int c = 0; c < nchunks; ++c) {
-      mbar_wait(&full[stage], phase);
+      mbar_wait_tag(&full[4 * stage + q], phase, 11);
       {
         // row t occupies the 128 B at (t/8)*1024 + (t%8)*128 (16 B chunks swizzled)
         const float4* src = reinterpret_cast<const float4*>(a_hi(stage) + (t >> 3) * 1024 + (t & 7) * 128);
@@ -183,9 +200,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
       {
-        const float4* src = reinterpret_cast<const float4*>(b_hi(stage));
-        float4* dst = reinterpret_cast<float4*>(b_lo(stage));
-        for (int i = t; i < bvec; i += 128) {
+        const float4* src = reinterpret_cast<const float4*>(b_hi(stage) + q * bq * 128);
+        float4* dst = reinterpret_cast<float4*>(b_lo(stage) + q * bq * 128);
+        for (int i = lane; i < bq * 8; i += 32) {
           const float4 v = src[i];
           float4 lo;
           lo.x = v.x - tf32_hi(v.x);
@@ -196,7 +213,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
       fence_proxy_async_smem();
-      mbar_arrive(&conv[stage]);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&conv[stage]);
+      if (c < 8 && t == 0) WTRACE(10 + c);
+      // Refill the previous stage once the MMAs of its chunk are done.
+      if (c >= 1 && c - 1 + S < nchunks) {
+        mbar_wait_tag(&empty[prev_stage], prev_phase, 12);
+        issue(prev_stage, q_begin + c - 1 + S);
+        if (c - 1 < 8 && t == 0) WTRACE(2 + (c - 1));
+      }
+      prev_stage = stage;
+      prev_phase = phase;
       advance(stage, phase, S);
     }
     if (a.has_bias && nc == 0) {
@@ -209,7 +236,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     float* dst = a.part + ((static_cast<int64_t>(split) * a.n_rt + rt) * a.n_nc + nc) * 128 * a.nw +
                  static_cast<int64_t>(row) * a.nw;
     if (nchunks > 0) {
-      mbar_wait(tfull, 0);
+      mbar_wait_tag(tfull, 0, 13);
       tc_fence_after();
       const uint32_t taddr = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
       for (int c0 = 0; c0 < a.nw; c0 += 16) {
@@ -223,6 +250,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     } else {
       for (int c0 = 0; c0 < a.nw; c0 += 4) *reinterpret_cast<float4*>(dst + c0) = make_float4(0.f, 0.f, 0.f, 0.f);
     }
+    if (row == 0) WTRACE(26);
   }
   tc_fence_before();
   __syncthreads();
@@ -300,6 +328,11 @@ WGrid weight_grid(const TcWeightPlan& tw, int64_t n, int64_t plane) {
 
 }  // namespace
 
+int tc_wtrace(unsigned long long* out, int n) {
+  if (n > 32) n = 32;
+  return cudaMemcpyFromSymbol(out, g_wtrace, n * sizeof(unsigned long long)) == cudaSuccess ? n : -1;
+}
+
 bool tc_weight_supported(const TcWeightPlan& tw, int64_t plane) {
   return tw.ok && plane % 4 == 0;
 }
@@ -322,7 +355,7 @@ cudaError_t launch_weight_tc(const TcWeightPlan& tw, const TcWeightCall& call, c
                               static_cast<uint64_t>(call.n) * tw.cls};
     const uint64_t strides[2] = {static_cast<uint64_t>(call.plane) * 4,
                                  static_cast<uint64_t>(call.plane) * 4 * tw.n_class};
-    const uint32_t box[3] = {kPix, 1, 8};
+    const uint32_t box[3] = {kPix, 1, static_cast<uint32_t>(tw.rba)};
     if (!encode_f32_sw128(&tdy, call.dy, 3, dims, strides, box)) return cudaErrorInvalidValue;
   }
   {
@@ -330,7 +363,7 @@ cudaError_t launch_weight_tc(const TcWeightPlan& tw, const TcWeightCall& call, c
                               static_cast<uint64_t>(call.n) * call.c_in};
     const uint64_t strides[2] = {static_cast<uint64_t>(call.plane) * 4,
                                  static_cast<uint64_t>(call.plane) * 4};
-    const uint32_t box[3] = {kPix, 1, 8};
+    const uint32_t box[3] = {kPix, 1, static_cast<uint32_t>(tw.rbb)};
     if (!encode_f32_sw128(&tx, call.x, 3, dims, strides, box)) return cudaErrorInvalidValue;
   }
   WArgs a{};
@@ -345,6 +378,8 @@ cudaError_t launch_weight_tc(const TcWeightPlan& tw, const TcWeightCall& call, c
   a.c_in = call.c_in;
   a.c_out = call.c_out;
   a.stages = g.stages;
+  a.rba = tw.rba;
+  a.rbb = tw.rbb;
   a.has_bias = call.dbias != nullptr;
   a.pcs = g.pcs;
   a.total_chunks = g.total_chunks;

@@ -34,3 +34,16 @@ for name, f in (("fwd", fwd), ("bwd_data", bwdd)):
     lab = {0:"start",1:"setup",2:"prod_first_tma",3:"dep_ok",4:"conv_first_full",5:"mma_first_conv",30:"end"}
     for i in range(8): lab[6+2*i] = f"mma_commit_t{i}"; lab[7+2*i] = f"epi_done_t{i}"
     print(name, " ".join(f"{lab[i]}={(buf[i]-t0)/1e3:.2f}" for i in sorted(lab) if buf[i] >= t0 and buf[i]-t0 < 1e9))
+ws = torch.empty(cfg.workspace_bytes(32, 32, 32), dtype=torch.uint8, device="cuda")
+dw = torch.empty(128 * 32, device="cuda"); db = torch.empty(128, device="cuda")
+def bwdw(): _lib.check(L.scc_backward_weight_f32(cfg.handle, 32, 32, 32, dy.data_ptr(), x.data_ptr(), dw.data_ptr(), db.data_ptr(), ws.data_ptr(), ws.numel(), s))
+for _ in range(5): bwdw()
+torch.cuda.synchronize()
+e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+e0.record(); [bwdw() for _ in range(50)]; e1.record(); e1.synchronize()
+print(f"bwd_weight events {1e3*e0.elapsed_time(e1)/50:.1f} us/call")
+buf64 = (_C.c_uint64 * 64)()
+L.scc_debug_trace(buf64, 64)
+w = [buf64[32 + i] for i in range(32)]
+t0 = w[0]
+print("wgrad: setup", (w[1]-t0)/1e3, "issue", [round((w[2+i]-t0)/1e3,2) for i in range(8)], "conv", [round((w[10+i]-t0)/1e3,2) for i in range(8)], "mma", [round((w[18+i]-t0)/1e3,2) for i in range(8)], "epi", (w[26]-t0)/1e3)
