@@ -56,15 +56,24 @@ constexpr int kABytes = TM * KC * 4;  // 16 KB per A buffer
 template <int NT>
 struct TcCfg {
   static_assert(NT == 64 || NT == 128, "row tile must be 64 or 128");
-  static constexpr int kBBytes = 2 * NT * KC * 4;        // hi + lo weight image
-  static constexpr int kStageBytes = kABytes + kBBytes;  // raw activations + weights
-  static constexpr int kStages = 3;
-  static constexpr int kAccCols = NT;                    // per accumulator buffer
-  static constexpr int kACol0 = 2 * NT;                  // first TMEM column of A stages
+  static constexpr int kBBytes = 2 * NT * KC * 4;  // hi + lo weight image of one chunk
+  static constexpr int kTStages = NT == 128 ? 3 : 4;  // TMEM A stages
+  static constexpr int kAccCols = NT;               // per accumulator buffer
+  static constexpr int kACol0 = 2 * NT;             // first TMEM column of A stages
   static constexpr int kTmemCols = 512;
-  static_assert(kACol0 + kStages * 2 * KC <= kTmemCols, "TMEM budget");
+  static_assert(kACol0 + kTStages * 2 * KC <= kTmemCols, "TMEM budget");
   static constexpr int kStoreBytes = 4 * 2 * 32 * 32 * 4;  // 4 warps x 2 bufs x [32 rows][32 px]
-  static constexpr int kSmem = kStages * kStageBytes + kStoreBytes + 1024 /*align*/ + 512 /*barriers*/;
+  static constexpr int kMaxAStages = 8;
+  static constexpr int kMaxBStages = 2;
+};
+
+// Shared-memory plan of one launch (host computes, kernel re-derives).
+struct BandSmem {
+  int a_stages;     // raw activation ring depth (16 KB each)
+  int b_resident;   // 1: whole panel in smem, loaded once
+  int b_stages;     // streamed panel ring depth
+  int b_bytes;      // resident panel bytes, or one chunk image
+  int total;        // dynamic smem bytes
 };
 
 struct TcBandArgs {
@@ -85,6 +94,8 @@ struct TcBandArgs {
   int32_t out_cls;           // output view rows per class
   int32_t store_ok;          // TMA-store epilogue usable
   int32_t ptiles;            // pixel tiles per sample
+  int32_t panel_floats;      // whole panel size (resident mode)
+  BandSmem sm;
   int64_t plane;
   int64_t n;
 };
@@ -111,38 +122,52 @@ __device__ __forceinline__ TileCoord tile_coord(const TcBandArgs& a, int64_t t) 
   return c;
 }
 
+__device__ __forceinline__ int chunks_of(const TcBandArgs& a, int rt) {
+  return (a.rt_info[4 * rt + 1] + 3) / 4;
+}
+
 template <int NT>
 __global__ void __launch_bounds__(kTcThreads, 1)
     tc_band_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap tout,
                    const TcBandArgs a) {
   using C = TcCfg<NT>;
-  constexpr int S = C::kStages;
+  constexpr int ST = C::kTStages;
+  const int SA = a.sm.a_stages;
+  const int SB = a.sm.b_stages;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
-  uint8_t* store_buf = smem + S * C::kStageBytes;  // [warp 0..3][2][32 rows][32 px]
+  // [A ring: SA x ([32 rows][128 px] = 16 KB)] [B: resident panel or SB chunk
+  // images] [store staging 32 KB] [barriers]
+  uint8_t* a_ring = smem;
+  uint8_t* b_base = a_ring + SA * kABytes;
+  uint8_t* store_buf = b_base + (a.sm.b_resident ? a.sm.b_bytes : SB * C::kBBytes);
   uint64_t* bars = reinterpret_cast<uint64_t*>(store_buf + C::kStoreBytes);
-  uint64_t* full_a = bars;              // [S][4] activations of one pixel quarter landed
-  uint64_t* full_b = bars + 4 * S;      // [S] weight panel landed
-  uint64_t* conv = bars + 5 * S;        // [S] A hi/lo written to TMEM (4 warp arrivals)
-  uint64_t* empty = bars + 6 * S;       // [S] MMAs done with the stage
-  uint64_t* tfull = bars + 7 * S;       // [2] accumulator ready
-  uint64_t* tempty = bars + 7 * S + 2;  // [2] accumulator drained
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 7 * S + 4);
-
-  // A raw stage: [quarter 0..3][KC ring rows][32 pixels] (4 KB per quarter).
-  auto a_raw = [&](int s, int q) { return smem + s * C::kStageBytes + q * (KC * 128); };
-  auto b_img = [&](int s) { return smem + s * C::kStageBytes + kABytes; };
+  uint64_t* a_full = bars;                              // [8]
+  uint64_t* a_free = bars + C::kMaxAStages;             // [8] 4 converter warps read it
+  uint64_t* b_full = bars + 2 * C::kMaxAStages;         // [2]
+  uint64_t* b_free = b_full + C::kMaxBStages;           // [2]
+  uint64_t* conv = b_free + C::kMaxBStages;             // [ST] TMEM A stage written
+  uint64_t* t_free = conv + ST;                         // [ST] MMAs done with TMEM stage
+  uint64_t* tfull = t_free + ST;                        // [2]
+  uint64_t* tempty = tfull + 2;                         // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const uint32_t warp = warp_id();
   const int lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     TRACE(0);
-    for (int s = 0; s < S; ++s) {
-      for (int q = 0; q < 4; ++q) mbar_init(&full_a[4 * s + q], 1);
-      mbar_init(&full_b[s], 1);
+    for (int s = 0; s < C::kMaxAStages; ++s) {
+      mbar_init(&a_full[s], 1);
+      mbar_init(&a_free[s], 4);
+    }
+    for (int s = 0; s < C::kMaxBStages; ++s) {
+      mbar_init(&b_full[s], 1);
+      mbar_init(&b_free[s], 1);
+    }
+    for (int s = 0; s < ST; ++s) {
       mbar_init(&conv[s], 4);
-      mbar_init(&empty[s], 1);
+      mbar_init(&t_free[s], 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
@@ -150,7 +175,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     }
     fence_mbar_init();
   }
-  if (warp == 2 && lane == 0) {
+  if (warp == 0 && lane == 0) {
     prefetch_tmap(&tmap);
     prefetch_tmap(&tout);
   }
@@ -164,61 +189,98 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   const int64_t total = a.n * a.ptiles * a.n_rt;
 
   if (warp == 0) {
-    // ---------------- weight-panel producer (one bulk copy per stage) ----------------
+    // ---------------- producer: activation ring (+ streamed weight panel) ----------------
     if (elect_one()) {
-      // The panel comes from the preceding panel-build kernel (programmatic
-      // dependent launch): wait for it once.
-      TRACE(2);
-      cudaGridDependencySynchronize();
-      TRACE(3);
-      int stage = 0;
-      uint32_t phase = 0;
+      int sa = 0;
+      uint32_t pa = 0;
+      int sb = 0;
+      uint32_t pb = 0;
+      bool dep_synced = false;
+      auto panel_ready = [&]() {
+        if (!dep_synced) {
+          TRACE(2);
+          cudaGridDependencySynchronize();  // the panel-build kernel (PDL)
+          TRACE(3);
+          dep_synced = true;
+        }
+      };
       for (int64_t t = blockIdx.x; t < total; t += gridDim.x) {
-        const int rt = static_cast<int>(t % a.n_rt);
-        const int nk8 = a.rt_info[4 * rt + 1];
-        const float* panel = a.panel + a.rt_info[4 * rt + 2];
+        const TileCoord tc = tile_coord(a, t);
+        const int start8 = a.rt_info[4 * tc.rt], nk8 = a.rt_info[4 * tc.rt + 1];
         const int nch = (nk8 + 3) / 4;
         for (int c = 0; c < nch; ++c) {
-          mbar_wait_tag(&empty[stage], phase ^ 1u, 1);
-          mbar_expect_tx(&full_b[stage], C::kBBytes);
-          bulk_load(b_img(stage), panel + static_cast<int64_t>(c) * (C::kBBytes / 4), C::kBBytes,
-                    &full_b[stage]);
-          advance(stage, phase, S);
+          // activations: [32 ring rows][128 px], boxes of rb rows
+          mbar_wait_tag(&a_free[sa], pa ^ 1u, 1);
+          const int steps = min(4, nk8 - 4 * c);
+          mbar_expect_tx(&a_full[sa], steps * 8 * TM * 4);
+          for (int r = 0; r < steps * 8; r += a.rb) {
+            int pos = start8 + 32 * c + r;
+            while (pos >= a.ring) pos -= a.ring;
+            const int cl = pos / a.cls, j = pos - cl * a.cls;
+            tma_load_3d(a_ring + sa * kABytes + r * (TM * 4), &tmap, &a_full[sa], tc.p0,
+                        __ldg(a.class_d + cl), tc.n * a.rows_per_sample_3d + j);
+          }
+          advance(sa, pa, SA);
+          if (a.sm.b_resident) {
+            if (t == blockIdx.x && c == 0) {
+              panel_ready();
+              mbar_expect_tx(&b_full[0], a.panel_floats * 4);
+              bulk_load(b_base, a.panel, a.panel_floats * 4, &b_full[0]);
+            }
+          } else {
+            panel_ready();
+            mbar_wait_tag(&b_free[sb], pb ^ 1u, 2);
+            mbar_expect_tx(&b_full[sb], C::kBBytes);
+            bulk_load(b_base + sb * C::kBBytes,
+                      a.panel + a.rt_info[4 * tc.rt + 2] + static_cast<int64_t>(c) * (C::kBBytes / 4),
+                      C::kBBytes, &b_full[sb]);
+            advance(sb, pb, SB);
+          }
         }
       }
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer (A from TMEM, B from SMEM) ----------------
     constexpr uint32_t idesc = idesc_tf32(TM, NT, 0, 0);
-    int stage = 0;
-    uint32_t phase = 0;
+    int st = 0;
+    uint32_t ps = 0;
+    int sb = 0;
+    uint32_t pb = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
+    if (a.sm.b_resident) mbar_wait_tag(&b_full[0], 0, 3);
     for (int64_t t = blockIdx.x; t < total; t += gridDim.x) {
       const int rt = static_cast<int>(t % a.n_rt);
       const int nk8 = a.rt_info[4 * rt + 1];
       const int nch = (nk8 + 3) / 4;
-      mbar_wait_tag(&tempty[acc], acc_phase ^ 1u, 2);
+      mbar_wait_tag(&tempty[acc], acc_phase ^ 1u, 4);
       tc_fence_after();
       const uint32_t d_tmem = tmem + acc * C::kAccCols;
       for (int c = 0; c < nch; ++c) {
-        mbar_wait_tag(&conv[stage], phase, 3);
-        mbar_wait_tag(&full_b[stage], phase, 4);
+        mbar_wait_tag(&conv[st], ps, 5);
+        uint8_t* bimg;
+        if (a.sm.b_resident) {
+          bimg = b_base + (a.rt_info[4 * rt + 2] + c * (C::kBBytes / 4)) * 4;
+        } else {
+          mbar_wait_tag(&b_full[sb], pb, 6);
+          bimg = b_base + sb * C::kBBytes;
+        }
         tc_fence_after();
         if (t == blockIdx.x && c == 0 && lane == 0) TRACE(5);
         const int steps = min(4, nk8 - 4 * c);
         if (elect_one()) {
-          const uint32_t a_hi = tmem + C::kACol0 + stage * 2 * KC;
+          const uint32_t a_hi = tmem + C::kACol0 + st * 2 * KC;
           const uint32_t a_lo = a_hi + KC;
-          const uint32_t bh = smem_u32(b_img(stage)), bl = bh + NT * KC * 4;
-          for (int st = 0; st < steps; ++st) {
-            const uint64_t dbh = desc_sw128(bh + st * 32, 16, 1024);
-            const uint64_t dbl = desc_sw128(bl + st * 32, 16, 1024);
-            mma_tf32_ts(d_tmem, a_hi + 8 * st, dbh, idesc, (c | st) != 0);
-            mma_tf32_ts(d_tmem, a_lo + 8 * st, dbh, idesc, 1);
-            mma_tf32_ts(d_tmem, a_hi + 8 * st, dbl, idesc, 1);
+          const uint32_t bh = smem_u32(bimg), bl = bh + NT * KC * 4;
+          for (int k = 0; k < steps; ++k) {
+            const uint64_t dbh = desc_sw128(bh + k * 32, 16, 1024);
+            const uint64_t dbl = desc_sw128(bl + k * 32, 16, 1024);
+            mma_tf32_ts(d_tmem, a_hi + 8 * k, dbh, idesc, (c | k) != 0);
+            mma_tf32_ts(d_tmem, a_lo + 8 * k, dbh, idesc, 1);
+            mma_tf32_ts(d_tmem, a_hi + 8 * k, dbl, idesc, 1);
           }
-          mma_commit(&empty[stage]);
+          mma_commit(&t_free[st]);
+          if (!a.sm.b_resident) mma_commit(&b_free[sb]);
           if (c == nch - 1) {
             mma_commit(&tfull[acc]);
             const int64_t ti = (t - blockIdx.x) / gridDim.x;
@@ -226,7 +288,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           }
         }
         __syncwarp();
-        advance(stage, phase, S);
+        advance(st, ps, ST);
+        if (!a.sm.b_resident) advance(sb, pb, SB);
       }
       if (++acc == 2) {
         acc = 0;
@@ -234,68 +297,41 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       }
     }
   } else if (warp < 6) {
-    // ---------------- activation loaders + converters ----------------
-    // Warp q owns pixels 32q..32q+31 of every tile == TMEM lanes 32q..32q+31:
-    // it loads its own [ring rows][32 px] boxes, then transposes them into
-    // TMEM as tf32 hi / lo columns.  Loads run S chunks ahead.
+    // ---------------- converters: smem [k][p] -> TMEM [p][k] hi / lo ----------------
+    // Warp q transposes pixels 32q..32q+31 (TMEM lanes 32q..32q+31).
     const int q = warp & 3;
     const uint32_t lane_base = static_cast<uint32_t>(q * 32) << 16;
-    // Chunk sequence of this CTA, for the look-ahead issue.
-    int64_t it_t = blockIdx.x;  // tile of the next chunk to issue
-    int it_c = 0;               // chunk within that tile
-    auto issue_next = [&](int s) {
-      if (it_t >= total) return;
-      const TileCoord tc = tile_coord(a, it_t);
-      const int start8 = a.rt_info[4 * tc.rt], nk8 = a.rt_info[4 * tc.rt + 1];
-      const int steps = min(4, nk8 - 4 * it_c);
-      if (lane == 0) {
-        mbar_expect_tx(&full_a[4 * s + q], steps * 8 * 128);
-        for (int r = 0; r < steps * 8; r += a.rb) {
-          int pos = start8 + 32 * it_c + r;
-          while (pos >= a.ring) pos -= a.ring;
-          const int cl = pos / a.cls, j = pos - cl * a.cls;
-          tma_load_3d(a_raw(s, q) + r * 128, &tmap, &full_a[4 * s + q], tc.p0 + 32 * q,
-                      __ldg(a.class_d + cl), tc.n * a.rows_per_sample_3d + j);
-        }
-      }
-      if (++it_c == (nk8 + 3) / 4) {
-        it_c = 0;
-        it_t += gridDim.x;
-      }
-    };
-    for (int s = 0; s < S; ++s) issue_next(s);
-    int stage = 0;
-    uint32_t phase = 0;
+    int sa = 0;
+    uint32_t pa = 0;
+    int st = 0;
+    uint32_t ps = 0;
     for (int64_t t = blockIdx.x; t < total; t += gridDim.x) {
-      const int rt = static_cast<int>(t % a.n_rt);
-      const int nk8 = a.rt_info[4 * rt + 1];
-      const int nch = (nk8 + 3) / 4;
+      const int nch = chunks_of(a, static_cast<int>(t % a.n_rt));
       for (int c = 0; c < nch; ++c) {
-        mbar_wait_tag(&full_a[4 * stage + q], phase, 5);
+        mbar_wait_tag(&a_full[sa], pa, 7);
         if (t == blockIdx.x && c == 0 && q == 0 && lane == 0) TRACE(4);
-        const float* src = reinterpret_cast<const float*>(a_raw(stage, q)) + lane;
+        const float* src = reinterpret_cast<const float*>(a_ring + sa * kABytes) + q * 32 + lane;
         uint32_t hi[KC], lo[KC];
 #pragma unroll
         for (int k = 0; k < KC; ++k) {
-          const float v = src[k * 32];
+          const float v = src[k * TM];
           const float h = tf32_hi(v);
           hi[k] = __float_as_uint(h);
           lo[k] = __float_as_uint(v - h);
         }
         __syncwarp();
-        // smem slot consumed: refill it for the chunk S ahead.
-        issue_next(stage);
-        // TMEM stage is free once the MMAs of the chunk S back are done.
-        mbar_wait_tag(&empty[stage], phase ^ 1u, 6);
+        if (lane == 0) mbar_arrive(&a_free[sa]);
+        advance(sa, pa, SA);
+        mbar_wait_tag(&t_free[st], ps ^ 1u, 8);
         tc_fence_after();
-        const uint32_t col = tmem + C::kACol0 + stage * 2 * KC + lane_base;
+        const uint32_t col = tmem + C::kACol0 + st * 2 * KC + lane_base;
         tmem_st32(col, hi);
         tmem_st32(col + KC, lo);
         tmem_st_wait();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&conv[stage]);
-        advance(stage, phase, S);
+        if (lane == 0) mbar_arrive(&conv[st]);
+        advance(st, ps, ST);
       }
     }
   } else {
@@ -325,7 +361,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         named_bar_sync(1, 128);
         cur_rt = rt;
       }
-      mbar_wait_tag(&tfull[acc], acc_phase, 7);
+      mbar_wait_tag(&tfull[acc], acc_phase, 9);
       tc_fence_after();
       const int64_t p = tc.p0 + q * 32 + lane;
       const bool pv = p < a.plane;
@@ -477,7 +513,7 @@ static cudaError_t launch_tc_nt(const TcBandPlan& tp, const TcDeviceTables& dt,
                               static_cast<uint64_t>(call.n) * tp.rows_per_sample_3d};
     const uint64_t strides[2] = {static_cast<uint64_t>(call.plane) * 4,
                                  static_cast<uint64_t>(call.plane) * 4 * tp.n_class};
-    const uint32_t box[3] = {32, 1, static_cast<uint32_t>(tp.rb)};
+    const uint32_t box[3] = {TM, 1, static_cast<uint32_t>(tp.rb)};
     if (!encode_f32(&tm, call.in, 3, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_NONE))
       return cudaErrorInvalidValue;
   }
@@ -514,6 +550,27 @@ static cudaError_t launch_tc_nt(const TcBandPlan& tp, const TcDeviceTables& dt,
   ka.ptiles = static_cast<int32_t>((call.plane + TM - 1) / TM);
   ka.plane = call.plane;
   ka.n = call.n;
+  // Shared memory: resident weight panel when it fits next to a >= 5-deep
+  // activation ring, else a streamed 2-deep panel ring.
+  {
+    constexpr int kBudget = 227 * 1024 - 1024 /*align*/ - 2048 /*barriers + static*/;
+    const int panel_bytes = static_cast<int>(tc_panel_bytes(tp));
+    BandSmem& sm = ka.sm;
+    const int rest = kBudget - C::kStoreBytes;
+    if (panel_bytes + 5 * kABytes <= rest) {
+      sm.b_resident = 1;
+      sm.b_bytes = panel_bytes;
+      sm.b_stages = 1;
+    } else {
+      sm.b_resident = 0;
+      sm.b_bytes = C::kBBytes;
+      sm.b_stages = C::kMaxBStages;
+    }
+    const int b_total = sm.b_resident ? sm.b_bytes : sm.b_stages * C::kBBytes;
+    sm.a_stages = std::min(C::kMaxAStages, (rest - b_total) / kABytes);
+    sm.total = sm.a_stages * kABytes + b_total + C::kStoreBytes + 1024 + 512;
+  }
+  ka.panel_floats = static_cast<int32_t>(tc_panel_bytes(tp) / 4);
   const int64_t tiles = call.n * ka.ptiles * tp.n_rt;
   int nsm = 148;
   {
@@ -527,7 +584,7 @@ static cudaError_t launch_tc_nt(const TcBandPlan& tp, const TcDeviceTables& dt,
     cudaGetDevice(&dev);
     if (dev < 0 || dev >= 64 || !attr_set[dev]) {
       e = cudaFuncSetAttribute(tc_band_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               C::kSmem);
+                               227 * 1024 - 1024);
       if (e != cudaSuccess) return e;
       if (dev >= 0 && dev < 64) attr_set[dev] = true;
     }
@@ -535,7 +592,7 @@ static cudaError_t launch_tc_nt(const TcBandPlan& tp, const TcDeviceTables& dt,
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(static_cast<unsigned>(std::min<int64_t>(tiles, nsm)));
   cfg.blockDim = dim3(kTcThreads);
-  cfg.dynamicSmemBytes = C::kSmem;
+  cfg.dynamicSmemBytes = ka.sm.total;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;

@@ -4,16 +4,21 @@
 //   dWband[oc, ic] = sum_{n,p} dy[n, oc, p] * x[n, ic, p]      (ic in the arc of oc's tile)
 //   db[oc]         = sum_{n,p} dy[n, oc, p]
 //
-// GEMM with M = 128 filters (cycle-sorted order), N = the tile's input-channel
-// arc (<= 256 columns per chunk), K = pixels.  Both operands are pixel-
-// contiguous, i.e. K-major, so TMA drops them straight into the canonical
-// SWIZZLE_128B layout (box {32 pixels, 8 rows}); converter warps add the tf32
-// "lo" copies (and the bias row sums) in shared memory.  The pixel range is
-// split across CTAs; every CTA writes its fp32 partial tile, and a second
-// kernel reduces the partials in a fixed order (warp per output, fixed lane
-// assignment and shuffle tree) and scatters the band entries into the
-// window-relative [oc][k] layout.  No atomics: results are bitwise
-// reproducible.
+// GEMM with M = 128 filters (cycle-sorted order, TMEM lanes), N = the tile's
+// input-channel arc (<= 256 columns per chunk), K = pixels.  Both operands are
+// pixel-contiguous, i.e. K-major:
+//   * dy goes through a deep shared-memory ring (SWIZZLE_128B boxes, 64 pixels
+//     per stage) into TMEM as tf32 hi/lo columns (TS-mode MMA).  The swizzle
+//     makes the row-per-thread reads bank-conflict free, and the ring slot is
+//     released as soon as it is converted, so loads run far ahead;
+//   * x stays in shared memory in the canonical SWIZZLE_128B K-major layout,
+//     plus a converted lo copy (SS-mode operand).
+// Loaded bytes in flight, not TMA issue slots, bound the kernel, so boxes are
+// as wide as the geometry allows (4-D boxes cover two 32-pixel atoms).
+// The pixel range is split across CTAs; each writes an fp32 partial tile and a
+// second kernel reduces the partials in a fixed order (warp per output, fixed
+// lane assignment and shuffle tree) into the window-relative [oc][k] layout.
+// No atomics: results are bitwise reproducible.
 #include <algorithm>
 
 #include "scc_kernels.hpp"
@@ -26,9 +31,9 @@ namespace {
 
 using namespace sm100;
 
-// Diagnostic timeline (CTA 0, ns): 0 start, 1 setup, 2+i refill of chunk
-// i issued (i<8), 10+i converter done with chunk i, 18+i MMA committed chunk
-// i, 26 epilogue done.
+// Diagnostic timeline (CTA 0, ns): 0 start, 1 setup, 2+i chunk i issued
+// (i<8), 10+i converter done with chunk i, 18+i MMA committed chunk i,
+// 26 epilogue done.
 __device__ unsigned long long g_wtrace[32];
 #define WTRACE(slot)                                            \
   do {                                                          \
@@ -36,20 +41,25 @@ __device__ unsigned long long g_wtrace[32];
   } while (0)
 
 constexpr int kThreads = 320;
-constexpr int kPix = 32;             // pixels (K) per stage
-constexpr int kABytes = 128 * kPix * 4;  // 16 KB: 128 filter rows x 32 pixels
-constexpr int kMaxStages = 4;
+constexpr int kAtom = 32;              // pixels per SWIZZLE_128B atom (128 B)
+constexpr int kMaxA = 8;               // dy ring depth cap
+constexpr int kMaxT = 3;               // TMEM / x stage depth cap
 
 struct WArgs {
   const int32_t* rt_info;  // per row tile: start8, ncols
   const int32_t* class_d;
   float* part;             // [split][rt][nc][128][nw]
   float* pbias;            // [split][rt][128]
-  int32_t n_rt, n_nc, nw, cls, c_in, c_out, stages;
-  int32_t rba, rbb;        // TMA box rows (dy per quarter, x)
+  int32_t n_rt, n_nc, nw, cls, c_in, c_out;
+  int32_t rba, rbb;        // TMA box rows (dy, x)
+  int32_t blk;             // 32-pixel atoms per stage (1 or 2)
+  int32_t a_stages, t_stages;
+  int32_t acol0;           // first TMEM column of the A stages
+  int32_t dy4d;            // dy boxes are 4-D (both atoms in one box)
   int32_t has_bias;
-  int64_t pcs;             // pixel chunks per sample
+  int64_t pcs;             // pixel chunks (of blk atoms) per sample
   int64_t total_chunks, chunks_per_split;
+  int64_t plane;
 };
 
 __device__ __forceinline__ void advance(int& stage, uint32_t& phase, int stages) {
@@ -65,19 +75,20 @@ __global__ void __launch_bounds__(kThreads, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
-  const int S = a.stages;
-  const int bbytes = a.nw * kPix * 4;
-  const int stage_bytes = 2 * kABytes + 2 * bbytes;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S * stage_bytes);
-  uint64_t* full = bars;                       // [kMaxStages][4] one per loader warp
-  uint64_t* conv = bars + 4 * kMaxStages;      // [kMaxStages] 4 warp arrivals
-  uint64_t* empty = bars + 5 * kMaxStages;     // [kMaxStages] MMA done with the stage
-  uint64_t* tfull = bars + 6 * kMaxStages;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 6 * kMaxStages + 1);
-  auto a_hi = [&](int s) { return smem + s * stage_bytes; };
-  auto a_lo = [&](int s) { return smem + s * stage_bytes + kABytes; };
-  auto b_hi = [&](int s) { return smem + s * stage_bytes + 2 * kABytes; };
-  auto b_lo = [&](int s) { return smem + s * stage_bytes + 2 * kABytes + bbytes; };
+  const int SA = a.a_stages, ST = a.t_stages, NB = a.blk;
+  const int a_stage_bytes = 128 * NB * kAtom * 4;     // 128 rows x NB atoms
+  const int b_blk_bytes = a.nw * kAtom * 4;           // one atom of x rows
+  const int b_stage_bytes = 2 * NB * b_blk_bytes;     // raw + lo
+  uint8_t* a_ring = smem;
+  uint8_t* b_ring = a_ring + SA * a_stage_bytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(b_ring + ST * b_stage_bytes);
+  uint64_t* a_full = bars;                 // [kMaxA]
+  uint64_t* a_free = bars + kMaxA;         // [kMaxA] 4 converter warps
+  uint64_t* b_full = bars + 2 * kMaxA;     // [kMaxT]
+  uint64_t* conv = b_full + kMaxT;         // [kMaxT] 4 converter warps
+  uint64_t* t_free = conv + kMaxT;         // [kMaxT] MMA done (TMEM A + x stage)
+  uint64_t* tfull = t_free + kMaxT;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
 
   const int nc = static_cast<int>(blockIdx.x % a.n_nc);
   const int rest = static_cast<int>(blockIdx.x / a.n_nc);
@@ -87,144 +98,186 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int64_t q_end = min(a.total_chunks, q_begin + a.chunks_per_split);
   const int nchunks = q_end > q_begin ? static_cast<int>(q_end - q_begin) : 0;
   const int start8 = a.rt_info[2 * rt], ncols = a.rt_info[2 * rt + 1];
+  const int kpix = NB * kAtom;
 
   const uint32_t warp = warp_id();
   const int lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     WTRACE(0);
-    for (int s = 0; s < S; ++s) {
-      for (int q = 0; q < 4; ++q) mbar_init(&full[4 * s + q], 1);
+    for (int s = 0; s < kMaxA; ++s) {
+      mbar_init(&a_full[s], 1);
+      mbar_init(&a_free[s], 4);
+    }
+    for (int s = 0; s < kMaxT; ++s) {
+      mbar_init(&b_full[s], 1);
       mbar_init(&conv[s], 4);
-      mbar_init(&empty[s], 1);
+      mbar_init(&t_free[s], 1);
     }
     mbar_init(tfull, 1);
     fence_mbar_init();
   }
-  if (warp == 2 && lane == 0) {
+  if (warp == 0 && lane == 0) {
     prefetch_tmap(&tdy);
     prefetch_tmap(&tx);
   }
-  if (warp == 1) tmem_alloc<256>(tmem_slot);
+  if (warp == 1) tmem_alloc<512>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   if (threadIdx.x == 0) WTRACE(1);
 
+  // Row r (0..127) of a dy stage: quarter q = r/32 holds boxes of rba rows,
+  // each box [NB atoms][rba rows][128 B].
+  auto a_row_off = [&](int r, int b) {
+    const int q = r >> 5, l = r & 31;
+    return q * (32 * NB * 128) + (l / a.rba) * (a.rba * NB * 128) + b * (a.rba * 128) +
+           (l % a.rba) * 128;
+  };
+
   if (warp == 0) {
-    // (loads are issued by the four converter warps, see below)
+    // ---------------- producer ----------------
+    if (elect_one()) {
+      int sa = 0, sb = 0;
+      uint32_t pa = 0, pb = 0;
+      const int rows_a = min(128, a.c_out - rt * 128);
+      const int cols_b = min(a.nw, ncols - nc * a.nw);
+      for (int64_t qc = q_begin; qc < q_end; ++qc) {
+        const int n = static_cast<int>(qc / a.pcs);
+        const int p0 = static_cast<int>(qc - static_cast<int64_t>(n) * a.pcs) * kpix;
+        // dy -> ring
+        mbar_wait_tag(&a_free[sa], pa ^ 1u, 20);
+        const int a_boxes_rows = (rows_a + a.rba - 1) / a.rba * a.rba;
+        mbar_expect_tx(&a_full[sa], a_boxes_rows * NB * 128);
+        uint8_t* ad = a_ring + sa * a_stage_bytes;
+        for (int r = 0; r < a_boxes_rows; r += a.rba) {
+          const int i0 = rt * 128 + r;
+          const int cl = i0 / a.cls, j = i0 - cl * a.cls;
+          const int d = __ldg(a.class_d + cl);
+          if (a.dy4d) {
+            tma_load_4d(ad + a_row_off(r, 0), &tdy, &a_full[sa], 0, d, n * a.cls + j, p0 / kAtom);
+          } else {
+            for (int b = 0; b < NB; ++b) {
+              tma_load_3d(ad + a_row_off(r, b), &tdy, &a_full[sa], p0 + b * kAtom, d,
+                          n * a.cls + j);
+            }
+          }
+        }
+        advance(sa, pa, SA);
+        // x -> stage (raw half)
+        mbar_wait_tag(&t_free[sb], pb ^ 1u, 21);
+        const int b_boxes_rows = (cols_b + a.rbb - 1) / a.rbb * a.rbb;
+        mbar_expect_tx(&b_full[sb], b_boxes_rows * NB * 128);
+        uint8_t* bd = b_ring + sb * b_stage_bytes;
+        for (int b = 0; b < NB; ++b) {
+          for (int r = 0; r < b_boxes_rows; r += a.rbb) {
+            int pos = start8 + nc * a.nw + r;
+            while (pos >= a.c_in) pos -= a.c_in;
+            tma_load_3d(bd + b * b_blk_bytes + r * 128, &tx, &b_full[sb], p0 + b * kAtom, 0,
+                        n * a.c_in + pos);
+          }
+        }
+        if (qc - q_begin < 8) WTRACE(2 + (qc - q_begin));
+        advance(sb, pb, ST);
+      }
+    }
   } else if (warp == 1) {
-    // ---------------- MMA issuer ----------------
+    // ---------------- MMA issuer (dy hi/lo from TMEM, x from SMEM) ----------------
     const uint32_t idesc = idesc_tf32(128, a.nw, 0, 0);
-    int stage = 0;
-    uint32_t phase = 0;
+    int st = 0;
+    uint32_t ps = 0;
     for (int c = 0; c < nchunks; ++c) {
-      mbar_wait_tag(&conv[stage], phase, 10);
+      mbar_wait_tag(&conv[st], ps, 22);
       tc_fence_after();
       if (elect_one()) {
-        const uint32_t ah = smem_u32(a_hi(stage)), al = smem_u32(a_lo(stage));
-        const uint32_t bh = smem_u32(b_hi(stage)), bl = smem_u32(b_lo(stage));
-#pragma unroll
-        for (int ks = 0; ks < kPix / 8; ++ks) {
-          const uint64_t dah = desc_sw128(ah + ks * 32, 16, 1024);
-          const uint64_t dal = desc_sw128(al + ks * 32, 16, 1024);
-          const uint64_t dbh = desc_sw128(bh + ks * 32, 16, 1024);
-          const uint64_t dbl = desc_sw128(bl + ks * 32, 16, 1024);
-          mma_tf32(tmem, dah, dbh, idesc, (c | ks) != 0);
-          mma_tf32(tmem, dal, dbh, idesc, 1);
-          mma_tf32(tmem, dah, dbl, idesc, 1);
+        const uint32_t ahi = tmem + a.acol0 + st * (2 * kpix);
+        const uint32_t alo = ahi + kpix;
+        const uint32_t braw = smem_u32(b_ring + st * b_stage_bytes);
+        const uint32_t blo = braw + NB * b_blk_bytes;
+        for (int k = 0; k < kpix / 8; ++k) {
+          const int b = k >> 2, kk = k & 3;
+          const uint64_t dbh = desc_sw128(braw + b * b_blk_bytes + kk * 32, 16, 1024);
+          const uint64_t dbl = desc_sw128(blo + b * b_blk_bytes + kk * 32, 16, 1024);
+          mma_tf32_ts(tmem, ahi + 8 * k, dbh, idesc, (c | k) != 0);
+          mma_tf32_ts(tmem, alo + 8 * k, dbh, idesc, 1);
+          mma_tf32_ts(tmem, ahi + 8 * k, dbl, idesc, 1);
         }
-        mma_commit(&empty[stage]);
+        mma_commit(&t_free[st]);
         if (c == nchunks - 1) mma_commit(tfull);
         if (c < 8) WTRACE(18 + c);
       }
       __syncwarp();
-      advance(stage, phase, S);
+      advance(st, ps, ST);
     }
   } else if (warp < 6) {
-    // ---------------- loaders + converters (+ bias row sums) ----------------
-    // Warp q loads and converts filter rows 32q..32q+31 of the tile and x
-    // rows [q*nw/4, (q+1)*nw/4) of the column chunk: the TMA issue cost is
-    // spread over four warps and nobody waits for another warp's loads.
+    // ---------------- converters (+ bias row sums) ----------------
     const int q = warp & 3;
-    const int t = q * 32 + lane;  // filter row of the tile owned by this thread
-    const int bq = a.nw / 4;      // x rows per warp
+    const int t = q * 32 + lane;  // filter row of the tile == TMEM lane
+    const uint32_t lane_base = static_cast<uint32_t>(q * 32) << 16;
     float bsum = 0.f;
-    int a_rows = 0, b_rows = 0;
-    {
-      const int i0 = rt * 128 + 32 * q;
-      a_rows = min(32, max(0, a.c_out - i0));
-      const int r0 = nc * a.nw + q * bq;
-      b_rows = min(bq, max(0, ncols - r0));
-      a_rows = (a_rows + a.rba - 1) / a.rba * a.rba;  // boxes are issued whole
-      b_rows = (b_rows + a.rbb - 1) / a.rbb * a.rbb;
-    }
-    auto issue = [&](int s, int64_t qc) {
-      if (lane != 0) return;
-      const int n = static_cast<int>(qc / a.pcs);
-      const int p0 = static_cast<int>(qc - static_cast<int64_t>(n) * a.pcs) * kPix;
-      mbar_expect_tx(&full[4 * s + q], (a_rows + b_rows) * 128);
-      for (int r = 0; r < a_rows; r += a.rba) {
-        const int i0 = rt * 128 + 32 * q + r;
-        const int cl = i0 / a.cls, j = i0 - cl * a.cls;
-        tma_load_3d(a_hi(s) + (32 * q + r) * 128, &tdy, &full[4 * s + q], p0, __ldg(a.class_d + cl),
-                    n * a.cls + j);
-      }
-      for (int r = 0; r < b_rows; r += a.rbb) {
-        int pos = start8 + nc * a.nw + q * bq + r;
-        while (pos >= a.c_in) pos -= a.c_in;
-        tma_load_3d(b_hi(s) + (q * bq + r) * 128, &tx, &full[4 * s + q], p0, 0, n * a.c_in + pos);
-      }
-    };
-    for (int c = 0; c < min(S, nchunks); ++c) issue(c, q_begin + c);
-    int stage = 0;
-    uint32_t phase = 0;
-    int prev_stage = 0;
-    uint32_t prev_phase = 0;
+    int sa = 0, st = 0;
+    uint32_t pa = 0, ps = 0;
+    const int bvec_q = NB * b_blk_bytes / 16 / 4;  // float4 of raw x per warp
     for (int c = 0; c < nchunks; ++c) {
-      mbar_wait_tag(&full[4 * stage + q], phase, 11);
-      {
-        // row t occupies the 128 B at (t/8)*1024 + (t%8)*128 (16 B chunks swizzled)
-        const float4* src = reinterpret_cast<const float4*>(a_hi(stage) + (t >> 3) * 1024 + (t & 7) * 128);
-        float4* dst = reinterpret_cast<float4*>(a_lo(stage) + (t >> 3) * 1024 + (t & 7) * 128);
+      mbar_wait_tag(&a_full[sa], pa, 23);
+      const uint8_t* ab = a_ring + sa * a_stage_bytes;
+      uint32_t hi[2][32], lo[2][32];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const float4 v = src[k];
-          float4 lo;
-          lo.x = v.x - tf32_hi(v.x);
-          lo.y = v.y - tf32_hi(v.y);
-          lo.z = v.z - tf32_hi(v.z);
-          lo.w = v.w - tf32_hi(v.w);
-          dst[k] = lo;
-          bsum += ((v.x + v.y) + v.z) + v.w;
+      for (int b = 0; b < 2; ++b) {
+        if (b < NB) {
+          const float4* src = reinterpret_cast<const float4*>(ab + a_row_off(t, b));
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            // 16 B chunk k of the row sits at chunk index (k ^ row%8): undo the
+            // swizzle so columns come out in pixel order.
+            const float4 v = src[k ^ (t & 7)];
+            const float e[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const float h = tf32_hi(e[i]);
+              hi[b][4 * k + i] = __float_as_uint(h);
+              lo[b][4 * k + i] = __float_as_uint(e[i] - h);
+            }
+            bsum += ((v.x + v.y) + v.z) + v.w;
+          }
         }
       }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&a_free[sa]);
+      advance(sa, pa, SA);
+      // x lo for this warp's quarter of the stage, once x has landed (the
+      // producer refilled the stage only after the MMAs of its previous use).
+      mbar_wait_tag(&b_full[st], ps, 24);
       {
-        const float4* src = reinterpret_cast<const float4*>(b_hi(stage) + q * bq * 128);
-        float4* dst = reinterpret_cast<float4*>(b_lo(stage) + q * bq * 128);
-        for (int i = lane; i < bq * 8; i += 32) {
+        uint8_t* bd = b_ring + st * b_stage_bytes;
+        const float4* src = reinterpret_cast<const float4*>(bd) + q * bvec_q;
+        float4* dst = reinterpret_cast<float4*>(bd + NB * b_blk_bytes) + q * bvec_q;
+        for (int i = lane; i < bvec_q; i += 32) {
           const float4 v = src[i];
-          float4 lo;
-          lo.x = v.x - tf32_hi(v.x);
-          lo.y = v.y - tf32_hi(v.y);
-          lo.z = v.z - tf32_hi(v.z);
-          lo.w = v.w - tf32_hi(v.w);
-          dst[i] = lo;
+          float4 l4;
+          l4.x = v.x - tf32_hi(v.x);
+          l4.y = v.y - tf32_hi(v.y);
+          l4.z = v.z - tf32_hi(v.z);
+          l4.w = v.w - tf32_hi(v.w);
+          dst[i] = l4;
         }
       }
       fence_proxy_async_smem();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&conv[stage]);
-      if (c < 8 && t == 0) WTRACE(10 + c);
-      // Refill the previous stage once the MMAs of its chunk are done.
-      if (c >= 1 && c - 1 + S < nchunks) {
-        mbar_wait_tag(&empty[prev_stage], prev_phase, 12);
-        issue(prev_stage, q_begin + c - 1 + S);
-        if (c - 1 < 8 && t == 0) WTRACE(2 + (c - 1));
+      tc_fence_after();
+      const uint32_t col = tmem + a.acol0 + st * (2 * kpix) + lane_base;
+#pragma unroll
+      for (int b = 0; b < 2; ++b) {
+        if (b < NB) {
+          tmem_st32(col + b * kAtom, hi[b]);
+          tmem_st32(col + kpix + b * kAtom, lo[b]);
+        }
       }
-      prev_stage = stage;
-      prev_phase = phase;
-      advance(stage, phase, S);
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&conv[st]);
+      if (c < 8 && t == 0) WTRACE(10 + c);
+      advance(st, ps, ST);
     }
     if (a.has_bias && nc == 0) {
       a.pbias[(static_cast<int64_t>(split) * a.n_rt + rt) * 128 + t] = bsum;
@@ -236,7 +289,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     float* dst = a.part + ((static_cast<int64_t>(split) * a.n_rt + rt) * a.n_nc + nc) * 128 * a.nw +
                  static_cast<int64_t>(row) * a.nw;
     if (nchunks > 0) {
-      mbar_wait_tag(tfull, 0, 13);
+      mbar_wait_tag(tfull, 0, 25);
       tc_fence_after();
       const uint32_t taddr = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
       for (int c0 = 0; c0 < a.nw; c0 += 16) {
@@ -254,7 +307,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 1) tmem_dealloc<256>(tmem);
+  if (warp == 1) tmem_dealloc<512>(tmem);
 }
 
 struct FArgs {
@@ -306,23 +359,29 @@ __global__ void __launch_bounds__(256) tc_weight_finalize(const FArgs a) {
 }
 
 struct WGrid {
+  int blk, a_stages, t_stages, acol0, smem;
   int64_t pcs, total_chunks, chunks_per_split;
-  int32_t splits, stages;
-  int smem;
+  int32_t splits;
 };
 
 WGrid weight_grid(const TcWeightPlan& tw, int64_t n, int64_t plane) {
   WGrid g{};
-  g.pcs = (plane + kPix - 1) / kPix;
+  g.blk = tw.nw <= 128 ? 2 : 1;
+  const int kpix = g.blk * kAtom;
+  g.acol0 = tw.nw <= 128 ? 128 : 256;
+  g.t_stages = std::min(kMaxT, (512 - g.acol0) / (2 * kpix));
+  const int a_stage = 128 * kpix * 4;
+  const int b_stage = 2 * tw.nw * kpix * 4;
+  constexpr int kBudget = 227 * 1024 - 1024 - 1024;
+  g.a_stages = std::min(kMaxA, (kBudget - g.t_stages * b_stage) / a_stage);
+  g.smem = g.a_stages * a_stage + g.t_stages * b_stage + 1024 + 512;
+  g.pcs = (plane + kpix - 1) / kpix;
   g.total_chunks = n * g.pcs;
   const int64_t items = static_cast<int64_t>(tw.n_rt) * tw.n_nc;
   int64_t splits = std::max<int64_t>(1, (148 + items - 1) / items);
   splits = std::min(splits, g.total_chunks);
   g.chunks_per_split = (g.total_chunks + splits - 1) / splits;
   g.splits = static_cast<int32_t>((g.total_chunks + g.chunks_per_split - 1) / g.chunks_per_split);
-  const int stage_bytes = 2 * kABytes + 2 * tw.nw * kPix * 4;
-  g.stages = std::min(kMaxStages, (200 * 1024) / stage_bytes);
-  g.smem = g.stages * stage_bytes + 1024 + 256;
   return g;
 }
 
@@ -345,25 +404,33 @@ size_t tc_weight_workspace_bytes(const TcWeightPlan& tw, int64_t n, int64_t plan
 
 cudaError_t launch_weight_tc(const TcWeightPlan& tw, const TcWeightCall& call, cudaStream_t s) {
   const WGrid g = weight_grid(tw, call.n, call.plane);
+  if (g.a_stages < 2 || g.t_stages < 1) return cudaErrorInvalidValue;
   if (tc_weight_workspace_bytes(tw, call.n, call.plane) > call.workspace_bytes) return cudaErrorInvalidValue;
   float* part = static_cast<float*>(call.workspace);
   float* pbias = part + static_cast<size_t>(g.splits) * tw.n_rt * tw.n_nc * 128 * tw.nw;
 
+  const uint64_t P = static_cast<uint64_t>(call.plane);
   CUtensorMap tdy, tx;
-  {
-    const uint64_t dims[3] = {static_cast<uint64_t>(call.plane), static_cast<uint64_t>(tw.n_class),
+  bool dy4d = false;
+  if (call.plane % kAtom == 0 && g.blk > 1) {
+    // dy as {32 px, D, N*cls rows, P/32 atoms}: one box = [atoms][rows][128 B]
+    const uint64_t dims[4] = {static_cast<uint64_t>(kAtom), static_cast<uint64_t>(tw.n_class),
+                              static_cast<uint64_t>(call.n) * tw.cls, P / kAtom};
+    const uint64_t strides[3] = {P * 4, P * 4 * tw.n_class, kAtom * 4};
+    const uint32_t box[4] = {kAtom, 1, static_cast<uint32_t>(tw.rba), static_cast<uint32_t>(g.blk)};
+    dy4d = encode_f32_sw128(&tdy, call.dy, 4, dims, strides, box);
+  }
+  if (!dy4d) {
+    const uint64_t dims[3] = {P, static_cast<uint64_t>(tw.n_class),
                               static_cast<uint64_t>(call.n) * tw.cls};
-    const uint64_t strides[2] = {static_cast<uint64_t>(call.plane) * 4,
-                                 static_cast<uint64_t>(call.plane) * 4 * tw.n_class};
-    const uint32_t box[3] = {kPix, 1, static_cast<uint32_t>(tw.rba)};
+    const uint64_t strides[2] = {P * 4, P * 4 * tw.n_class};
+    const uint32_t box[3] = {kAtom, 1, static_cast<uint32_t>(tw.rba)};
     if (!encode_f32_sw128(&tdy, call.dy, 3, dims, strides, box)) return cudaErrorInvalidValue;
   }
   {
-    const uint64_t dims[3] = {static_cast<uint64_t>(call.plane), 1,
-                              static_cast<uint64_t>(call.n) * call.c_in};
-    const uint64_t strides[2] = {static_cast<uint64_t>(call.plane) * 4,
-                                 static_cast<uint64_t>(call.plane) * 4};
-    const uint32_t box[3] = {kPix, 1, static_cast<uint32_t>(tw.rbb)};
+    const uint64_t dims[3] = {P, 1, static_cast<uint64_t>(call.n) * call.c_in};
+    const uint64_t strides[2] = {P * 4, P * 4};
+    const uint32_t box[3] = {kAtom, 1, static_cast<uint32_t>(tw.rbb)};
     if (!encode_f32_sw128(&tx, call.x, 3, dims, strides, box)) return cudaErrorInvalidValue;
   }
   WArgs a{};
@@ -377,20 +444,25 @@ cudaError_t launch_weight_tc(const TcWeightPlan& tw, const TcWeightCall& call, c
   a.cls = tw.cls;
   a.c_in = call.c_in;
   a.c_out = call.c_out;
-  a.stages = g.stages;
   a.rba = tw.rba;
   a.rbb = tw.rbb;
+  a.blk = g.blk;
+  a.a_stages = g.a_stages;
+  a.t_stages = g.t_stages;
+  a.acol0 = g.acol0;
+  a.dy4d = dy4d ? 1 : 0;
   a.has_bias = call.dbias != nullptr;
   a.pcs = g.pcs;
   a.total_chunks = g.total_chunks;
   a.chunks_per_split = g.chunks_per_split;
+  a.plane = call.plane;
   {
     static bool attr_set[64] = {false};
     int dev = 0;
     cudaGetDevice(&dev);
     if (dev < 0 || dev >= 64 || !attr_set[dev]) {
       cudaError_t e = cudaFuncSetAttribute(tc_weight_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           227 * 1024);
+                                           227 * 1024 - 1024);
       if (e != cudaSuccess) return e;
       if (dev >= 0 && dev < 64) attr_set[dev] = true;
     }
