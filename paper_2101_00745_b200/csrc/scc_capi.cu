@@ -164,8 +164,10 @@ int32_t choose_path(const Plan& p, int64_t /*n*/, int64_t h, int64_t w, int dir 
   const bool tc_ok = dir == 2 ? tc_weight_supported(p.tc_wgt, h * w)
                               : tc_band_supported(dir == 0 ? p.tc_fwd : p.tc_bwd, h * w);
   if (p.path == SCC_PATH_CUDA_CORE) return SCC_PATH_CUDA_CORE;
-  if (p.path == SCC_PATH_TENSOR) return tc_ok ? SCC_PATH_TENSOR : SCC_PATH_CUDA_CORE;
-  return SCC_PATH_CUDA_CORE;
+  // AUTO: the tensor-core kernels win on every shape they can express
+  // (profiles/README.md); CUDA cores take the rest (ragged planes, rings
+  // that are not multiples of 8, uneven window classes).
+  return tc_ok ? SCC_PATH_TENSOR : SCC_PATH_CUDA_CORE;
 }
 
 float* panel_buffer(Plan& p, int dir, cudaStream_t s) {

@@ -146,7 +146,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int n = static_cast<int>(qc / a.pcs);
         const int p0 = static_cast<int>(qc - static_cast<int64_t>(n) * a.pcs) * kpix;
         // dy -> ring
+        if (qc - q_begin == 1) WTRACE(27);
         mbar_wait_tag(&a_free[sa], pa ^ 1u, 20);
+        if (qc - q_begin == 1) WTRACE(28);
         const int a_boxes_rows = (rows_a + a.rba - 1) / a.rba * a.rba;
         mbar_expect_tx(&a_full[sa], a_boxes_rows * NB * 128);
         uint8_t* ad = a_ring + sa * a_stage_bytes;
@@ -164,8 +166,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
         advance(sa, pa, SA);
+        if (qc - q_begin == 1) WTRACE(29);
         // x -> stage (raw half)
         mbar_wait_tag(&t_free[sb], pb ^ 1u, 21);
+        if (qc - q_begin == 1) WTRACE(30);
         const int b_boxes_rows = (cols_b + a.rbb - 1) / a.rbb * a.rbb;
         mbar_expect_tx(&b_full[sb], b_boxes_rows * NB * 128);
         uint8_t* bd = b_ring + sb * b_stage_bytes;
@@ -178,6 +182,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
         if (qc - q_begin < 8) WTRACE(2 + (qc - q_begin));
+        if (qc - q_begin == 1) WTRACE(31);
         advance(sb, pb, ST);
       }
     }

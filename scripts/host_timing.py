@@ -46,4 +46,4 @@ buf64 = (_C.c_uint64 * 64)()
 L.scc_debug_trace(buf64, 64)
 w = [buf64[32 + i] for i in range(32)]
 t0 = w[0]
-print("wgrad: setup", (w[1]-t0)/1e3, "issue", [round((w[2+i]-t0)/1e3,2) for i in range(8)], "conv", [round((w[10+i]-t0)/1e3,2) for i in range(8)], "mma", [round((w[18+i]-t0)/1e3,2) for i in range(8)], "epi", (w[26]-t0)/1e3)
+print("wgrad: setup", (w[1]-t0)/1e3, "issue", [round((w[2+i]-t0)/1e3,2) for i in range(8)], "conv", [round((w[10+i]-t0)/1e3,2) for i in range(8)], "mma", [round((w[18+i]-t0)/1e3,2) for i in range(8)], "epi", (w[26]-t0)/1e3, "chunk1 prod: start/afree/A/tfree/B", [round((w[i]-t0)/1e3, 2) for i in (27, 28, 29, 30, 31)])
