@@ -57,7 +57,8 @@ typedef enum { SCC_OVERLAP_CHANNELS = 0, SCC_OVERLAP_RATIO = 1 } scc_overlap_kin
 typedef enum {
   SCC_PATH_AUTO = 0,
   SCC_PATH_CUDA_CORE = 1, /* fp32 FFMA banded kernels                */
-  SCC_PATH_TENSOR = 2     /* tcgen05 3xTF32 banded-GEMM kernels       */
+  SCC_PATH_TENSOR = 2,    /* tcgen05 3xTF32 banded-GEMM kernels       */
+  SCC_PATH_TENSOR_V1 = 3  /* diagnostic: generation-1 tensor kernels   */
 } scc_path_t;
 
 typedef struct scc_plan scc_plan_t;

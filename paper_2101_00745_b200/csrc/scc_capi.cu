@@ -127,6 +127,7 @@ const DeviceTables& tables(Plan& p) {
     d.out_class_d = b + o[4];
     d.starts = t.starts;
     d.perm = t.perm;
+    d.inv_perm = t.inv_perm;
   }
   t.tcw_rt_info = b + o_tw[0];
   t.tcw_class_d = b + o_tw[1];
@@ -269,6 +270,11 @@ void do_forward(Plan& p, int64_t n, int64_t h, int64_t w, const float* x, const 
   const DeviceTables& t = tables(p);
   if (choose_path(p, n, h, w, 0) == SCC_PATH_TENSOR) {
     TcBandCall c = tc_call(p, false, n, h * w, x, y, wt, b);
+    if (p.path != SCC_PATH_TENSOR_V1 && tc_band2_supported(p.tc_fwd, h * w, static_cast<int32_t>(p.cfg.c_out))) {
+      cuda_check(launch_band_tc2(p.tc_fwd, t.tc_fwd, c, p.cfg.shift, static_cast<int32_t>(p.cfg.c_out), s),
+                 "forward (tensor) launch");
+      return;
+    }
     c.panel = panel_buffer(p, 0, s);
     cuda_check(launch_band_tc(p.tc_fwd, t.tc_fwd, c, s), "forward (tensor) launch");
     return;
@@ -285,6 +291,11 @@ void do_backward_data(Plan& p, int64_t n, int64_t h, int64_t w, const float* dy,
   const DeviceTables& t = tables(p);
   if (choose_path(p, n, h, w, 1) == SCC_PATH_TENSOR) {
     TcBandCall c = tc_call(p, true, n, h * w, dy, dx, wt, nullptr);
+    if (p.path != SCC_PATH_TENSOR_V1 && tc_band2_supported(p.tc_bwd, h * w, static_cast<int32_t>(p.cfg.c_out))) {
+      cuda_check(launch_band_tc2(p.tc_bwd, t.tc_bwd, c, p.cfg.shift, static_cast<int32_t>(p.cfg.c_out), s),
+                 "backward-data (tensor) launch");
+      return;
+    }
     c.panel = panel_buffer(p, 1, s);
     cuda_check(launch_band_tc(p.tc_bwd, t.tc_bwd, c, s), "backward-data (tensor) launch");
     return;
@@ -418,7 +429,9 @@ int scc_debug_trace(uint64_t* out, int n) {
   unsigned int hang[64];
   if (scc::tc_hang(hang) < 0) return -1;
   for (int i = 0; i < 64; ++i) out[64 + i] = hang[i];  // watchdog builds only
-  return 128;
+  if (n < 192) return 128;
+  // slots [128, 192): generation-2 band kernel
+  return scc::tc2_trace(reinterpret_cast<unsigned long long*>(out) + 128, 64) < 0 ? -1 : 192;
 }
 
 scc_status_t scc_overlap_parse(const char* text, int32_t* kind, double* ratio, int64_t* count) {
@@ -543,7 +556,8 @@ scc_status_t scc_forward_macs(const scc_plan_t* plan, int64_t n, int64_t h, int6
 scc_status_t scc_plan_set_path(scc_plan_t* plan, int32_t path) {
   return guard([&] {
     scc::check_ptr(plan, "plan");
-    if (path != SCC_PATH_AUTO && path != SCC_PATH_CUDA_CORE && path != SCC_PATH_TENSOR) {
+    if (path != SCC_PATH_AUTO && path != SCC_PATH_CUDA_CORE && path != SCC_PATH_TENSOR &&
+        path != SCC_PATH_TENSOR_V1) {
       scc::fail(SCC_ERR_ARGUMENT, "unknown path " + std::to_string(path));
     }
     plan->path = path;

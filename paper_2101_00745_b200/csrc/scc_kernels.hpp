@@ -96,6 +96,11 @@ cudaError_t launch_weight_cc(const WeightLaunch& a, size_t ws_bytes, cudaStream_
 
 // Tensor-core family -----------------------------------------------------------
 bool tc_band_supported(const TcBandPlan& tp, int64_t plane);
+// Generation 2 (scc_tc2.cu): MN-major TMA operands, in-kernel weight panel.
+bool tc_band2_supported(const TcBandPlan& tp, int64_t plane, int32_t c_out);
+cudaError_t launch_band_tc2(const TcBandPlan& tp, const TcDeviceTables& dt, const TcBandCall& call,
+                            int64_t shift, int32_t c_out, cudaStream_t s);
+int tc2_trace(unsigned long long* out, int n);
 cudaError_t launch_band_tc(const TcBandPlan& tp, const TcDeviceTables& dt, const TcBandCall& call,
                            cudaStream_t s);
 

@@ -97,6 +97,7 @@ struct TcDeviceTables {
   const int32_t* starts = nullptr;
   const int32_t* perm = nullptr;
   const int32_t* out_class_d = nullptr;
+  const int32_t* inv_perm = nullptr;
 };
 
 // Device copy of the tables (one per CUDA device).

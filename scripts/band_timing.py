@@ -1,0 +1,53 @@
+"""Per-call device time of forward / backward-data on config 1 for each
+tensor-core generation (CUDA events over a CUDA graph of 20 calls, inputs
+rotated over 8 buffer sets > L2), plus the gen-2 CTA-0 timeline."""
+import ctypes as C, os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+import paper_2101_00745_b200 as scc
+from paper_2101_00745_b200 import _lib
+L = _lib.lib()
+shape = [int(v) for v in (sys.argv[1:7] or ["32", "64", "128", "32", "32", "2"])]
+N, CI, CO, H, W, CG = shape
+cfg = scc.scc_config_new(CI, CO, CG, "50%", True)
+R = 8
+xs = [torch.randn(N, CI, H, W, device="cuda") for _ in range(R)]
+dys = [torch.randn(N, CO, H, W, device="cuda") for _ in range(R)]
+ys = [torch.empty(N, CO, H, W, device="cuda") for _ in range(R)]
+dxs = [torch.empty(N, CI, H, W, device="cuda") for _ in range(R)]
+wts = scc.scc_weights_init(cfg)
+def fwd(i, s):
+    _lib.check(L.scc_forward_f32(cfg.handle, N, H, W, xs[i].data_ptr(), wts.weight.data_ptr(), wts.bias.data_ptr(), ys[i].data_ptr(), s))
+def bwdd(i, s):
+    _lib.check(L.scc_backward_data_f32(cfg.handle, N, H, W, dys[i].data_ptr(), wts.weight.data_ptr(), dxs[i].data_ptr(), s))
+for path, name in ((_lib.SCC_PATH_TENSOR_V1, "gen1"), (_lib.SCC_PATH_TENSOR, "gen2")):
+    cfg.set_path(path)
+    for op, f, nbytes in (("fwd", fwd, 4 * N * H * W * (CI + CO)), ("bwd_data", bwdd, 4 * N * H * W * (CI + CO))):
+        if path == _lib.SCC_PATH_TENSOR_V1 and len(sys.argv) > 7: continue
+        st = torch.cuda.Stream()
+        with torch.cuda.stream(st):
+            for i in range(R): f(i, st.cuda_stream)
+            st.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=st):
+                for k in range(20): f(k % R, st.cuda_stream)
+            g.replay(); st.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            for _ in range(10): g.replay()
+            e1.record(st); e1.synchronize()
+        us = e0.elapsed_time(e1) * 1e3 / 200
+        print(f"{name} {op}: {us:.2f} us/call  {nbytes / us / 1e3:.0f} GB/s", flush=True)
+    if path == _lib.SCC_PATH_TENSOR:
+        for op, f in (("fwd", fwd), ("bwd_data", bwdd)):
+            f(0, torch.cuda.current_stream().cuda_stream); torch.cuda.synchronize()
+            buf = (C.c_uint64 * 192)()
+            n = L.scc_debug_trace(buf, 192)
+            t = [buf[128 + i] for i in range(64)]
+            t0 = t[0]
+            lab = {0: "start", 1: "dep", 2: "tma0", 46: "tma_last", 3: "panel", 4: "tabs", 5: "w", 63: "end", 50: "b_loop0", 51: "b_loop1", 52: "b_fence"}
+            for i in range(8): lab[6 + i] = f"mma{i}"; lab[14 + i] = f"epi{i}"; lab[22 + i] = f"cv{i}s"; lab[30 + i] = f"cv{i}e"
+            for g in range(4): lab[38 + g] = f"eg{g}ld"; lab[42 + g] = f"eg{g}st"
+            print(op, "SM clock MHz (CTA0):", (t[48] - t[47]) * 1e3 / max(t[t[49]] - t[0], 1))
+            t[47] = t[48] = t[49] = 0
+            print(op, " ".join(f"{lab[i]}={(t[i] - t0) / 1e3:.2f}" for i in sorted(lab) if t[i] >= t0 and t[i] - t0 < 1e8))
