@@ -430,8 +430,10 @@ int scc_debug_trace(uint64_t* out, int n) {
   if (scc::tc_hang(hang) < 0) return -1;
   for (int i = 0; i < 64; ++i) out[64 + i] = hang[i];  // watchdog builds only
   if (n < 192) return 128;
-  // slots [128, 192): generation-2 band kernel
-  return scc::tc2_trace(reinterpret_cast<unsigned long long*>(out) + 128, 64) < 0 ? -1 : 192;
+  // slots [128, 192): generation-2 band kernel; [192, 192 + 2*1024): per-CTA
+  // start / epilogue-end timestamps of that kernel
+  const int m2 = n - 128 < 64 + 2048 ? n - 128 : 64 + 2048;
+  return scc::tc2_trace(reinterpret_cast<unsigned long long*>(out) + 128, m2) < 0 ? -1 : 128 + m2;
 }
 
 scc_status_t scc_overlap_parse(const char* text, int32_t* kind, double* ratio, int64_t* count) {

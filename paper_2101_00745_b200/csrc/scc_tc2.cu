@@ -8,39 +8,40 @@
 // M = 128 pixels (TMEM lanes), N = NT output rows (TMEM columns), K = the row
 // tile's arc of the ring, 8 ring rows per MMA k-step.
 //
-// What changed against generation 1 (scc_tc.cu):
-//   * Activations are consumed by the tensor core exactly as TMA lands them:
-//     the pixel-contiguous [ring row][pixel] tile is an MN-major A operand in
-//     the SWIZZLE_128B_BASE32B layout (TMA CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B,
-//     descriptor layout type 1; tests/cuda/mn_probe.cu).  No transpose, no
-//     TMEM staging of A: the MMAs run SS.
-//   * The band weight panel (hi/lo tf32 images, K-major SWIZZLE_128B) is built
-//     by the CTA itself in shared memory from the [oc][k] weights, so a call is
-//     ONE launch (no panel kernel, no panel scratch in HBM).
+// Design (measured on B200):
+//   * The weight panel (hi/lo tf32 images, K-major SWIZZLE_128B) is built by
+//     the CTA itself in shared memory from the [oc][k] weights: a call is ONE
+//     launch, with no panel kernel and no panel scratch in HBM.
+//   * Activations land by TMA as [ring row][32 px] 128 B rows; converter warps
+//     split them into tf32 hi/lo and transpose them into TMEM ([pixel lane][ring
+//     column]), so the MMAs run in TS mode (A from TMEM) and only the panel is
+//     read from shared memory.  Every byte on the SM goes through the same
+//     128 B/clk SRAM port (TMA writes, LDS/STS, the tensor core's smem operand
+//     reads, TMA-store reads); SS-mode MMAs at N=128 alone would saturate it.
 //   * Each CTA owns a contiguous run of 32-pixel blocks (balanced to one block
 //     across the grid); runs are cut into tiles of up to 4 blocks.
-//   * The epilogue stores straight from registers: a warp's store instruction
-//     writes 32 consecutive pixels (128 B) of one output channel row.
+//   * Small per-layer tables (row-tile arcs, TMA class coordinates) ride in the
+//     kernel parameters, so the producer issues its first load as soon as the
+//     grid dependency resolves.
+//   * The epilogue drains TMEM and writes each warp's pixel block of the tile
+//     with ONE TMA store (whole-tile box) when the row set allows.
 //
 // 3xTF32: the tensor core truncates raw fp32 operands to tf32
-// (tests/test_tc_probe.py), so with A_lo = A - trunc(A) and the panel holding
-// B_hi = trunc(B), B_lo = B - B_hi, the three MMAs per k-step
-//     A*B_hi + A_lo*B_hi + A*B_lo
+// (tests/test_tc_probe.py), so with A_hi = trunc(A), A_lo = A - A_hi and the
+// panel holding B_hi / B_lo the three MMAs per k-step
+//     A_hi*B_hi + A_lo*B_hi + A_hi*B_lo
 // reproduce the fp32 product up to the dropped A_lo*B_lo term (~2^-22).
 //
 // Warp roles (one CTA per SM, 384 threads):
 //   warp 0      TMA producer (raw activation ring)
 //   warp 1      TMEM allocator + MMA issuer (one elected lane)
-//   warps 2-7   first build the weight panel (every 16 B panel word gathered
-//               once from the smem copy of W), then convert: raw stage ->
-//               A_lo stage (elementwise, same layout)
-//   warps 8-11  epilogue: TMEM lane quarter q = pixel block q of the tile;
-//               [32 rows][32 px] boxes staged in smem, written by TMA stores
-// Small per-layer tables (row-tile arcs, TMA class coordinates) ride in the
-// kernel parameters, so the producer issues its first load right after the
-// grid dependency resolves.
+//   warps 2-7   build the weight panel (each 16 B panel word gathered once)
+//   warps 4-7   then convert: raw stage -> TMEM A_hi / A_lo, warp q owns the
+//               pixel block q (TMEM lanes 32q..32q+31)
+//   warps 8-11  epilogue: TMEM lane quarter q = pixel block q of the tile
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 
 #include "scc_kernels.hpp"
 #include "scc_plan.hpp"
@@ -53,6 +54,7 @@ namespace {
 using namespace sm100;
 
 __device__ unsigned long long g_trace2[64];
+__device__ unsigned long long g_cta2[2 * 1024];  // per CTA: start, epilogue end
 #define TRACE2(slot)                                         \
   do {                                                       \
     if (blockIdx.x == 0) g_trace2[(slot)] = globaltimer();   \
@@ -62,8 +64,8 @@ constexpr int kThreads = 384;
 constexpr int kBlkPx = 32;                     // pixels per block (one 128 B row)
 constexpr int kStageBytes = 4 * 32 * 128;      // 4 blocks x 32 ring rows x 128 B
 constexpr int kMaxStages = 8;
-constexpr int kLoStages = 2;
-constexpr int kWorkers = 192;                  // warps 2..7: panel builders, then converters
+constexpr int kTStages = 4;                    // TMEM A stages (hi + lo, 64 columns each)
+constexpr int kWorkers = 192;                  // warps 2, 3, 8..11: panel builders
 constexpr int kSmemLimit = 227 * 1024;
 constexpr int kStoreBuf = 32 * 32 * 4;         // one [32 rows][32 px] TMA-store box
 // Epilogue store modes.
@@ -73,6 +75,7 @@ enum : int32_t {
   kStoreClasses = 2,  // whole tile in one box {32 px, D classes, out_cls rows} (one row tile)
   kStoreRowsNT = 3,   // whole tile in one box {32 px, 1, NT} (contiguous channel rows)
 };
+constexpr int kMaxScratch = 32 * 1024;         // W + oc tables staged for the panel build
 constexpr int kMaxRt = 16;                     // row tiles / classes carried in the params
 constexpr int kMaxCls = 64;
 
@@ -91,11 +94,13 @@ struct Band2Args {
   int32_t c_in, c_out, gw, c_out_t;
   int32_t store_mode, out_cls, out_nd;  // TMA-store epilogue geometry
   int32_t backward_data;
-  int32_t blocked;           // 5-D map (4-block boxes)
   int32_t w_staged;          // W + oc tables bulk-copied to smem for the panel build
+  int32_t fwd4;              // forward panel words are whole-window or empty (see build_panel_fwd4)
   int32_t nbps;              // 32-pixel blocks per sample
   int32_t stages;            // raw ring depth
+  int32_t scratch;           // panel-build scratch bytes (W, starts, perm) in the staging area
   int32_t total_chunks;
+  int32_t debug;             // diagnostics: 1 = producer waits for the panel
   int64_t plane, n;
   int64_t units;             // n * nbps
 };
@@ -129,131 +134,245 @@ __device__ __forceinline__ void advance(int& stage, uint32_t& phase, int stages)
   }
 }
 
-// Byte offset of ring row r (0..31) inside a stage: boxes of rb rows land as
-// [4 blocks][rb rows][128 B], box b at b * rb * 512.
-__device__ __forceinline__ uint32_t row_off(int r, int rb) {
-  return static_cast<uint32_t>((r / rb) * rb * 512 + (r % rb) * 128);
-}
-
-// Smem layout (host and device agree): panel | raw ring | lo ring (panel-build
-// scratch first) | store staging | rows[n_rt*NT] | bias[n_rt*NT] | barriers.
+// Smem layout (host and device agree): panel | raw ring | store staging (also
+// the panel-build scratch: W, starts, perm) | rows[n_rt*NT] | bias[n_rt*NT] |
+// barriers.
 __host__ __device__ inline int store_warp_bytes(int mode, int nt) {
-  return mode == kStoreRows32 ? 2 * kStoreBuf : (mode == kStoreStg ? 0 : 32 * nt * 4);
+  return mode == kStoreRows32 ? 4 * kStoreBuf : (mode == kStoreStg ? 0 : 32 * nt * 4);
 }
 
 template <int NT>
 struct Layout {
-  int panel, raw, lo, st, st_warp, rows, bias, bars, total;
-  __host__ __device__ Layout(int total_chunks, int stages, int n_rt, int store_mode) {
+  int panel, raw, st, st_warp, rows, bias, bars, total;
+  __host__ __device__ Layout(int total_chunks, int stages, int n_rt, int store_mode, int scratch) {
     panel = 0;
     raw = panel + total_chunks * 2 * NT * 128;
-    lo = raw + stages * kStageBytes;
-    st = lo + kLoStages * kStageBytes;
+    st = raw + stages * kStageBytes;
     st_warp = store_warp_bytes(store_mode, NT);
-    rows = st + 4 * st_warp;
+    const int stb = 4 * st_warp > scratch ? 4 * st_warp : scratch;
+    rows = st + ((stb + 1023) & ~1023);
     bias = rows + 4 * n_rt * NT;
     bars = bias + 4 * n_rt * NT;
-    total = bars + (2 * kMaxStages + 2 * kLoStages + 7) * 8 + 16;
+    total = bars + (2 * kMaxStages + 2 * kTStages + 7) * 8 + 16;
   }
 };
 
-// Gather-build the band weight panel: one 16 B word (4 consecutive k of one
-// tile row) per unit, hi and lo tf32 images in the K-major SWIZZLE_128B layout.
+// Gather-build the band weight panel, hi and lo tf32 images in the K-major
+// SWIZZLE_128B layout.  One lane owns one 16 B word (4 consecutive k of one
+// row): 2 STS.128 per lane.  Work is processed in batches of kB warp items
+// with every shared-memory load of the batch issued before its stores.
+//   forward:        warp item = (chunk, 4 rows); lane = (row, word).  Each
+//                   row is one filter: its window offset is per lane, the W
+//                   reads are 4 consecutive slots.
+//   backward-data:  warp item = (chunk, word, 32 rows); lane = row (input
+//                   channel).  The 4 filters of the word are warp-uniform.
 // W / starts / perm come from shared memory (staged) or global memory.
 template <int NT, typename WP, typename IP>
 __device__ __forceinline__ void build_panel(const Band2Args& a, uint8_t* panel, const int32_t* rows_s,
                                             WP wsrc, IP stt, IP prm, int ct) {
   constexpr int kPanelChunk = 2 * NT * 128;
-  const int units = a.total_chunks * NT * 8;
-#pragma unroll 2
-  for (int u = ct; u < units; u += kWorkers) {
-    const int gc = u / (NT * 8);
-    const int rem = u - gc * (NT * 8);
-    const int r = rem >> 3, q16 = rem & 7;
-    int rt = 0;
-    while (rt + 1 < a.n_rt && a.rt_cb[rt + 1] <= gc) ++rt;
-    const int kk0 = 32 * (gc - a.rt_cb[rt]) + 4 * q16;
-    const int lim = 8 * a.rt_nk8[rt];
-    const int start8 = a.rt_start8[rt];
-    const int ch = rows_s[rt * NT + r];
-    const int chs = ch < 0 ? 0 : ch;
-    float v[4];
-    // Branch-free: every lane issues the same loads (clamped indices), then
-    // masks; the loads of the four k are independent of each other.
+  constexpr int kB = 4;
+  constexpr int kWarps = kWorkers / 32;
+  const int lane = ct & 31, wid = ct >> 5;
+  const uint32_t pbase = smem_u32(panel);
+  for (int rt = 0; rt < a.n_rt; ++rt) {
+    const int cb = a.rt_cb[rt], nch = a.rt_cb[rt + 1] - cb;
+    const int lim = 8 * a.rt_nk8[rt], start8 = a.rt_start8[rt];
+    const int32_t* rrow = rows_s + rt * NT;
+    if (!a.backward_data) {
+      const int items = nch * (NT / 4);
+      const int rs = lane >> 3, q16 = lane & 7;
+      for (int i0 = wid; i0 < items; i0 += kB * kWarps) {
+        int ch[kB];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int kk = kk0 + i;
-      int pos = start8 + kk;
-      pos -= pos >= a.ring ? a.ring : 0;
-      pos = pos < a.ring ? pos : 0;
-      const int oc = a.backward_data ? prm[pos] : chs;
-      const int ic = a.backward_data ? chs : pos;
-      int sl = ic - stt[oc];
-      sl += sl < 0 ? a.c_in : 0;
-      const bool ok = ch >= 0 && kk < lim && sl < a.gw;
-      const float w = wsrc[oc * a.gw + (ok ? sl : 0)];
-      v[i] = ok ? w : 0.f;
+        for (int b = 0; b < kB; ++b) {
+          const int it = min(i0 + b * kWarps, items - 1);
+          ch[b] = rrow[(it % (NT / 4)) * 4 + rs];
+        }
+        int st[kB];
+#pragma unroll
+        for (int b = 0; b < kB; ++b) st[b] = stt[ch[b] < 0 ? 0 : ch[b]];
+        float w[kB][4];
+#pragma unroll
+        for (int b = 0; b < kB; ++b) {
+          const int it = min(i0 + b * kWarps, items - 1);
+          const int kk0 = 32 * (it / (NT / 4)) + 4 * q16;
+          int ic = start8 + kk0;
+          ic -= ic >= a.ring ? a.ring : 0;
+          int sl0 = ic - st[b];
+          sl0 += sl0 < 0 ? a.c_in : 0;
+          const int base = (ch[b] < 0 ? 0 : ch[b]) * a.gw;
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            int sl = sl0 + i;
+            sl -= sl >= a.c_in ? a.c_in : 0;
+            const bool ok = ch[b] >= 0 && kk0 + i < lim && sl < a.gw;
+            const float v = wsrc[base + (ok ? sl : 0)];
+            w[b][i] = ok ? v : 0.f;
+          }
+        }
+#pragma unroll
+        for (int b = 0; b < kB; ++b) {
+          const int it = i0 + b * kWarps;
+          if (it < items) {
+            const int c = it / (NT / 4), r = (it - c * (NT / 4)) * 4 + rs;
+            float4 h, l;
+            h.x = tf32_hi(w[b][0]); l.x = w[b][0] - h.x;
+            h.y = tf32_hi(w[b][1]); l.y = w[b][1] - h.y;
+            h.z = tf32_hi(w[b][2]); l.z = w[b][2] - h.z;
+            h.w = tf32_hi(w[b][3]); l.w = w[b][3] - h.w;
+            const uint32_t img = pbase + (cb + c) * kPanelChunk;
+            const uint32_t off = (r >> 3) * 1024 + (r & 7) * 128 + ((q16 ^ (r & 7)) << 4);
+            sts_v4(img + off, h);
+            sts_v4(img + NT * 128 + off, l);
+          }
+        }
+      }
+    } else {
+      constexpr int kRb = NT / 32;  // 32-row blocks per tile
+      const int items = nch * 8 * kRb;
+      for (int i0 = wid; i0 < items; i0 += kB * kWarps) {
+        int ic[kB], oc[kB][4];
+#pragma unroll
+        for (int b = 0; b < kB; ++b) {
+          const int it = min(i0 + b * kWarps, items - 1);
+          const int kw = it / kRb;  // chunk * 8 + word
+          ic[b] = rrow[(it % kRb) * 32 + lane];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            int pos = start8 + 4 * kw + i;
+            pos -= pos >= a.ring ? a.ring : 0;
+            oc[b][i] = prm[pos < a.ring ? pos : 0];
+          }
+        }
+        int st[kB][4];
+#pragma unroll
+        for (int b = 0; b < kB; ++b)
+#pragma unroll
+          for (int i = 0; i < 4; ++i) st[b][i] = stt[oc[b][i]];
+        float w[kB][4];
+#pragma unroll
+        for (int b = 0; b < kB; ++b) {
+          const int it = min(i0 + b * kWarps, items - 1);
+          const int kw = it / kRb;
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            int sl = (ic[b] < 0 ? 0 : ic[b]) - st[b][i];
+            sl += sl < 0 ? a.c_in : 0;
+            const bool ok = ic[b] >= 0 && 4 * kw + i < lim && sl < a.gw;
+            const float v = wsrc[oc[b][i] * a.gw + (ok ? sl : 0)];
+            w[b][i] = ok ? v : 0.f;
+          }
+        }
+#pragma unroll
+        for (int b = 0; b < kB; ++b) {
+          const int it = i0 + b * kWarps;
+          if (it < items) {
+            const int kw = it / kRb, c = kw >> 3, q16 = kw & 7;
+            const int r = (it % kRb) * 32 + lane;
+            float4 h, l;
+            h.x = tf32_hi(w[b][0]); l.x = w[b][0] - h.x;
+            h.y = tf32_hi(w[b][1]); l.y = w[b][1] - h.y;
+            h.z = tf32_hi(w[b][2]); l.z = w[b][2] - h.z;
+            h.w = tf32_hi(w[b][3]); l.w = w[b][3] - h.w;
+            const uint32_t img = pbase + (cb + c) * kPanelChunk;
+            const uint32_t off = (r >> 3) * 1024 + (r & 7) * 128 + ((q16 ^ (r & 7)) << 4);
+            sts_v4(img + off, h);
+            sts_v4(img + NT * 128 + off, l);
+          }
+        }
+      }
     }
-    float4 h, w;
-    h.x = tf32_hi(v[0]);
-    h.y = tf32_hi(v[1]);
-    h.z = tf32_hi(v[2]);
-    h.w = tf32_hi(v[3]);
-    w.x = v[0] - h.x;
-    w.y = v[1] - h.y;
-    w.z = v[2] - h.z;
-    w.w = v[3] - h.w;
-    uint8_t* img = panel + gc * kPanelChunk;
-    const int off = (r >> 3) * 1024 + (r & 7) * 128 + ((q16 ^ (r & 7)) << 4);
-    *reinterpret_cast<float4*>(img + off) = h;
-    *reinterpret_cast<float4*>(img + NT * 128 + off) = w;
+  }
+}
+
+// Forward panel fast path: when every window start and gw are multiples of 4,
+// each 16 B panel word (4 consecutive input channels) lies wholly inside or
+// wholly outside its filter's window, so it is one 16 B load of W (staged in
+// smem) or zero.  Lane = (row, word); a warp covers 4 rows of one chunk.
+template <int NT>
+__device__ __forceinline__ void build_panel_fwd4(const Band2Args& a, uint8_t* panel,
+                                                 const int32_t* rows_s, const float* w_s,
+                                                 const int32_t* start_s, int ct) {
+  constexpr int kPanelChunk = 2 * NT * 128;
+  constexpr int kWarps = kWorkers / 32;
+  const int lane = ct & 31, wid = ct >> 5;
+  const int rs = lane >> 3, q16 = lane & 7;
+  const uint32_t pbase = smem_u32(panel);
+  for (int rt = 0; rt < a.n_rt; ++rt) {
+    const int cb = a.rt_cb[rt], nch = a.rt_cb[rt + 1] - cb;
+    const int lim = 8 * a.rt_nk8[rt], start8 = a.rt_start8[rt];
+    const int items = nch * (NT / 4);
+#pragma unroll 4
+    for (int it = wid; it < items; it += kWarps) {
+      const int c = it / (NT / 4), r = (it - c * (NT / 4)) * 4 + rs;
+      const int ch = rows_s[rt * NT + r];
+      const int chs = ch < 0 ? 0 : ch;
+      const int kk0 = 32 * c + 4 * q16;
+      int sl0 = start8 + kk0 - start_s[chs];  // ring = c_in in the forward direction
+      sl0 += sl0 < 0 ? a.c_in : 0;
+      sl0 -= sl0 >= a.c_in ? a.c_in : 0;
+      const bool ok = ch >= 0 && kk0 < lim && sl0 < a.gw;
+      float4 v = *reinterpret_cast<const float4*>(w_s + chs * a.gw + (ok ? sl0 : 0));
+      if (!ok) v = make_float4(0.f, 0.f, 0.f, 0.f);
+      float4 h, l;
+      h.x = tf32_hi(v.x); l.x = v.x - h.x;
+      h.y = tf32_hi(v.y); l.y = v.y - h.y;
+      h.z = tf32_hi(v.z); l.z = v.z - h.z;
+      h.w = tf32_hi(v.w); l.w = v.w - h.w;
+      const uint32_t img = pbase + (cb + c) * kPanelChunk;
+      const uint32_t off = (r >> 3) * 1024 + (r & 7) * 128 + ((q16 ^ (r & 7)) << 4);
+      sts_v4(img + off, h);
+      sts_v4(img + NT * 128 + off, l);
+    }
   }
 }
 
 template <int NT>
 __global__ void __launch_bounds__(kThreads, 1)
-    tc_band2_kernel(const __grid_constant__ CUtensorMap t4, const __grid_constant__ CUtensorMap t1,
-                    const __grid_constant__ CUtensorMap tout, const __grid_constant__ Band2Args a) {
+    tc_band2_kernel(const __grid_constant__ CUtensorMap t1, const __grid_constant__ CUtensorMap tout,
+                    const __grid_constant__ Band2Args a) {
   constexpr int kPanelChunk = 2 * NT * 128;  // hi + lo image of one 32-k chunk
   // No static shared memory in this kernel: the dynamic window starts
   // 1024-aligned and every derived pointer stays in the shared address space.
   extern __shared__ __align__(1024) uint8_t smem[];
-  const Layout<NT> L(a.total_chunks, a.stages, a.n_rt, a.store_mode);
+  const Layout<NT> L(a.total_chunks, a.stages, a.n_rt, a.store_mode, a.scratch);
   uint8_t* panel = smem + L.panel;
   uint8_t* raw = smem + L.raw;
-  uint8_t* lo = smem + L.lo;
   uint8_t* stbuf = smem + L.st;
   int32_t* rows_s = reinterpret_cast<int32_t*>(smem + L.rows);
   float* bias_s = reinterpret_cast<float*>(smem + L.bias);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bars);
   uint64_t* full = bars;
   uint64_t* afree = bars + kMaxStages;
-  uint64_t* lofull = afree + kMaxStages;
-  uint64_t* lofree = lofull + kLoStages;
-  uint64_t* tfull = lofree + kLoStages;
+  uint64_t* conv = afree + kMaxStages;
+  uint64_t* tfree = conv + kTStages;
+  uint64_t* tfull = tfree + kTStages;
   uint64_t* tempty = tfull + 2;
   uint64_t* panel_bar = tempty + 2;
   uint64_t* tab_bar = panel_bar + 1;
   uint64_t* w_bar = tab_bar + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(w_bar + 1);
-  // Panel-build scratch in the lo ring (dead until the first conversion).
-  float* w_s = reinterpret_cast<float*>(lo);
-  int32_t* start_s = reinterpret_cast<int32_t*>(lo) + pad4(a.c_out * a.gw);
+  // Panel-build scratch in the store staging (dead until the first epilogue).
+  float* w_s = reinterpret_cast<float*>(stbuf);
+  int32_t* start_s = reinterpret_cast<int32_t*>(stbuf) + pad4(a.c_out * a.gw);
   int32_t* perm_s = start_s + pad4(a.c_out);
+  constexpr uint32_t kACol0 = 2 * NT;  // TMEM: [0, 2NT) accumulators, then A stages
 
   const uint32_t warp = warp_id();
   const int lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     TRACE2(0);
+    if (blockIdx.x < 1024) g_cta2[2 * blockIdx.x] = globaltimer();
     if (blockIdx.x == 0) g_trace2[47] = clock64();
     if (smem_u32(smem) & 1023u) __trap();
     for (int s = 0; s < kMaxStages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&afree[s], 1);
+      mbar_init(&afree[s], 4);  // the 4 converter warps
     }
-    for (int s = 0; s < kLoStages; ++s) {
-      mbar_init(&lofull[s], kWorkers / 32);
-      mbar_init(&lofree[s], 1);
+    for (int s = 0; s < kTStages; ++s) {
+      mbar_init(&conv[s], 4);
+      mbar_init(&tfree[s], 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
@@ -274,11 +393,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (b_perm) bulk_load(perm_s, a.perm, b_perm, tab_bar);
   }
   if (warp == 0 && lane == 0) {
-    prefetch_tmap(&t4);
     prefetch_tmap(&t1);
     prefetch_tmap(&tout);
   }
-  if (warp == 1) tmem_alloc<2 * NT>(tmem_slot);
+  if (warp == 1) tmem_alloc<512>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -292,6 +410,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0) {
     // ---------------- producer ----------------
     if (elect_one()) {
+      if (a.debug & 1) mbar_wait_sleep(panel_bar, 0);
       int s = 0;
       uint32_t ph = 0;
       TileIter it(a);
@@ -303,23 +422,16 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int c = 0; c < nch; ++c) {
             mbar_wait_sleep(&afree[s], ph ^ 1u);
             const int rows = min(4, nk8 - 4 * c) * 8;
-            // Full tiles and (when the plane is block-aligned) partial ones
-            // both use one 4-block box per rb rows; a partial tile over-reads
-            // the neighbour's blocks (or zero-fills past the sample).
-            mbar_expect_tx(&full[s], rows * 128 * (a.blocked ? 4 : it.cnt));
+            // One box {128 px, rb rows} per rb rows: stage = [32 rows][128 px].
+            // A partial tile over-reads the neighbour's pixels (or zero-fills
+            // past the end of the sample); the epilogue never stores them.
+            mbar_expect_tx(&full[s], rows * 512);
             uint8_t* st = raw + s * kStageBytes;
             for (int r = 0; r < rows; r += a.rb) {
               int pos = start8 + 32 * c + r;
               while (pos >= a.ring) pos -= a.ring;
               const int cl = pos / a.cls, j = pos - cl * a.cls;
-              const int d = a.class_d[cl];
-              uint8_t* dst = st + r * 512;
-              if (a.blocked) {
-                tma_load_5d(dst, &t4, &full[s], 0, j, it.b0, d, it.n);
-              } else {
-                for (int b = 0; b < it.cnt; ++b)
-                  tma_load_4d(dst + b * a.rb * 128, &t1, &full[s], (it.b0 + b) * kBlkPx, j, d, it.n);
-              }
+              tma_load_4d(st + r * 512, &t1, &full[s], it.b0 * kBlkPx, j, a.class_d[cl], it.n);
             }
             if (first) {
               TRACE2(2);
@@ -332,12 +444,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    // ---------------- MMA issuer ----------------
-    constexpr uint32_t idesc = idesc_tf32(128, NT, 1, 0);
-    const uint32_t lbo = static_cast<uint32_t>(a.rb) * 128u;
-    int s = 0, l = 0, acc = 0;
-    uint32_t ph = 0, lph = 0, aph = 0;
-    mbar_wait_sleep(panel_bar, 0);
+    // ---------------- MMA issuer (A from TMEM, B = panel from smem) ----------------
+    constexpr uint32_t idesc = idesc_tf32(128, NT, 0, 0);
+    int st = 0, acc = 0;
+    uint32_t tph = 0, aph = 0;
+    if (a.debug & 8) {
+      if (lane == 0)
+        while (!mbar_try_wait(panel_bar, 0)) __nanosleep(1000);
+      __syncwarp();
+    } else {
+      mbar_wait_sleep(panel_bar, 0);
+    }
     tc_fence_after();
     TileIter it(a);
     int ti = 0;
@@ -350,34 +467,27 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_after();
         const uint32_t d_tmem = tmem + acc * NT;
         for (int c = 0; c < nch; ++c) {
-          mbar_wait_sleep(&full[s], ph);
-          mbar_wait_sleep(&lofull[l], lph);
+          mbar_wait_sleep(&conv[st], tph);
           tc_fence_after();
           if (elect_one()) {
             const int steps = min(4, nk8 - 4 * c);
-            const uint32_t a_hi = smem_u32(raw + s * kStageBytes);
-            const uint32_t a_lo = smem_u32(lo + l * kStageBytes);
+            const uint32_t a_hi = tmem + kACol0 + st * 64, a_lo = a_hi + 32;
             const uint32_t bh = smem_u32(panel + (cb + c) * kPanelChunk), bl = bh + NT * 128;
             for (int k = 0; k < steps; ++k) {
-              const uint32_t off = row_off(8 * k, a.rb);
-              const uint64_t dah = desc_mn32(a_hi + off, lbo, 512);
-              const uint64_t dal = desc_mn32(a_lo + off, lbo, 512);
               const uint64_t dbh = desc_sw128(bh + k * 32, 16, 1024);
               const uint64_t dbl = desc_sw128(bl + k * 32, 16, 1024);
-              mma_tf32(d_tmem, dah, dbh, idesc, (c | k) != 0);
-              mma_tf32(d_tmem, dal, dbh, idesc, 1);
-              mma_tf32(d_tmem, dah, dbl, idesc, 1);
+              mma_tf32_ts(d_tmem, a_hi + 8 * k, dbh, idesc, (c | k) != 0);
+              mma_tf32_ts(d_tmem, a_lo + 8 * k, dbh, idesc, 1);
+              mma_tf32_ts(d_tmem, a_hi + 8 * k, dbl, idesc, 1);
             }
-            mma_commit(&afree[s]);
-            mma_commit(&lofree[l]);
+            mma_commit(&tfree[st]);
             if (c == nch - 1) {
               mma_commit(&tfull[acc]);
               if (ti < 8) TRACE2(6 + ti);
             }
           }
           __syncwarp();
-          advance(s, ph, a.stages);
-          advance(l, lph, kLoStages);
+          advance(st, tph, kTStages);
         }
         ++ti;
         if (++acc == 2) {
@@ -386,10 +496,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
-  } else if (warp < 8) {
-    // ---------------- panel build (warps 2..7) ----------------
-    const int ct = threadIdx.x - 64;  // 0..191
-    {
+  } else {
+    // ---------------- panel build (warps 2, 3, 8..11; the converters start at once) ----------------
+    if (warp < 4 || warp >= 8) {
+      const int ct = warp < 4 ? threadIdx.x - 64 : threadIdx.x - 192;  // 0..191
       if (ct == 0 && a.w_staged) {
         const uint32_t bytes = 4u * a.c_out * a.gw;
         mbar_expect_tx(w_bar, bytes);
@@ -401,68 +511,67 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait_sleep(w_bar, 0);
         if (ct == 0) TRACE2(5);
       }
-      // One 16 B word (4 consecutive k of one row) per unit: gather 4 band
-      // weights, write the hi and lo images (K-major SWIZZLE_128B).  The
-      // staged path reads W and the oc tables through shared-space pointers.
       if (ct == 0) TRACE2(50);
-      if (a.w_staged)
+      if (a.fwd4)
+        build_panel_fwd4<NT>(a, panel, rows_s, w_s, start_s, ct);
+      else if (a.w_staged)
         build_panel<NT>(a, panel, rows_s, w_s, start_s, perm_s, ct);
       else
         build_panel<NT>(a, panel, rows_s, a.weight, a.starts, a.perm, ct);
       if (ct == 0) TRACE2(51);
       fence_proxy_async_smem();
-      if (ct == 0) TRACE2(52);
       named_bar_sync(1, kWorkers);
       if (ct == 0) {
         TRACE2(3);
         mbar_arrive(panel_bar);
       }
     }
-    // ---------------- lo converters ----------------
-    int s = 0, l = 0;
-    uint32_t ph = 0, lph = 0;
-    TileIter it(a);
-    int cc = 0;
-    while (it.next()) {
-      for (int rt = 0; rt < a.n_rt; ++rt) {
-        const int nk8 = a.rt_nk8[rt];
-        const int nch = (nk8 + 3) >> 2;
-        for (int c = 0; c < nch; ++c) {
-          mbar_wait_sleep(&full[s], ph);
-          mbar_wait_sleep(&lofree[l], lph ^ 1u);
-          if (ct == 0 && cc < 8) TRACE2(22 + cc);
-          const int words = min(4, nk8 - 4 * c) * 8 * 512 / 16;  // <= 1024
-          const float4* src = reinterpret_cast<const float4*>(raw + s * kStageBytes);
-          float4* dst = reinterpret_cast<float4*>(lo + l * kStageBytes);
-          float4 v[6];
+    if (warp >= 4 && warp < 8) {
+      // ---------------- converters: raw [row][px] -> TMEM [px lane][row] hi / lo ----------------
+      const int q = warp & 3;  // pixel block of the tile = TMEM lane quarter
+      const uint32_t lane_base = static_cast<uint32_t>(q * 32) << 16;
+      int s = 0, st = 0;
+      uint32_t ph = 0, tph = 0;
+      TileIter it(a);
+      int cc = 0;
+      while (it.next()) {
+        for (int rt = 0; rt < a.n_rt; ++rt) {
+          const int nk8 = a.rt_nk8[rt];
+          const int nch = (nk8 + 3) >> 2;
+          for (int c = 0; c < nch; ++c) {
+            mbar_wait_sleep(&full[s], ph);
+            if (q == 0 && lane == 0 && cc < 8) TRACE2(22 + cc);
+            // Element (row r, pixel 32q + lane) of the [32 rows][128 px] stage.
+            // Rows past the chunk's k-steps hold stale data that lands in TMEM
+            // columns the MMAs never read.
+            const float* src = reinterpret_cast<const float*>(raw + s * kStageBytes) + q * 32 + lane;
+            uint32_t hi[32], lo[32];
 #pragma unroll
-          for (int u = 0; u < 6; ++u) {
-            const int i = ct + u * kWorkers;
-            if (i < words) v[u] = src[i];
-          }
-#pragma unroll
-          for (int u = 0; u < 6; ++u) {
-            const int i = ct + u * kWorkers;
-            if (i < words) {
-              float4 o;
-              o.x = v[u].x - tf32_hi(v[u].x);
-              o.y = v[u].y - tf32_hi(v[u].y);
-              o.z = v[u].z - tf32_hi(v[u].z);
-              o.w = v[u].w - tf32_hi(v[u].w);
-              dst[i] = o;
+            for (int r = 0; r < 32; ++r) {
+              const float v = src[r * 128];
+              const float h = tf32_hi(v);
+              hi[r] = __float_as_uint(h);
+              lo[r] = __float_as_uint(v - h);
             }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&afree[s]);
+            mbar_wait_sleep(&tfree[st], tph ^ 1u);
+            tc_fence_after();
+            const uint32_t col = tmem + kACol0 + st * 64 + lane_base;
+            tmem_st32(col, hi);
+            tmem_st32(col + 32, lo);
+            tmem_st_wait();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&conv[st]);
+            if (q == 0 && lane == 0 && cc < 8) TRACE2(30 + cc);
+            ++cc;
+            advance(s, ph, a.stages);
+            advance(st, tph, kTStages);
           }
-          fence_proxy_async_smem();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&lofull[l]);
-          if (ct == 0 && cc < 8) TRACE2(30 + cc);
-          ++cc;
-          advance(s, ph, a.stages);
-          advance(l, lph, kLoStages);
         }
       }
-    }
-  } else {
+    } else if (warp >= 8) {
     // ---------------- epilogue (warps 8..11) ----------------
     const int et = threadIdx.x - 256;  // 0..127
     mbar_wait_sleep(tab_bar, 0);
@@ -477,6 +586,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     TileIter it(a);
     int ti = 0;
     uint8_t* wbuf = stbuf + q * L.st_warp;  // this warp's staging
+    const uint32_t wbuf_a = smem_u32(wbuf);
     const bool whole = a.store_mode == kStoreClasses || a.store_mode == kStoreRowsNT;
     while (it.next()) {
       const int px = (it.b0 + q) * kBlkPx + lane;
@@ -506,28 +616,32 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (a.store_mode == kStoreClasses) {
               // box {32 px, D, out_cls}: smem [j][d][px]
               const int cl = g0 / a.out_cls, j0 = g0 - cl * a.out_cls, d = a.out_class_d[cl];
-              float* buf = reinterpret_cast<float*>(wbuf) + (j0 * a.out_nd + d) * 32 + lane;
+              const uint32_t buf = wbuf_a + ((j0 * a.out_nd + d) * 32 + lane) * 4;
+              const uint32_t jstride = a.out_nd * 128;
 #pragma unroll
-              for (int j = 0; j < 32; ++j) buf[j * a.out_nd * 32] = __uint_as_float(v[j]) + bb[j];
+              for (int j = 0; j < 32; ++j) sts_f32(buf + j * jstride, __uint_as_float(v[j]) + bb[j]);
             } else if (a.store_mode == kStoreRowsNT) {
-              float* buf = reinterpret_cast<float*>(wbuf) + c0 * 32 + lane;
+              const uint32_t buf = wbuf_a + (c0 * 32 + lane) * 4;
 #pragma unroll
-              for (int j = 0; j < 32; ++j) buf[j * 32] = __uint_as_float(v[j]) + bb[j];
+              for (int j = 0; j < 32; ++j) sts_f32(buf + j * 128, __uint_as_float(v[j]) + bb[j]);
             } else if (a.store_mode == kStoreRows32) {
-              // Stage [32 rows][32 px] and write it with one TMA store; 2 buffers.
-              float* buf = reinterpret_cast<float*>(wbuf + sbuf * kStoreBuf);
-              if (lane == 0) bulk_wait_read<1>();
+              // Stage [32 rows][32 px] and write it with one TMA store as soon
+              // as it is staged; 4 buffers per warp rotate.
+              if (lane == 0) bulk_wait_read<3>();
               __syncwarp();
+              const uint32_t buf = wbuf_a + sbuf * kStoreBuf + lane * 4;
 #pragma unroll
-              for (int j = 0; j < 32; ++j) buf[j * 32 + lane] = __uint_as_float(v[j]) + bb[j];
+              for (int j = 0; j < 32; ++j) sts_f32(buf + j * 128, __uint_as_float(v[j]) + bb[j]);
               fence_proxy_async_smem();
               __syncwarp();
               if (lane == 0) {
                 const int cl = g0 / a.out_cls, jj = g0 - cl * a.out_cls;
-                tma_store_3d(&tout, buf, (it.b0 + q) * kBlkPx, a.out_class_d[cl], it.n * a.out_cls + jj);
+                tma_store_3d(&tout, wbuf + sbuf * kStoreBuf, (it.b0 + q) * kBlkPx, a.out_class_d[cl],
+                             it.n * a.out_cls + jj);
                 bulk_commit();
+                if (ti == 0 && q == 0 && c0 < 128) TRACE2(42 + c0 / 32);
               }
-              sbuf ^= 1;
+              sbuf = (sbuf + 1) & 3;
             } else if (valid) {
               int32_t rr[32];
 #pragma unroll
@@ -567,57 +681,52 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
     if (lane == 0) bulk_wait<0>();
+    if (lane == 0 && q == 0 && blockIdx.x < 1024) g_cta2[2 * blockIdx.x + 1] = globaltimer();
+    }
   }
   tc_fence_before();
   __syncthreads();
   if (threadIdx.x == 0) TRACE2(63);
-  if (warp == 1) tmem_dealloc<2 * NT>(tmem);
+  if (warp == 1) tmem_dealloc<512>(tmem);
 }
 
 template <int NT>
-int band2_stages(const TcBandPlan& tp, int mode) {
+int band2_stages(const TcBandPlan& tp, int mode, int scratch) {
   int st = kMaxStages;
-  while (st >= 2 && 1024 + Layout<NT>(tp.total_chunks, st, tp.n_rt, mode).total > kSmemLimit) --st;
+  while (st >= 2 && 1024 + Layout<NT>(tp.total_chunks, st, tp.n_rt, mode, scratch).total > kSmemLimit) --st;
   return st;
 }
 
 template <int NT>
 cudaError_t launch_tc2_nt(const TcBandPlan& tp, const TcDeviceTables& dt, const TcBandCall& call,
-                          int32_t c_out, cudaStream_t s) {
+                          int64_t shift, int32_t c_out, cudaStream_t s) {
   const int64_t P = call.plane;
   const int32_t C = tp.cls * tp.n_class;  // channels of the activation tensor
-  CUtensorMap t4, t1;
+  // Activations {P, cls, n_class, N}, box {128 px, rb rows}, no swizzle.
+  CUtensorMap t1;
   {
     const uint64_t dims[4] = {static_cast<uint64_t>(P), static_cast<uint64_t>(tp.cls),
                               static_cast<uint64_t>(tp.n_class), static_cast<uint64_t>(call.n)};
     const uint64_t strides[3] = {static_cast<uint64_t>(tp.n_class) * P * 4, static_cast<uint64_t>(P) * 4,
                                  static_cast<uint64_t>(C) * P * 4};
-    const uint32_t box[4] = {32, static_cast<uint32_t>(tp.rb), 1, 1};
-    if (!encode_f32(&t1, call.in, 4, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B))
+    const uint32_t box[4] = {128, static_cast<uint32_t>(tp.rb), 1, 1};
+    if (!encode_f32(&t1, call.in, 4, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_NONE))
       return cudaErrorInvalidValue;
-  }
-  const bool blocked = P % 32 == 0;
-  if (blocked) {
-    const uint64_t dims[5] = {32, static_cast<uint64_t>(tp.cls), static_cast<uint64_t>(P / 32),
-                              static_cast<uint64_t>(tp.n_class), static_cast<uint64_t>(call.n)};
-    const uint64_t strides[4] = {static_cast<uint64_t>(tp.n_class) * P * 4, 128,
-                                 static_cast<uint64_t>(P) * 4, static_cast<uint64_t>(C) * P * 4};
-    const uint32_t box[5] = {32, static_cast<uint32_t>(tp.rb), 4, 1, 1};
-    if (!encode_f32(&t4, call.in, 5, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B))
-      return cudaErrorInvalidValue;
-  } else {
-    t4 = t1;
   }
   // Epilogue store mode and the output view its TMA stores use.
   const bool cls_ok = tp.store_ok && static_cast<int>(tp.out_class_d.size()) <= kMaxCls;
-  int32_t mode = kStoreStg;
-  if (call.backward_data && call.c_out_t % NT == 0) {
-    mode = kStoreRowsNT;  // dx rows are the input channels in order
-  } else if (!call.backward_data && cls_ok && tp.n_rt == 1 && tp.out_n_class <= 256 &&
-             tp.out_cls <= 256 && tp.out_n_class * tp.out_cls == call.c_out_t) {
-    mode = kStoreClasses;  // one row tile holds every filter: {32 px, D, c_out/D}
-  } else if (cls_ok) {
-    mode = kStoreRows32;
+  // Default: 32-row boxes stored as soon as staged (stores start after the
+  // first 32 columns of a tile).  SCC_TC2_STORE=2/3 selects the whole-tile
+  // boxes (one store per warp and tile) for comparison.
+  int32_t mode = cls_ok ? kStoreRows32 : kStoreStg;
+  {
+    const char* sm = getenv("SCC_TC2_STORE");
+    const int want = sm ? atoi(sm) : -1;
+    if (want == kStoreRowsNT && call.backward_data && call.c_out_t % NT == 0) mode = kStoreRowsNT;
+    if (want == kStoreClasses && !call.backward_data && cls_ok && tp.n_rt == 1 && tp.out_n_class <= 256 &&
+        tp.out_cls <= 256 && tp.out_n_class * tp.out_cls == call.c_out_t)
+      mode = kStoreClasses;
+    if (want == kStoreStg) mode = kStoreStg;
   }
   CUtensorMap tout;
   {
@@ -664,22 +773,31 @@ cudaError_t launch_tc2_nt(const TcBandPlan& tp, const TcDeviceTables& dt, const 
   a.gw = call.gw;
   a.c_out_t = call.c_out_t;
   a.backward_data = call.backward_data ? 1 : 0;
-  a.blocked = blocked ? 1 : 0;
   a.nbps = static_cast<int32_t>((P + 31) / 32);
-  a.stages = band2_stages<NT>(tp, mode);
+
   a.total_chunks = tp.total_chunks;
-  // W + starts (+ perm) go to the lo ring by bulk copy when they fit and the
+  {
+    const char* dbg = getenv("SCC_TC2_DEBUG");
+    a.debug = dbg ? atoi(dbg) : 0;
+  }
+  // W + starts (+ perm) go to the staging area by bulk copy when they fit and the
   // weight pointer/size suit cp.async.bulk.
   {
     const int64_t wbytes = 4ll * c_out * call.gw;
     const int64_t need = 4ll * (pad4(c_out * call.gw) + 2 * pad4(c_out));
-    a.w_staged = (need <= kLoStages * kStageBytes && wbytes % 16 == 0 &&
+    a.w_staged = (need <= kMaxScratch && wbytes % 16 == 0 &&
                   reinterpret_cast<uintptr_t>(call.weight) % 16 == 0) ? 1 : 0;
+    a.scratch = a.w_staged ? static_cast<int32_t>(need) : 0;
+    // window starts (oc * shift mod c_in) and arc starts (multiples of 8) are
+    // multiples of 4 when shift and c_in are
+    a.fwd4 = (!call.backward_data && a.w_staged && call.gw % 4 == 0 && call.c_in % 4 == 0 &&
+              shift % 4 == 0) ? 1 : 0;
   }
+  a.stages = band2_stages<NT>(tp, mode, a.scratch);
   a.plane = P;
   a.n = call.n;
   a.units = call.n * a.nbps;
-  const int smem = 1024 + Layout<NT>(a.total_chunks, a.stages, a.n_rt, mode).total;
+  const int smem = 1024 + Layout<NT>(a.total_chunks, a.stages, a.n_rt, mode, a.scratch).total;
 
   static int nsm_cache[64] = {0};
   static bool attr_set[64] = {false};
@@ -708,7 +826,7 @@ cudaError_t launch_tc2_nt(const TcBandPlan& tp, const TcDeviceTables& dt, const 
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, tc_band2_kernel<NT>, t4, t1, tout, a);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, tc_band2_kernel<NT>, t1, tout, a);
   if (e != cudaSuccess) return e;
   note_launches(1);
   return cudaSuccess;
@@ -722,26 +840,30 @@ bool tc_band2_supported(const TcBandPlan& tp, int64_t plane, int32_t c_out) {
   if (tp.rb % 8 != 0 || tp.n_rt > kMaxRt || tp.n_class > kMaxCls) return false;
   // The whole panel stays resident next to >= 4 raw stages.
   // (store staging is chosen at launch; size the check for the largest mode)
-  const int st = tp.nt == 128 ? band2_stages<128>(tp, kStoreClasses) : band2_stages<64>(tp, kStoreClasses);
+  const int st = tp.nt == 128 ? band2_stages<128>(tp, kStoreClasses, kMaxScratch)
+                               : band2_stages<64>(tp, kStoreClasses, kMaxScratch);
   return st >= 4;
 }
 
 cudaError_t launch_band_tc2(const TcBandPlan& tp, const TcDeviceTables& dt, const TcBandCall& call,
                             int64_t shift, int32_t c_out, cudaStream_t s) {
-  (void)shift;
   switch (tp.nt) {
     case 64:
-      return launch_tc2_nt<64>(tp, dt, call, c_out, s);
+      return launch_tc2_nt<64>(tp, dt, call, shift, c_out, s);
     case 128:
-      return launch_tc2_nt<128>(tp, dt, call, c_out, s);
+      return launch_tc2_nt<128>(tp, dt, call, shift, c_out, s);
     default:
       return cudaErrorInvalidValue;
   }
 }
 
 int tc2_trace(unsigned long long* out, int n) {
-  if (n > 64) n = 64;
-  return cudaMemcpyFromSymbol(out, g_trace2, n * sizeof(unsigned long long)) == cudaSuccess ? n : -1;
+  if (n > 64 + 2048) n = 64 + 2048;
+  const int a = n < 64 ? n : 64;
+  if (cudaMemcpyFromSymbol(out, g_trace2, a * sizeof(unsigned long long)) != cudaSuccess) return -1;
+  if (n > 64 && cudaMemcpyFromSymbol(out + 64, g_cta2, (n - 64) * sizeof(unsigned long long)) != cudaSuccess)
+    return -1;
+  return n;
 }
 
 }  // namespace scc

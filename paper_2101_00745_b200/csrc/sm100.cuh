@@ -30,6 +30,19 @@ __device__ __forceinline__ bool elect_one() {
   return pred != 0;
 }
 
+// Shared-memory stores through a 32-bit shared-window address.  No "memory"
+// clobber on purpose: ordinary loads may be scheduled across them (the
+// callers never read back what they store before a fence / barrier, which are
+// volatile asm and keep their order relative to these volatile stores), so a
+// loop of load-compute-store iterations overlaps instead of serialising.
+__device__ __forceinline__ void sts_f32(uint32_t addr, float v) {
+  asm volatile("st.shared.f32 [%0], %1;" ::"r"(addr), "f"(v));
+}
+__device__ __forceinline__ void sts_v4(uint32_t addr, float4 v) {
+  asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(v.x), "f"(v.y), "f"(v.z),
+               "f"(v.w));
+}
+
 // ---- mbarrier ---------------------------------------------------------------
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));

@@ -41,13 +41,22 @@ for path, name in ((_lib.SCC_PATH_TENSOR_V1, "gen1"), (_lib.SCC_PATH_TENSOR, "ge
     if path == _lib.SCC_PATH_TENSOR:
         for op, f in (("fwd", fwd), ("bwd_data", bwdd)):
             f(0, torch.cuda.current_stream().cuda_stream); torch.cuda.synchronize()
-            buf = (C.c_uint64 * 192)()
-            n = L.scc_debug_trace(buf, 192)
+            buf = (C.c_uint64 * (192 + 2048))()
+            n = L.scc_debug_trace(buf, 192 + 2048)
+            import statistics
+            st = [buf[192 + 2 * i] for i in range(148)]; en = [buf[193 + 2 * i] for i in range(148)]
+            t00 = min(st)
+            ends = sorted((e - t00) / 1e3 for e in en)
+            starts = sorted((x - t00) / 1e3 for x in st)
+            print(op, "CTA starts: min %.2f med %.2f max %.2f | epilogue ends: min %.2f med %.2f p90 %.2f max %.2f" % (
+                starts[0], statistics.median(starts), starts[-1], ends[0], statistics.median(ends), ends[int(0.9 * len(ends))], ends[-1]))
             t = [buf[128 + i] for i in range(64)]
             t0 = t[0]
             lab = {0: "start", 1: "dep", 2: "tma0", 46: "tma_last", 3: "panel", 4: "tabs", 5: "w", 63: "end", 50: "b_loop0", 51: "b_loop1", 52: "b_fence"}
             for i in range(8): lab[6 + i] = f"mma{i}"; lab[14 + i] = f"epi{i}"; lab[22 + i] = f"cv{i}s"; lab[30 + i] = f"cv{i}e"
             for g in range(4): lab[38 + g] = f"eg{g}ld"; lab[42 + g] = f"eg{g}st"
+            print(op, "diag slots 54..61:", [t[54 + i] for i in range(8)])
+            for i in range(8): t[54 + i] = 0
             print(op, "SM clock MHz (CTA0):", (t[48] - t[47]) * 1e3 / max(t[t[49]] - t[0], 1))
             t[47] = t[48] = t[49] = 0
             print(op, " ".join(f"{lab[i]}={(t[i] - t0) / 1e3:.2f}" for i in sorted(lab) if t[i] >= t0 and t[i] - t0 < 1e8))
