@@ -189,6 +189,32 @@ float* panel_buffer(Plan& p, int dir, cudaStream_t s) {
   return static_cast<float*>(b.ptr);
 }
 
+// Grid-barrier words {count, generation} of the generation-2 backward-weight
+// kernel, one zeroed pair per (device, stream) so concurrent calls on
+// different streams never share a barrier.
+unsigned int* sync_buffer(Plan& p, cudaStream_t s) {
+  const int dev = current_device();
+  std::lock_guard<std::mutex> lk(p.panel_mu);
+  for (PanelBuf& b : p.panels) {
+    if (b.device == dev && b.stream == static_cast<void*>(s) && b.dir == 3) return static_cast<unsigned int*>(b.ptr);
+  }
+  PanelBuf b;
+  b.device = dev;
+  b.stream = s;
+  b.dir = 3;
+  b.bytes = 256;
+  cuda_check(cudaMalloc(&b.ptr, b.bytes), "cudaMalloc(grid barrier)");
+  cuda_check(cudaMemset(b.ptr, 0, b.bytes), "cudaMemset(grid barrier)");
+  p.panels.push_back(b);
+  return static_cast<unsigned int*>(b.ptr);
+}
+
+int device_sms() {
+  int dev = 0, n = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  return n;
+}
+
 TcBandCall tc_call(const Plan& p, bool bwd, int64_t n, int64_t plane, const float* in, float* out,
                    const float* weight, const float* bias) {
   TcBandCall c{};
@@ -257,7 +283,11 @@ WeightLaunch weight_args(const Plan& p, const DeviceTables& t, int64_t n, int64_
 size_t weight_ws_bytes(const Plan& p, int64_t n, int64_t plane) {
   const size_t cc = weight_cc_workspace_bytes(p.fwd.nblk(), p.fwd.max_block_len, n, plane);
   const size_t tc = tc_weight_supported(p.tc_wgt, plane) ? tc_weight_workspace_bytes(p.tc_wgt, n, plane) : 0;
-  return std::max(cc, tc);
+  const size_t tc2 = tc_wgrad2_supported(p.tc_wgt, plane, static_cast<int32_t>(p.cfg.group_width))
+                         ? tc_wgrad2_workspace_bytes(static_cast<int32_t>(p.cfg.c_out),
+                                                     static_cast<int32_t>(p.cfg.group_width), device_sms())
+                         : 0;
+  return std::max(std::max(cc, tc), tc2);
 }
 
 void do_forward(Plan& p, int64_t n, int64_t h, int64_t w, const float* x, const float* wt,
@@ -333,6 +363,10 @@ void do_backward_weight(Plan& p, int64_t n, int64_t h, int64_t w, const float* d
     c.inv_perm = t.inv_perm;
     c.rt_info = t.tcw_rt_info;
     c.class_d = t.tcw_class_d;
+    if (p.path != SCC_PATH_TENSOR_V1 && tc_wgrad2_supported(p.tc_wgt, h * w, c.gw)) {
+      cuda_check(launch_wgrad2(p.tc_wgt, c, t.perm, sync_buffer(p, s), s), "backward-weight (tensor) launch");
+      return;
+    }
     cuda_check(launch_weight_tc(p.tc_wgt, c, s), "backward-weight (tensor) launch");
     return;
   }
@@ -432,6 +466,14 @@ int scc_debug_trace(uint64_t* out, int n) {
   if (n < 192) return 128;
   // slots [128, 192): generation-2 band kernel; [192, 192 + 2*1024): per-CTA
   // start / epilogue-end timestamps of that kernel
+  if (n >= 128 + 64 + 2048 + 64) {
+    // slots [128, 192 + 2048): band gen 2; then 64 + 3*256 slots of backward-weight gen 2
+    if (scc::tc2_trace(reinterpret_cast<unsigned long long*>(out) + 128, 64 + 2048) < 0) return -1;
+    const int m = n - (128 + 64 + 2048);
+    return scc::tc_w2trace(reinterpret_cast<unsigned long long*>(out) + 128 + 64 + 2048, m) < 0
+               ? -1
+               : 128 + 64 + 2048 + m;
+  }
   const int m2 = n - 128 < 64 + 2048 ? n - 128 : 64 + 2048;
   return scc::tc2_trace(reinterpret_cast<unsigned long long*>(out) + 128, m2) < 0 ? -1 : 128 + m2;
 }

@@ -410,7 +410,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0) {
     // ---------------- producer ----------------
     if (elect_one()) {
-      if (a.debug & 1) mbar_wait_sleep(panel_bar, 0);
+      if (a.debug & 1) mbar_wait(panel_bar, 0);
       int s = 0;
       uint32_t ph = 0;
       TileIter it(a);
@@ -420,7 +420,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int start8 = a.rt_start8[rt], nk8 = a.rt_nk8[rt];
           const int nch = (nk8 + 3) >> 2;
           for (int c = 0; c < nch; ++c) {
-            mbar_wait_sleep(&afree[s], ph ^ 1u);
+            mbar_wait(&afree[s], ph ^ 1u);
             const int rows = min(4, nk8 - 4 * c) * 8;
             // One box {128 px, rb rows} per rb rows: stage = [32 rows][128 px].
             // A partial tile over-reads the neighbour's pixels (or zero-fills
@@ -453,7 +453,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         while (!mbar_try_wait(panel_bar, 0)) __nanosleep(1000);
       __syncwarp();
     } else {
-      mbar_wait_sleep(panel_bar, 0);
+      mbar_wait(panel_bar, 0);
     }
     tc_fence_after();
     TileIter it(a);
@@ -463,11 +463,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int nk8 = a.rt_nk8[rt];
         const int nch = (nk8 + 3) >> 2;
         const int cb = a.rt_cb[rt];
-        mbar_wait_sleep(&tempty[acc], aph ^ 1u);
+        mbar_wait(&tempty[acc], aph ^ 1u);
         tc_fence_after();
         const uint32_t d_tmem = tmem + acc * NT;
         for (int c = 0; c < nch; ++c) {
-          mbar_wait_sleep(&conv[st], tph);
+          mbar_wait(&conv[st], tph);
           tc_fence_after();
           if (elect_one()) {
             const int steps = min(4, nk8 - 4 * c);
@@ -505,10 +505,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_expect_tx(w_bar, bytes);
         bulk_load(w_s, a.weight, bytes, w_bar);
       }
-      mbar_wait_sleep(tab_bar, 0);
+      mbar_wait(tab_bar, 0);
       if (ct == 0) TRACE2(4);
       if (a.w_staged) {
-        mbar_wait_sleep(w_bar, 0);
+        mbar_wait(w_bar, 0);
         if (ct == 0) TRACE2(5);
       }
       if (ct == 0) TRACE2(50);
@@ -539,7 +539,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int nk8 = a.rt_nk8[rt];
           const int nch = (nk8 + 3) >> 2;
           for (int c = 0; c < nch; ++c) {
-            mbar_wait_sleep(&full[s], ph);
+            mbar_wait(&full[s], ph);
             if (q == 0 && lane == 0 && cc < 8) TRACE2(22 + cc);
             // Element (row r, pixel 32q + lane) of the [32 rows][128 px] stage.
             // Rows past the chunk's k-steps hold stale data that lands in TMEM
@@ -554,13 +554,18 @@ __global__ void __launch_bounds__(kThreads, 1)
               lo[r] = __float_as_uint(v - h);
             }
             __syncwarp();
+            const bool trc = q == 0 && lane == 0 && blockIdx.x == 0 && cc < 2;
+            if (trc) g_trace2[54 + 4 * cc] = globaltimer();
             if (lane == 0) mbar_arrive(&afree[s]);
-            mbar_wait_sleep(&tfree[st], tph ^ 1u);
+            mbar_wait(&tfree[st], tph ^ 1u);
             tc_fence_after();
+            if (trc) g_trace2[55 + 4 * cc] = globaltimer();
             const uint32_t col = tmem + kACol0 + st * 64 + lane_base;
             tmem_st32(col, hi);
             tmem_st32(col + 32, lo);
+            if (trc) g_trace2[56 + 4 * cc] = globaltimer();
             tmem_st_wait();
+            if (trc) g_trace2[57 + 4 * cc] = globaltimer();
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&conv[st]);
@@ -574,7 +579,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     } else if (warp >= 8) {
     // ---------------- epilogue (warps 8..11) ----------------
     const int et = threadIdx.x - 256;  // 0..127
-    mbar_wait_sleep(tab_bar, 0);
+    mbar_wait(tab_bar, 0);
     for (int i = et; i < a.n_rt * NT; i += 128) {
       const int row = rows_s[i];
       bias_s[i] = (a.bias != nullptr && row >= 0) ? __ldg(a.bias + row) : 0.f;
@@ -593,7 +598,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const bool valid = q < it.cnt && px < a.plane;
       float* obase = a.out + static_cast<int64_t>(it.n) * a.c_out_t * a.plane + px;
       for (int rt = 0; rt < a.n_rt; ++rt) {
-        mbar_wait_sleep(&tfull[acc], aph);
+        mbar_wait(&tfull[acc], aph);
         tc_fence_after();
         if (q < it.cnt) {
           if (whole) {
