@@ -7,6 +7,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <cstdlib>
 #include <cstring>
 #include <exception>
 #include <mutex>
@@ -285,7 +286,7 @@ size_t weight_ws_bytes(const Plan& p, int64_t n, int64_t plane) {
   const size_t tc = tc_weight_supported(p.tc_wgt, plane) ? tc_weight_workspace_bytes(p.tc_wgt, n, plane) : 0;
   const size_t tc2 = tc_wgrad2_supported(p.tc_wgt, plane, static_cast<int32_t>(p.cfg.group_width))
                          ? tc_wgrad2_workspace_bytes(static_cast<int32_t>(p.cfg.c_out),
-                                                     static_cast<int32_t>(p.cfg.group_width), device_sms())
+                                                     static_cast<int32_t>(p.cfg.group_width), 148)
                          : 0;
   return std::max(std::max(cc, tc), tc2);
 }
@@ -313,7 +314,7 @@ void do_forward(Plan& p, int64_t n, int64_t h, int64_t w, const float* x, const 
 }
 
 void do_backward_data(Plan& p, int64_t n, int64_t h, int64_t w, const float* dy, const float* wt,
-                      float* dx, cudaStream_t s) {
+                      float* dx, cudaStream_t s, int32_t max_ctas = 0) {
   check_extents(n, h, w);
   check_ptr(dy, "dy");
   check_ptr(wt, "weight");
@@ -321,6 +322,7 @@ void do_backward_data(Plan& p, int64_t n, int64_t h, int64_t w, const float* dy,
   const DeviceTables& t = tables(p);
   if (choose_path(p, n, h, w, 1) == SCC_PATH_TENSOR) {
     TcBandCall c = tc_call(p, true, n, h * w, dy, dx, wt, nullptr);
+    c.max_ctas = max_ctas;
     if (p.path != SCC_PATH_TENSOR_V1 && tc_band2_supported(p.tc_bwd, h * w, static_cast<int32_t>(p.cfg.c_out))) {
       cuda_check(launch_band_tc2(p.tc_bwd, t.tc_bwd, c, p.cfg.shift, static_cast<int32_t>(p.cfg.c_out), s),
                  "backward-data (tensor) launch");
@@ -335,7 +337,8 @@ void do_backward_data(Plan& p, int64_t n, int64_t h, int64_t w, const float* dy,
 }
 
 void do_backward_weight(Plan& p, int64_t n, int64_t h, int64_t w, const float* dy, const float* x,
-                        float* dw, float* db, void* ws, size_t ws_bytes, cudaStream_t s) {
+                        float* dw, float* db, void* ws, size_t ws_bytes, cudaStream_t s,
+                        int32_t max_ctas = 0) {
   check_extents(n, h, w);
   check_ptr(dy, "dy");
   check_ptr(x, "x");
@@ -363,6 +366,7 @@ void do_backward_weight(Plan& p, int64_t n, int64_t h, int64_t w, const float* d
     c.inv_perm = t.inv_perm;
     c.rt_info = t.tcw_rt_info;
     c.class_d = t.tcw_class_d;
+    c.max_ctas = max_ctas;
     if (p.path != SCC_PATH_TENSOR_V1 && tc_wgrad2_supported(p.tc_wgt, h * w, c.gw)) {
       cuda_check(launch_wgrad2(p.tc_wgt, c, t.perm, sync_buffer(p, s), s), "backward-weight (tensor) launch");
       return;
@@ -372,6 +376,59 @@ void do_backward_weight(Plan& p, int64_t n, int64_t h, int64_t w, const float* d
   }
   cuda_check(launch_weight_cc(weight_args(p, t, n, h * w, dy, x, dw, db, ws), ws_bytes, s),
              "backward-weight launch");
+}
+
+ForkJoin& fork_join(Plan& p, cudaStream_t s) {
+  const int dev = current_device();
+  std::lock_guard<std::mutex> lk(p.panel_mu);
+  for (ForkJoin& f : p.forks) {
+    if (f.device == dev && f.stream == static_cast<void*>(s)) return f;
+  }
+  ForkJoin f;
+  f.device = dev;
+  f.stream = s;
+  cudaStream_t side;
+  cudaEvent_t a, b;
+  cuda_check(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking), "cudaStreamCreate(side)");
+  cuda_check(cudaEventCreateWithFlags(&a, cudaEventDisableTiming), "cudaEventCreate");
+  cuda_check(cudaEventCreateWithFlags(&b, cudaEventDisableTiming), "cudaEventCreate");
+  f.side = side;
+  f.ev_fork = a;
+  f.ev_join = b;
+  p.forks.push_back(f);
+  return p.forks.back();
+}
+
+// scc_backward (kernel.cpp:183-189): backward-data and backward-weight read
+// the same dy but are otherwise independent.  When both run the generation-2
+// tensor-core kernels, they run concurrently on disjoint halves of the SMs
+// (backward-weight on a side stream, joined back into the caller's stream),
+// so each one's start-up and tail overlap the other's streaming.
+void do_backward(Plan& p, int64_t n, int64_t h, int64_t w, const float* dy, const float* x,
+                 const float* wt, float* dx, float* dw, float* db, void* ws, size_t ws_bytes,
+                 cudaStream_t s) {
+  const int64_t plane = h * w;
+  const bool both2 = p.path != SCC_PATH_TENSOR_V1 && p.path != SCC_PATH_CUDA_CORE &&
+                     choose_path(p, n, h, w, 1) == SCC_PATH_TENSOR &&
+                     choose_path(p, n, h, w, 2) == SCC_PATH_TENSOR &&
+                     tc_band2_supported(p.tc_bwd, plane, static_cast<int32_t>(p.cfg.c_out)) &&
+                     tc_wgrad2_supported(p.tc_wgt, plane, static_cast<int32_t>(p.cfg.group_width));
+  const char* env = getenv("SCC_SERIAL_BACKWARD");
+  if (!both2 || (env != nullptr && env[0] == '1')) {
+    do_backward_data(p, n, h, w, dy, wt, dx, s);
+    do_backward_weight(p, n, h, w, dy, x, dw, db, ws, ws_bytes, s);
+    return;
+  }
+  const int nsm = device_sms();
+  const int32_t half = nsm / 2;
+  ForkJoin& f = fork_join(p, s);
+  cudaStream_t side = static_cast<cudaStream_t>(f.side);
+  cuda_check(cudaEventRecord(static_cast<cudaEvent_t>(f.ev_fork), s), "cudaEventRecord(fork)");
+  cuda_check(cudaStreamWaitEvent(side, static_cast<cudaEvent_t>(f.ev_fork), 0), "cudaStreamWaitEvent(fork)");
+  do_backward_weight(p, n, h, w, dy, x, dw, db, ws, ws_bytes, side, nsm - half);
+  do_backward_data(p, n, h, w, dy, wt, dx, s, half);
+  cuda_check(cudaEventRecord(static_cast<cudaEvent_t>(f.ev_join), side), "cudaEventRecord(join)");
+  cuda_check(cudaStreamWaitEvent(s, static_cast<cudaEvent_t>(f.ev_join), 0), "cudaStreamWaitEvent(join)");
 }
 
 // Host-buffer staging ------------------------------------------------------
@@ -529,6 +586,13 @@ scc_status_t scc_plan_destroy(scc_plan_t* plan) {
       if (s.buf) cudaFree(s.buf);
       if (s.stream) cudaStreamDestroy(static_cast<cudaStream_t>(s.stream));
     }
+    for (const scc::ForkJoin& f : plan->forks) {
+      cudaSetDevice(f.device);
+      cudaStreamSynchronize(static_cast<cudaStream_t>(f.side));
+      cudaStreamDestroy(static_cast<cudaStream_t>(f.side));
+      cudaEventDestroy(static_cast<cudaEvent_t>(f.ev_fork));
+      cudaEventDestroy(static_cast<cudaEvent_t>(f.ev_join));
+    }
     if (prev >= 0) cudaSetDevice(prev);
     delete plan;
   });
@@ -665,8 +729,7 @@ scc_status_t scc_backward_f32(const scc_plan_t* plan, int64_t n, int64_t h, int6
     scc::check_ptr(plan, "plan");
     auto& p = *const_cast<scc_plan_t*>(plan);
     const auto s = static_cast<cudaStream_t>(stream);
-    scc::do_backward_data(p, n, h, w, dy, weight, dx, s);
-    scc::do_backward_weight(p, n, h, w, dy, x, dweight, dbias, workspace, workspace_bytes, s);
+    scc::do_backward(p, n, h, w, dy, x, weight, dx, dweight, dbias, workspace, workspace_bytes, s);
   });
 }
 
@@ -712,8 +775,7 @@ scc_status_t scc_backward_host_f32(scc_plan_t* plan, int64_t n, int64_t h, int64
     scc::h2d(g.dy, dy, ny, g.s);
     scc::h2d(g.x, x, nx, g.s);
     scc::h2d(g.w, weight, c.c_out * c.group_width * 4, g.s);
-    scc::do_backward_data(*plan, n, h, w, g.dy, g.w, g.dx, g.s);
-    scc::do_backward_weight(*plan, n, h, w, g.dy, g.x, g.dw, dbias ? g.db : nullptr, g.ws,
+    scc::do_backward(*plan, n, h, w, g.dy, g.x, g.w, g.dx, g.dw, dbias ? g.db : nullptr, g.ws,
                             g.ws_bytes, g.s);
     scc::d2h(dx, g.dx, nx, g.s);
     scc::d2h(dweight, g.dw, c.c_out * c.group_width * 4, g.s);
@@ -746,8 +808,7 @@ scc_status_t scc_fwd_bwd_host_f32(scc_plan_t* plan, int64_t n, int64_t h, int64_
     if (bias) scc::h2d(g.b, bias, c.c_out * 4, g.s);
     scc::h2d(g.dy, dy, ny, g.s);
     scc::do_forward(*plan, n, h, w, g.x, g.w, bias ? g.b : nullptr, g.y, g.s);
-    scc::do_backward_data(*plan, n, h, w, g.dy, g.w, g.dx, g.s);
-    scc::do_backward_weight(*plan, n, h, w, g.dy, g.x, g.dw, dbias ? g.db : nullptr, g.ws,
+    scc::do_backward(*plan, n, h, w, g.dy, g.x, g.w, g.dx, g.dw, dbias ? g.db : nullptr, g.ws,
                             g.ws_bytes, g.s);
     scc::d2h(y, g.y, ny, g.s);
     scc::d2h(dx, g.dx, nx, g.s);

@@ -59,6 +59,7 @@ struct TcBandCall {
   int32_t c_out_t;      // channels of the output tensor
   bool backward_data;
   float* panel;         // scratch for the band weight images (tc_panel_bytes)
+  int32_t max_ctas = 0; // grid cap (0 = one CTA per SM); the concurrent backward splits the SMs
 };
 
 size_t tc_panel_bytes(const TcBandPlan& tp);
@@ -77,6 +78,7 @@ struct TcWeightCall {
   const int32_t* inv_perm;  // oc -> sorted position
   const int32_t* rt_info;   // TcWeightPlan::rt_info (device)
   const int32_t* class_d;
+  int32_t max_ctas = 0;     // grid cap (0 = one CTA per SM)
 };
 bool tc_weight_supported(const TcWeightPlan& tw, int64_t plane);
 size_t tc_weight_workspace_bytes(const TcWeightPlan& tw, int64_t n, int64_t plane);

@@ -136,6 +136,16 @@ struct PanelBuf {
   size_t bytes = 0;
 };
 
+// Fork/join resources of the concurrent backward (backward-data on the caller
+// stream, backward-weight on a side stream), per (device, caller stream).
+struct ForkJoin {
+  int device = -1;
+  void* stream = nullptr;  // caller stream
+  void* side = nullptr;    // cudaStream_t
+  void* ev_fork = nullptr; // cudaEvent_t
+  void* ev_join = nullptr;
+};
+
 struct Plan {
   scc_config_t cfg{};
   std::vector<int64_t> cycle_starts;  // compute_channel_cycle order
@@ -152,6 +162,7 @@ struct Plan {
   std::deque<PanelBuf> panels;
   std::mutex host_mu;
   std::deque<HostStaging> staging;
+  std::deque<ForkJoin> forks;  // guarded by panel_mu
 
   int64_t start_of(int64_t oc) const { return (oc * cfg.shift) % cfg.c_in; }
   // Forward-band weight of output channel oc on input channel ic (0 outside

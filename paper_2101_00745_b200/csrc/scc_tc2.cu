@@ -822,7 +822,8 @@ cudaError_t launch_tc2_nt(const TcBandPlan& tp, const TcDeviceTables& dt, const 
     if (dev >= 0 && dev < 64) attr_set[dev] = true;
   }
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(static_cast<unsigned>(std::min<int64_t>(a.units, nsm)));
+  const int64_t cap = call.max_ctas > 0 ? std::min(call.max_ctas, nsm) : nsm;
+  cfg.gridDim = dim3(static_cast<unsigned>(std::min<int64_t>(a.units, cap)));
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;

@@ -53,7 +53,8 @@ constexpr int kThreads = 384;
 constexpr int kDyBytes = 128 * 128;   // [128 rows][32 px]
 constexpr int kMaxStages = 6;
 constexpr int kTStages = 4;           // TMEM A stages (hi + lo, 64 columns each)
-constexpr int kACol0 = 128;           // TMEM: [0, 128) accumulator, then A stages
+constexpr int kACol0 = 256;           // TMEM: two 128-column accumulators, then A stages
+constexpr int kSlices = 148;          // pixel slices (partials) of a launch
 constexpr int kMaxRt = 16;
 constexpr int kMaxCls = 64;
 constexpr int kSmemLimit = 227 * 1024;
@@ -79,7 +80,8 @@ struct W2Args {
   int32_t stages;
   int32_t nbps;              // 32-pixel blocks per sample
   int32_t units;             // n * nbps
-  int32_t elems;             // c_out*gw + c_out
+  int32_t elems;             // per-slice partial floats: n_rt * (128*gw + 128)
+  int32_t slices;            // pixel slices (partials), fixed per launch geometry
 };
 
 // Filter of tile row `pos` (row tile * 128 + row): cycle-sorted order, or the
@@ -92,6 +94,13 @@ __device__ __forceinline__ int row_oc(const W2Args& a, int pos) {
   return __ldg(a.perm + pos);
 }
 
+// Pixel slices: a fixed number of contiguous block ranges (independent of the
+// grid size), each accumulated in its own TMEM pass and written as its own
+// partial, so the reduction order -- and the bits of dW -- do not depend on
+// how many CTAs run.
+__device__ __forceinline__ int slice_u(const W2Args& a, int k) {
+  return static_cast<int>((static_cast<int64_t>(k) * a.units) / a.slices);
+}
 __device__ __forceinline__ void advance(int& stage, uint32_t& phase, int stages) {
   if (++stage == stages) {
     stage = 0;
@@ -109,7 +118,7 @@ struct WLayout {
     ring = 0;
     stg = stages * stage;        // epilogue row dump: [128][xr + 4] floats
     bars = stg + ((128 * (xr + 4) * 4 + 1023) & ~1023);
-    total = bars + (3 * kMaxStages + 2 * kTStages + 4) * 8 + 16;
+    total = bars + (3 * kMaxStages + 2 * kTStages + 6) * 8 + 16;
   }
 };
 
@@ -124,15 +133,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* xlo = sfree + kMaxStages;          // 2 lo-converter warps
   uint64_t* conv = xlo + kMaxStages;           // 4 row converters
   uint64_t* tfree = conv + kTStages;           // MMA commit
-  uint64_t* accfull = tfree + kTStages;        // MMA final commit of a row tile
-  uint64_t* accempty = accfull + 1;            // 4 epilogue warps
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accempty + 1);
+  uint64_t* accfull = tfree + kTStages;        // [2] MMA final commit of a (slice, row tile)
+  uint64_t* accempty = accfull + 2;            // [2] 4 epilogue warps
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accempty + 2);
   float* stg = reinterpret_cast<float*>(smem + L.stg);
 
   const uint32_t warp = warp_id();
   const int lane = threadIdx.x & 31;
-  const int u0 = static_cast<int>((static_cast<int64_t>(blockIdx.x) * a.units) / gridDim.x);
-  const int u1 = static_cast<int>((static_cast<int64_t>(blockIdx.x + 1) * a.units) / gridDim.x);
   if (threadIdx.x == 0) {
     W2T(0);
     if (blockIdx.x < 256) g_w2cta[3 * blockIdx.x] = globaltimer();
@@ -145,8 +152,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&conv[s], 4);
       mbar_init(&tfree[s], 1);
     }
-    mbar_init(accfull, 1);
-    mbar_init(accempty, 4);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&accfull[i], 1);
+      mbar_init(&accempty[i], 4);
+    }
     fence_mbar_init();
   }
   if (warp == 0 && lane == 0) {
@@ -173,84 +182,90 @@ __global__ void __launch_bounds__(kThreads, 1)
       int s = 0;
       uint32_t ph = 0;
       const uint32_t bytes = (a.dybox ? a.c_out * 128 : kDyBytes) + a.nx * 128;
-      for (int rt = 0; rt < a.n_rt; ++rt) {
-        const int start8 = a.rt_start8[rt];
-        for (int u = u0; u < u1; ++u) {
-          if (u == u0) W2T(40);
-          const int n = u / a.nbps, px0 = (u - n * a.nbps) * 32;
-          mbar_wait(&sfree[s], ph ^ 1u);
-          if (u == u0) W2T(41);
-          mbar_expect_tx(&full[s], bytes);
-          if (u == u0) W2T(42);
-          uint8_t* st = smem + s * L.stage;
-          if (a.dybox) {
-            tma_load_4d(st, &tdy, &full[s], px0, 0, 0, n);
-          } else
-          for (int r = 0; r < 128; r += a.rba) {
-            // sorted filter position rt*128 + r -> (class, j); positions past
-            // c_out read the next rows (zero-filled past the tensor) and feed
-            // accumulator rows the epilogue ignores
-            int pos = rt * 128 + r;
-            pos = pos < a.c_out ? pos : a.c_out - a.rba;
-            const int cl = pos / a.cls, j = pos - cl * a.cls;
-            tma_load_4d(st + r * 128, &tdy, &full[s], px0, j, a.class_d[cl], n);
-            if (u == u0 && r == 0) W2T(43);
+      for (int sl = blockIdx.x; sl < a.slices; sl += gridDim.x) {
+        const int u0 = slice_u(a, sl), u1 = slice_u(a, sl + 1);
+        for (int rt = 0; rt < a.n_rt; ++rt) {
+          const int start8 = a.rt_start8[rt];
+          for (int u = u0; u < u1; ++u) {
+            if (u == u0) W2T(40);
+            const int n = u / a.nbps, px0 = (u - n * a.nbps) * 32;
+            mbar_wait(&sfree[s], ph ^ 1u);
+            if (u == u0) W2T(41);
+            mbar_expect_tx(&full[s], bytes);
+            if (u == u0) W2T(42);
+            uint8_t* st = smem + s * L.stage;
+            if (a.dybox) {
+              tma_load_4d(st, &tdy, &full[s], px0, 0, 0, n);
+            } else
+            for (int r = 0; r < 128; r += a.rba) {
+              // sorted filter position rt*128 + r -> (class, j); positions past
+              // c_out read the next rows (zero-filled past the tensor) and feed
+              // accumulator rows the epilogue ignores
+              int pos = rt * 128 + r;
+              pos = pos < a.c_out ? pos : a.c_out - a.rba;
+              const int cl = pos / a.cls, j = pos - cl * a.cls;
+              tma_load_4d(st + r * 128, &tdy, &full[s], px0, j, a.class_d[cl], n);
+              if (u == u0 && r == 0) W2T(43);
+            }
+            if (u == u0) W2T(44);
+            if (a.xbox) {
+              tma_load_3d(st + L.xoff, &tx, &full[s], px0, start8, n);
+            } else
+            for (int r = 0; r < a.nx; r += a.rbb) {
+              int ic = start8 + r;
+              ic -= ic >= a.c_in ? a.c_in : 0;
+              tma_load_3d(st + L.xoff + r * 128, &tx, &full[s], px0, ic, n);
+            }
+            if (u - u0 < 8) W2T(2 + u - u0);
+            advance(s, ph, a.stages);
           }
-          if (u == u0) W2T(44);
-          if (a.xbox) {
-            tma_load_3d(st + L.xoff, &tx, &full[s], px0, start8, n);
-          } else
-          for (int r = 0; r < a.nx; r += a.rbb) {
-            int ic = start8 + r;
-            ic -= ic >= a.c_in ? a.c_in : 0;
-            tma_load_3d(st + L.xoff + r * 128, &tx, &full[s], px0, ic, n);
-          }
-          if (u - u0 < 8) W2T(2 + u - u0);
-          advance(s, ph, a.stages);
         }
       }
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer ----------------
     const uint32_t idesc = idesc_tf32(128, static_cast<uint32_t>(a.xr), 0, 0);
-    int s = 0, st = 0;
+    int s = 0, st = 0, acc = 0;
     uint32_t ph = 0, tph = 0, aph = 0;
-    for (int rt = 0; rt < a.n_rt; ++rt) {
-      mbar_wait(accempty, aph ^ 1u);
-      tc_fence_after();
-      bool first = true;
-      for (int u = u0; u < u1; ++u) {
-        mbar_wait(&xlo[s], ph);
-        mbar_wait(&conv[st], tph);
+    for (int sl = blockIdx.x; sl < a.slices; sl += gridDim.x) {
+      const int u0 = slice_u(a, sl), u1 = slice_u(a, sl + 1);
+      for (int rt = 0; rt < a.n_rt; ++rt) {
+        mbar_wait(&accempty[acc], aph ^ 1u);
         tc_fence_after();
-        if (elect_one()) {
-          const uint32_t bx = smem_u32(smem + s * L.stage + L.xoff);
-          const uint32_t bl = smem_u32(smem + s * L.stage + L.xlo);
-          const uint32_t ah = tmem + kACol0 + st * 64, al = ah + 32;
-          for (int k = 0; k < 4; ++k) {
-            const uint64_t dbx = desc_sw128(bx + k * 32, 16, 1024);
-            const uint64_t dbl = desc_sw128(bl + k * 32, 16, 1024);
-            mma_tf32_ts(tmem, ah + 8 * k, dbx, idesc, (first && k == 0) ? 0u : 1u);
-            mma_tf32_ts(tmem, al + 8 * k, dbx, idesc, 1);
-            mma_tf32_ts(tmem, ah + 8 * k, dbl, idesc, 1);
+        const uint32_t dacc = tmem + acc * 128;
+        bool first = true;
+        for (int u = u0; u < u1; ++u) {
+          mbar_wait(&xlo[s], ph);
+          mbar_wait(&conv[st], tph);
+          tc_fence_after();
+          if (elect_one()) {
+            const uint32_t bx = smem_u32(smem + s * L.stage + L.xoff);
+            const uint32_t bl = smem_u32(smem + s * L.stage + L.xlo);
+            const uint32_t ah = tmem + kACol0 + st * 64, al = ah + 32;
+            for (int k = 0; k < 4; ++k) {
+              const uint64_t dbx = desc_sw128(bx + k * 32, 16, 1024);
+              const uint64_t dbl = desc_sw128(bl + k * 32, 16, 1024);
+              mma_tf32_ts(dacc, ah + 8 * k, dbx, idesc, (first && k == 0) ? 0u : 1u);
+              mma_tf32_ts(dacc, al + 8 * k, dbx, idesc, 1);
+              mma_tf32_ts(dacc, ah + 8 * k, dbl, idesc, 1);
+            }
+            mma_commit(&tfree[st]);
+            mma_commit(&sfree[s]);
+            if (u - u0 < 8) W2T(10 + u - u0);
           }
-          mma_commit(&tfree[st]);
-          mma_commit(&sfree[s]);
-          if (u - u0 < 8) W2T(10 + u - u0);
+          __syncwarp();
+          first = false;
+          advance(s, ph, a.stages);
+          advance(st, tph, kTStages);
         }
+        // (an empty slice accumulates nothing; the epilogue writes zeros)
+        if (elect_one()) mma_commit(&accfull[acc]);
         __syncwarp();
-        first = false;
-        advance(s, ph, a.stages);
-        advance(st, tph, kTStages);
-      }
-      if (elect_one()) {
-        if (first) {
-          // no pixels for this CTA: nothing accumulated; the epilogue writes zeros
+        if (++acc == 2) {
+          acc = 0;
+          aph ^= 1u;
         }
-        mma_commit(accfull);
       }
-      __syncwarp();
-      aph ^= 1u;
     }
   } else if (warp < 4) {
     // ---------------- x lo converters ----------------
@@ -271,31 +286,34 @@ __global__ void __launch_bounds__(kThreads, 1)
     int s = 0;
     uint32_t ph = 0;
     const int words = a.nx * 8;  // float4 per x stage
-    for (int rt = 0; rt < a.n_rt; ++rt) {
-      for (int u = u0; u < u1; ++u) {
-        mbar_wait(&full[s], ph);
-        const float4* src = reinterpret_cast<const float4*>(smem + s * L.stage + L.xoff);
-        const uint32_t dst = smem_u32(smem + s * L.stage + L.xlo);
-        for (int i0 = ct; i0 < words; i0 += 64 * 4) {
-          float4 v[4];
-#pragma unroll
-          for (int b = 0; b < 4; ++b) v[b] = src[min(i0 + 64 * b, words - 1)];
-#pragma unroll
-          for (int b = 0; b < 4; ++b) {
-            if (i0 + 64 * b < words) {
-              float4 o;
-              o.x = v[b].x - tf32_hi(v[b].x);
-              o.y = v[b].y - tf32_hi(v[b].y);
-              o.z = v[b].z - tf32_hi(v[b].z);
-              o.w = v[b].w - tf32_hi(v[b].w);
-              sts_v4(dst + (i0 + 64 * b) * 16, o);
+    for (int sl = blockIdx.x; sl < a.slices; sl += gridDim.x) {
+      const int u0 = slice_u(a, sl), u1 = slice_u(a, sl + 1);
+      for (int rt = 0; rt < a.n_rt; ++rt) {
+        for (int u = u0; u < u1; ++u) {
+          mbar_wait(&full[s], ph);
+          const float4* src = reinterpret_cast<const float4*>(smem + s * L.stage + L.xoff);
+          const uint32_t dst = smem_u32(smem + s * L.stage + L.xlo);
+          for (int i0 = ct; i0 < words; i0 += 64 * 4) {
+            float4 v[4];
+  #pragma unroll
+            for (int b = 0; b < 4; ++b) v[b] = src[min(i0 + 64 * b, words - 1)];
+  #pragma unroll
+            for (int b = 0; b < 4; ++b) {
+              if (i0 + 64 * b < words) {
+                float4 o;
+                o.x = v[b].x - tf32_hi(v[b].x);
+                o.y = v[b].y - tf32_hi(v[b].y);
+                o.z = v[b].z - tf32_hi(v[b].z);
+                o.w = v[b].w - tf32_hi(v[b].w);
+                sts_v4(dst + (i0 + 64 * b) * 16, o);
+              }
             }
           }
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&xlo[s]);
+          advance(s, ph, a.stages);
         }
-        fence_proxy_async_smem();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&xlo[s]);
-        advance(s, ph, a.stages);
       }
     }
   } else if (warp < 8) {
@@ -305,37 +323,40 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t lane_base = static_cast<uint32_t>(q * 32) << 16;
     int s = 0, st = 0;
     uint32_t ph = 0, tph = 0;
-    for (int rt = 0; rt < a.n_rt; ++rt) {
-      for (int u = u0; u < u1; ++u) {
-        mbar_wait(&full[s], ph);
-        if (row == 0 && u - u0 < 8) W2T(18 + u - u0);
-        const float4* rp = reinterpret_cast<const float4*>(smem + s * L.stage + row * 128);
-        uint32_t hi[32], lo[32];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const float4 v = rp[j ^ (row & 7)];  // SWIZZLE_128B: logical chunk j
-          const float e[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-          for (int t = 0; t < 4; ++t) {
-            const float h = tf32_hi(e[t]);
-            hi[4 * j + t] = __float_as_uint(h);
-            lo[4 * j + t] = __float_as_uint(e[t] - h);
+    for (int sl = blockIdx.x; sl < a.slices; sl += gridDim.x) {
+      const int u0 = slice_u(a, sl), u1 = slice_u(a, sl + 1);
+      for (int rt = 0; rt < a.n_rt; ++rt) {
+        for (int u = u0; u < u1; ++u) {
+          mbar_wait(&full[s], ph);
+          if (row == 0 && u - u0 < 8) W2T(18 + u - u0);
+          const float4* rp = reinterpret_cast<const float4*>(smem + s * L.stage + row * 128);
+          uint32_t hi[32], lo[32];
+  #pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const float4 v = rp[j ^ (row & 7)];  // SWIZZLE_128B: logical chunk j
+            const float e[4] = {v.x, v.y, v.z, v.w};
+  #pragma unroll
+            for (int t = 0; t < 4; ++t) {
+              const float h = tf32_hi(e[t]);
+              hi[4 * j + t] = __float_as_uint(h);
+              lo[4 * j + t] = __float_as_uint(e[t] - h);
+            }
           }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&sfree[s]);
+          mbar_wait(&tfree[st], tph ^ 1u);
+          tc_fence_after();
+          const uint32_t col = tmem + kACol0 + st * 64 + lane_base;
+          tmem_st32(col, hi);
+          tmem_st32(col + 32, lo);
+          tmem_st_wait();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&conv[st]);
+          if (row == 0 && u - u0 < 8) W2T(26 + u - u0);
+          advance(s, ph, a.stages);
+          advance(st, tph, kTStages);
         }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&sfree[s]);
-        mbar_wait(&tfree[st], tph ^ 1u);
-        tc_fence_after();
-        const uint32_t col = tmem + kACol0 + st * 64 + lane_base;
-        tmem_st32(col, hi);
-        tmem_st32(col + 32, lo);
-        tmem_st_wait();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&conv[st]);
-        if (row == 0 && u - u0 < 8) W2T(26 + u - u0);
-        advance(s, ph, a.stages);
-        advance(st, tph, kTStages);
       }
     }
   } else {
@@ -347,57 +368,64 @@ __global__ void __launch_bounds__(kThreads, 1)
     float* prow = stg + i * rstride;
     const uint32_t prow_a = smem_u32(prow);
     uint32_t aph = 0;
-    for (int rt = 0; rt < a.n_rt; ++rt) {
-      mbar_wait(accfull, aph);
-      tc_fence_after();
-      if (i == 0) {
-        W2T(34);
-        if (blockIdx.x < 256) g_w2cta[3 * blockIdx.x + 1] = globaltimer();
+    int acc = 0;
+    for (int sl = blockIdx.x; sl < a.slices; sl += gridDim.x) {
+      const int u0 = slice_u(a, sl), u1 = slice_u(a, sl + 1);
+      for (int rt = 0; rt < a.n_rt; ++rt) {
+        mbar_wait(&accfull[acc], aph);
+        tc_fence_after();
+        if (i == 0) {
+          W2T(34);
+          if (blockIdx.x < 256) g_w2cta[3 * blockIdx.x + 1] = globaltimer();
+        }
+        // own TMEM row (lane = tile row) -> own smem dump row
+        for (int c0 = 0; c0 < a.xr; c0 += 32) {
+          uint32_t v[32];
+          tmem_ld32_nowait(taddr + acc * 128 + c0, v);
+          tmem_ld_wait();
+  #pragma unroll
+          for (int t = 0; t < 32; t += 4)
+            if (c0 + t < a.xr)
+              sts_v4(prow_a + (c0 + t) * 4, make_float4(__uint_as_float(v[t]), __uint_as_float(v[t + 1]),
+                                                        __uint_as_float(v[t + 2]), __uint_as_float(v[t + 3])));
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&accempty[acc]);
+        if (++acc == 2) {
+          acc = 0;
+          aph ^= 1u;
+        }
+        // window-relative values of this row, written straight to the CTA's
+        // partial tile [128 rows][gw] | db[128] (each thread a contiguous row)
+        const int pos = rt * 128 + i;
+        const bool live = pos < a.c_out && u0 < u1;
+        int j0 = 0;
+        if (live) {
+          j0 = __ldg(a.starts + row_oc(a, pos)) - a.rt_start8[rt];
+          j0 += j0 < 0 ? a.c_in : 0;
+        }
+        float* dst = a.part + static_cast<int64_t>(sl) * a.elems +
+                     static_cast<int64_t>(rt) * (128 * a.gw + 128);
+        float wv[kMaxGw];
+  #pragma unroll
+        for (int sl = 0; sl < kMaxGw; ++sl) {
+          int j = j0 + sl;
+          j -= j >= a.c_in ? a.c_in : 0;
+          wv[sl] = (live && sl < a.gw) ? prow[j] : 0.f;
+        }
+        if ((a.gw & 3) == 0) {
+  #pragma unroll
+          for (int sl = 0; sl < kMaxGw; sl += 4)
+            if (sl < a.gw)
+              *reinterpret_cast<float4*>(dst + i * a.gw + sl) = make_float4(wv[sl], wv[sl + 1], wv[sl + 2], wv[sl + 3]);
+        } else {
+  #pragma unroll
+          for (int sl = 0; sl < kMaxGw; ++sl)
+            if (sl < a.gw) dst[i * a.gw + sl] = wv[sl];
+        }
+        dst[128 * a.gw + i] = live ? prow[a.nx] : 0.f;
       }
-      // own TMEM row (lane = tile row) -> own smem dump row
-      for (int c0 = 0; c0 < a.xr; c0 += 32) {
-        uint32_t v[32];
-        tmem_ld32_nowait(taddr + c0, v);
-        tmem_ld_wait();
-#pragma unroll
-        for (int t = 0; t < 32; t += 4)
-          if (c0 + t < a.xr)
-            sts_v4(prow_a + (c0 + t) * 4, make_float4(__uint_as_float(v[t]), __uint_as_float(v[t + 1]),
-                                                      __uint_as_float(v[t + 2]), __uint_as_float(v[t + 3])));
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(accempty);
-      aph ^= 1u;
-      // window-relative values of this row, written straight to the CTA's
-      // partial tile [128 rows][gw] | db[128] (each thread a contiguous row)
-      const int pos = rt * 128 + i;
-      const bool live = pos < a.c_out && u0 < u1;
-      int j0 = 0;
-      if (live) {
-        j0 = __ldg(a.starts + row_oc(a, pos)) - a.rt_start8[rt];
-        j0 += j0 < 0 ? a.c_in : 0;
-      }
-      float* dst = a.part + static_cast<int64_t>(blockIdx.x) * a.elems +
-                   static_cast<int64_t>(rt) * (128 * a.gw + 128);
-      float wv[kMaxGw];
-#pragma unroll
-      for (int sl = 0; sl < kMaxGw; ++sl) {
-        int j = j0 + sl;
-        j -= j >= a.c_in ? a.c_in : 0;
-        wv[sl] = (live && sl < a.gw) ? prow[j] : 0.f;
-      }
-      if ((a.gw & 3) == 0) {
-#pragma unroll
-        for (int sl = 0; sl < kMaxGw; sl += 4)
-          if (sl < a.gw)
-            *reinterpret_cast<float4*>(dst + i * a.gw + sl) = make_float4(wv[sl], wv[sl + 1], wv[sl + 2], wv[sl + 3]);
-      } else {
-#pragma unroll
-        for (int sl = 0; sl < kMaxGw; ++sl)
-          if (sl < a.gw) dst[i * a.gw + sl] = wv[sl];
-      }
-      dst[128 * a.gw + i] = live ? prow[a.nx] : 0.f;
     }
   }
 
@@ -434,7 +462,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
       for (int m = 0; m < kRedMax; ++m) {
         const int k = grp + 12 * m;
-        v[m] = (e < e1 && k < static_cast<int>(gridDim.x)) ? __ldcg(a.part + static_cast<int64_t>(k) * a.elems + e) : 0.f;
+        v[m] = (e < e1 && k < a.slices) ? __ldcg(a.part + static_cast<int64_t>(k) * a.elems + e) : 0.f;
       }
       float acc = 0.f;
 #pragma unroll
@@ -496,9 +524,9 @@ int tc_w2trace(unsigned long long* out, int n) {
   return n;
 }
 
-size_t tc_wgrad2_workspace_bytes(int32_t c_out, int32_t gw, int nsm) {
+size_t tc_wgrad2_workspace_bytes(int32_t c_out, int32_t gw, int slices) {
   const size_t n_rt = (c_out + 127) / 128;
-  return static_cast<size_t>(nsm) * n_rt * (128 * static_cast<size_t>(gw) + 128) * sizeof(float);
+  return static_cast<size_t>(slices) * n_rt * (128 * static_cast<size_t>(gw) + 128) * sizeof(float);
 }
 
 cudaError_t launch_wgrad2(const TcWeightPlan& tw, const TcWeightCall& call, const int32_t* perm,
@@ -542,8 +570,10 @@ cudaError_t launch_wgrad2(const TcWeightPlan& tw, const TcWeightCall& call, cons
   if (units > (1ll << 30)) return cudaErrorInvalidValue;
   a.units = static_cast<int32_t>(units);
   a.elems = tw.n_rt * (128 * call.gw + 128);
-  const int grid = static_cast<int>(std::min<int64_t>(std::min<int64_t>(units, nsm), 12 * kRedMax));
-  if (tc_wgrad2_workspace_bytes(call.c_out, call.gw, grid) > call.workspace_bytes) return cudaErrorInvalidValue;
+  a.slices = static_cast<int32_t>(std::min<int64_t>(units, kSlices));
+  const int cap = call.max_ctas > 0 ? std::min(call.max_ctas, nsm) : nsm;
+  const int grid = std::min(a.slices, cap);
+  if (tc_wgrad2_workspace_bytes(call.c_out, call.gw, a.slices) > call.workspace_bytes) return cudaErrorInvalidValue;
   a.part = static_cast<float*>(call.workspace);
   a.dweight = call.dweight;
   a.dbias = call.dbias;
