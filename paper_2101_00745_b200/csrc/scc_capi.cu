@@ -286,7 +286,7 @@ size_t weight_ws_bytes(const Plan& p, int64_t n, int64_t plane) {
   const size_t tc = tc_weight_supported(p.tc_wgt, plane) ? tc_weight_workspace_bytes(p.tc_wgt, n, plane) : 0;
   const size_t tc2 = tc_wgrad2_supported(p.tc_wgt, plane, static_cast<int32_t>(p.cfg.group_width))
                          ? tc_wgrad2_workspace_bytes(static_cast<int32_t>(p.cfg.c_out),
-                                                     static_cast<int32_t>(p.cfg.group_width), 148)
+                                                     static_cast<int32_t>(p.cfg.group_width), 74)
                          : 0;
   return std::max(std::max(cc, tc), tc2);
 }
@@ -420,13 +420,16 @@ void do_backward(Plan& p, int64_t n, int64_t h, int64_t w, const float* dy, cons
     return;
   }
   const int nsm = device_sms();
-  const int32_t half = nsm / 2;
+  int32_t half = nsm / 2;
+  if (const char* sp = getenv("SCC_BWD_SPLIT")) half = atoi(sp);
   ForkJoin& f = fork_join(p, s);
   cudaStream_t side = static_cast<cudaStream_t>(f.side);
   cuda_check(cudaEventRecord(static_cast<cudaEvent_t>(f.ev_fork), s), "cudaEventRecord(fork)");
   cuda_check(cudaStreamWaitEvent(side, static_cast<cudaEvent_t>(f.ev_fork), 0), "cudaStreamWaitEvent(fork)");
-  do_backward_weight(p, n, h, w, dy, x, dw, db, ws, ws_bytes, side, nsm - half);
+  // backward-data first: the kernel enqueued second starts ~1 us later, and
+  // backward-data has the longer critical path
   do_backward_data(p, n, h, w, dy, wt, dx, s, half);
+  do_backward_weight(p, n, h, w, dy, x, dw, db, ws, ws_bytes, side, nsm - half);
   cuda_check(cudaEventRecord(static_cast<cudaEvent_t>(f.ev_join), side), "cudaEventRecord(join)");
   cuda_check(cudaStreamWaitEvent(s, static_cast<cudaEvent_t>(f.ev_join), 0), "cudaStreamWaitEvent(join)");
 }

@@ -53,28 +53,37 @@ namespace {
 
 using namespace sm100;
 
+// Diagnostic timeline (build with -DSCC_TRACE): CTA-0 %globaltimer slots and
+// per-CTA start / epilogue-end stamps; scripts/band_timing.py reads them.
+#if defined(SCC_TRACE)
 __device__ unsigned long long g_trace2[64];
-__device__ unsigned long long g_cta2[2 * 1024];  // per CTA: start, epilogue end
+__device__ unsigned long long g_cta2[2 * 1024];
 #define TRACE2(slot)                                         \
   do {                                                       \
     if (blockIdx.x == 0) g_trace2[(slot)] = globaltimer();   \
   } while (0)
+#define CTA_STAMP(k)                                                          \
+  do {                                                                        \
+    if (blockIdx.x < 1024) g_cta2[2 * blockIdx.x + (k)] = globaltimer();      \
+  } while (0)
+#else
+#define TRACE2(slot) \
+  do {               \
+  } while (0)
+#define CTA_STAMP(k) \
+  do {               \
+  } while (0)
+#endif
 
 constexpr int kThreads = 384;
 constexpr int kBlkPx = 32;                     // pixels per block (one 128 B row)
-constexpr int kStageBytes = 4 * 32 * 128;      // 4 blocks x 32 ring rows x 128 B
+constexpr int kStageBytes = 32 * 128 * 4;      // [32 ring rows][128 px]
 constexpr int kMaxStages = 8;
 constexpr int kTStages = 4;                    // TMEM A stages (hi + lo, 64 columns each)
 constexpr int kWorkers = 192;                  // warps 2, 3, 8..11: panel builders
 constexpr int kSmemLimit = 227 * 1024;
 constexpr int kStoreBuf = 32 * 32 * 4;         // one [32 rows][32 px] TMA-store box
-// Epilogue store modes.
-enum : int32_t {
-  kStoreStg = 0,      // plain stores from registers (ragged row sets)
-  kStoreRows32 = 1,   // [32 rows][32 px] boxes, 2 staging buffers per warp
-  kStoreClasses = 2,  // whole tile in one box {32 px, D classes, out_cls rows} (one row tile)
-  kStoreRowsNT = 3,   // whole tile in one box {32 px, 1, NT} (contiguous channel rows)
-};
+constexpr int kStoreBufs = 4;                  // per epilogue warp
 constexpr int kMaxScratch = 32 * 1024;         // W + oc tables staged for the panel build
 constexpr int kMaxRt = 16;                     // row tiles / classes carried in the params
 constexpr int kMaxCls = 64;
@@ -92,36 +101,33 @@ struct Band2Args {
   int32_t class_d[kMaxCls], out_class_d[kMaxCls];
   int32_t n_rt, ring, cls, rb;
   int32_t c_in, c_out, gw, c_out_t;
-  int32_t store_mode, out_cls, out_nd;  // TMA-store epilogue geometry
-  int32_t backward_data;
+  int32_t tma_store, out_cls;  // 1: [32 rows][32 px] TMA-store boxes; else plain stores
   int32_t w_staged;          // W + oc tables bulk-copied to smem for the panel build
-  int32_t fwd4;              // forward panel words are whole-window or empty (see build_panel_fwd4)
+  int32_t fwd4;              // forward panel words are whole-window or empty (build_panel_fwd4)
   int32_t nbps;              // 32-pixel blocks per sample
   int32_t stages;            // raw ring depth
   int32_t scratch;           // panel-build scratch bytes (W, starts, perm) in the staging area
   int32_t total_chunks;
-  int32_t debug;             // diagnostics: 1 = producer waits for the panel
-  int64_t plane, n;
-  int64_t units;             // n * nbps
+  int32_t units;             // n * nbps
+  int64_t plane;
 };
 
 // Contiguous run of blocks owned by this CTA, cut into tiles of <= 4 blocks
 // that never straddle a sample.
 struct TileIter {
-  int64_t u, u1;
-  int32_t nbps;
+  int32_t u, u1, nbps;
   int32_t n, b0, cnt;
-  __device__ TileIter(const Band2Args& a) {
-    u = blockIdx.x * a.units / gridDim.x;
-    u1 = (blockIdx.x + 1ll) * a.units / gridDim.x;
+  __device__ explicit TileIter(const Band2Args& a) {
+    u = static_cast<int32_t>((static_cast<int64_t>(blockIdx.x) * a.units) / gridDim.x);
+    u1 = static_cast<int32_t>((static_cast<int64_t>(blockIdx.x + 1) * a.units) / gridDim.x);
     nbps = a.nbps;
     n = b0 = cnt = 0;
   }
   __device__ bool next() {
     if (u >= u1) return false;
-    n = static_cast<int32_t>(u / nbps);
-    b0 = static_cast<int32_t>(u - static_cast<int64_t>(n) * nbps);
-    cnt = static_cast<int32_t>(min(static_cast<int64_t>(min(4, nbps - b0)), u1 - u));
+    n = u / nbps;
+    b0 = u - n * nbps;
+    cnt = min(min(4, nbps - b0), u1 - u);
     u += cnt;
     return true;
   }
@@ -137,18 +143,14 @@ __device__ __forceinline__ void advance(int& stage, uint32_t& phase, int stages)
 // Smem layout (host and device agree): panel | raw ring | store staging (also
 // the panel-build scratch: W, starts, perm) | rows[n_rt*NT] | bias[n_rt*NT] |
 // barriers.
-__host__ __device__ inline int store_warp_bytes(int mode, int nt) {
-  return mode == kStoreRows32 ? 4 * kStoreBuf : (mode == kStoreStg ? 0 : 32 * nt * 4);
-}
-
 template <int NT>
 struct Layout {
   int panel, raw, st, st_warp, rows, bias, bars, total;
-  __host__ __device__ Layout(int total_chunks, int stages, int n_rt, int store_mode, int scratch) {
+  __host__ __device__ Layout(int total_chunks, int stages, int n_rt, int tma_store, int scratch) {
     panel = 0;
     raw = panel + total_chunks * 2 * NT * 128;
     st = raw + stages * kStageBytes;
-    st_warp = store_warp_bytes(store_mode, NT);
+    st_warp = tma_store ? kStoreBufs * kStoreBuf : 0;
     const int stb = 4 * st_warp > scratch ? 4 * st_warp : scratch;
     rows = st + ((stb + 1023) & ~1023);
     bias = rows + 4 * n_rt * NT;
@@ -167,7 +169,7 @@ struct Layout {
 //   backward-data:  warp item = (chunk, word, 32 rows); lane = row (input
 //                   channel).  The 4 filters of the word are warp-uniform.
 // W / starts / perm come from shared memory (staged) or global memory.
-template <int NT, typename WP, typename IP>
+template <int NT, bool BWD, typename WP, typename IP>
 __device__ __forceinline__ void build_panel(const Band2Args& a, uint8_t* panel, const int32_t* rows_s,
                                             WP wsrc, IP stt, IP prm, int ct) {
   constexpr int kPanelChunk = 2 * NT * 128;
@@ -179,7 +181,7 @@ __device__ __forceinline__ void build_panel(const Band2Args& a, uint8_t* panel, 
     const int cb = a.rt_cb[rt], nch = a.rt_cb[rt + 1] - cb;
     const int lim = 8 * a.rt_nk8[rt], start8 = a.rt_start8[rt];
     const int32_t* rrow = rows_s + rt * NT;
-    if (!a.backward_data) {
+    if constexpr (!BWD) {
       const int items = nch * (NT / 4);
       const int rs = lane >> 3, q16 = lane & 7;
       for (int i0 = wid; i0 < items; i0 += kB * kWarps) {
@@ -328,27 +330,28 @@ __device__ __forceinline__ void build_panel_fwd4(const Band2Args& a, uint8_t* pa
   }
 }
 
-template <int NT>
+template <int NT, bool BWD>
 __global__ void __launch_bounds__(kThreads, 1)
     tc_band2_kernel(const __grid_constant__ CUtensorMap t1, const __grid_constant__ CUtensorMap tout,
                     const __grid_constant__ Band2Args a) {
   constexpr int kPanelChunk = 2 * NT * 128;  // hi + lo image of one 32-k chunk
+  constexpr uint32_t kACol0 = 2 * NT;        // TMEM: [0, 2NT) accumulators, then A stages
   // No static shared memory in this kernel: the dynamic window starts
   // 1024-aligned and every derived pointer stays in the shared address space.
   extern __shared__ __align__(1024) uint8_t smem[];
-  const Layout<NT> L(a.total_chunks, a.stages, a.n_rt, a.store_mode, a.scratch);
+  const Layout<NT> L(a.total_chunks, a.stages, a.n_rt, a.tma_store, a.scratch);
   uint8_t* panel = smem + L.panel;
   uint8_t* raw = smem + L.raw;
   uint8_t* stbuf = smem + L.st;
   int32_t* rows_s = reinterpret_cast<int32_t*>(smem + L.rows);
   float* bias_s = reinterpret_cast<float*>(smem + L.bias);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bars);
-  uint64_t* full = bars;
-  uint64_t* afree = bars + kMaxStages;
-  uint64_t* conv = afree + kMaxStages;
-  uint64_t* tfree = conv + kTStages;
-  uint64_t* tfull = tfree + kTStages;
-  uint64_t* tempty = tfull + 2;
+  uint64_t* full = bars;                   // raw stage landed (TMA)
+  uint64_t* afree = bars + kMaxStages;     // 4 converter warps done reading it
+  uint64_t* conv = afree + kMaxStages;     // TMEM A stage written (4 converter warps)
+  uint64_t* tfree = conv + kTStages;       // MMAs done with the TMEM A stage
+  uint64_t* tfull = tfree + kTStages;      // [2] accumulator complete
+  uint64_t* tempty = tfull + 2;            // [2] accumulator drained (4 epilogue warps)
   uint64_t* panel_bar = tempty + 2;
   uint64_t* tab_bar = panel_bar + 1;
   uint64_t* w_bar = tab_bar + 1;
@@ -357,18 +360,15 @@ __global__ void __launch_bounds__(kThreads, 1)
   float* w_s = reinterpret_cast<float*>(stbuf);
   int32_t* start_s = reinterpret_cast<int32_t*>(stbuf) + pad4(a.c_out * a.gw);
   int32_t* perm_s = start_s + pad4(a.c_out);
-  constexpr uint32_t kACol0 = 2 * NT;  // TMEM: [0, 2NT) accumulators, then A stages
 
   const uint32_t warp = warp_id();
   const int lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     TRACE2(0);
-    if (blockIdx.x < 1024) g_cta2[2 * blockIdx.x] = globaltimer();
-    if (blockIdx.x == 0) g_trace2[47] = clock64();
-    if (smem_u32(smem) & 1023u) __trap();
+    CTA_STAMP(0);
     for (int s = 0; s < kMaxStages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&afree[s], 4);  // the 4 converter warps
+      mbar_init(&afree[s], 4);
     }
     for (int s = 0; s < kTStages; ++s) {
       mbar_init(&conv[s], 4);
@@ -386,7 +386,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // kernel), so they load before the grid dependency wait.
     const uint32_t b_rows = 4u * a.n_rt * NT;
     const uint32_t b_oc = a.w_staged ? 4u * pad4(a.c_out) : 0u;
-    const uint32_t b_perm = a.backward_data ? b_oc : 0u;
+    const uint32_t b_perm = BWD ? b_oc : 0u;
     mbar_expect_tx(tab_bar, b_rows + b_oc + b_perm);
     bulk_load(rows_s, a.rows, b_rows, tab_bar);
     if (b_oc) bulk_load(start_s, a.starts, b_oc, tab_bar);
@@ -404,18 +404,17 @@ __global__ void __launch_bounds__(kThreads, 1)
   // Let the next kernel in the stream start its prologue; it waits for this
   // grid's completion before touching memory (griddepcontrol.wait).
   cudaTriggerProgrammaticLaunchCompletion();
-  cudaGridDependencySynchronize();
-  if (threadIdx.x == 0) TRACE2(1);
 
   if (warp == 0) {
     // ---------------- producer ----------------
     if (elect_one()) {
-      if (a.debug & 1) mbar_wait(panel_bar, 0);
+      TileIter it(a);
+      bool have = it.next();  // tile geometry needs no input data: before the wait
+      cudaGridDependencySynchronize();
+      TRACE2(1);
       int s = 0;
       uint32_t ph = 0;
-      TileIter it(a);
-      bool first = true;
-      while (it.next()) {
+      for (; have; have = it.next()) {
         for (int rt = 0; rt < a.n_rt; ++rt) {
           const int start8 = a.rt_start8[rt], nk8 = a.rt_nk8[rt];
           const int nch = (nk8 + 3) >> 2;
@@ -433,11 +432,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               const int cl = pos / a.cls, j = pos - cl * a.cls;
               tma_load_4d(st + r * 512, &t1, &full[s], it.b0 * kBlkPx, j, a.class_d[cl], it.n);
             }
-            if (first) {
-              TRACE2(2);
-              first = false;
-            }
-            TRACE2(46);
+            TRACE2(2);
             advance(s, ph, a.stages);
           }
         }
@@ -448,13 +443,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     constexpr uint32_t idesc = idesc_tf32(128, NT, 0, 0);
     int st = 0, acc = 0;
     uint32_t tph = 0, aph = 0;
-    if (a.debug & 8) {
-      if (lane == 0)
-        while (!mbar_try_wait(panel_bar, 0)) __nanosleep(1000);
-      __syncwarp();
-    } else {
-      mbar_wait(panel_bar, 0);
-    }
+    mbar_wait(panel_bar, 0);
     tc_fence_after();
     TileIter it(a);
     int ti = 0;
@@ -481,14 +470,12 @@ __global__ void __launch_bounds__(kThreads, 1)
               mma_tf32_ts(d_tmem, a_hi + 8 * k, dbl, idesc, 1);
             }
             mma_commit(&tfree[st]);
-            if (c == nch - 1) {
-              mma_commit(&tfull[acc]);
-              if (ti < 8) TRACE2(6 + ti);
-            }
+            if (c == nch - 1) mma_commit(&tfull[acc]);
           }
           __syncwarp();
           advance(st, tph, kTStages);
         }
+        if (ti < 8) TRACE2(6 + ti);
         ++ti;
         if (++acc == 2) {
           acc = 0;
@@ -497,28 +484,30 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else {
-    // ---------------- panel build (warps 2, 3, 8..11; the converters start at once) ----------------
     if (warp < 4 || warp >= 8) {
+      // ---------------- panel build (warps 2, 3, 8..11; the converters start at once) ----------------
       const int ct = warp < 4 ? threadIdx.x - 64 : threadIdx.x - 192;  // 0..191
+      cudaGridDependencySynchronize();  // W may come from the previous kernel
       if (ct == 0 && a.w_staged) {
         const uint32_t bytes = 4u * a.c_out * a.gw;
         mbar_expect_tx(w_bar, bytes);
         bulk_load(w_s, a.weight, bytes, w_bar);
       }
       mbar_wait(tab_bar, 0);
-      if (ct == 0) TRACE2(4);
-      if (a.w_staged) {
-        mbar_wait(w_bar, 0);
-        if (ct == 0) TRACE2(5);
+      if (a.w_staged) mbar_wait(w_bar, 0);
+      if constexpr (BWD) {
+        if (a.w_staged)
+          build_panel<NT, true>(a, panel, rows_s, w_s, start_s, perm_s, ct);
+        else
+          build_panel<NT, true>(a, panel, rows_s, a.weight, a.starts, a.perm, ct);
+      } else {
+        if (a.fwd4)
+          build_panel_fwd4<NT>(a, panel, rows_s, w_s, start_s, ct);
+        else if (a.w_staged)
+          build_panel<NT, false>(a, panel, rows_s, w_s, start_s, perm_s, ct);
+        else
+          build_panel<NT, false>(a, panel, rows_s, a.weight, a.starts, a.perm, ct);
       }
-      if (ct == 0) TRACE2(50);
-      if (a.fwd4)
-        build_panel_fwd4<NT>(a, panel, rows_s, w_s, start_s, ct);
-      else if (a.w_staged)
-        build_panel<NT>(a, panel, rows_s, w_s, start_s, perm_s, ct);
-      else
-        build_panel<NT>(a, panel, rows_s, a.weight, a.starts, a.perm, ct);
-      if (ct == 0) TRACE2(51);
       fence_proxy_async_smem();
       named_bar_sync(1, kWorkers);
       if (ct == 0) {
@@ -533,14 +522,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       int s = 0, st = 0;
       uint32_t ph = 0, tph = 0;
       TileIter it(a);
-      int cc = 0;
       while (it.next()) {
         for (int rt = 0; rt < a.n_rt; ++rt) {
           const int nk8 = a.rt_nk8[rt];
           const int nch = (nk8 + 3) >> 2;
           for (int c = 0; c < nch; ++c) {
             mbar_wait(&full[s], ph);
-            if (q == 0 && lane == 0 && cc < 8) TRACE2(22 + cc);
             // Element (row r, pixel 32q + lane) of the [32 rows][128 px] stage.
             // Rows past the chunk's k-steps hold stale data that lands in TMEM
             // columns the MMAs never read.
@@ -554,155 +541,111 @@ __global__ void __launch_bounds__(kThreads, 1)
               lo[r] = __float_as_uint(v - h);
             }
             __syncwarp();
-            const bool trc = q == 0 && lane == 0 && blockIdx.x == 0 && cc < 2;
-            if (trc) g_trace2[54 + 4 * cc] = globaltimer();
             if (lane == 0) mbar_arrive(&afree[s]);
             mbar_wait(&tfree[st], tph ^ 1u);
             tc_fence_after();
-            if (trc) g_trace2[55 + 4 * cc] = globaltimer();
             const uint32_t col = tmem + kACol0 + st * 64 + lane_base;
             tmem_st32(col, hi);
             tmem_st32(col + 32, lo);
-            if (trc) g_trace2[56 + 4 * cc] = globaltimer();
             tmem_st_wait();
-            if (trc) g_trace2[57 + 4 * cc] = globaltimer();
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&conv[st]);
-            if (q == 0 && lane == 0 && cc < 8) TRACE2(30 + cc);
-            ++cc;
             advance(s, ph, a.stages);
             advance(st, tph, kTStages);
           }
         }
       }
-    } else if (warp >= 8) {
-    // ---------------- epilogue (warps 8..11) ----------------
-    const int et = threadIdx.x - 256;  // 0..127
-    mbar_wait(tab_bar, 0);
-    for (int i = et; i < a.n_rt * NT; i += 128) {
-      const int row = rows_s[i];
-      bias_s[i] = (a.bias != nullptr && row >= 0) ? __ldg(a.bias + row) : 0.f;
     }
-    named_bar_sync(2, 128);
-    const int q = warp & 3;
-    int acc = 0, sbuf = 0;
-    uint32_t aph = 0;
-    TileIter it(a);
-    int ti = 0;
-    uint8_t* wbuf = stbuf + q * L.st_warp;  // this warp's staging
-    const uint32_t wbuf_a = smem_u32(wbuf);
-    const bool whole = a.store_mode == kStoreClasses || a.store_mode == kStoreRowsNT;
-    while (it.next()) {
-      const int px = (it.b0 + q) * kBlkPx + lane;
-      const bool valid = q < it.cnt && px < a.plane;
-      float* obase = a.out + static_cast<int64_t>(it.n) * a.c_out_t * a.plane + px;
-      for (int rt = 0; rt < a.n_rt; ++rt) {
-        mbar_wait(&tfull[acc], aph);
-        tc_fence_after();
-        if (q < it.cnt) {
-          if (whole) {
-            // The previous tile's store must have read the staging buffer.
-            if (lane == 0) bulk_wait_read<0>();
-            __syncwarp();
-          }
-          const uint32_t taddr = tmem + acc * NT + (static_cast<uint32_t>(q * 32) << 16);
+    if (warp >= 8) {
+      // ---------------- epilogue (warps 8..11) ----------------
+      const int et = threadIdx.x - 256;  // 0..127
+      for (int i = et; i < a.n_rt * NT; i += 128) {
+        const int row = rows_s[i];
+        bias_s[i] = (!BWD && a.bias != nullptr && row >= 0) ? __ldg(a.bias + row) : 0.f;
+      }
+      named_bar_sync(2, 128);
+      const int q = warp & 3;
+      int acc = 0, sbuf = 0;
+      uint32_t aph = 0;
+      TileIter it(a);
+      int ti = 0;
+      uint8_t* wbuf = stbuf + q * L.st_warp;  // this warp's staging
+      const uint32_t wbuf_a = smem_u32(wbuf);
+      while (it.next()) {
+        const int px = (it.b0 + q) * kBlkPx + lane;
+        const bool valid = q < it.cnt && px < a.plane;
+        float* obase = a.out + static_cast<int64_t>(it.n) * a.c_out_t * a.plane + px;
+        for (int rt = 0; rt < a.n_rt; ++rt) {
+          mbar_wait(&tfull[acc], aph);
+          tc_fence_after();
+          if (q < it.cnt) {
+            const uint32_t taddr = tmem + acc * NT + (static_cast<uint32_t>(q * 32) << 16);
 #pragma unroll 1
-          for (int c0 = 0; c0 < NT; c0 += 32) {
-            const int g0 = rt * NT + c0;  // first tile row of this 32-row group
-            if (a.store_mode == kStoreClasses && g0 >= a.c_out_t) break;
-            uint32_t v[32];
-            tmem_ld32_nowait(taddr + c0, v);
-            tmem_ld_wait();
-            if (ti == 0 && q == 0 && lane == 0 && c0 < 128) TRACE2(38 + c0 / 32);
-            float bb[32];
+            for (int c0 = 0; c0 < NT; c0 += 32) {
+              const int g0 = rt * NT + c0;  // first tile row of this 32-row group
+              uint32_t v[32];
+              tmem_ld32_nowait(taddr + c0, v);
+              tmem_ld_wait();
+              float bb[32];
 #pragma unroll
-            for (int j = 0; j < 32; ++j) bb[j] = bias_s[g0 + j];
-            if (a.store_mode == kStoreClasses) {
-              // box {32 px, D, out_cls}: smem [j][d][px]
-              const int cl = g0 / a.out_cls, j0 = g0 - cl * a.out_cls, d = a.out_class_d[cl];
-              const uint32_t buf = wbuf_a + ((j0 * a.out_nd + d) * 32 + lane) * 4;
-              const uint32_t jstride = a.out_nd * 128;
+              for (int j = 0; j < 32; ++j) bb[j] = bias_s[g0 + j];
+              if (a.tma_store) {
+                // Stage [32 rows][32 px] (lanes own consecutive words: no
+                // conflicts) and write it with one TMA store; 4 buffers rotate.
+                if (lane == 0) bulk_wait_read<kStoreBufs - 1>();
+                __syncwarp();
+                const uint32_t buf = wbuf_a + sbuf * kStoreBuf + lane * 4;
 #pragma unroll
-              for (int j = 0; j < 32; ++j) sts_f32(buf + j * jstride, __uint_as_float(v[j]) + bb[j]);
-            } else if (a.store_mode == kStoreRowsNT) {
-              const uint32_t buf = wbuf_a + (c0 * 32 + lane) * 4;
+                for (int j = 0; j < 32; ++j) sts_f32(buf + j * 128, __uint_as_float(v[j]) + bb[j]);
+                fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) {
+                  const int cl = g0 / a.out_cls, jj = g0 - cl * a.out_cls;
+                  tma_store_3d(&tout, wbuf + sbuf * kStoreBuf, (it.b0 + q) * kBlkPx, a.out_class_d[cl],
+                               it.n * a.out_cls + jj);
+                  bulk_commit();
+                }
+                sbuf = (sbuf + 1) & (kStoreBufs - 1);
+              } else if (valid) {
+                int32_t rr[32];
 #pragma unroll
-              for (int j = 0; j < 32; ++j) sts_f32(buf + j * 128, __uint_as_float(v[j]) + bb[j]);
-            } else if (a.store_mode == kStoreRows32) {
-              // Stage [32 rows][32 px] and write it with one TMA store as soon
-              // as it is staged; 4 buffers per warp rotate.
-              if (lane == 0) bulk_wait_read<3>();
-              __syncwarp();
-              const uint32_t buf = wbuf_a + sbuf * kStoreBuf + lane * 4;
+                for (int j = 0; j < 32; ++j) rr[j] = rows_s[g0 + j];
 #pragma unroll
-              for (int j = 0; j < 32; ++j) sts_f32(buf + j * 128, __uint_as_float(v[j]) + bb[j]);
-              fence_proxy_async_smem();
-              __syncwarp();
-              if (lane == 0) {
-                const int cl = g0 / a.out_cls, jj = g0 - cl * a.out_cls;
-                tma_store_3d(&tout, wbuf + sbuf * kStoreBuf, (it.b0 + q) * kBlkPx, a.out_class_d[cl],
-                             it.n * a.out_cls + jj);
-                bulk_commit();
-                if (ti == 0 && q == 0 && c0 < 128) TRACE2(42 + c0 / 32);
-              }
-              sbuf = (sbuf + 1) & 3;
-            } else if (valid) {
-              int32_t rr[32];
-#pragma unroll
-              for (int j = 0; j < 32; ++j) rr[j] = rows_s[g0 + j];
-#pragma unroll
-              for (int j = 0; j < 32; ++j) {
-                if (rr[j] >= 0) obase[static_cast<int64_t>(rr[j]) * a.plane] = __uint_as_float(v[j]) + bb[j];
+                for (int j = 0; j < 32; ++j) {
+                  if (rr[j] >= 0) obase[static_cast<int64_t>(rr[j]) * a.plane] = __uint_as_float(v[j]) + bb[j];
+                }
               }
             }
           }
-          if (whole) {
-            fence_proxy_async_smem();
-            __syncwarp();
-            if (lane == 0) {
-              const int z = a.store_mode == kStoreClasses ? it.n * a.out_cls : it.n * a.c_out_t + rt * NT;
-              tma_store_3d(&tout, wbuf, (it.b0 + q) * kBlkPx, 0, z);
-              bulk_commit();
-              if (ti == 0 && q == 0) TRACE2(42);
-            }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty[acc]);
+          if (ti < 8 && q == 0 && lane == 0) TRACE2(14 + ti);
+          ++ti;
+          if (++acc == 2) {
+            acc = 0;
+            aph ^= 1u;
           }
-        }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&tempty[acc]);
-        if (ti < 8 && q == 0 && lane == 0) {
-          TRACE2(14 + ti);
-          if (blockIdx.x == 0) {
-            g_trace2[48] = clock64();
-            g_trace2[49] = 14 + ti;
-          }
-        }
-        ++ti;
-        if (++acc == 2) {
-          acc = 0;
-          aph ^= 1u;
         }
       }
-    }
-    if (lane == 0) bulk_wait<0>();
-    if (lane == 0 && q == 0 && blockIdx.x < 1024) g_cta2[2 * blockIdx.x + 1] = globaltimer();
+      if (lane == 0) bulk_wait<0>();
+      if (lane == 0 && q == 0) CTA_STAMP(1);
     }
   }
   tc_fence_before();
   __syncthreads();
-  if (threadIdx.x == 0) TRACE2(63);
   if (warp == 1) tmem_dealloc<512>(tmem);
 }
 
 template <int NT>
-int band2_stages(const TcBandPlan& tp, int mode, int scratch) {
+int band2_stages(const TcBandPlan& tp, int tma_store, int scratch) {
   int st = kMaxStages;
-  while (st >= 2 && 1024 + Layout<NT>(tp.total_chunks, st, tp.n_rt, mode, scratch).total > kSmemLimit) --st;
+  while (st >= 2 && 1024 + Layout<NT>(tp.total_chunks, st, tp.n_rt, tma_store, scratch).total > kSmemLimit) --st;
   return st;
 }
 
-template <int NT>
+template <int NT, bool BWD>
 cudaError_t launch_tc2_nt(const TcBandPlan& tp, const TcDeviceTables& dt, const TcBandCall& call,
                           int64_t shift, int32_t c_out, cudaStream_t s) {
   const int64_t P = call.plane;
@@ -718,36 +661,18 @@ cudaError_t launch_tc2_nt(const TcBandPlan& tp, const TcDeviceTables& dt, const 
     if (!encode_f32(&t1, call.in, 4, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_NONE))
       return cudaErrorInvalidValue;
   }
-  // Epilogue store mode and the output view its TMA stores use.
-  const bool cls_ok = tp.store_ok && static_cast<int>(tp.out_class_d.size()) <= kMaxCls;
-  // Default: 32-row boxes stored as soon as staged (stores start after the
-  // first 32 columns of a tile).  SCC_TC2_STORE=2/3 selects the whole-tile
-  // boxes (one store per warp and tile) for comparison.
-  int32_t mode = cls_ok ? kStoreRows32 : kStoreStg;
-  {
-    const char* sm = getenv("SCC_TC2_STORE");
-    const int want = sm ? atoi(sm) : -1;
-    if (want == kStoreRowsNT && call.backward_data && call.c_out_t % NT == 0) mode = kStoreRowsNT;
-    if (want == kStoreClasses && !call.backward_data && cls_ok && tp.n_rt == 1 && tp.out_n_class <= 256 &&
-        tp.out_cls <= 256 && tp.out_n_class * tp.out_cls == call.c_out_t)
-      mode = kStoreClasses;
-    if (want == kStoreStg) mode = kStoreStg;
-  }
+  // Output view for TMA stores of 32-row groups: {P, D_out, N * out_cls}
+  // (store_ok: every 32 consecutive tile rows are one equally strided class
+  // run); otherwise plain per-row stores.
+  const bool tma_store = tp.store_ok && static_cast<int>(tp.out_class_d.size()) <= kMaxCls;
   CUtensorMap tout;
   {
-    const bool cls_view = mode == kStoreClasses || mode == kStoreRows32;
-    const int32_t ocls = cls_view ? tp.out_cls : call.c_out_t;
-    const int32_t ond = cls_view ? tp.out_n_class : 1;
+    const int32_t ocls = tma_store ? tp.out_cls : call.c_out_t;
+    const int32_t ond = tma_store ? tp.out_n_class : 1;
     const uint64_t dims[3] = {static_cast<uint64_t>(P), static_cast<uint64_t>(ond),
                               static_cast<uint64_t>(call.n) * ocls};
     const uint64_t strides[2] = {static_cast<uint64_t>(P) * 4, static_cast<uint64_t>(P) * 4 * ond};
-    uint32_t box[3] = {32, 1, 32};
-    if (mode == kStoreClasses) {
-      box[1] = static_cast<uint32_t>(tp.out_n_class);
-      box[2] = static_cast<uint32_t>(tp.out_cls);
-    } else if (mode == kStoreRowsNT) {
-      box[2] = NT;
-    }
+    const uint32_t box[3] = {32, 1, 32};
     if (!encode_f32(&tout, call.out, 3, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_NONE))
       return cudaErrorInvalidValue;
   }
@@ -764,11 +689,10 @@ cudaError_t launch_tc2_nt(const TcBandPlan& tp, const TcDeviceTables& dt, const 
   }
   for (int rt = 0; rt <= tp.n_rt; ++rt) a.rt_cb[rt] = tp.chunk_base[rt];
   for (size_t i = 0; i < tp.class_d.size(); ++i) a.class_d[i] = tp.class_d[i];
-  if (cls_ok)
+  if (tma_store)
     for (size_t i = 0; i < tp.out_class_d.size(); ++i) a.out_class_d[i] = tp.out_class_d[i];
-  a.store_mode = mode;
+  a.tma_store = tma_store ? 1 : 0;
   a.out_cls = tp.out_cls;
-  a.out_nd = tp.out_n_class;
   a.n_rt = tp.n_rt;
   a.ring = tp.ring;
   a.cls = tp.cls;
@@ -777,16 +701,10 @@ cudaError_t launch_tc2_nt(const TcBandPlan& tp, const TcDeviceTables& dt, const 
   a.c_out = c_out;
   a.gw = call.gw;
   a.c_out_t = call.c_out_t;
-  a.backward_data = call.backward_data ? 1 : 0;
   a.nbps = static_cast<int32_t>((P + 31) / 32);
-
   a.total_chunks = tp.total_chunks;
-  {
-    const char* dbg = getenv("SCC_TC2_DEBUG");
-    a.debug = dbg ? atoi(dbg) : 0;
-  }
-  // W + starts (+ perm) go to the staging area by bulk copy when they fit and the
-  // weight pointer/size suit cp.async.bulk.
+  // W + starts (+ perm) go to the staging area by bulk copy when they fit and
+  // the weight pointer/size suit cp.async.bulk.
   {
     const int64_t wbytes = 4ll * c_out * call.gw;
     const int64_t need = 4ll * (pad4(c_out * call.gw) + 2 * pad4(c_out));
@@ -795,14 +713,14 @@ cudaError_t launch_tc2_nt(const TcBandPlan& tp, const TcDeviceTables& dt, const 
     a.scratch = a.w_staged ? static_cast<int32_t>(need) : 0;
     // window starts (oc * shift mod c_in) and arc starts (multiples of 8) are
     // multiples of 4 when shift and c_in are
-    a.fwd4 = (!call.backward_data && a.w_staged && call.gw % 4 == 0 && call.c_in % 4 == 0 &&
-              shift % 4 == 0) ? 1 : 0;
+    a.fwd4 = (!BWD && a.w_staged && call.gw % 4 == 0 && call.c_in % 4 == 0 && shift % 4 == 0) ? 1 : 0;
   }
-  a.stages = band2_stages<NT>(tp, mode, a.scratch);
+  a.stages = band2_stages<NT>(tp, a.tma_store, a.scratch);
   a.plane = P;
-  a.n = call.n;
-  a.units = call.n * a.nbps;
-  const int smem = 1024 + Layout<NT>(a.total_chunks, a.stages, a.n_rt, mode, a.scratch).total;
+  const int64_t units = call.n * a.nbps;
+  if (units > (1ll << 30)) return cudaErrorInvalidValue;
+  a.units = static_cast<int32_t>(units);
+  const int smem = 1024 + Layout<NT>(a.total_chunks, a.stages, a.n_rt, a.tma_store, a.scratch).total;
 
   static int nsm_cache[64] = {0};
   static bool attr_set[64] = {false};
@@ -816,7 +734,7 @@ cudaError_t launch_tc2_nt(const TcBandPlan& tp, const TcDeviceTables& dt, const 
     if (dev >= 0 && dev < 64) nsm_cache[dev] = nsm;
   }
   if (dev < 0 || dev >= 64 || !attr_set[dev]) {
-    cudaError_t e = cudaFuncSetAttribute(tc_band2_kernel<NT>,
+    cudaError_t e = cudaFuncSetAttribute(tc_band2_kernel<NT, BWD>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit);
     if (e != cudaSuccess) return e;
     if (dev >= 0 && dev < 64) attr_set[dev] = true;
@@ -832,7 +750,7 @@ cudaError_t launch_tc2_nt(const TcBandPlan& tp, const TcDeviceTables& dt, const 
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, tc_band2_kernel<NT>, t1, tout, a);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, tc_band2_kernel<NT, BWD>, t1, tout, a);
   if (e != cudaSuccess) return e;
   note_launches(1);
   return cudaSuccess;
@@ -845,31 +763,37 @@ bool tc_band2_supported(const TcBandPlan& tp, int64_t plane, int32_t c_out) {
   if (!tp.ok || plane % 4 != 0 || plane < 4) return false;
   if (tp.rb % 8 != 0 || tp.n_rt > kMaxRt || tp.n_class > kMaxCls) return false;
   // The whole panel stays resident next to >= 4 raw stages.
-  // (store staging is chosen at launch; size the check for the largest mode)
-  const int st = tp.nt == 128 ? band2_stages<128>(tp, kStoreClasses, kMaxScratch)
-                               : band2_stages<64>(tp, kStoreClasses, kMaxScratch);
+  const int st = tp.nt == 128 ? band2_stages<128>(tp, 1, kMaxScratch) : band2_stages<64>(tp, 1, kMaxScratch);
   return st >= 4;
 }
 
 cudaError_t launch_band_tc2(const TcBandPlan& tp, const TcDeviceTables& dt, const TcBandCall& call,
                             int64_t shift, int32_t c_out, cudaStream_t s) {
+  const bool bwd = call.backward_data;
   switch (tp.nt) {
     case 64:
-      return launch_tc2_nt<64>(tp, dt, call, shift, c_out, s);
+      return bwd ? launch_tc2_nt<64, true>(tp, dt, call, shift, c_out, s)
+                 : launch_tc2_nt<64, false>(tp, dt, call, shift, c_out, s);
     case 128:
-      return launch_tc2_nt<128>(tp, dt, call, shift, c_out, s);
+      return bwd ? launch_tc2_nt<128, true>(tp, dt, call, shift, c_out, s)
+                 : launch_tc2_nt<128, false>(tp, dt, call, shift, c_out, s);
     default:
       return cudaErrorInvalidValue;
   }
 }
 
 int tc2_trace(unsigned long long* out, int n) {
+#if defined(SCC_TRACE)
   if (n > 64 + 2048) n = 64 + 2048;
   const int a = n < 64 ? n : 64;
   if (cudaMemcpyFromSymbol(out, g_trace2, a * sizeof(unsigned long long)) != cudaSuccess) return -1;
   if (n > 64 && cudaMemcpyFromSymbol(out + 64, g_cta2, (n - 64) * sizeof(unsigned long long)) != cudaSuccess)
     return -1;
   return n;
+#else
+  for (int i = 0; i < n; ++i) out[i] = 0;
+  return n;
+#endif
 }
 
 }  // namespace scc

@@ -54,7 +54,8 @@ constexpr int kDyBytes = 128 * 128;   // [128 rows][32 px]
 constexpr int kMaxStages = 6;
 constexpr int kTStages = 4;           // TMEM A stages (hi + lo, 64 columns each)
 constexpr int kACol0 = 256;           // TMEM: two 128-column accumulators, then A stages
-constexpr int kSlices = 148;          // pixel slices (partials) of a launch
+constexpr int kSlices = 74;           // pixel slices (partials) of a launch: one per CTA of
+                                      // the concurrent backward (half of a B200's 148 SMs)
 constexpr int kMaxRt = 16;
 constexpr int kMaxCls = 64;
 constexpr int kSmemLimit = 227 * 1024;
@@ -570,7 +571,9 @@ cudaError_t launch_wgrad2(const TcWeightPlan& tw, const TcWeightCall& call, cons
   if (units > (1ll << 30)) return cudaErrorInvalidValue;
   a.units = static_cast<int32_t>(units);
   a.elems = tw.n_rt * (128 * call.gw + 128);
-  a.slices = static_cast<int32_t>(std::min<int64_t>(units, kSlices));
+  int kslices = kSlices;
+  if (const char* ks = getenv("SCC_W2_SLICES")) kslices = atoi(ks);
+  a.slices = static_cast<int32_t>(std::min<int64_t>(units, kslices));
   const int cap = call.max_ctas > 0 ? std::min(call.max_ctas, nsm) : nsm;
   const int grid = std::min(a.slices, cap);
   if (tc_wgrad2_workspace_bytes(call.c_out, call.gw, a.slices) > call.workspace_bytes) return cudaErrorInvalidValue;

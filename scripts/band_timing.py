@@ -55,7 +55,7 @@ for path, name in ((_lib.SCC_PATH_TENSOR_V1, "gen1"), (_lib.SCC_PATH_TENSOR, "ge
             lab = {0: "start", 1: "dep", 2: "tma0", 46: "tma_last", 3: "panel", 4: "tabs", 5: "w", 63: "end", 50: "b_loop0", 51: "b_loop1", 52: "b_fence"}
             for i in range(8): lab[6 + i] = f"mma{i}"; lab[14 + i] = f"epi{i}"; lab[22 + i] = f"cv{i}s"; lab[30 + i] = f"cv{i}e"
             for g in range(4): lab[38 + g] = f"eg{g}ld"; lab[42 + g] = f"eg{g}st"
-            print(op, "converter c0/c1 [lds done, tfree ok, st issued, st waited] (us):", [round((t[54 + i] - t0) / 1e3, 2) if t[54 + i] > t0 else 0 for i in range(8)])
+            print(op, "epi tile1 grp1 [start, ld done, wait_read done, sts done, fence done, tma issued] (us):", [round((t[54 + i] - t0) / 1e3, 3) if t[54 + i] > t0 else 0 for i in range(6)])
             for i in range(8): t[54 + i] = 0
             print(op, "SM clock MHz (CTA0):", (t[48] - t[47]) * 1e3 / max(t[t[49]] - t[0], 1))
             t[47] = t[48] = t[49] = 0
