@@ -190,26 +190,6 @@ float* panel_buffer(Plan& p, int dir, cudaStream_t s) {
   return static_cast<float*>(b.ptr);
 }
 
-// Grid-barrier words {count, generation} of the generation-2 backward-weight
-// kernel, one zeroed pair per (device, stream) so concurrent calls on
-// different streams never share a barrier.
-unsigned int* sync_buffer(Plan& p, cudaStream_t s) {
-  const int dev = current_device();
-  std::lock_guard<std::mutex> lk(p.panel_mu);
-  for (PanelBuf& b : p.panels) {
-    if (b.device == dev && b.stream == static_cast<void*>(s) && b.dir == 3) return static_cast<unsigned int*>(b.ptr);
-  }
-  PanelBuf b;
-  b.device = dev;
-  b.stream = s;
-  b.dir = 3;
-  b.bytes = 256;
-  cuda_check(cudaMalloc(&b.ptr, b.bytes), "cudaMalloc(grid barrier)");
-  cuda_check(cudaMemset(b.ptr, 0, b.bytes), "cudaMemset(grid barrier)");
-  p.panels.push_back(b);
-  return static_cast<unsigned int*>(b.ptr);
-}
-
 int device_sms() {
   int dev = 0, n = 148;
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
@@ -368,7 +348,7 @@ void do_backward_weight(Plan& p, int64_t n, int64_t h, int64_t w, const float* d
     c.class_d = t.tcw_class_d;
     c.max_ctas = max_ctas;
     if (p.path != SCC_PATH_TENSOR_V1 && tc_wgrad2_supported(p.tc_wgt, h * w, c.gw)) {
-      cuda_check(launch_wgrad2(p.tc_wgt, c, t.perm, sync_buffer(p, s), s), "backward-weight (tensor) launch");
+      cuda_check(launch_wgrad2(p.tc_wgt, c, t.perm, s), "backward-weight (tensor) launch");
       return;
     }
     cuda_check(launch_weight_tc(p.tc_wgt, c, s), "backward-weight (tensor) launch");

@@ -103,13 +103,13 @@ bool tc_band2_supported(const TcBandPlan& tp, int64_t plane, int32_t c_out);
 cudaError_t launch_band_tc2(const TcBandPlan& tp, const TcDeviceTables& dt, const TcBandCall& call,
                             int64_t shift, int32_t c_out, cudaStream_t s);
 int tc2_trace(unsigned long long* out, int n);
-// Backward-weight generation 2 (scc_tc_wgrad2.cu): TS-mode MMAs, in-kernel
-// fixed-order cross-CTA reduction behind a grid barrier (cooperative launch).
+// Backward-weight generation 2 (scc_tc_wgrad2.cu): TS-mode MMAs, per-slice
+// partials reduced in a fixed order by a PDL-chained second kernel.
 bool tc_wgrad2_supported(const TcWeightPlan& tw, int64_t plane, int32_t gw);
 size_t tc_wgrad2_workspace_bytes(int32_t c_out, int32_t gw, int nsm);
 int tc_w2trace(unsigned long long* out, int n);
 cudaError_t launch_wgrad2(const TcWeightPlan& tw, const TcWeightCall& call, const int32_t* perm,
-                          unsigned int* gbar, cudaStream_t s);
+                          cudaStream_t s);
 cudaError_t launch_band_tc(const TcBandPlan& tp, const TcDeviceTables& dt, const TcBandCall& call,
                            cudaStream_t s);
 

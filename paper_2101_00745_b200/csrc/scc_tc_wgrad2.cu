@@ -16,18 +16,19 @@
 // 3xTF32 per k-step: dy_hi*x + dy_lo*x + dy_hi*x_lo (x raw = x_hi: the tensor
 // core truncates).
 //
-// Every CTA owns a contiguous run of pixel blocks and accumulates its row
-// tile in TMEM; the epilogue writes the CTA's window-relative partial dW / db
-// to the workspace, all CTAs meet at a grid barrier (cooperative launch: the
-// grid is co-resident), and each CTA then reduces a slice of the partials in
-// a fixed order.  One launch, no atomics on the data: bitwise reproducible.
-//
+// The pixel blocks are cut into a fixed number of contiguous slices (not tied
+// to the grid size); each slice accumulates in TMEM (two accumulators, so one
+// slice's epilogue overlaps the next slice's MMAs) and the epilogue writes the
+// slice's window-relative partial dW / db to the workspace.  A second, PDL-
+// chained kernel sums the partials in a fixed order.  No atomics on the data:
+// the bits of dW do not depend on how many CTAs run.
+
 // Warp roles (384 threads, one CTA per SM):
 //   warp 0      TMA producer
 //   warp 1      TMEM allocator + MMA issuer
 //   warps 2-3   x lo converters (+ the constant ones / zero rows)
 //   warps 4-7   dy row converters (warp q: filter rows 32q..32q+31)
-//   warps 8-11  epilogue (TMEM -> partial) ; all warps: cross-CTA reduction
+//   warps 8-11  epilogue (TMEM -> smem row dump -> window-relative partial)
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
@@ -55,18 +56,17 @@ constexpr int kMaxStages = 6;
 constexpr int kTStages = 4;           // TMEM A stages (hi + lo, 64 columns each)
 constexpr int kACol0 = 256;           // TMEM: two 128-column accumulators, then A stages
 constexpr int kSlices = 74;           // pixel slices (partials) of a launch: one per CTA of
-                                      // the concurrent backward (half of a B200's 148 SMs)
+                                      // the concurrent backward (half of a B200's 148 SMs);
+                                      // the reduce kernel sums at most 8 x 10 slices
 constexpr int kMaxRt = 16;
 constexpr int kMaxCls = 64;
 constexpr int kSmemLimit = 227 * 1024;
 constexpr int kMaxGw = 32;            // window slots per filter handled in registers
-constexpr int kRedMax = 13;           // partials per reducing thread (12 groups x 13 >= 148 CTAs)
 
 struct W2Args {
   float* part;               // [grid][c_out*gw + c_out] partial dW | db
   float* dweight;            // [c_out*gw]
   float* dbias;              // [c_out] or nullptr
-  unsigned int* gbar;        // grid barrier: count at [0], generation at [32] (separate lines)
   const int32_t* perm;       // sorted position -> oc
   const int32_t* starts;     // oc -> window start
   int32_t rt_start8[kMaxRt]; // per row tile: first arc ring position (input channel)
@@ -169,13 +169,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   cudaGridDependencySynchronize();
-  // Generation of the grid barrier for this launch: it only changes when every
-  // CTA of this launch has arrived, so read it now, off the critical path.
-  unsigned int gen0 = 0;
-  if (threadIdx.x == 0) {
-    gen0 = *reinterpret_cast<volatile unsigned int*>(a.gbar + 32);
-    W2T(1);
-  }
+  // the dependent reduce kernel may launch now (it waits for this grid)
+  cudaTriggerProgrammaticLaunchCompletion();
+  if (threadIdx.x == 0) W2T(1);
 
   if (warp == 0) {
     // ---------------- producer ----------------
@@ -430,69 +426,50 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   }
 
-  // ---------------- grid barrier, then a fixed-order reduction of the partials ----------------
-  tc_fence_before();
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    W2T(35);
-    if (blockIdx.x < 256) g_w2cta[3 * blockIdx.x + 2] = globaltimer();
-  }
-  if (threadIdx.x == 0) {
-    // Sense-reversing grid barrier.  The acq_rel arrival publishes this CTA's
-    // partial writes (ordered before it by the bar.sync above); the last
-    // arrival resets the count and bumps the generation the others poll.
-    const unsigned int arrived = atom_add_acq_rel_gpu(a.gbar, 1u);
-    if (arrived == gridDim.x - 1) {
-      st_relaxed_gpu(a.gbar, 0u);
-      red_add_release_gpu(a.gbar + 32, 1u);
-    } else {
-      while (ld_acquire_gpu(a.gbar + 32) == gen0) __nanosleep(32);
-    }
-    W2T(36);
-  }
-  __syncthreads();
-  {
-    const int e0 = static_cast<int>((static_cast<int64_t>(blockIdx.x) * a.elems) / gridDim.x);
-    const int e1 = static_cast<int>((static_cast<int64_t>(blockIdx.x + 1) * a.elems) / gridDim.x);
-    const int grp = threadIdx.x >> 5;  // 12 groups: partials grp, grp+12, ...
-    float* red = stg;                  // [12][32]
-    const int tstride = 128 * a.gw + 128;  // one row tile's partial
-    for (int eb = e0; eb < e1; eb += 32) {
-      const int e = eb + lane;
-      float v[kRedMax];
-#pragma unroll
-      for (int m = 0; m < kRedMax; ++m) {
-        const int k = grp + 12 * m;
-        v[m] = (e < e1 && k < a.slices) ? __ldcg(a.part + static_cast<int64_t>(k) * a.elems + e) : 0.f;
-      }
-      float acc = 0.f;
-#pragma unroll
-      for (int m = 0; m < kRedMax; ++m) acc += v[m];  // fixed order
-      red[grp * 32 + lane] = acc;
-      __syncthreads();
-      if (grp == 0 && e < e1) {
-        float t = 0.f;
-#pragma unroll
-        for (int g = 0; g < 12; ++g) t += red[g * 32 + lane];
-        const int rt = e / tstride, rem = e - rt * tstride;
-        const bool isb = rem >= 128 * a.gw;
-        const int i = isb ? rem - 128 * a.gw : rem / a.gw;
-        const int pos = rt * 128 + i;
-        if (pos < a.c_out) {
-          const int oc = row_oc(a, pos);
-          if (!isb)
-            a.dweight[static_cast<int64_t>(oc) * a.gw + (rem - i * a.gw)] = t;
-          else if (a.dbias != nullptr)
-            a.dbias[oc] = t;
-        }
-      }
-      __syncthreads();
-    }
-  }
-  if (threadIdx.x == 0) W2T(37);
+  if (threadIdx.x == 0 && blockIdx.x < 256) g_w2cta[3 * blockIdx.x + 2] = globaltimer();
   tc_fence_before();
   __syncthreads();
   if (warp == 1) tmem_dealloc<512>(tmem);
+}
+
+// Fixed-order reduction of the per-slice partials (the kernel boundary with
+// tc_wgrad2_kernel is the grid-wide sync; launched with programmatic stream
+// serialization its CTAs are resident -- next to the big CTAs, it needs no
+// shared memory -- and start the moment the partials are complete).
+// 8 lanes per output: lane g sums slices g, g+8, ... in order, then a fixed
+// shuffle tree combines the 8 group sums.  Bitwise reproducible.
+__global__ void __launch_bounds__(256) tc_wgrad2_reduce(const __grid_constant__ W2Args a) {
+  cudaGridDependencySynchronize();
+  const int gtid = blockIdx.x * 256 + threadIdx.x;
+  const int e = gtid >> 3, g = gtid & 7;
+  float acc = 0.f;
+  if (e < a.elems) {
+    float v[10];
+#pragma unroll
+    for (int m = 0; m < 10; ++m) {
+      const int k = g + 8 * m;
+      v[m] = k < a.slices ? __ldcg(a.part + static_cast<int64_t>(k) * a.elems + e) : 0.f;
+    }
+#pragma unroll
+    for (int m = 0; m < 10; ++m) acc += v[m];
+  }
+  acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+  acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+  acc += __shfl_xor_sync(0xffffffffu, acc, 4);
+  if (g == 0 && e < a.elems) {
+    const int tstride = 128 * a.gw + 128;  // one row tile's partial
+    const int rt = e / tstride, rem = e - rt * tstride;
+    const bool isb = rem >= 128 * a.gw;
+    const int i = isb ? rem - 128 * a.gw : rem / a.gw;
+    const int pos = rt * 128 + i;
+    if (pos < a.c_out) {
+      const int oc = row_oc(a, pos);
+      if (!isb)
+        a.dweight[static_cast<int64_t>(oc) * a.gw + (rem - i * a.gw)] = acc;
+      else if (a.dbias != nullptr)
+        a.dbias[oc] = acc;
+    }
+  }
 }
 
 int w2_stages(int xr) {
@@ -531,7 +508,7 @@ size_t tc_wgrad2_workspace_bytes(int32_t c_out, int32_t gw, int slices) {
 }
 
 cudaError_t launch_wgrad2(const TcWeightPlan& tw, const TcWeightCall& call, const int32_t* perm,
-                          unsigned int* gbar, cudaStream_t s) {
+                          cudaStream_t s) {
   int dev = 0;
   cudaGetDevice(&dev);
   static int nsm_cache[64] = {0};
@@ -571,16 +548,13 @@ cudaError_t launch_wgrad2(const TcWeightPlan& tw, const TcWeightCall& call, cons
   if (units > (1ll << 30)) return cudaErrorInvalidValue;
   a.units = static_cast<int32_t>(units);
   a.elems = tw.n_rt * (128 * call.gw + 128);
-  int kslices = kSlices;
-  if (const char* ks = getenv("SCC_W2_SLICES")) kslices = atoi(ks);
-  a.slices = static_cast<int32_t>(std::min<int64_t>(units, kslices));
+  a.slices = static_cast<int32_t>(std::min<int64_t>(units, kSlices));
   const int cap = call.max_ctas > 0 ? std::min(call.max_ctas, nsm) : nsm;
   const int grid = std::min(a.slices, cap);
   if (tc_wgrad2_workspace_bytes(call.c_out, call.gw, a.slices) > call.workspace_bytes) return cudaErrorInvalidValue;
   a.part = static_cast<float*>(call.workspace);
   a.dweight = call.dweight;
   a.dbias = call.dbias;
-  a.gbar = gbar;
   a.perm = perm;
   a.starts = call.starts;
 
@@ -614,21 +588,22 @@ cudaError_t launch_wgrad2(const TcWeightPlan& tw, const TcWeightCall& call, cons
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = 1024 + WLayout(a.xr, a.stages).total;
   cfg.stream = s;
-  cudaLaunchAttribute attr[2];
-  attr[0].id = cudaLaunchAttributeCooperative;  // the grid barrier needs co-residency
-  attr[0].val.cooperative = 1;
-  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 2;
+  cfg.numAttrs = 1;
   cudaError_t e = cudaLaunchKernelEx(&cfg, tc_wgrad2_kernel, tdy, tx, a);
-  if (e != cudaSuccess) {
-    (void)cudaGetLastError();
-    cfg.numAttrs = 1;  // cooperative only
-    e = cudaLaunchKernelEx(&cfg, tc_wgrad2_kernel, tdy, tx, a);
-  }
   if (e != cudaSuccess) return e;
-  note_launches(1);
+  cudaLaunchConfig_t rc{};
+  rc.gridDim = dim3(static_cast<unsigned>((a.elems * 8 + 255) / 256));
+  rc.blockDim = dim3(256);
+  rc.stream = s;
+  rc.attrs = attr;
+  rc.numAttrs = 1;
+  e = cudaLaunchKernelEx(&rc, tc_wgrad2_reduce, a);
+  if (e != cudaSuccess) return e;
+  note_launches(2);
   return cudaSuccess;
 }
 

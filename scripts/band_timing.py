@@ -52,7 +52,7 @@ for path, name in ((_lib.SCC_PATH_TENSOR_V1, "gen1"), (_lib.SCC_PATH_TENSOR, "ge
                 starts[0], statistics.median(starts), starts[-1], ends[0], statistics.median(ends), ends[int(0.9 * len(ends))], ends[-1]))
             t = [buf[128 + i] for i in range(64)]
             t0 = t[0]
-            lab = {0: "start", 1: "dep", 2: "tma0", 46: "tma_last", 3: "panel", 4: "tabs", 5: "w", 63: "end", 50: "b_loop0", 51: "b_loop1", 52: "b_fence"}
+            lab = {0: "start", 1: "dep", 2: "tma_c0_last_tile", 3: "panel", 40: "bar_init", 41: "tab_bulk", 42: "tmem_alloc", 43: "sync", 44: "tileiter"}
             for i in range(8): lab[6 + i] = f"mma{i}"; lab[14 + i] = f"epi{i}"; lab[22 + i] = f"cv{i}s"; lab[30 + i] = f"cv{i}e"
             for g in range(4): lab[38 + g] = f"eg{g}ld"; lab[42 + g] = f"eg{g}st"
             print(op, "epi tile1 grp1 [start, ld done, wait_read done, sts done, fence done, tma issued] (us):", [round((t[54 + i] - t0) / 1e3, 3) if t[54 + i] > t0 else 0 for i in range(6)])
