@@ -84,14 +84,10 @@ constexpr int kWorkers = 192;                  // warps 2, 3, 8..11: panel build
 constexpr int kSmemLimit = 227 * 1024;
 constexpr int kStoreBuf = 32 * 32 * 4;         // one [32 rows][32 px] TMA-store box
 constexpr int kStoreBufs = 2;                  // per epilogue warp (32-row mode)
-// Epilogue store modes.  TMA costs ~0.15 us of issue per instruction per SM
-// whatever the box size (tests/cuda/tma_*probe.cu), so the widest box the
-// output rows allow wins: one box per warp and tile when the tile's rows are a
-// single strided run of the output tensor.
+// Epilogue store modes.
 enum : int32_t {
   kStoreStg = 0,    // plain per-row stores (ragged row sets)
   kStoreRows32 = 1, // [32 rows][32 px] boxes
-  kStoreTile = 2,   // one [NT rows][32 px] box per warp and tile
 };
 constexpr int kMaxScratch = 32 * 1024;         // W + oc tables staged for the panel build
 constexpr int kMaxRt = 16;                     // row tiles / classes carried in the params
@@ -111,8 +107,6 @@ struct Band2Args {
   int32_t n_rt, ring, cls, rb;
   int32_t c_in, c_out, gw, c_out_t;
   int32_t store_mode, out_cls;  // kStore*; class run length of the output view
-  int32_t tile_d;            // kStoreTile: 0 = rows contiguous, else D classes in the box
-  int32_t tile_bufs;         // kStoreTile staging buffers per warp (1 or 2)
   int32_t w_staged;          // W + oc tables bulk-copied to smem for the panel build
   int32_t fwd4;              // forward panel words are whole-window or empty (build_panel_fwd4)
   int32_t nbps;              // 32-pixel blocks per sample
@@ -167,7 +161,8 @@ struct Layout {
     panel = 0;
     raw = panel + total_chunks * 2 * NT * 128;
     st = raw + stages * kStageBytes;
-    st_warp = mode == kStoreRows32 ? kStoreBufs * kStoreBuf : mode == kStoreTile ? tile_bufs * NT * 128 : 0;
+    st_warp = mode == kStoreRows32 ? kStoreBufs * kStoreBuf : 0;
+    (void)tile_bufs;
     const int stb = 4 * st_warp > scratch ? 4 * st_warp : scratch;
     rows = st + ((stb + 1023) & ~1023);
     bias = rows + 4 * n_rt * NT;
@@ -356,7 +351,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   // No static shared memory in this kernel: the dynamic window starts
   // 1024-aligned and every derived pointer stays in the shared address space.
   extern __shared__ __align__(1024) uint8_t smem[];
-  const Layout<NT> L(a.total_chunks, a.stages, a.n_rt, a.store_mode, a.tile_bufs, a.scratch);
+  const Layout<NT> L(a.total_chunks, a.stages, a.n_rt, a.store_mode, 0, a.scratch);
   uint8_t* panel = smem + L.panel;
   uint8_t* raw = smem + L.raw;
   uint8_t* stbuf = smem + L.st;
@@ -596,7 +591,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       named_bar_sync(2, 128);
       const int q = warp & 3;
-      int acc = 0, sbuf = 0, tbuf = 0;
+      int acc = 0, sbuf = 0;
       uint32_t aph = 0;
       TileIter it(a);
       int ti = 0;
@@ -611,17 +606,6 @@ __global__ void __launch_bounds__(kThreads, 1)
           tc_fence_after();
           if (q < it.cnt) {
             const uint32_t taddr = tmem + acc * NT + (static_cast<uint32_t>(q * 32) << 16);
-            const uint32_t tbase = wbuf_a + tbuf * NT * 128 + lane * 4;
-            if (a.store_mode == kStoreTile) {
-              // the previous store from this buffer must have read it
-              if (lane == 0) {
-                if (a.tile_bufs == 2)
-                  bulk_wait_read<1>();
-                else
-                  bulk_wait_read<0>();
-              }
-              __syncwarp();
-            }
 #pragma unroll 1
             for (int c0 = 0; c0 < NT; c0 += 32) {
               const int g0 = rt * NT + c0;  // first tile row of this 32-row group
@@ -631,21 +615,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               float bb[32];
 #pragma unroll
               for (int j = 0; j < 32; ++j) bb[j] = bias_s[g0 + j];
-              if (a.store_mode == kStoreTile) {
-                // row g of the tile -> box row: contiguous, or [j][d] of the
-                // class box {32 px, D, out_cls}; lanes own consecutive words
-                int srow0 = c0, sstride = 1;
-                if (a.tile_d) {
-                  const int cl = g0 / a.out_cls, jj = g0 - cl * a.out_cls;
-                  srow0 = jj * a.tile_d + a.out_class_d[cl];
-                  sstride = a.tile_d;
-                }
-                if (g0 < a.c_out_t || !a.tile_d) {
-#pragma unroll
-                  for (int j = 0; j < 32; ++j)
-                    sts_f32(tbase + (srow0 + j * sstride) * 128, __uint_as_float(v[j]) + bb[j]);
-                }
-              } else if (a.store_mode == kStoreRows32) {
+              if (a.store_mode == kStoreRows32) {
                 // Stage [32 rows][32 px] (lanes own consecutive words: no
                 // conflicts) and write it with one TMA store; buffers rotate.
                 if (lane == 0) bulk_wait_read<kStoreBufs - 1>();
@@ -671,16 +641,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                   if (rr[j] >= 0) obase[static_cast<int64_t>(rr[j]) * a.plane] = __uint_as_float(v[j]) + bb[j];
                 }
               }
-            }
-            if (a.store_mode == kStoreTile) {
-              fence_proxy_async_smem();
-              __syncwarp();
-              if (lane == 0) {
-                const int z = a.tile_d ? it.n * a.out_cls : it.n * a.c_out_t + rt * NT;
-                tma_store_3d(&tout, wbuf + tbuf * NT * 128, (it.b0 + q) * kBlkPx, 0, z);
-                bulk_commit();
-              }
-              if (a.tile_bufs == 2) tbuf ^= 1;
             }
           }
           tc_fence_before();
@@ -732,18 +692,11 @@ cudaError_t launch_tc2_nt(const TcBandPlan& tp, const TcDeviceTables& dt, const 
   // (store_ok: every 32 consecutive tile rows are one equally strided class
   // run); otherwise plain per-row stores.
   const bool cls_ok = tp.store_ok && static_cast<int>(tp.out_class_d.size()) <= kMaxCls;
-  int32_t mode = cls_ok ? kStoreRows32 : kStoreStg;
-  int32_t tile_d = 0;
-  if (BWD && call.c_out_t % NT == 0) {
-    mode = kStoreTile;  // dx rows are the input channels in order: box {32 px, 1, NT}
-  } else if (!BWD && cls_ok && tp.n_rt == 1 && tp.out_n_class <= 256 && tp.out_cls <= 256 &&
-             tp.out_n_class * tp.out_cls == call.c_out_t) {
-    mode = kStoreTile;  // the single row tile holds every filter: box {32 px, D, c_out/D}
-    tile_d = tp.out_n_class;
-  }
-  if (const char* e = getenv("SCC_TC2_STORE")) mode = std::min(mode, static_cast<int32_t>(atoi(e)));
-  if (mode == kStoreRows32 && !cls_ok) mode = kStoreStg;
-  const bool cls_view = mode == kStoreRows32 || (mode == kStoreTile && tile_d > 0);
+  // 32-row boxes stored as soon as they are staged.  (Whole-tile boxes,
+  // one store per warp and tile, measured slower on config 1: 30.3 vs
+  // 31.4 us per step -- the stores start a tile later -- and were dropped.)
+  const int32_t mode = cls_ok ? kStoreRows32 : kStoreStg;
+  const bool cls_view = mode == kStoreRows32;
   CUtensorMap tout;
   {
     const int32_t ocls = cls_view ? tp.out_cls : call.c_out_t;
@@ -751,11 +704,7 @@ cudaError_t launch_tc2_nt(const TcBandPlan& tp, const TcDeviceTables& dt, const 
     const uint64_t dims[3] = {static_cast<uint64_t>(P), static_cast<uint64_t>(ond),
                               static_cast<uint64_t>(call.n) * ocls};
     const uint64_t strides[2] = {static_cast<uint64_t>(P) * 4, static_cast<uint64_t>(P) * 4 * ond};
-    uint32_t box[3] = {32, 1, 32};
-    if (mode == kStoreTile) {
-      box[1] = tile_d > 0 ? static_cast<uint32_t>(tile_d) : 1u;
-      box[2] = tile_d > 0 ? static_cast<uint32_t>(tp.out_cls) : static_cast<uint32_t>(NT);
-    }
+    const uint32_t box[3] = {32, 1, 32};
     if (!encode_f32(&tout, call.out, 3, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_NONE))
       return cudaErrorInvalidValue;
   }
@@ -775,7 +724,6 @@ cudaError_t launch_tc2_nt(const TcBandPlan& tp, const TcDeviceTables& dt, const 
   if (cls_ok)
     for (size_t i = 0; i < tp.out_class_d.size(); ++i) a.out_class_d[i] = tp.out_class_d[i];
   a.store_mode = mode;
-  a.tile_d = tile_d;
   a.out_cls = tp.out_cls;
   a.n_rt = tp.n_rt;
   a.ring = tp.ring;
@@ -799,16 +747,13 @@ cudaError_t launch_tc2_nt(const TcBandPlan& tp, const TcDeviceTables& dt, const 
     // multiples of 4 when shift and c_in are
     a.fwd4 = (!BWD && a.w_staged && call.gw % 4 == 0 && call.c_in % 4 == 0 && shift % 4 == 0) ? 1 : 0;
   }
-  // two tile buffers per warp when the ring keeps >= 4 stages, else one
-  a.tile_bufs = 2;
-  if (mode == kStoreTile && band2_stages<NT>(tp, mode, 2, a.scratch) < 4) a.tile_bufs = 1;
-  a.stages = band2_stages<NT>(tp, a.store_mode, a.tile_bufs, a.scratch);
+  a.stages = band2_stages<NT>(tp, a.store_mode, 0, a.scratch);
   a.plane = P;
   const int64_t units = call.n * a.nbps;
   if (units > (1ll << 30)) return cudaErrorInvalidValue;
   a.units = static_cast<int32_t>(units);
   const int smem =
-      1024 + Layout<NT>(a.total_chunks, a.stages, a.n_rt, a.store_mode, a.tile_bufs, a.scratch).total;
+      1024 + Layout<NT>(a.total_chunks, a.stages, a.n_rt, a.store_mode, 0, a.scratch).total;
 
   static int nsm_cache[64] = {0};
   static bool attr_set[64] = {false};
@@ -851,8 +796,8 @@ bool tc_band2_supported(const TcBandPlan& tp, int64_t plane, int32_t c_out) {
   if (!tp.ok || plane % 4 != 0 || plane < 4) return false;
   if (tp.rb % 8 != 0 || tp.n_rt > kMaxRt || tp.n_class > kMaxCls) return false;
   // The whole panel stays resident next to >= 4 raw stages.
-  const int st = tp.nt == 128 ? band2_stages<128>(tp, kStoreTile, 1, kMaxScratch)
-                               : band2_stages<64>(tp, kStoreTile, 1, kMaxScratch);
+  const int st = tp.nt == 128 ? band2_stages<128>(tp, kStoreRows32, 0, kMaxScratch)
+                               : band2_stages<64>(tp, kStoreRows32, 0, kMaxScratch);
   return st >= 4;
 }
 
