@@ -101,6 +101,7 @@ struct Band2Args {
   float* out;
   const int32_t* rows;       // [n_rt*NT] output channel per tile row, -1 = none
   const int32_t* perm;       // cycle-sorted position -> oc
+  const int32_t* inv_perm;   // oc -> cycle-sorted position
   const int32_t* starts;     // oc -> window start
   int32_t rt_start8[kMaxRt], rt_nk8[kMaxRt], rt_cb[kMaxRt + 1];
   int32_t class_d[kMaxCls], out_class_d[kMaxCls];
@@ -714,6 +715,7 @@ cudaError_t launch_tc2_nt(const TcBandPlan& tp, const TcDeviceTables& dt, const 
   a.out = call.out;
   a.rows = dt.rows;
   a.perm = dt.perm;
+  a.inv_perm = dt.inv_perm;
   a.starts = dt.starts;
   for (int rt = 0; rt < tp.n_rt; ++rt) {
     a.rt_start8[rt] = tp.rt_info[4 * rt];
@@ -748,6 +750,7 @@ cudaError_t launch_tc2_nt(const TcBandPlan& tp, const TcDeviceTables& dt, const 
     a.fwd4 = (!BWD && a.w_staged && call.gw % 4 == 0 && call.c_in % 4 == 0 && shift % 4 == 0) ? 1 : 0;
   }
   a.stages = band2_stages<NT>(tp, a.store_mode, 0, a.scratch);
+  if (const char* e = getenv("SCC_TC2_MAXSTAGES")) a.stages = std::max(2, std::min(a.stages, atoi(e)));
   a.plane = P;
   const int64_t units = call.n * a.nbps;
   if (units > (1ll << 30)) return cudaErrorInvalidValue;
