@@ -448,6 +448,17 @@ def run_ours(args):
                "ms_per_step": round(dt * 1e3, 4),
                "api": "scc_fwd_bwd_host_f32 (include/scc_b200.h)"}
 
+    # ---- BASELINE configs C2/C3: SCC-ResNet-18 / SCC-VGG16 training images/sec ----
+    models = None
+    if not args.no_models:
+        from paper_2101_00745_b200.train import train_throughput
+        models = {}
+        for name in ("resnet18", "vgg16"):
+            try:
+                models[name] = train_throughput(name, batch=128, steps=20, warmup=5)
+            except Exception as ex:  # reported, never required for the headline
+                models[name] = {"error": str(ex)[:200]}
+
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
         try:
@@ -477,6 +488,7 @@ def run_ours(args):
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": int(launches),
+            "models": models,
             "clocks": clocks,
         }
         print(json.dumps(line), flush=True)
@@ -496,6 +508,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch each step eagerly")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-models", action="store_true", help="skip the SCC-ResNet-18/VGG16 images/sec")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     args = ap.parse_args()
     if args.warmup < 3:

@@ -372,13 +372,21 @@ struct WGrid {
 WGrid weight_grid(const TcWeightPlan& tw, int64_t n, int64_t plane) {
   WGrid g{};
   g.blk = tw.nw <= 128 ? 2 : 1;
-  const int kpix = g.blk * kAtom;
   g.acol0 = tw.nw <= 128 ? 128 : 256;
-  g.t_stages = std::min(kMaxT, (512 - g.acol0) / (2 * kpix));
-  const int a_stage = 128 * kpix * 4;
-  const int b_stage = 2 * tw.nw * kpix * 4;
   constexpr int kBudget = 227 * 1024 - 1024 - 1024;
-  g.a_stages = std::min(kMaxA, (kBudget - g.t_stages * b_stage) / a_stage);
+  // Keep >= 2 dy stages: shed x/TMEM stages first, then halve the stage width
+  // (nw = 128 with 2-atom stages needs 64 KB per x stage).
+  int kpix = 0, a_stage = 0, b_stage = 0;
+  for (;;) {
+    kpix = g.blk * kAtom;
+    g.t_stages = std::min(kMaxT, (512 - g.acol0) / (2 * kpix));
+    a_stage = 128 * kpix * 4;
+    b_stage = 2 * tw.nw * kpix * 4;
+    while (g.t_stages > 1 && (kBudget - g.t_stages * b_stage) / a_stage < 2) --g.t_stages;
+    g.a_stages = std::min(kMaxA, (kBudget - g.t_stages * b_stage) / a_stage);
+    if (g.a_stages >= 2 || g.blk == 1) break;
+    g.blk = 1;
+  }
   g.smem = g.a_stages * a_stage + g.t_stages * b_stage + 1024 + 512;
   g.pcs = (plane + kpix - 1) / kpix;
   g.total_chunks = n * g.pcs;

@@ -1,0 +1,114 @@
+"""SCC model zoo (CIFAR-shape SCC-ResNet-18 and SCC-VGG16).
+
+The reference's model harness is a sequential JSON-described network of
+conv / SCC stages (model.cpp:190-232, the "dsc_block" of model.cpp:213-220:
+depthwise 3x3 then SCC, nothing in between).  It has no BN, residuals or
+pooling, so it cannot express the paper's VGG / ResNet models; these are
+built here from the rule SURVEY.md section 7.3 derives from the paper's
+parameter counts:
+
+    every 3x3 conv except the stem -> DW3x3(stride s) + SCC(cg=2, co=50%),
+    1x1 shortcut convs stay dense, BN + ReLU after the SCC.
+
+The SCC layers run the libscc_b200 kernels (``SCC2d``); depthwise convs, BN,
+pooling and the head are stock PyTorch (library ops on the non-hot path).
+The DW -> SCC pair keeps the reference's ordering (no BN between them), which
+is what a fused DW+SCC kernel needs.
+"""
+from __future__ import annotations
+
+from typing import List
+
+import torch
+from torch import nn
+
+from .module import SCC2d
+
+
+class DSC(nn.Module):
+    """dsc_block (model.cpp:213-220): depthwise 3x3 (stride s) then SCC."""
+
+    def __init__(self, cin: int, cout: int, stride: int = 1, cg: int = 2, co="50%", device=None):
+        super().__init__()
+        self.dw = nn.Conv2d(cin, cin, 3, stride=stride, padding=1, groups=cin, bias=False, device=device)
+        self.scc = SCC2d(cin, cout, cg, co, bias=False, device=device)
+
+    def forward(self, x):
+        return self.scc(self.dw(x))
+
+
+class BasicBlock(nn.Module):
+    def __init__(self, cin: int, cout: int, stride: int, cg: int, co, device=None):
+        super().__init__()
+        self.c1 = DSC(cin, cout, stride, cg, co, device)
+        self.b1 = nn.BatchNorm2d(cout, device=device)
+        self.c2 = DSC(cout, cout, 1, cg, co, device)
+        self.b2 = nn.BatchNorm2d(cout, device=device)
+        self.short = None
+        if stride != 1 or cin != cout:
+            self.short = nn.Sequential(
+                nn.Conv2d(cin, cout, 1, stride=stride, bias=False, device=device),
+                nn.BatchNorm2d(cout, device=device))
+
+    def forward(self, x):
+        y = torch.relu(self.b1(self.c1(x)))
+        y = self.b2(self.c2(y))
+        return torch.relu(y + (x if self.short is None else self.short(x)))
+
+
+class SCCResNet18(nn.Module):
+    """CIFAR ResNet-18 with every 3x3 conv but the stem as DW3x3 + SCC."""
+
+    def __init__(self, num_classes: int = 10, cg: int = 2, co="50%", device=None):
+        super().__init__()
+        self.stem = nn.Sequential(nn.Conv2d(3, 64, 3, padding=1, bias=False, device=device),
+                                  nn.BatchNorm2d(64, device=device), nn.ReLU())
+        blocks: List[nn.Module] = []
+        cin = 64
+        for cout, stride in ((64, 1), (128, 2), (256, 2), (512, 2)):
+            blocks += [BasicBlock(cin, cout, stride, cg, co, device), BasicBlock(cout, cout, 1, cg, co, device)]
+            cin = cout
+        self.blocks = nn.Sequential(*blocks)
+        self.fc = nn.Linear(512, num_classes, device=device)
+
+    def forward(self, x):
+        y = self.blocks(self.stem(x))
+        return self.fc(torch.flatten(nn.functional.adaptive_avg_pool2d(y, 1), 1))
+
+
+class SCCVGG16(nn.Module):
+    """CIFAR VGG16 (13 conv layers, BN) with every 3x3 conv but the first as
+    DW3x3 + SCC."""
+
+    CFG = (64, 64, "M", 128, 128, "M", 256, 256, 256, "M", 512, 512, 512, "M", 512, 512, 512, "M")
+
+    def __init__(self, num_classes: int = 10, cg: int = 2, co="50%", device=None):
+        super().__init__()
+        layers: List[nn.Module] = []
+        cin = 3
+        for i, v in enumerate(self.CFG):
+            if v == "M":
+                layers.append(nn.MaxPool2d(2))
+                continue
+            conv = (nn.Conv2d(cin, v, 3, padding=1, bias=False, device=device) if i == 0
+                    else DSC(cin, v, 1, cg, co, device))
+            layers += [conv, nn.BatchNorm2d(v, device=device), nn.ReLU()]
+            cin = v
+        self.features = nn.Sequential(*layers)
+        self.fc = nn.Linear(512, num_classes, device=device)
+
+    def forward(self, x):
+        return self.fc(torch.flatten(self.features(x), 1))
+
+
+MODELS = {"resnet18": SCCResNet18, "vgg16": SCCVGG16}
+
+
+def scc_layers(model: nn.Module):
+    return [m for m in model.modules() if isinstance(m, SCC2d)]
+
+
+def param_counts(model: nn.Module):
+    scc = sum(p.numel() for m in scc_layers(model) for p in m.parameters())
+    total = sum(p.numel() for p in model.parameters())
+    return {"total": total, "scc": scc}

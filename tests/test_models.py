@@ -1,0 +1,82 @@
+"""Model-path coverage: every SCC layer shape of SCC-ResNet-18 / SCC-VGG16
+(PAPER.md:351-365 via SURVEY.md section 7.3) through the kernels against a
+torch fp64 dense reference of the same operator (a masked 1x1 conv), the
+parameter counts the paper states, and a short training run whose loss
+falls (the BASELINE C2/C3 harness, paper_2101_00745_b200/train.py)."""
+import pytest
+
+torch = pytest.importorskip("torch")
+
+import paper_2101_00745_b200 as scc  # noqa: E402
+from paper_2101_00745_b200 import models  # noqa: E402
+
+FWD_TOL, GRAD_TOL = 1e-5, 1e-4
+
+
+def test_param_counts_match_paper():
+    # SCC-VGG16 0.87 M, SCC-ResNet-18 0.84 M parameters
+    r = models.param_counts(models.SCCResNet18())
+    v = models.param_counts(models.SCCVGG16())
+    assert r["scc"] == 610304 and abs(r["total"] - 0.84e6) / 0.84e6 < 0.02
+    assert v["scc"] == 817152 and abs(v["total"] - 0.87e6) / 0.87e6 < 0.02
+    assert len(models.scc_layers(models.SCCResNet18())) == 16
+
+
+def _shapes():
+    out = set()
+    for name, cls in models.MODELS.items():
+        m = cls()
+        size = {"resnet18": [32, 32, 16, 16, 8, 8, 4, 4], "vgg16": [32, 16, 16, 8, 8, 8, 4, 4, 4, 2, 2, 2]}[name]
+        for layer, hw in zip(models.scc_layers(m), [s for s in size for _ in range(2)] if name == "resnet18" else size):
+            out.add((layer.cfg.c_in, layer.cfg.c_out, hw))
+    return sorted(out)
+
+
+def _dense(cfg, w):
+    ci, co, gw = cfg.c_in, cfg.c_out, cfg.group_width
+    idx = torch.tensor([[((oc * cfg.shift) % ci + s) % ci for s in range(gw)] for oc in range(co)],
+                       device=w.device)
+    full = torch.zeros(co, ci, device=w.device, dtype=torch.float64)
+    full.scatter_add_(1, idx, w.view(co, gw).double())
+    return full, idx
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("shape", _shapes(), ids=lambda s: f"{s[0]}to{s[1]}_{s[2]}x{s[2]}")
+def test_model_layer_shapes(shape):
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    ci, co, hw = shape
+    cfg = scc.scc_config_new(ci, co, 2, "50%", True)
+    n = 8
+    g = torch.Generator(device="cuda").manual_seed(ci * 7 + co + hw)
+    x = torch.randn(n, ci, hw, hw, device="cuda", generator=g)
+    gy = torch.randn(n, co, hw, hw, device="cuda", generator=g)
+    wts = scc.scc_weights_init(cfg)
+    wts.bias.uniform_(-0.5, 0.5)
+    y = scc.scc_forward(x, wts, cfg)
+    gr = scc.scc_backward(gy, x, wts, cfg)
+    W, idx = _dense(cfg, wts.weight)
+    yr = torch.einsum("oc,nchw->nohw", W, x.double()) + wts.bias.double().view(1, -1, 1, 1)
+    dxr = torch.einsum("oc,nohw->nchw", W, gy.double())
+    dwr = torch.gather(torch.einsum("nohw,nchw->oc", gy.double(), x.double()), 1, idx).reshape(-1)
+    dbr = gy.double().sum((0, 2, 3))
+
+    def nrel(a, b):
+        return float((a.double() - b).abs().max() / b.abs().max())
+
+    assert nrel(y, yr) <= FWD_TOL
+    assert nrel(gr.grad_input, dxr) <= GRAD_TOL
+    assert nrel(gr.params.grad_weight, dwr) <= GRAD_TOL
+    assert nrel(gr.params.grad_bias, dbr) <= GRAD_TOL
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["resnet18", "vgg16"])
+def test_training_loss_falls(name):
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2101_00745_b200.train import train_throughput
+    r = train_throughput(name, batch=32, steps=15, warmup=1)
+    assert r["images_per_s"] > 0
+    assert r["loss_last"] < r["loss_first"], r
