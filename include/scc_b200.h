@@ -84,6 +84,10 @@ uint64_t scc_launch_count(void);
  * backward-weight launch (slots 32..63, map in scc_tc_wgrad.cu) on the
  * current device.  Copies min(n, 64) values; returns the count or -1. */
 int scc_debug_trace(uint64_t* out, int n);
+/* Diagnostic: the same for the fused backward kernel (scc_tc_bwd.cu; 64
+ * CTA-0 slots, then start / end stamps of up to 256 CTAs).  Zeros unless the
+ * library was built with -DSCC_TRACE. */
+int scc_debug_trace_fused(uint64_t* out, int n);
 
 /* ---- geometry (host only; replaces config.cpp / cycle.cpp) --------------- */
 

@@ -34,7 +34,7 @@ SCC_PATH_TENSOR_V1 = 3
 
 # Every symbol include/scc_b200.h declares (tests assert the .so exports them).
 EXPORTS = (
-    "scc_last_error", "scc_abi_version", "scc_launch_count", "scc_debug_trace",
+    "scc_last_error", "scc_abi_version", "scc_launch_count", "scc_debug_trace", "scc_debug_trace_fused",
     "scc_overlap_parse", "scc_overlap_resolve",
     "scc_plan_create", "scc_plan_destroy", "scc_plan_config", "scc_plan_cycle_starts",
     "scc_plan_window_of", "scc_plan_covering_filters", "scc_forward_macs",
@@ -114,6 +114,7 @@ def _declare(L):
         "scc_abi_version": ([], C.c_int),
         "scc_launch_count": ([], C.c_uint64),
         "scc_debug_trace": ([C.POINTER(C.c_uint64), C.c_int], C.c_int),
+        "scc_debug_trace_fused": ([C.POINTER(C.c_uint64), C.c_int], C.c_int),
         "scc_overlap_parse": ([C.c_char_p, P(i32), P(C.c_double), P(i64)], C.c_int),
         "scc_overlap_resolve": ([i32, C.c_double, i64, i64, P(i64)], C.c_int),
         "scc_plan_create": ([i64, i64, i64, i32, C.c_double, i64, i32, P(vp)], C.c_int),

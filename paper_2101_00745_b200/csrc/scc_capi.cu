@@ -261,6 +261,20 @@ WeightLaunch weight_args(const Plan& p, const DeviceTables& t, int64_t n, int64_
   return a;
 }
 
+// The fused backward kernel (scc_tc_bwd.cu) serves scc_backward and, so
+// that fused and separate calls agree bitwise, the separate backward-data and
+// backward-weight entry points too, whenever its geometry fits.
+bool fused_bwd_supported(const Plan& p, int64_t plane) {
+  if (p.path == SCC_PATH_TENSOR_V1 || p.path == SCC_PATH_CUDA_CORE) return false;
+  static const bool off = [] {
+    const char* e = getenv("SCC_NO_FUSED_BWD");
+    return e != nullptr && e[0] == '1';
+  }();
+  if (off) return false;
+  return tc_bwd_supported(p.tc_wgt, plane, static_cast<int32_t>(p.cfg.c_in), static_cast<int32_t>(p.cfg.c_out),
+                          static_cast<int32_t>(p.cfg.group_width));
+}
+
 size_t weight_ws_bytes(const Plan& p, int64_t n, int64_t plane) {
   const size_t cc = weight_cc_workspace_bytes(p.fwd.nblk(), p.fwd.max_block_len, n, plane);
   const size_t tc = tc_weight_supported(p.tc_wgt, plane) ? tc_weight_workspace_bytes(p.tc_wgt, n, plane) : 0;
@@ -268,7 +282,11 @@ size_t weight_ws_bytes(const Plan& p, int64_t n, int64_t plane) {
                          ? tc_wgrad2_workspace_bytes(static_cast<int32_t>(p.cfg.c_out),
                                                      static_cast<int32_t>(p.cfg.group_width), 74)
                          : 0;
-  return std::max(std::max(cc, tc), tc2);
+  const size_t tc3 = fused_bwd_supported(p, plane)
+                         ? tc_bwd_workspace_bytes(static_cast<int32_t>(p.cfg.c_out),
+                                                  static_cast<int32_t>(p.cfg.group_width), n, plane)
+                         : 0;
+  return std::max(std::max(cc, tc), std::max(tc2, tc3));
 }
 
 void do_forward(Plan& p, int64_t n, int64_t h, int64_t w, const float* x, const float* wt,
@@ -293,12 +311,43 @@ void do_forward(Plan& p, int64_t n, int64_t h, int64_t w, const float* x, const 
   cuda_check(launch_band_cc(band_args(p, t, false, n, h * w, x, y, wt, b), s), "forward launch");
 }
 
+bool use_fused(Plan& p, int64_t n, int64_t h, int64_t w) {
+  return choose_path(p, n, h, w, 2) == SCC_PATH_TENSOR && fused_bwd_supported(p, h * w);
+}
+
+void launch_fused(Plan& p, int64_t n, int64_t h, int64_t w, const float* dy, const float* x, const float* wt,
+                  float* dx, float* dw, float* db, void* ws, size_t ws_bytes, cudaStream_t s) {
+  const DeviceTables& t = tables(p);
+  TcBwdCall c{};
+  c.dy = dy;
+  c.x = x;
+  c.weight = wt;
+  c.dx = dx;
+  c.dweight = dw;
+  c.dbias = db;
+  c.workspace = ws;
+  c.workspace_bytes = ws_bytes;
+  c.n = n;
+  c.plane = h * w;
+  c.c_in = static_cast<int32_t>(p.cfg.c_in);
+  c.c_out = static_cast<int32_t>(p.cfg.c_out);
+  c.gw = static_cast<int32_t>(p.cfg.group_width);
+  c.starts = t.starts;
+  c.do_dx = dx != nullptr;
+  c.do_dw = dw != nullptr;
+  cuda_check(launch_tc_bwd(p.tc_wgt, c, s), "backward (fused tensor) launch");
+}
+
 void do_backward_data(Plan& p, int64_t n, int64_t h, int64_t w, const float* dy, const float* wt,
                       float* dx, cudaStream_t s, int32_t max_ctas = 0) {
   check_extents(n, h, w);
   check_ptr(dy, "dy");
   check_ptr(wt, "weight");
   check_ptr(dx, "dx");
+  if (use_fused(p, n, h, w)) {
+    launch_fused(p, n, h, w, dy, nullptr, wt, dx, nullptr, nullptr, nullptr, 0, s);
+    return;
+  }
   const DeviceTables& t = tables(p);
   if (choose_path(p, n, h, w, 1) == SCC_PATH_TENSOR) {
     TcBandCall c = tc_call(p, true, n, h * w, dy, dx, wt, nullptr);
@@ -327,6 +376,10 @@ void do_backward_weight(Plan& p, int64_t n, int64_t h, int64_t w, const float* d
   const size_t need = weight_ws_bytes(p, n, h * w);
   if (ws_bytes < need || (need > 0 && ws == nullptr)) {
     fail(SCC_ERR_ARGUMENT, "workspace too small: need " + std::to_string(need) + " bytes");
+  }
+  if (use_fused(p, n, h, w)) {
+    launch_fused(p, n, h, w, dy, x, nullptr, nullptr, dw, db, ws, ws_bytes, s);
+    return;
   }
   const DeviceTables& t = tables(p);
   if (choose_path(p, n, h, w, 2) == SCC_PATH_TENSOR) {
@@ -388,6 +441,21 @@ void do_backward(Plan& p, int64_t n, int64_t h, int64_t w, const float* dy, cons
                  const float* wt, float* dx, float* dw, float* db, void* ws, size_t ws_bytes,
                  cudaStream_t s) {
   const int64_t plane = h * w;
+  if (use_fused(p, n, h, w)) {
+    check_extents(n, h, w);
+    check_ptr(dy, "dy");
+    check_ptr(x, "x");
+    check_ptr(wt, "weight");
+    check_ptr(dx, "dx");
+    check_ptr(dw, "dweight");
+    check_bias(p, db, "dbias");
+    const size_t need = weight_ws_bytes(p, n, plane);
+    if (ws_bytes < need || (need > 0 && ws == nullptr)) {
+      fail(SCC_ERR_ARGUMENT, "workspace too small: need " + std::to_string(need) + " bytes");
+    }
+    launch_fused(p, n, h, w, dy, x, wt, dx, dw, db, ws, ws_bytes, s);
+    return;
+  }
   const bool both2 = p.path != SCC_PATH_TENSOR_V1 && p.path != SCC_PATH_CUDA_CORE &&
                      choose_path(p, n, h, w, 1) == SCC_PATH_TENSOR &&
                      choose_path(p, n, h, w, 2) == SCC_PATH_TENSOR &&
@@ -516,6 +584,10 @@ int scc_debug_trace(uint64_t* out, int n) {
   }
   const int m2 = n - 128 < 64 + 2048 ? n - 128 : 64 + 2048;
   return scc::tc2_trace(reinterpret_cast<unsigned long long*>(out) + 128, m2) < 0 ? -1 : 128 + m2;
+}
+
+int scc_debug_trace_fused(uint64_t* out, int n) {
+  return scc::tc_bwd_trace(reinterpret_cast<unsigned long long*>(out), n);
 }
 
 scc_status_t scc_overlap_parse(const char* text, int32_t* kind, double* ratio, int64_t* count) {

@@ -113,4 +113,27 @@ cudaError_t launch_wgrad2(const TcWeightPlan& tw, const TcWeightCall& call, cons
 cudaError_t launch_band_tc(const TcBandPlan& tp, const TcDeviceTables& dt, const TcBandCall& call,
                            cudaStream_t s);
 
+// Fused backward (scc_tc_bwd.cu): backward-data and backward-weight from one
+// pass over dy (either half can be switched off; the arithmetic of each half
+// does not depend on the other, so fused and separate calls agree bitwise).
+struct TcBwdCall {
+  const float* dy;
+  const float* x;        // backward-weight only
+  const float* weight;   // backward-data only
+  float* dx;
+  float* dweight;
+  float* dbias;          // nullptr when the layer has no bias
+  void* workspace;
+  size_t workspace_bytes;
+  int64_t n, plane;
+  int32_t c_in, c_out, gw;
+  const int32_t* starts;  // oc -> window start
+  bool do_dx = false, do_dw = false;
+  int32_t max_ctas = 0;
+};
+bool tc_bwd_supported(const TcWeightPlan& tw, int64_t plane, int32_t c_in, int32_t c_out, int32_t gw);
+size_t tc_bwd_workspace_bytes(int32_t c_out, int32_t gw, int64_t n, int64_t plane);
+cudaError_t launch_tc_bwd(const TcWeightPlan& tw, const TcBwdCall& call, cudaStream_t s);
+int tc_bwd_trace(unsigned long long* out, int n);
+
 }  // namespace scc

@@ -1,0 +1,857 @@
+// Fused tensor-core backward (tcgen05, 3xTF32), sm_100a: backward-data and
+// backward-weight of one SCC layer from a single pass over dy
+// (replaces scc_backward_input + scc_backward_params, kernel.cpp:100-189):
+//
+//   dx[n, ic, p]  = sum_oc  W^T[ic, oc] * dy[n, oc, p]          (W^T: window-relative W scattered)
+//   dW[oc, ic]    = sum_{n,p} dy[n, oc, p] * x[n, ic, p]        (ic in the arc of the filters)
+//   db[oc]        = sum_{n,p} dy[n, oc, p]                      (a ones row appended to x)
+//
+// Geometry: one row tile of filters (c_out <= 128, in the class-major order
+// of a single {32 px, cls, D} dy box) and c_in <= 64 input channels.  The
+// pipeline moves PAIRS of 32-pixel blocks (any two consecutive blocks of the
+// CTA's pixel slice):
+//   * dy [c_out rows][32 px] of each block lands by TMA in the
+//     SWIZZLE_128B_BASE32B layout, which is at once an MN-major B operand of
+//     the dx GEMM (D[ic][px] = W^T[ic][oc] * dy[oc][px], K = oc; the pair's two
+//     blocks are the two 32-px atoms of an N = 64 operand) and row-readable by
+//     the converter warps, which write its tf32 lo part to the lo buffers (dx
+//     B lo) and its hi / lo rows to TMEM (A of the dW GEMM, lanes = filters);
+//   * x [arc rows][32 px] (SWIZZLE_128B, K-major) plus a converted lo copy is
+//     B of the dW GEMM (D[oc][ic] = dy[oc][px] * x[ic][px], K = px).
+// W^T stays resident in TMEM, stacked: lanes 0-63 hold W_hi, lanes 64-127
+// W_lo, so one M = 128 MMA yields W_hi*B and W_lo*B in the two lane halves
+// (the epilogue adds them); 3xTF32 for dx is then two MMAs per k-step
+// ([W_hi; W_lo] * dy and [W_hi; W_lo] * dy_lo, the lo*lo term included for
+// free).  Every GEMM runs in TS mode (A from TMEM); shared memory only feeds
+// B operands.  Per pair the MMAs that read the lo buffers go first, so the
+// converters refill them while the rest of the pair's MMAs run.
+//
+// dW accumulates over the CTA's pixel slice in TMEM and is written as that
+// slice's window-relative partial; a PDL-chained kernel sums the partials in
+// a fixed order (the slice count is fixed per geometry, so the bits of dW do
+// not depend on the grid).  dx is drained from TMEM per pair, staged and
+// stored by TMA.  The same kernel, with either GEMM switched off, serves
+// scc_backward_input / scc_backward_params alone, so the fused and separate
+// entry points agree bit for bit.
+//
+// Warp roles (384 threads, one CTA per SM, one slice per CTA):
+//   warp 0      TMA producer
+//   warp 1      TMEM allocator + MMA issuer
+//   warps 2-3   x lo converters (+ the constant ones / zero rows)
+//   warps 4-7   dy row converters (warp q: filter rows 32q..32q+31)
+//   warps 8-11  W^T build (prologue), dx epilogue, dW slice epilogue
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+
+#include "scc_kernels.hpp"
+#include "scc_plan.hpp"
+#include "sm100.cuh"
+#include "tmap.hpp"
+
+namespace scc {
+namespace {
+
+using namespace sm100;
+
+// Diagnostic timeline (build with -DSCC_TRACE): CTA-0 %globaltimer slots and
+// per-CTA start / end stamps; scripts/bwd_timing.py reads them.
+#if defined(SCC_TRACE)
+__device__ unsigned long long g_trace3[64];
+__device__ unsigned long long g_cta3[2 * 256];
+#define TRACE3(slot)                                         \
+  do {                                                       \
+    if (blockIdx.x == 0) g_trace3[(slot)] = globaltimer();   \
+  } while (0)
+#define TRACE3K(base, k)                   \
+  do {                                     \
+    if ((k) < 8) TRACE3((base) + (k));     \
+  } while (0)
+#else
+#define TRACE3(slot) \
+  do {               \
+  } while (0)
+#define TRACE3K(base, k) \
+  do {                   \
+  } while (0)
+#endif
+
+constexpr int kThreads = 384;
+constexpr int kSlots = 3;             // TMA pair slots in the ring
+constexpr int kSlices = 148;          // pixel slices (dW partials) per launch
+constexpr int kSmemLimit = 227 * 1024;
+constexpr int kMaxGw = 32;
+// TMEM columns (512 allocated)
+constexpr uint32_t kWt = 0;          // W^T: [ic lane (hi) | 64 + ic lane (lo)][oc column]
+constexpr uint32_t kDwAcc = 128;     // dW accumulator: [filter lane][x row column]
+constexpr uint32_t kDwA = 256;       // dy hi | lo of the pair's two blocks: [filter lane][px]
+constexpr uint32_t kDxAcc = 384;     // two dx accumulators: [ic lane (+64: lo part)][64 px]
+
+struct BArgs {
+  float* part;               // [slices][c_out*gw + c_out] partial dW | db (c_out <= 128)
+  float* dweight;            // [c_out*gw]
+  float* dbias;              // [c_out] or nullptr
+  const float* weight;       // [c_out*gw]
+  const int32_t* starts;     // oc -> window start
+  int32_t c_in, c_out, gw, cls, n_class;
+  int32_t start8;            // first x row (input channel) of the filters' arc
+  int32_t nx;                // x rows loaded (8-aligned arc)
+  int32_t xr;                // x stage rows (nx + ones row, rounded to 16) = dW MMA N
+  int32_t rbb;               // x TMA box rows when the arc wraps
+  int32_t xbox;              // 1: one x box {32 px, nx rows}
+  int32_t nbps;              // 32-pixel blocks per sample
+  int32_t units;             // n * nbps
+  int32_t elems;             // per-slice partial floats: c_out*gw + c_out
+  int32_t slices;
+  int32_t do_dx, do_dw;
+  int32_t w_bulk;            // 1: W staged by one bulk copy (16 B aligned, size % 16 == 0)
+};
+
+// Filter of class-major dy row `i` (row (d, j) = oc d + D*j).
+__device__ __forceinline__ int row_oc(const BArgs& a, int i) {
+  const int d = i / a.cls;
+  return d + a.n_class * (i - d * a.cls);
+}
+__device__ __forceinline__ int slice_u(const BArgs& a, int k) {
+  return static_cast<int>((static_cast<int64_t>(k) * a.units) / a.slices);
+}
+__device__ __forceinline__ void advance(int& stage, uint32_t& phase, int stages) {
+  if (++stage == stages) {
+    stage = 0;
+    phase ^= 1u;
+  }
+}
+
+__host__ __device__ constexpr int round1k(int b) { return (b + 1023) & ~1023; }
+
+// Shared memory: kSlots TMA pair slots (per block: raw dy | x), one lo pair
+// (per block: dy_lo | x_lo) and one dx staging pair.
+// The W staging of the prologue aliases the lo pair (its writers wait for
+// W^T to be built) and so does the dW row dump of the epilogue (each CTA runs
+// exactly one slice, so the lo pair is idle by then).
+struct BLayout {
+  int blk, x, slot, lo0, xlo, stg, stgb, wst, dump, bars, total;
+  __host__ __device__ BLayout(int c_in, int c_out, int gw, int xr) {
+    const int dyb = round1k(c_out * 128), xb = round1k(xr * 128);
+    blk = dyb + xb;                       // one block: dy (or dy_lo) | x (or x_lo)
+    x = dyb;
+    slot = 2 * blk;
+    lo0 = kSlots * slot;
+    xlo = dyb;
+    stgb = round1k(c_in * 128);           // one block's dx [c_in rows][32 px] (SWIZZLE_128B)
+    stg = lo0 + 2 * blk;                  // one staging pair
+    int end = stg + 2 * stgb;
+    const int wneed = c_out * gw * 4 + c_out * 8;  // W + (oc*gw - start, start) table
+    if (wneed <= 2 * blk) {
+      wst = lo0;
+    } else {
+      wst = end;
+      end += round1k(wneed);
+    }
+    const int dneed = 128 * (xr + 4) * 4;  // dW row dump [128][xr + 4]
+    if (dneed <= 2 * blk) {
+      dump = lo0;
+    } else {
+      dump = end;
+      end += round1k(dneed);
+    }
+    bars = end;
+    total = bars + 64 * 8;
+  }
+};
+
+// Row `L` (this thread's TMEM lane) of the resident stacked W^T operand:
+// lane ic (< 64) holds W_hi, lane 64 + ic holds W_lo, class-major filter
+// columns, zero outside each filter's window; built from W and the
+// (oc*gw - start, start) table staged in shared memory.
+__device__ __forceinline__ void build_wt(const BArgs& a, uint32_t tmem, uint32_t lane_base, int L,
+                                         const float* wst) {
+  const float* ws = wst;
+  const int2* kt = reinterpret_cast<const int2*>(wst + a.c_out * a.gw);
+  const int ic = L & 63;
+  const bool lo_lane = L >= 64;
+  const bool live = ic < a.c_in;
+  for (int c0 = 0; c0 < a.c_out; c0 += 32) {
+    float v[32];
+    if (a.cls % 32 == 0) {
+      // the chunk is one window class: one start, filters D apart in W
+      const int2 e = kt[c0];
+      const int wrap = ic < e.y ? a.c_in : 0;
+      const bool in = live && static_cast<unsigned>(ic - e.y + wrap) < static_cast<unsigned>(a.gw);
+      const float* p = ws + (in ? e.x + ic + wrap : 0);
+      const int stride = a.n_class * a.gw;
+#pragma unroll
+      for (int t = 0; t < 32; ++t) v[t] = in ? p[t * stride] : 0.f;
+    } else {
+      int idx[32];
+#pragma unroll
+      for (int t = 0; t < 32; ++t) {
+        const int2 e = kt[min(c0 + t, a.c_out - 1)];
+        const int wrap = ic < e.y ? a.c_in : 0;
+        const bool in = live && static_cast<unsigned>(ic - e.y + wrap) < static_cast<unsigned>(a.gw) &&
+                        c0 + t < a.c_out;
+        idx[t] = in ? e.x + ic + wrap : -1;
+      }
+#pragma unroll
+      for (int t = 0; t < 32; ++t) {
+        const float w = ws[max(idx[t], 0)];
+        v[t] = idx[t] >= 0 ? w : 0.f;
+      }
+    }
+    uint32_t r[32];
+#pragma unroll
+    for (int t = 0; t < 32; ++t) {
+      const float h = tf32_hi(v[t]);
+      r[t] = __float_as_uint(lo_lane ? v[t] - h : h);
+    }
+    tmem_st32(tmem + kWt + c0 + lane_base, r);
+  }
+  tmem_st_wait();
+  tc_fence_before();
+}
+
+__device__ __forceinline__ float4 f4(const uint32_t* v) {
+  return make_float4(__uint_as_float(v[0]), __uint_as_float(v[1]), __uint_as_float(v[2]), __uint_as_float(v[3]));
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+    tc_bwd_kernel(const __grid_constant__ CUtensorMap tdy, const __grid_constant__ CUtensorMap tx,
+                  const __grid_constant__ CUtensorMap tdx, const __grid_constant__ BArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const BLayout L(a.c_in, a.c_out, a.gw, a.xr);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bars);
+  uint64_t* full = bars;                       // [slot] TMA landed
+  uint64_t* sfree = full + kSlots;             // [slot] MMA commit: slot consumed
+  uint64_t* xlo = sfree + kSlots;              // 2 x-lo warps: x_lo of the pair written
+  uint64_t* conv = xlo + 1;                    // 4 dy converter warps: dy_lo + dW A written
+  uint64_t* lofree = conv + 1;                 // MMA commit: lo pair consumed
+  uint64_t* tfree = lofree + 1;                // MMA commit: dW A (TMEM) consumed
+  uint64_t* dxfull = tfree + 1;                // [2] MMA commit
+  uint64_t* dxempty = dxfull + 2;              // [2] 4 epilogue warps
+  uint64_t* accfull = dxempty + 2;             // MMA commit: the slice's dW done
+  uint64_t* wt_ready = accfull + 1;            // 4 epilogue warps: W^T in TMEM
+  uint64_t* w_bar = wt_ready + 1;              // W bulk copy landed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(w_bar + 1);
+
+  const uint32_t warp = warp_id();
+  const int lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    TRACE3(48);
+#if defined(SCC_TRACE)
+    if (blockIdx.x < 256) g_cta3[2 * blockIdx.x] = globaltimer();
+#endif
+    for (int s = 0; s < kSlots; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&sfree[s], 1);
+    }
+    mbar_init(xlo, 2);
+    mbar_init(conv, 4);
+    mbar_init(lofree, 1);
+    mbar_init(tfree, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&dxfull[i], 1);
+      mbar_init(&dxempty[i], 4);
+    }
+    mbar_init(accfull, 1);
+    mbar_init(wt_ready, 4);
+    mbar_init(w_bar, 1);
+    fence_mbar_init();
+  }
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&tdy);
+    if (a.do_dw) prefetch_tmap(&tx);
+    if (a.do_dx) prefetch_tmap(&tdx);
+  }
+  if (warp == 1) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  if (threadIdx.x == 0) TRACE3(49);
+  // the next kernel may start its prologue; it waits for this grid before
+  // touching memory
+  cudaTriggerProgrammaticLaunchCompletion();
+
+  // this CTA's slice (exactly one, see the launch) and its block pairs
+  const int sl = blockIdx.x;
+  const int u0 = slice_u(a, sl), u1 = slice_u(a, sl + 1);
+  const int npairs = (u1 - u0 + 1) >> 1;
+
+  if (warp == 0) {
+    // ---------------- producer ----------------
+    cudaGridDependencySynchronize();
+    if (elect_one()) {
+      if (a.do_dx && a.w_bulk) {
+        // W first: the dx GEMM's operand is built from it
+        const uint32_t wb = 4u * a.c_out * a.gw;
+        mbar_expect_tx(w_bar, wb);
+        bulk_load(smem + L.wst, a.weight, wb, w_bar);
+      }
+      int s = 0;
+      uint32_t ph = 0;
+      const uint32_t bytes = a.c_out * 128 + (a.do_dw ? a.nx * 128 : 0);
+      for (int p = 0; p < npairs; ++p) {
+        const int ub = u0 + 2 * p, nb = min(2, u1 - ub);
+        mbar_wait(&sfree[s], ph ^ 1u);
+        TRACE3K(0, p);
+        mbar_expect_tx(&full[s], bytes * nb);
+        for (int k = 0; k < nb; ++k) {
+          const int u = ub + k;
+          const int n = u / a.nbps, px0 = (u - n * a.nbps) * 32;
+          uint8_t* st = smem + s * L.slot + k * L.blk;
+          tma_load_4d(st, &tdy, &full[s], px0, 0, 0, n);
+          if (a.do_dw) {
+            if (a.xbox) {
+              tma_load_3d(st + L.x, &tx, &full[s], px0, a.start8, n);
+            } else {
+              for (int r = 0; r < a.nx; r += a.rbb) {
+                int ic = a.start8 + r;
+                ic -= ic >= a.c_in ? a.c_in : 0;
+                tma_load_3d(st + L.x + r * 128, &tx, &full[s], px0, ic, n);
+              }
+            }
+          }
+        }
+        advance(s, ph, kSlots);
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer ----------------
+    const uint32_t idw = idesc_tf32(128, static_cast<uint32_t>(a.xr), 0, 0);
+    const uint32_t idx = idesc_tf32(128, 64, 0, 1);  // B = dy of the pair, MN-major (pixels contiguous)
+    const int ksteps = a.c_out >> 3;
+    const uint32_t lbo = static_cast<uint32_t>(L.blk);  // the pair's second 32-px atom
+    int s = 0, b = 0;
+    uint32_t ph = 0, dph = 0, cph = 0;
+    if (a.do_dx) mbar_wait(wt_ready, 0);
+    for (int p = 0; p < npairs; ++p) {
+      const int nb = min(2, u1 - (u0 + 2 * p));
+      mbar_wait(conv, cph);
+      if (a.do_dw) mbar_wait(xlo, cph);
+      cph ^= 1u;
+      if (a.do_dx) mbar_wait(&dxempty[b], dph ^ 1u);
+      tc_fence_after();
+      const uint32_t st = smem_u32(smem + s * L.slot);
+      const uint32_t lb = smem_u32(smem + L.lo0);
+      const uint32_t d = tmem + kDxAcc + 64 * b;
+      if (elect_one()) {
+        // 1. everything that reads the lo pair
+        if (a.do_dw) {
+          for (int k = 0; k < nb; ++k) {
+            const uint32_t ah = tmem + kDwA + 64 * k;
+            for (int q = 0; q < 4; ++q)
+              mma_tf32_ts(tmem + kDwAcc, ah + 8 * q, desc_sw128(lb + k * L.blk + L.xlo + q * 32, 16, 1024), idw,
+                          (p == 0 && k == 0 && q == 0) ? 0u : 1u);
+          }
+        }
+        if (a.do_dx) {
+          for (int q = 0; q < ksteps; ++q)
+            mma_tf32_ts(d, tmem + kWt + 8 * q, desc_mn32(lb + q * 1024, lbo, 512), idx, q == 0 ? 0u : 1u);
+        }
+        mma_commit(lofree);
+        // 2. the rest of dW (frees the TMEM A pair), then dx * dy
+        if (a.do_dw) {
+          for (int k = 0; k < nb; ++k) {
+            const uint32_t ah = tmem + kDwA + 64 * k, al = ah + 32;
+            for (int q = 0; q < 4; ++q) {
+              const uint64_t dbx = desc_sw128(st + k * L.blk + L.x + q * 32, 16, 1024);
+              mma_tf32_ts(tmem + kDwAcc, ah + 8 * q, dbx, idw, 1);
+              mma_tf32_ts(tmem + kDwAcc, al + 8 * q, dbx, idw, 1);
+            }
+          }
+          mma_commit(tfree);
+          TRACE3K(16, p);
+        }
+        if (a.do_dx) {
+          for (int q = 0; q < ksteps; ++q)
+            mma_tf32_ts(d, tmem + kWt + 8 * q, desc_mn32(st + q * 1024, lbo, 512), idx, 1);
+          mma_commit(&dxfull[b]);
+          TRACE3K(24, p);
+        }
+        mma_commit(&sfree[s]);
+      }
+      __syncwarp();
+      if (a.do_dx && ++b == 2) {
+        b = 0;
+        dph ^= 1u;
+      }
+      advance(s, ph, kSlots);
+    }
+    // (an empty slice accumulates nothing; the epilogue writes zeros)
+    if (a.do_dw && elect_one()) mma_commit(accfull);
+    __syncwarp();
+  } else if (warp < 4) {
+    // ---------------- x lo converters ----------------
+    if (a.do_dw) {
+      const int ct = threadIdx.x - 64;  // 0..63
+      // constant rows [nx, xr): row nx = 1 (x) / 0 (x_lo), the rest 0 (the lo
+      // pair once the W staging it aliases is consumed)
+      for (int s = 0; s < 2 * kSlots + 2; ++s) {
+        if (s == 2 * kSlots && a.do_dx) mbar_wait(wt_ready, 0);
+        float* xs = reinterpret_cast<float*>(s < 2 * kSlots ? smem + s * L.blk + L.x
+                                                            : smem + L.lo0 + (s - 2 * kSlots) * L.blk + L.xlo);
+        const float one = s < 2 * kSlots ? 1.f : 0.f;
+        for (int i = ct; i < (a.xr - a.nx) * 32; i += 64) {
+          const int r = a.nx + (i >> 5), c = i & 31;
+          const int off = r * 32 + ((((c >> 2) ^ (r & 7)) << 2) | (c & 3));
+          xs[off] = r == a.nx ? one : 0.f;
+        }
+      }
+      fence_proxy_async_smem();
+      int s = 0;
+      uint32_t ph = 0, lph = 0;
+      const int words = a.nx * 8;  // float4 per x block
+      for (int p = 0; p < npairs; ++p) {
+        const int nb = min(2, u1 - (u0 + 2 * p));
+        mbar_wait(&full[s], ph);
+        mbar_wait(lofree, lph ^ 1u);
+        lph ^= 1u;
+        for (int k = 0; k < nb; ++k) {
+          const float4* src = reinterpret_cast<const float4*>(smem + s * L.slot + k * L.blk + L.x);
+          const uint32_t dst = smem_u32(smem + L.lo0 + k * L.blk + L.xlo);
+          for (int i0 = ct; i0 < words; i0 += 64 * 4) {
+            float4 v[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) v[q] = src[min(i0 + 64 * q, words - 1)];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              if (i0 + 64 * q < words) {
+                float4 o;
+                o.x = v[q].x - tf32_hi(v[q].x);
+                o.y = v[q].y - tf32_hi(v[q].y);
+                o.z = v[q].z - tf32_hi(v[q].z);
+                o.w = v[q].w - tf32_hi(v[q].w);
+                sts_v4(dst + (i0 + 64 * q) * 16, o);
+              }
+            }
+          }
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(xlo);
+        advance(s, ph, kSlots);
+      }
+    }
+  } else if (warp < 8) {
+    // ---------------- dy row converters ----------------
+    // Row `row` of a block: 128 B, 32 B chunk c at physical chunk c ^ (row % 4)
+    // (SWIZZLE_128B_BASE32B).  Writes the lo row to the lo pair (dx B lo) and,
+    // for dW, the hi / lo row to TMEM lane `row`.
+    const int q = warp & 3;
+    const int row = q * 32 + lane;
+    const bool live = row < a.c_out;
+    const bool warp_live = q * 32 < a.c_out;  // tcgen05.st is warp-collective
+    const uint32_t lane_base = static_cast<uint32_t>(q * 32) << 16;
+    int s = 0;
+    uint32_t ph = 0, tph = 0, lph = 0;
+    for (int p = 0; p < npairs; ++p) {
+      const int nb = min(2, u1 - (u0 + 2 * p));
+      mbar_wait(&full[s], ph);
+      for (int k = 0; k < nb; ++k) {
+        uint32_t hi[32], lo[32];
+#pragma unroll
+        for (int c = 0; c < 32; ++c) hi[c] = lo[c] = 0u;
+        if (live) {
+          const float4* rp = reinterpret_cast<const float4*>(smem + s * L.slot + k * L.blk + row * 128);
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            const float4 v = rp[((((c >> 1) ^ row) & 3) << 1) | (c & 1)];
+            const float e[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+              const float h = tf32_hi(e[t]);
+              hi[4 * c + t] = __float_as_uint(h);
+              lo[4 * c + t] = __float_as_uint(e[t] - h);
+            }
+          }
+        }
+        if (k == 0) {
+          mbar_wait(lofree, lph ^ 1u);
+          lph ^= 1u;
+          if (p == 0 && a.do_dx) mbar_wait(wt_ready, 0);  // the W staging aliases the lo pair
+        }
+        if (live) {
+          const uint32_t lo_row = smem_u32(smem + L.lo0 + k * L.blk + row * 128);
+#pragma unroll
+          for (int c = 0; c < 8; ++c)
+            sts_v4(lo_row + (((((c >> 1) ^ row) & 3) << 1) | (c & 1)) * 16, f4(lo + 4 * c));
+        }
+        if (a.do_dw) {
+          if (k == 0) {
+            mbar_wait(tfree, tph ^ 1u);
+            tph ^= 1u;
+            tc_fence_after();
+          }
+          if (warp_live) {
+            const uint32_t col = tmem + kDwA + 64 * k + lane_base;
+            tmem_st32(col, hi);
+            tmem_st32(col + 32, lo);
+          }
+        }
+      }
+      fence_proxy_async_smem();
+      if (a.do_dw) {
+        tmem_st_wait();
+        tc_fence_before();
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(conv);
+      if (row == 0) TRACE3K(8, p);
+      advance(s, ph, kSlots);
+    }
+  } else {
+    // ---------------- W^T build, dx epilogue, dW slice epilogue ----------------
+    const int q = warp & 3;
+    const int et = threadIdx.x - 256;  // 0..127
+    const int i = q * 32 + lane;       // TMEM lane: input channel (+64: lo part) / filter row (dW)
+    const uint32_t lane_base = static_cast<uint32_t>(q * 32) << 16;
+    float* wst = reinterpret_cast<float*>(smem + L.wst);
+    cudaGridDependencySynchronize();
+    if (et == 0) TRACE3(53);
+    if (a.do_dx) {
+      // W (bulk copy by the producer, or loads here, all in flight at once)
+      // and per class-major column k the (oc*gw - start, start) pair; then
+      // this lane's row of W^T -> TMEM
+      int2* kt = reinterpret_cast<int2*>(wst + a.c_out * a.gw);
+      const int nw = a.c_out * a.gw;
+      if (et < a.c_out) {
+        const int oc = row_oc(a, et);
+        const int st = __ldg(a.starts + oc);
+        kt[et] = make_int2(oc * a.gw - st, st);
+      }
+      if (!a.w_bulk) {
+        for (int k0 = 0; k0 < nw; k0 += 128 * 32) {
+          float v[32];
+#pragma unroll
+          for (int t = 0; t < 32; ++t) {
+            const int k = k0 + t * 128 + et;
+            v[t] = k < nw ? __ldg(a.weight + k) : 0.f;
+          }
+#pragma unroll
+          for (int t = 0; t < 32; ++t) {
+            const int k = k0 + t * 128 + et;
+            if (k < nw) wst[k] = v[t];
+          }
+        }
+      }
+      named_bar_sync(1, 128);
+      if (a.w_bulk) mbar_wait(w_bar, 0);
+      if (et == 0) TRACE3(55);
+      build_wt(a, tmem, lane_base, i, wst);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(wt_ready);
+      if (et == 0) TRACE3(50);
+    }
+    // rows 0-63 of the dx accumulator hold W_hi * dy, rows 64-127 W_lo * dy
+    const int dx_row = i & 63;
+    const bool bottom = i >= 64;
+    const bool dx_live = dx_row < a.c_in;
+    const bool dx_warp = (q & 1) * 32 < a.c_in;
+    const bool leader = et == 0;
+    int b = 0;
+    uint32_t dph = 0;
+    if (a.do_dx) {
+      for (int p = 0; p < npairs; ++p) {
+        const int ub = u0 + 2 * p, nb = min(2, u1 - ub);
+        mbar_wait(&dxfull[b], dph);
+        if (et == 0) TRACE3K(32, p);
+        tc_fence_after();
+        uint32_t v0[32], v1[32];
+        if (dx_warp) {
+          tmem_ld32_nowait(tmem + kDxAcc + 64 * b + lane_base, v0);
+          tmem_ld32_nowait(tmem + kDxAcc + 64 * b + 32 + lane_base, v1);
+          tmem_ld_wait();
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&dxempty[b]);
+        // the staging pair was last read by the stores of the previous pair
+        if (leader) bulk_wait_read<0>();
+        named_bar_sync(1, 128);
+        // rows 64-127 (the W_lo part) -> staging, then rows 0-63 add theirs in place
+        const uint32_t r0 = smem_u32(smem + L.stg + dx_row * 128), r1 = r0 + L.stgb;
+        if (bottom && dx_warp && dx_live) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            sts_v4(r0 + ((j ^ (dx_row & 7)) << 4), f4(v0 + 4 * j));
+            sts_v4(r1 + ((j ^ (dx_row & 7)) << 4), f4(v1 + 4 * j));
+          }
+        }
+        named_bar_sync(1, 128);
+        if (!bottom && dx_warp && dx_live) {
+          const float4* s0 = reinterpret_cast<const float4*>(smem + L.stg + dx_row * 128);
+          const float4* s1 = reinterpret_cast<const float4*>(smem + L.stg + L.stgb + dx_row * 128);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const int pj = j ^ (dx_row & 7);
+            const float4 o0 = s0[pj], o1 = s1[pj];
+            const float4 a0 = f4(v0 + 4 * j), a1 = f4(v1 + 4 * j);
+            sts_v4(r0 + (pj << 4), make_float4(a0.x + o0.x, a0.y + o0.y, a0.z + o0.z, a0.w + o0.w));
+            sts_v4(r1 + (pj << 4), make_float4(a1.x + o1.x, a1.y + o1.y, a1.z + o1.z, a1.w + o1.w));
+          }
+        }
+        fence_proxy_async_smem();
+        named_bar_sync(1, 128);
+        if (leader) {
+          for (int k = 0; k < nb; ++k) {
+            const int u = ub + k;
+            const int n = u / a.nbps, px0 = (u - n * a.nbps) * 32;
+            tma_store_3d(&tdx, smem + L.stg + k * L.stgb, px0, 0, n);
+          }
+          bulk_commit();
+          TRACE3K(40, p);
+        }
+        if (++b == 2) {
+          b = 0;
+          dph ^= 1u;
+        }
+      }
+    }
+    if (a.do_dw) {
+      float* dump = reinterpret_cast<float*>(smem + L.dump);
+      const int rstride = a.xr + 4;
+      float* prow = dump + i * rstride;
+      const uint32_t prow_a = smem_u32(prow);
+      mbar_wait(accfull, 0);
+      if (et == 0) TRACE3(51);
+      tc_fence_after();
+      for (int c0 = 0; c0 < a.xr; c0 += 32) {
+        uint32_t v[32];
+        tmem_ld32_nowait(tmem + kDwAcc + c0 + lane_base, v);
+        tmem_ld_wait();
+#pragma unroll
+        for (int t = 0; t < 32; t += 4)
+          if (c0 + t < a.xr) sts_v4(prow_a + (c0 + t) * 4, f4(v + t));
+      }
+      // window-relative values of filter row i -> the slice's partial
+      const bool live = i < a.c_out && u0 < u1;
+      int j0 = 0;
+      if (live) {
+        j0 = __ldg(a.starts + row_oc(a, i)) - a.start8;
+        j0 += j0 < 0 ? a.c_in : 0;
+      }
+      float* dst = a.part + static_cast<int64_t>(sl) * a.elems;
+      float wv[kMaxGw];
+#pragma unroll
+      for (int t = 0; t < kMaxGw; ++t) {
+        int j = j0 + t;
+        j -= j >= a.c_in ? a.c_in : 0;
+        wv[t] = (live && t < a.gw) ? prow[j] : 0.f;
+      }
+      if (i < a.c_out) {
+        if ((a.gw & 3) == 0) {
+#pragma unroll
+          for (int t = 0; t < kMaxGw; t += 4)
+            if (t < a.gw)
+              *reinterpret_cast<float4*>(dst + i * a.gw + t) = make_float4(wv[t], wv[t + 1], wv[t + 2], wv[t + 3]);
+        } else {
+#pragma unroll
+          for (int t = 0; t < kMaxGw; ++t)
+            if (t < a.gw) dst[i * a.gw + t] = wv[t];
+        }
+        dst[a.c_out * a.gw + i] = live ? prow[a.nx] : 0.f;
+      }
+    }
+    if (leader) {
+      bulk_wait<0>();
+      TRACE3(52);
+#if defined(SCC_TRACE)
+      if (blockIdx.x < 256) g_cta3[2 * blockIdx.x + 1] = globaltimer();
+#endif
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc<512>(tmem);
+}
+
+// Fixed-order reduction of the per-slice partials, PDL-chained behind the main
+// kernel (its CTAs launch while the main kernel runs and wait for it).  Block
+// = 32 consecutive partial elements; warp w sums slices w, w+8, ... in order
+// (each load a coalesced 128 B row piece), then warp 0 adds the 8 warp sums
+// in order.  Bitwise reproducible.
+__global__ void __launch_bounds__(256) tc_bwd_reduce(const __grid_constant__ BArgs a) {
+  __shared__ float red[8][33];
+  cudaGridDependencySynchronize();
+  // the next kernel may start its prologue (it waits for this grid)
+  cudaTriggerProgrammaticLaunchCompletion();
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  const int e = blockIdx.x * 32 + l;
+  float acc = 0.f;
+  if (e < a.elems) {
+    constexpr int kPer = (kSlices + 7) / 8;
+    float v[kPer];
+#pragma unroll
+    for (int m = 0; m < kPer; ++m) {
+      const int k = w + 8 * m;
+      v[m] = k < a.slices ? __ldcg(a.part + static_cast<int64_t>(k) * a.elems + e) : 0.f;
+    }
+#pragma unroll
+    for (int m = 0; m < kPer; ++m) acc += v[m];
+  }
+  red[w][l] = acc;
+  __syncthreads();
+  if (w == 0 && e < a.elems) {
+    float t = red[0][l];
+#pragma unroll
+    for (int q = 1; q < 8; ++q) t += red[q][l];
+    const int nw = a.c_out * a.gw;
+    if (e < nw) {
+      const int i = e / a.gw;
+      a.dweight[static_cast<int64_t>(row_oc(a, i)) * a.gw + (e - i * a.gw)] = t;
+    } else if (a.dbias != nullptr) {
+      a.dbias[row_oc(a, e - nw)] = t;
+    }
+  }
+}
+
+struct Geo {
+  int nx = 0, xr = 0, start8 = 0;
+  bool fits = false;
+};
+
+Geo geometry(const TcWeightPlan& tw, int32_t c_in, int32_t c_out, int32_t gw) {
+  Geo g;
+  g.start8 = tw.rt_info[0];
+  g.nx = tw.rt_info[1];
+  g.xr = (g.nx + 1 + 15) / 16 * 16;
+  g.fits = BLayout(c_in, c_out, gw, g.xr).total <= kSmemLimit;
+  return g;
+}
+
+}  // namespace
+
+int tc_bwd_trace(unsigned long long* out, int n) {
+#if defined(SCC_TRACE)
+  if (n > 64 + 512) n = 64 + 512;
+  const int m = n < 64 ? n : 64;
+  if (cudaMemcpyFromSymbol(out, g_trace3, m * sizeof(unsigned long long)) != cudaSuccess) return -1;
+  if (n > 64 && cudaMemcpyFromSymbol(out + 64, g_cta3, (n - 64) * sizeof(unsigned long long)) != cudaSuccess)
+    return -1;
+  return n;
+#else
+  for (int i = 0; i < n; ++i) out[i] = 0;
+  return n;
+#endif
+}
+
+bool tc_bwd_supported(const TcWeightPlan& tw, int64_t plane, int32_t c_in, int32_t c_out, int32_t gw) {
+  if (!tw.ok || plane % 4 != 0 || tw.n_rt != 1 || tw.rt_info.size() < 2) return false;
+  if (c_out > 128 || c_out % 8 != 0 || c_out != tw.n_class * tw.cls || tw.cls > 256 || tw.n_class > 256)
+    return false;
+  if (c_in > 64 || gw > kMaxGw) return false;
+  const Geo g = geometry(tw, c_in, c_out, gw);
+  if (g.xr > 128 || g.nx % tw.rbb != 0) return false;
+  return g.fits;
+}
+
+size_t tc_bwd_workspace_bytes(int32_t c_out, int32_t gw, int64_t n, int64_t plane) {
+  const int64_t units = n * ((plane + 31) / 32);
+  const int64_t slices = std::min<int64_t>(units, kSlices);
+  return static_cast<size_t>(slices) * (static_cast<size_t>(c_out) * gw + c_out) * sizeof(float);
+}
+
+cudaError_t launch_tc_bwd(const TcWeightPlan& tw, const TcBwdCall& call, cudaStream_t s) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  static bool attr_set[64] = {false};
+  static int nsm_cache[64] = {0};
+  int nsm = 148;
+  if (dev >= 0 && dev < 64 && nsm_cache[dev] > 0) {
+    nsm = nsm_cache[dev];
+  } else {
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    if (dev >= 0 && dev < 64) nsm_cache[dev] = nsm;
+  }
+  if (!call.do_dx && !call.do_dw) return cudaSuccess;
+  const Geo g = geometry(tw, call.c_in, call.c_out, call.gw);
+  BArgs a{};
+  a.c_in = call.c_in;
+  a.c_out = call.c_out;
+  a.gw = call.gw;
+  a.cls = tw.cls;
+  a.n_class = tw.n_class;
+  a.start8 = g.start8;
+  a.nx = g.nx;
+  a.xr = g.xr;
+  a.rbb = tw.rbb;
+  a.xbox = (g.start8 + g.nx <= call.c_in && g.nx <= 256) ? 1 : 0;
+  a.nbps = static_cast<int32_t>((call.plane + 31) / 32);
+  const int64_t units = call.n * a.nbps;
+  if (units > (1ll << 30) || units == 0) return units == 0 ? cudaSuccess : cudaErrorInvalidValue;
+  a.units = static_cast<int32_t>(units);
+  a.elems = call.c_out * call.gw + call.c_out;
+  a.slices = static_cast<int32_t>(std::min<int64_t>(units, kSlices));
+  a.do_dx = call.do_dx ? 1 : 0;
+  a.do_dw = call.do_dw ? 1 : 0;
+  a.w_bulk = (reinterpret_cast<uintptr_t>(call.weight) % 16 == 0 && (call.c_out * call.gw) % 4 == 0) ? 1 : 0;
+
+  if (a.do_dw && tc_bwd_workspace_bytes(call.c_out, call.gw, call.n, call.plane) > call.workspace_bytes)
+    return cudaErrorInvalidValue;
+  a.part = static_cast<float*>(call.workspace);
+  a.dweight = call.dweight;
+  a.dbias = call.dbias;
+  a.weight = call.weight;
+  a.starts = call.starts;
+  // one slice per CTA (the dW dump aliases the lo pair, see BLayout)
+  const int grid = a.slices;
+  (void)nsm;
+
+  const uint64_t P = static_cast<uint64_t>(call.plane);
+  CUtensorMap tdy{}, tx{}, tdx{};
+  {
+    // dy {P, cls, D, N}: row (d, j) = filter d + D*j; one box per block
+    const uint64_t dims[4] = {P, static_cast<uint64_t>(tw.cls), static_cast<uint64_t>(tw.n_class),
+                              static_cast<uint64_t>(call.n)};
+    const uint64_t strides[3] = {P * 4 * tw.n_class, P * 4, P * 4 * call.c_out};
+    const uint32_t box[4] = {32, static_cast<uint32_t>(tw.cls), static_cast<uint32_t>(tw.n_class), 1};
+    if (!encode_f32(&tdy, call.dy, 4, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B))
+      return cudaErrorInvalidValue;
+  }
+  const uint64_t dimx[3] = {P, static_cast<uint64_t>(call.c_in), static_cast<uint64_t>(call.n)};
+  const uint64_t strx[2] = {P * 4, P * 4 * call.c_in};
+  if (a.do_dw) {
+    const uint32_t box[3] = {32, static_cast<uint32_t>(a.xbox ? g.nx : tw.rbb), 1};
+    if (!encode_f32(&tx, call.x, 3, dimx, strx, box, CU_TENSOR_MAP_SWIZZLE_128B)) return cudaErrorInvalidValue;
+  }
+  if (a.do_dx) {
+    const uint32_t box[3] = {32, static_cast<uint32_t>(call.c_in), 1};
+    if (!encode_f32(&tdx, call.dx, 3, dimx, strx, box, CU_TENSOR_MAP_SWIZZLE_128B)) return cudaErrorInvalidValue;
+  }
+  if (dev < 0 || dev >= 64 || !attr_set[dev]) {
+    cudaError_t e = cudaFuncSetAttribute(tc_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit);
+    if (e != cudaSuccess) return e;
+    if (dev >= 0 && dev < 64) attr_set[dev] = true;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>(grid));
+  cfg.blockDim = dim3(kThreads);
+  // (no slack: the extern smem array is 1024-aligned; staying under 227 KB - 2 KB lets
+  // the small reduce CTAs be resident next to these and wait on the dependency)
+  cfg.dynamicSmemBytes = BLayout(a.c_in, a.c_out, a.gw, a.xr).total;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, tc_bwd_kernel, tdy, tx, tdx, a);
+  if (e != cudaSuccess) return e;
+  int launches = 1;
+  if (a.do_dw) {
+    cudaLaunchConfig_t rc{};
+    rc.gridDim = dim3(static_cast<unsigned>((a.elems + 31) / 32));
+    rc.blockDim = dim3(256);
+    rc.stream = s;
+    rc.attrs = attr;
+    rc.numAttrs = 1;
+    e = cudaLaunchKernelEx(&rc, tc_bwd_reduce, a);
+    if (e != cudaSuccess) return e;
+    ++launches;
+  }
+  note_launches(launches);
+  return cudaSuccess;
+}
+
+}  // namespace scc
