@@ -488,7 +488,8 @@ struct Staged {
   float *x, *w, *b, *dy, *y, *dx, *dw, *db;
   void* ws;
   size_t ws_bytes;
-  cudaStream_t s;
+  cudaStream_t s, s_in, s_out;
+  HostStaging* st;
 };
 
 Staged stage(Plan& p, int64_t n, int64_t h, int64_t wd) {
@@ -512,6 +513,20 @@ Staged stage(Plan& p, int64_t n, int64_t h, int64_t wd) {
     cudaStream_t s;
     cuda_check(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "cudaStreamCreate");
     st->stream = s;
+    cuda_check(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "cudaStreamCreate");
+    st->stream_in = s;
+    cuda_check(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "cudaStreamCreate");
+    st->stream_out = s;
+    auto mk = [](void** e) {
+      cudaEvent_t ev;
+      cuda_check(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "cudaEventCreate");
+      *e = ev;
+    };
+    for (int i = 0; i < kMaxHostChunks; ++i) {
+      mk(&st->ev_in[i]);
+      mk(&st->ev_done[i]);
+    }
+    mk(&st->ev_out);
   }
   if (st->bytes < total) {
     if (st->buf) cuda_check(cudaFree(st->buf), "cudaFree(staging)");
@@ -537,6 +552,9 @@ Staged stage(Plan& p, int64_t n, int64_t h, int64_t wd) {
   g.ws = take(wsb);
   g.ws_bytes = wsb;
   g.s = static_cast<cudaStream_t>(st->stream);
+  g.s_in = static_cast<cudaStream_t>(st->stream_in);
+  g.s_out = static_cast<cudaStream_t>(st->stream_out);
+  g.st = st;
   return g;
 }
 
@@ -545,6 +563,67 @@ void h2d(void* d, const void* h, size_t bytes, cudaStream_t s) {
 }
 void d2h(void* h, const void* d, size_t bytes, cudaStream_t s) {
   cuda_check(cudaMemcpyAsync(h, d, bytes, cudaMemcpyDeviceToHost, s), "cudaMemcpyAsync D2H");
+}
+
+// Host-buffer operator, pipelined over batch chunks so PCIe H2D, the kernels
+// and PCIe D2H overlap (the link is full duplex):
+//   copy-in stream : w, b, then per chunk x_c / dy_c          -> ev_in[c]
+//   compute stream : per chunk forward and backward-data      -> ev_done[c]
+//                    then backward-weight over the whole batch (it reduces
+//                    over n, so its bits equal the device entry point's)
+//   copy-out stream: per chunk y_c / dx_c; dW / db last
+// Forward and backward-data are per sample (kernel.cpp:45-60, :107-137) and
+// the kernels' per-element arithmetic does not depend on n, so chunked
+// results are bitwise equal to one full-batch call.
+struct HostIo {
+  const float *x = nullptr, *w = nullptr, *b = nullptr, *dy = nullptr;
+  float *y = nullptr, *dx = nullptr, *dw = nullptr, *db = nullptr;
+};
+
+int host_chunks(int64_t n, size_t bytes_per_sample) {
+  // >= ~1 MB of traffic per chunk keeps each copy near full PCIe speed
+  const int64_t by_size = static_cast<int64_t>(bytes_per_sample * n / (1u << 20));
+  int64_t k = std::min<int64_t>({n, kMaxHostChunks / 4, std::max<int64_t>(by_size, 1)});
+  if (const char* e = getenv("SCC_HOST_CHUNKS")) k = std::max<int64_t>(1, std::min<int64_t>({atoi(e), n, kMaxHostChunks}));
+  return static_cast<int>(k);
+}
+
+void run_host(Plan& p, int64_t n, int64_t h, int64_t wd, const HostIo& io) {
+  const scc_config_t& c = p.cfg;
+  const int64_t P = h * wd;
+  Staged g = stage(p, n, h, wd);
+  const bool fwd = io.y != nullptr, bwd = io.dx != nullptr;
+  const size_t sx = static_cast<size_t>(c.c_in * P) * 4, sy = static_cast<size_t>(c.c_out * P) * 4;
+  const size_t nw = static_cast<size_t>(c.c_out * c.group_width) * 4, nb = static_cast<size_t>(c.c_out) * 4;
+  const int k = host_chunks(n, (fwd ? sx + sy : 0) + (bwd ? sx + sy : 0) + (bwd && !fwd ? sx : 0));
+  h2d(g.w, io.w, nw, g.s_in);
+  if (fwd && io.b) h2d(g.b, io.b, nb, g.s_in);
+  int64_t n0 = 0;
+  for (int i = 0; i < k; ++i) {
+    const int64_t m = n / k + (i < n % k ? 1 : 0);  // parallel_chunks split (parallel.cpp:36-66)
+    const size_t ox = static_cast<size_t>(n0) * sx / 4, oy = static_cast<size_t>(n0) * sy / 4;
+    cudaEvent_t ein = static_cast<cudaEvent_t>(g.st->ev_in[i]);
+    cudaEvent_t edone = static_cast<cudaEvent_t>(g.st->ev_done[i]);
+    h2d(g.x + ox, io.x + ox, m * sx, g.s_in);
+    if (bwd) h2d(g.dy + oy, io.dy + oy, m * sy, g.s_in);
+    cuda_check(cudaEventRecord(ein, g.s_in), "cudaEventRecord");
+    cuda_check(cudaStreamWaitEvent(g.s, ein, 0), "cudaStreamWaitEvent");
+    if (fwd) do_forward(p, m, h, wd, g.x + ox, g.w, io.b ? g.b : nullptr, g.y + oy, g.s);
+    if (bwd) do_backward_data(p, m, h, wd, g.dy + oy, g.w, g.dx + ox, g.s);
+    cuda_check(cudaEventRecord(edone, g.s), "cudaEventRecord");
+    cuda_check(cudaStreamWaitEvent(g.s_out, edone, 0), "cudaStreamWaitEvent");
+    if (fwd) d2h(io.y + oy, g.y + oy, m * sy, g.s_out);
+    if (bwd) d2h(io.dx + ox, g.dx + ox, m * sx, g.s_out);
+    n0 += m;
+  }
+  if (bwd) {
+    do_backward_weight(p, n, h, wd, g.dy, g.x, g.dw, io.db ? g.db : nullptr, g.ws, g.ws_bytes, g.s);
+    d2h(io.dw, g.dw, nw, g.s);
+    if (io.db) d2h(io.db, g.db, nb, g.s);
+  }
+  cuda_check(cudaEventRecord(static_cast<cudaEvent_t>(g.st->ev_out), g.s_out), "cudaEventRecord");
+  cuda_check(cudaStreamWaitEvent(g.s, static_cast<cudaEvent_t>(g.st->ev_out), 0), "cudaStreamWaitEvent");
+  cuda_check(cudaStreamSynchronize(g.s), "cudaStreamSynchronize");
 }
 
 }  // namespace
@@ -639,7 +718,14 @@ scc_status_t scc_plan_destroy(scc_plan_t* plan) {
     for (const scc::HostStaging& s : plan->staging) {
       cudaSetDevice(s.device);
       if (s.buf) cudaFree(s.buf);
-      if (s.stream) cudaStreamDestroy(static_cast<cudaStream_t>(s.stream));
+      for (void* q : {s.stream, s.stream_in, s.stream_out}) {
+        if (q) cudaStreamDestroy(static_cast<cudaStream_t>(q));
+      }
+      for (int i = 0; i < scc::kMaxHostChunks; ++i) {
+        if (s.ev_in[i]) cudaEventDestroy(static_cast<cudaEvent_t>(s.ev_in[i]));
+        if (s.ev_done[i]) cudaEventDestroy(static_cast<cudaEvent_t>(s.ev_done[i]));
+      }
+      if (s.ev_out) cudaEventDestroy(static_cast<cudaEvent_t>(s.ev_out));
     }
     for (const scc::ForkJoin& f : plan->forks) {
       cudaSetDevice(f.device);
@@ -799,15 +885,12 @@ scc_status_t scc_forward_host_f32(scc_plan_t* plan, int64_t n, int64_t h, int64_
     scc::check_ptr(y, "y");
     scc::check_bias(*plan, bias, "bias");
     std::lock_guard<std::mutex> lk(plan->host_mu);
-    const scc_config_t& c = plan->cfg;
-    scc::Staged g = scc::stage(*plan, n, h, w);
-    const size_t nx = n * c.c_in * h * w * 4, ny = n * c.c_out * h * w * 4;
-    scc::h2d(g.x, x, nx, g.s);
-    scc::h2d(g.w, weight, c.c_out * c.group_width * 4, g.s);
-    if (bias) scc::h2d(g.b, bias, c.c_out * 4, g.s);
-    scc::do_forward(*plan, n, h, w, g.x, g.w, bias ? g.b : nullptr, g.y, g.s);
-    scc::d2h(y, g.y, ny, g.s);
-    scc::cuda_check(cudaStreamSynchronize(g.s), "cudaStreamSynchronize");
+    scc::HostIo io;
+    io.x = x;
+    io.w = weight;
+    io.b = bias;
+    io.y = y;
+    scc::run_host(*plan, n, h, w, io);
   });
 }
 
@@ -824,18 +907,14 @@ scc_status_t scc_backward_host_f32(scc_plan_t* plan, int64_t n, int64_t h, int64
     scc::check_ptr(dweight, "dweight");
     scc::check_bias(*plan, dbias, "dbias");
     std::lock_guard<std::mutex> lk(plan->host_mu);
-    const scc_config_t& c = plan->cfg;
-    scc::Staged g = scc::stage(*plan, n, h, w);
-    const size_t nx = n * c.c_in * h * w * 4, ny = n * c.c_out * h * w * 4;
-    scc::h2d(g.dy, dy, ny, g.s);
-    scc::h2d(g.x, x, nx, g.s);
-    scc::h2d(g.w, weight, c.c_out * c.group_width * 4, g.s);
-    scc::do_backward(*plan, n, h, w, g.dy, g.x, g.w, g.dx, g.dw, dbias ? g.db : nullptr, g.ws,
-                            g.ws_bytes, g.s);
-    scc::d2h(dx, g.dx, nx, g.s);
-    scc::d2h(dweight, g.dw, c.c_out * c.group_width * 4, g.s);
-    if (dbias) scc::d2h(dbias, g.db, c.c_out * 4, g.s);
-    scc::cuda_check(cudaStreamSynchronize(g.s), "cudaStreamSynchronize");
+    scc::HostIo io;
+    io.x = x;
+    io.w = weight;
+    io.dy = dy;
+    io.dx = dx;
+    io.dw = dweight;
+    io.db = dbias;
+    scc::run_host(*plan, n, h, w, io);
   });
 }
 
@@ -854,22 +933,16 @@ scc_status_t scc_fwd_bwd_host_f32(scc_plan_t* plan, int64_t n, int64_t h, int64_
     scc::check_bias(*plan, bias, "bias");
     scc::check_bias(*plan, dbias, "dbias");
     std::lock_guard<std::mutex> lk(plan->host_mu);
-    const scc_config_t& c = plan->cfg;
-    scc::Staged g = scc::stage(*plan, n, h, w);
-    const size_t nx = n * c.c_in * h * w * 4, ny = n * c.c_out * h * w * 4;
-    const size_t nw = c.c_out * c.group_width * 4;
-    scc::h2d(g.x, x, nx, g.s);
-    scc::h2d(g.w, weight, nw, g.s);
-    if (bias) scc::h2d(g.b, bias, c.c_out * 4, g.s);
-    scc::h2d(g.dy, dy, ny, g.s);
-    scc::do_forward(*plan, n, h, w, g.x, g.w, bias ? g.b : nullptr, g.y, g.s);
-    scc::do_backward(*plan, n, h, w, g.dy, g.x, g.w, g.dx, g.dw, dbias ? g.db : nullptr, g.ws,
-                            g.ws_bytes, g.s);
-    scc::d2h(y, g.y, ny, g.s);
-    scc::d2h(dx, g.dx, nx, g.s);
-    scc::d2h(dweight, g.dw, nw, g.s);
-    if (dbias) scc::d2h(dbias, g.db, c.c_out * 4, g.s);
-    scc::cuda_check(cudaStreamSynchronize(g.s), "cudaStreamSynchronize");
+    scc::HostIo io;
+    io.x = x;
+    io.w = weight;
+    io.b = bias;
+    io.dy = dy;
+    io.y = y;
+    io.dx = dx;
+    io.dw = dweight;
+    io.db = dbias;
+    scc::run_host(*plan, n, h, w, io);
   });
 }
 

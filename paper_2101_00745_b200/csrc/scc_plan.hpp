@@ -119,11 +119,19 @@ struct DeviceTables {
 };
 
 // Device staging for the host-buffer entry points.
+// Host-buffer entry points pipeline over batch chunks: copy-in stream,
+// compute stream, copy-out stream, one event pair per chunk.
+constexpr int kMaxHostChunks = 16;
 struct HostStaging {
   int device = -1;
   void* buf = nullptr;
   size_t bytes = 0;
-  void* stream = nullptr;  // cudaStream_t
+  void* stream = nullptr;     // cudaStream_t: compute
+  void* stream_in = nullptr;  // cudaStream_t: H2D copies
+  void* stream_out = nullptr; // cudaStream_t: D2H copies
+  void* ev_in[kMaxHostChunks] = {};    // cudaEvent_t: chunk inputs resident
+  void* ev_done[kMaxHostChunks] = {};  // cudaEvent_t: chunk outputs written
+  void* ev_out = nullptr;              // cudaEvent_t: all D2H issued
 };
 
 // Per (device, stream, direction) scratch for the tensor-core weight panels,

@@ -373,3 +373,39 @@ def test_host_buffer_entry_points(port):
     y2 = np.empty_like(y)
     _lib.check(_lib.lib().scc_forward_host_f32(cfg.handle, 4, 8, 8, p(x), p(wt), p(b), p(y2)))
     assert np.array_equal(y, y2)
+
+
+@pytest.mark.parametrize("chunks", ["1", "3", "8"])
+def test_host_pipeline_bitwise(chunks, monkeypatch):
+    """The host-buffer entry points pipeline H2D / kernels / D2H over batch
+    chunks (ragged split of n=10 here); forward and backward-data are per
+    sample and backward-weight runs once over the whole batch, so every output
+    is bitwise equal to the device-buffer entry points' on the same inputs."""
+    import ctypes as C
+    import paper_2101_00745_b200 as scc
+    from paper_2101_00745_b200 import _lib
+    monkeypatch.setenv("SCC_HOST_CHUNKS", chunks)
+    rng = np.random.default_rng(11)
+    n = 10
+    cfg = scc.scc_config_new(64, 128, 2, "50%", True)
+    x, wt, b, dy = rand_problem(rng, 64, 128, 32, n, 16, 16, True)
+    y = np.empty((n, 128, 16, 16), np.float32)
+    dx, dw, db = np.empty_like(x), np.empty_like(wt), np.empty_like(b)
+    p = lambda a: a.ctypes.data_as(C.c_void_p)  # noqa: E731
+    _lib.check(_lib.lib().scc_fwd_bwd_host_f32(cfg.handle, n, 16, 16, p(x), p(wt), p(b), p(dy), p(y),
+                                               p(dx), p(dw), p(db)))
+    wts = scc.SccWeights(torch.from_numpy(wt).cuda(), torch.from_numpy(b).cuda())
+    xt, gt = torch.from_numpy(x).cuda(), torch.from_numpy(dy).cuda()
+    yd = scc.scc_forward(xt, wts, cfg).cpu().numpy()
+    g = scc.scc_backward(gt, xt, wts, cfg)
+    assert np.array_equal(y, yd)
+    assert np.array_equal(dx, g.grad_input.cpu().numpy())
+    assert np.array_equal(dw, g.params.grad_weight.cpu().numpy())
+    assert np.array_equal(db, g.params.grad_bias.cpu().numpy())
+    dx2, dw2, db2 = np.empty_like(x), np.empty_like(wt), np.empty_like(b)
+    _lib.check(_lib.lib().scc_backward_host_f32(cfg.handle, n, 16, 16, p(dy), p(x), p(wt), p(dx2),
+                                                p(dw2), p(db2)))
+    assert np.array_equal(dx, dx2) and np.array_equal(dw, dw2) and np.array_equal(db, db2)
+    y2 = np.empty_like(y)
+    _lib.check(_lib.lib().scc_forward_host_f32(cfg.handle, n, 16, 16, p(x), p(wt), p(b), p(y2)))
+    assert np.array_equal(y, y2)
