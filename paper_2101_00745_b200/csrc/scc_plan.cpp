@@ -287,6 +287,25 @@ void build_tc_weight(const Plan& p, TcWeightPlan& tw) {
       break;
     }
   }
+  // Generation-1 kernel: the producer tiles each chunk's arc rows with boxes
+  // of rbb1 rows; the tallest box (multiple of 8: 1 KB swizzle atoms) that
+  // divides the chunk width and never straddles the ring end.  Fewer, larger
+  // boxes keep more bytes in flight per TMA issue.
+  tw.rbb1 = 8;
+  for (int32_t rb = std::min(tw.nw, 256); rb > 8; rb -= 8) {
+    bool ok = tw.nw % rb == 0;
+    for (int32_t rt = 0; rt < tw.n_rt && ok; ++rt) {
+      for (int32_t r = 0; r < tw.n_nc * tw.nw && ok; r += rb) {
+        if (r >= tw.rt_info[2 * rt + 1]) break;
+        const int32_t pos = (tw.rt_info[2 * rt] + r) % ring;
+        ok = pos + rb <= ring;
+      }
+    }
+    if (ok) {
+      tw.rbb1 = rb;
+      break;
+    }
+  }
   tw.ok = true;
 }
 

@@ -110,7 +110,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int s = 0; s < kMaxT; ++s) {
       mbar_init(&b_full[s], 1);
-      mbar_init(&conv[s], 4);
+      mbar_init(&conv[s], 8);  // 4 dy converter warps + 4 x-lo converter warps
       mbar_init(&t_free[s], 1);
     }
     mbar_init(tfull, 1);
@@ -222,7 +222,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     float bsum = 0.f;
     int sa = 0, st = 0;
     uint32_t pa = 0, ps = 0;
-    const int bvec_q = NB * b_blk_bytes / 16 / 4;  // float4 of raw x per warp
     for (int c = 0; c < nchunks; ++c) {
       mbar_wait_tag(&a_full[sa], pa, 23);
       const uint8_t* ab = a_ring + sa * a_stage_bytes;
@@ -230,12 +229,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
       for (int b = 0; b < 2; ++b) {
         if (b < NB) {
-          const float4* src = reinterpret_cast<const float4*>(ab + a_row_off(t, b));
+          const uint32_t src = smem_u32(ab + a_row_off(t, b));
 #pragma unroll
           for (int k = 0; k < 8; ++k) {
             // 16 B chunk k of the row sits at chunk index (k ^ row%8): undo the
             // swizzle so columns come out in pixel order.
-            const float4 v = src[k ^ (t & 7)];
+            const float4 v = lds_v4(src + 16 * (k ^ (t & 7)));
             const float e[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
@@ -250,24 +249,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&a_free[sa]);
       advance(sa, pa, SA);
-      // x lo for this warp's quarter of the stage, once x has landed (the
-      // producer refilled the stage only after the MMAs of its previous use).
-      mbar_wait_tag(&b_full[st], ps, 24);
-      {
-        uint8_t* bd = b_ring + st * b_stage_bytes;
-        const float4* src = reinterpret_cast<const float4*>(bd) + q * bvec_q;
-        float4* dst = reinterpret_cast<float4*>(bd + NB * b_blk_bytes) + q * bvec_q;
-        for (int i = lane; i < bvec_q; i += 32) {
-          const float4 v = src[i];
-          float4 l4;
-          l4.x = v.x - tf32_hi(v.x);
-          l4.y = v.y - tf32_hi(v.y);
-          l4.z = v.z - tf32_hi(v.z);
-          l4.w = v.w - tf32_hi(v.w);
-          dst[i] = l4;
-        }
-      }
-      fence_proxy_async_smem();
       tc_fence_after();
       const uint32_t col = tmem + a.acol0 + st * (2 * kpix) + lane_base;
 #pragma unroll
@@ -288,8 +269,35 @@ __global__ void __launch_bounds__(kThreads, 1)
       a.pbias[(static_cast<int64_t>(split) * a.n_rt + rt) * 128 + t] = bsum;
     }
   } else {
+    // ---------------- x lo converters, then the epilogue ----------------
+    // x lo for this warp's quarter of each stage, once x has landed (the
+    // producer refills a stage only after the MMAs of its previous use), in
+    // parallel with the dy converters.
+    const int quarter = warp & 3;  // TMEM lane quarter this warp may access
+    {
+      const int bvec_q = NB * b_blk_bytes / 16 / 4;  // float4 of raw x per warp
+      int st = 0;
+      uint32_t ps = 0;
+      for (int c = 0; c < nchunks; ++c) {
+        mbar_wait_tag(&b_full[st], ps, 24);
+        const uint32_t src = smem_u32(b_ring + st * b_stage_bytes) + 16u * quarter * bvec_q;
+        const uint32_t dst = src + NB * b_blk_bytes;
+        for (int i = lane; i < bvec_q; i += 32) {
+          const float4 v = lds_v4(src + 16u * i);
+          float4 l4;
+          l4.x = v.x - tf32_hi(v.x);
+          l4.y = v.y - tf32_hi(v.y);
+          l4.z = v.z - tf32_hi(v.z);
+          l4.w = v.w - tf32_hi(v.w);
+          sts_v4(dst + 16u * i, l4);
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&conv[st]);
+        advance(st, ps, ST);
+      }
+    }
     // ---------------- epilogue: accumulator -> partial tile ----------------
-    const int quarter = warp & 3;
     const int row = quarter * 32 + lane;
     float* dst = a.part + ((static_cast<int64_t>(split) * a.n_rt + rt) * a.n_nc + nc) * 128 * a.nw +
                  static_cast<int64_t>(row) * a.nw;
@@ -326,8 +334,44 @@ struct FArgs {
   int32_t splits, n_rt, n_nc, nw, c_in, c_out, gw;
 };
 
-// Warp per output: lane l sums splits l, l+32, ... in order, then a fixed
-// butterfly combines the lanes.
+// Partial-tile location of window slot k of filter oc.
+__device__ __forceinline__ int64_t fin_base(const FArgs& a, int oc, int k) {
+  const int pos = a.inv_perm[oc];
+  const int rt = pos >> 7, row = pos & 127;
+  int col = a.starts[oc] + k - a.rt_info[2 * rt];
+  while (col < 0) col += a.c_in;
+  while (col >= a.c_in) col -= a.c_in;
+  const int nc = col / a.nw, c = col - nc * a.nw;
+  return ((static_cast<int64_t>(rt) * a.n_nc + nc) * 128 + row) * a.nw + c;
+}
+
+// Thread per output (many outputs, few splits): the split partials are summed
+// in ascending order; neighbouring threads read neighbouring window slots, so
+// every split plane is read coalesced.
+__global__ void __launch_bounds__(256) tc_weight_finalize_wide(const FArgs a) {
+  const int64_t nw_out = static_cast<int64_t>(a.c_out) * a.gw;
+  const int64_t total = nw_out + (a.dbias ? a.c_out : 0);
+  const int64_t stride = static_cast<int64_t>(a.n_rt) * a.n_nc * 128 * a.nw;
+  for (int64_t o = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; o < total;
+       o += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    float s = 0.f;
+    if (o < nw_out) {
+      const int oc = static_cast<int>(o / a.gw);
+      const int64_t base = fin_base(a, oc, static_cast<int>(o - static_cast<int64_t>(oc) * a.gw));
+      for (int sp = 0; sp < a.splits; ++sp) s += a.part[base + sp * stride];
+      a.dweight[o] = s;
+    } else {
+      const int oc = static_cast<int>(o - nw_out);
+      const int pos = a.inv_perm[oc];
+      const int rt = pos >> 7, row = pos & 127;
+      for (int sp = 0; sp < a.splits; ++sp) s += a.pbias[(static_cast<int64_t>(sp) * a.n_rt + rt) * 128 + row];
+      a.dbias[oc] = s;
+    }
+  }
+}
+
+// Warp per output (few outputs, many splits): lane l sums splits l, l+32, ...
+// in order, then a fixed butterfly combines the lanes.
 __global__ void __launch_bounds__(256) tc_weight_finalize(const FArgs a) {
   const int64_t nw_out = static_cast<int64_t>(a.c_out) * a.gw;
   const int64_t total = nw_out + (a.dbias ? a.c_out : 0);
@@ -384,14 +428,18 @@ WGrid weight_grid(const TcWeightPlan& tw, int64_t n, int64_t plane) {
     b_stage = 2 * tw.nw * kpix * 4;
     while (g.t_stages > 1 && (kBudget - g.t_stages * b_stage) / a_stage < 2) --g.t_stages;
     g.a_stages = std::min(kMaxA, (kBudget - g.t_stages * b_stage) / a_stage);
-    if (g.a_stages >= 2 || g.blk == 1) break;
+    // A single x stage serialises load -> lo convert -> MMA per chunk
+    // (measured ~4x slower at nw = 192), so halve the stage width instead.
+    if ((g.a_stages >= 2 && g.t_stages >= 2) || g.blk == 1) break;
     g.blk = 1;
   }
   g.smem = g.a_stages * a_stage + g.t_stages * b_stage + 1024 + 512;
   g.pcs = (plane + kpix - 1) / kpix;
   g.total_chunks = n * g.pcs;
   const int64_t items = static_cast<int64_t>(tw.n_rt) * tw.n_nc;
-  int64_t splits = std::max<int64_t>(1, (148 + items - 1) / items);
+  // One CTA per SM (shared memory): a grid just over 148 runs a second,
+  // nearly empty wave, so round the split count down.
+  int64_t splits = std::max<int64_t>(1, 148 / items);
   splits = std::min(splits, g.total_chunks);
   g.chunks_per_split = (g.total_chunks + splits - 1) / splits;
   g.splits = static_cast<int32_t>((g.total_chunks + g.chunks_per_split - 1) / g.chunks_per_split);
@@ -443,7 +491,7 @@ cudaError_t launch_weight_tc(const TcWeightPlan& tw, const TcWeightCall& call, c
   {
     const uint64_t dims[3] = {P, 1, static_cast<uint64_t>(call.n) * call.c_in};
     const uint64_t strides[2] = {P * 4, P * 4};
-    const uint32_t box[3] = {kAtom, 1, static_cast<uint32_t>(tw.rbb)};
+    const uint32_t box[3] = {kAtom, 1, static_cast<uint32_t>(tw.rbb1)};
     if (!encode_f32_sw128(&tx, call.x, 3, dims, strides, box)) return cudaErrorInvalidValue;
   }
   WArgs a{};
@@ -458,7 +506,7 @@ cudaError_t launch_weight_tc(const TcWeightPlan& tw, const TcWeightCall& call, c
   a.c_in = call.c_in;
   a.c_out = call.c_out;
   a.rba = tw.rba;
-  a.rbb = tw.rbb;
+  a.rbb = tw.rbb1;
   a.blk = g.blk;
   a.a_stages = g.a_stages;
   a.t_stages = g.t_stages;
@@ -500,8 +548,13 @@ cudaError_t launch_weight_tc(const TcWeightPlan& tw, const TcWeightCall& call, c
   f.c_out = call.c_out;
   f.gw = call.gw;
   const int64_t outs = static_cast<int64_t>(call.c_out) * call.gw + (call.dbias ? call.c_out : 0);
-  const int fgrid = static_cast<int>(std::min<int64_t>((outs + 7) / 8, 148 * 16));
-  tc_weight_finalize<<<fgrid, 256, 0, s>>>(f);
+  if (outs >= 65536) {
+    const int fgrid = static_cast<int>(std::min<int64_t>((outs + 255) / 256, 148 * 8));
+    tc_weight_finalize_wide<<<fgrid, 256, 0, s>>>(f);
+  } else {
+    const int fgrid = static_cast<int>(std::min<int64_t>((outs + 7) / 8, 148 * 16));
+    tc_weight_finalize<<<fgrid, 256, 0, s>>>(f);
+  }
   note_launches(2);
   return cudaGetLastError();
 }
