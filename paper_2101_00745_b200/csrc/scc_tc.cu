@@ -48,7 +48,7 @@ __device__ unsigned long long g_trace[32];
     if (blockIdx.x == 0) g_trace[(slot)] = globaltimer();     \
   } while (0)
 
-constexpr int kTcThreads = 320;
+constexpr int kTcThreads = 352;  // 11 warps: + a streamed-panel producer
 constexpr int KC = 32;          // ring positions per pipeline stage (4 k-steps of 8)
 constexpr int TM = 128;         // pixels per tile
 constexpr int kABytes = TM * KC * 4;  // 16 KB per A buffer
@@ -64,7 +64,7 @@ struct TcCfg {
   static_assert(kACol0 + kTStages * 2 * KC <= kTmemCols, "TMEM budget");
   static constexpr int kStoreBytes = 4 * 2 * 32 * 32 * 4;  // 4 warps x 2 bufs x [32 rows][32 px]
   static constexpr int kMaxAStages = 8;
-  static constexpr int kMaxBStages = 2;
+  static constexpr int kMaxBStages = 4;
 };
 
 // Shared-memory plan of one launch (host computes, kernel re-derives).
@@ -221,21 +221,34 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                         __ldg(a.class_d + cl), tc.n * a.rows_per_sample_3d + j);
           }
           advance(sa, pa, SA);
-          if (a.sm.b_resident) {
-            if (t == blockIdx.x && c == 0) {
-              panel_ready();
-              mbar_expect_tx(&b_full[0], a.panel_floats * 4);
-              bulk_load(b_base, a.panel, a.panel_floats * 4, &b_full[0]);
-            }
-          } else {
+          if (a.sm.b_resident && t == blockIdx.x && c == 0) {
             panel_ready();
-            mbar_wait_tag(&b_free[sb], pb ^ 1u, 2);
-            mbar_expect_tx(&b_full[sb], C::kBBytes);
-            bulk_load(b_base + sb * C::kBBytes,
-                      a.panel + a.rt_info[4 * tc.rt + 2] + static_cast<int64_t>(c) * (C::kBBytes / 4),
-                      C::kBBytes, &b_full[sb]);
-            advance(sb, pb, SB);
+            mbar_expect_tx(&b_full[0], a.panel_floats * 4);
+            bulk_load(b_base, a.panel, a.panel_floats * 4, &b_full[0]);
           }
+        }
+      }
+      (void)sb;
+      (void)pb;
+    }
+  } else if (warp == 10) {
+    // ---------------- streamed panel producer ----------------
+    // Its own warp, so the activation ring runs SA stages ahead of the MMAs
+    // instead of being throttled by the panel ring's b_free waits.
+    if (!a.sm.b_resident && elect_one()) {
+      cudaGridDependencySynchronize();  // the panel-build kernel (PDL)
+      int sb = 0;
+      uint32_t pb = 0;
+      for (int64_t t = blockIdx.x; t < total; t += gridDim.x) {
+        const int rt = static_cast<int>(t % a.n_rt);
+        const int nch = chunks_of(a, rt);
+        for (int c = 0; c < nch; ++c) {
+          mbar_wait_tag(&b_free[sb], pb ^ 1u, 2);
+          mbar_expect_tx(&b_full[sb], C::kBBytes);
+          bulk_load(b_base + sb * C::kBBytes,
+                    a.panel + a.rt_info[4 * rt + 2] + static_cast<int64_t>(c) * (C::kBBytes / 4),
+                    C::kBBytes, &b_full[sb]);
+          advance(sb, pb, SB);
         }
       }
     }
@@ -310,11 +323,11 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       for (int c = 0; c < nch; ++c) {
         mbar_wait_tag(&a_full[sa], pa, 7);
         if (t == blockIdx.x && c == 0 && q == 0 && lane == 0) TRACE(4);
-        const float* src = reinterpret_cast<const float*>(a_ring + sa * kABytes) + q * 32 + lane;
+        const uint32_t src = smem_u32(a_ring + sa * kABytes) + 4u * (q * 32 + lane);
         uint32_t hi[KC], lo[KC];
 #pragma unroll
         for (int k = 0; k < KC; ++k) {
-          const float v = src[k * TM];
+          const float v = lds_f32(src + 4u * k * TM);
           const float h = tf32_hi(v);
           hi[k] = __float_as_uint(h);
           lo[k] = __float_as_uint(v - h);
@@ -378,10 +391,11 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         tmem_ld_wait();
         if (tma_group) {
           float* buf = reinterpret_cast<float*>(store_buf + (q * 2 + sbuf) * 4096);
+          const uint32_t bufa = smem_u32(buf) + 4u * lane;
           if (lane == 0) bulk_wait_read<1>();  // this buffer's previous store has read it
           __syncwarp();
 #pragma unroll
-          for (int j = 0; j < 32; ++j) buf[j * 32 + lane] = __uint_as_float(v[j]) + bb[j];
+          for (int j = 0; j < 32; ++j) sts_f32(bufa + 128u * j, __uint_as_float(v[j]) + bb[j]);
           fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) {
@@ -564,7 +578,8 @@ static cudaError_t launch_tc_nt(const TcBandPlan& tp, const TcDeviceTables& dt,
     } else {
       sm.b_resident = 0;
       sm.b_bytes = C::kBBytes;
-      sm.b_stages = C::kMaxBStages;
+      sm.b_stages = 3;
+      if (const char* e = getenv("SCC_BAND_BSTAGES")) sm.b_stages = std::max(2, std::min(C::kMaxBStages, atoi(e)));
     }
     const int b_total = sm.b_resident ? sm.b_bytes : sm.b_stages * C::kBBytes;
     sm.a_stages = std::min(C::kMaxAStages, (rest - b_total) / kABytes);

@@ -44,6 +44,11 @@ __device__ __forceinline__ void sts_v4(uint32_t addr, float4 v) {
 }
 // Shared-memory load through a 32-bit shared-window address (volatile: the
 // callers read data that TMA wrote behind an mbarrier wait).
+__device__ __forceinline__ float lds_f32(uint32_t addr) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
+  return v;
+}
 __device__ __forceinline__ float4 lds_v4(uint32_t addr) {
   float4 v;
   asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
