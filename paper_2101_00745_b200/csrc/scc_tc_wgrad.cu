@@ -40,7 +40,7 @@ __device__ unsigned long long g_wtrace[32];
     if (blockIdx.x == 0) g_wtrace[(slot)] = globaltimer();      \
   } while (0)
 
-constexpr int kThreads = 320;
+constexpr int kThreads = 352;  // 11 warps: dy loads from warp 0, x loads from warp 10
 constexpr int kAtom = 32;              // pixels per SWIZZLE_128B atom (128 B)
 constexpr int kMaxA = 8;               // dy ring depth cap
 constexpr int kMaxT = 3;               // TMEM / x stage depth cap
@@ -135,21 +135,25 @@ __global__ void __launch_bounds__(kThreads, 1)
            (l % a.rba) * 128;
   };
 
-  if (warp == 0) {
-    // ---------------- producer ----------------
+  // Producers.  A TMA instruction occupies its issuing thread for ~0.1-0.4 us,
+  // so dy and x loads are issued from two warps (one elected thread each),
+  // each running ahead on its own ring.  (Dealing a side's boxes over two
+  // issuers measured slower: the interleaved prefetches delay the boxes the
+  // MMA needs first.)
+  const bool dy_role = warp == 0;
+  const bool x_role = warp == 10;
+  if (dy_role) {
     if (elect_one()) {
-      int sa = 0, sb = 0;
-      uint32_t pa = 0, pb = 0;
+      int sa = 0;
+      uint32_t pa = 0;
       const int rows_a = min(128, a.c_out - rt * 128);
-      const int cols_b = min(a.nw, ncols - nc * a.nw);
+      const int a_boxes_rows = (rows_a + a.rba - 1) / a.rba * a.rba;
       for (int64_t qc = q_begin; qc < q_end; ++qc) {
         const int n = static_cast<int>(qc / a.pcs);
         const int p0 = static_cast<int>(qc - static_cast<int64_t>(n) * a.pcs) * kpix;
-        // dy -> ring
         if (qc - q_begin == 1) WTRACE(27);
         mbar_wait_tag(&a_free[sa], pa ^ 1u, 20);
         if (qc - q_begin == 1) WTRACE(28);
-        const int a_boxes_rows = (rows_a + a.rba - 1) / a.rba * a.rba;
         mbar_expect_tx(&a_full[sa], a_boxes_rows * NB * 128);
         uint8_t* ad = a_ring + sa * a_stage_bytes;
         for (int r = 0; r < a_boxes_rows; r += a.rba) {
@@ -160,17 +164,26 @@ __global__ void __launch_bounds__(kThreads, 1)
             tma_load_4d(ad + a_row_off(r, 0), &tdy, &a_full[sa], 0, d, n * a.cls + j, p0 / kAtom);
           } else {
             for (int b = 0; b < NB; ++b) {
-              tma_load_3d(ad + a_row_off(r, b), &tdy, &a_full[sa], p0 + b * kAtom, d,
-                          n * a.cls + j);
+              tma_load_3d(ad + a_row_off(r, b), &tdy, &a_full[sa], p0 + b * kAtom, d, n * a.cls + j);
             }
           }
         }
         advance(sa, pa, SA);
         if (qc - q_begin == 1) WTRACE(29);
-        // x -> stage (raw half)
+        if (qc - q_begin < 8) WTRACE(2 + (qc - q_begin));
+      }
+    }
+  } else if (x_role) {
+    if (elect_one()) {
+      int sb = 0;
+      uint32_t pb = 0;
+      const int cols_b = min(a.nw, ncols - nc * a.nw);
+      const int b_boxes_rows = (cols_b + a.rbb - 1) / a.rbb * a.rbb;
+      for (int64_t qc = q_begin; qc < q_end; ++qc) {
+        const int n = static_cast<int>(qc / a.pcs);
+        const int p0 = static_cast<int>(qc - static_cast<int64_t>(n) * a.pcs) * kpix;
         mbar_wait_tag(&t_free[sb], pb ^ 1u, 21);
         if (qc - q_begin == 1) WTRACE(30);
-        const int b_boxes_rows = (cols_b + a.rbb - 1) / a.rbb * a.rbb;
         mbar_expect_tx(&b_full[sb], b_boxes_rows * NB * 128);
         uint8_t* bd = b_ring + sb * b_stage_bytes;
         for (int b = 0; b < NB; ++b) {
@@ -181,7 +194,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                         n * a.c_in + pos);
           }
         }
-        if (qc - q_begin < 8) WTRACE(2 + (qc - q_begin));
         if (qc - q_begin == 1) WTRACE(31);
         advance(sb, pb, ST);
       }
@@ -249,6 +261,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&a_free[sa]);
       advance(sa, pa, SA);
+      // TMEM A stage st is free once the MMAs of its previous use completed
+      // (the same commit that lets the producer refill x stage st).
+      mbar_wait_tag(&t_free[st], ps ^ 1u, 24);
       tc_fence_after();
       const uint32_t col = tmem + a.acol0 + st * (2 * kpix) + lane_base;
 #pragma unroll
@@ -481,11 +496,23 @@ cudaError_t launch_weight_tc(const TcWeightPlan& tw, const TcWeightCall& call, c
     const uint32_t box[4] = {kAtom, 1, static_cast<uint32_t>(tw.rba), static_cast<uint32_t>(g.blk)};
     dy4d = encode_f32_sw128(&tdy, call.dy, 4, dims, strides, box);
   }
+  // With one atom per stage the dy stage is plain [128 rows][128 B], so a box
+  // may span every row of one class run (up to the whole tile): fewer TMA
+  // instructions per chunk (each one holds its issuing thread ~0.3 us).
+  int rba = tw.rba;
+  if (!dy4d && g.blk == 1) {
+    for (int rb : {128, 64}) {
+      if (rb > rba && tw.cls % rb == 0) {
+        rba = rb;
+        break;
+      }
+    }
+  }
   if (!dy4d) {
     const uint64_t dims[3] = {P, static_cast<uint64_t>(tw.n_class),
                               static_cast<uint64_t>(call.n) * tw.cls};
     const uint64_t strides[2] = {P * 4, P * 4 * tw.n_class};
-    const uint32_t box[3] = {kAtom, 1, static_cast<uint32_t>(tw.rba)};
+    const uint32_t box[3] = {kAtom, 1, static_cast<uint32_t>(rba)};
     if (!encode_f32_sw128(&tdy, call.dy, 3, dims, strides, box)) return cudaErrorInvalidValue;
   }
   {
@@ -505,7 +532,7 @@ cudaError_t launch_weight_tc(const TcWeightPlan& tw, const TcWeightCall& call, c
   a.cls = tw.cls;
   a.c_in = call.c_in;
   a.c_out = call.c_out;
-  a.rba = tw.rba;
+  a.rba = rba;
   a.rbb = tw.rbb1;
   a.blk = g.blk;
   a.a_stages = g.a_stages;
