@@ -187,6 +187,36 @@ scc_status_t scc_fwd_bwd_host_f32(scc_plan_t* plan, int64_t n, int64_t h, int64_
                                   const float* dy, float* y, float* dx, float* dweight,
                                   float* dbias);
 
+/* ---- fused dsc_block forward (model.cpp:213-220) ------------------------- */
+/* y = SCC(DW3x3(x)): the depthwise 3x3 stage (groups = c_in, padding 1,
+ * stride 1 or 2; conv_forward_impl, reference.cpp:74-123) computed inside the
+ * SCC kernel's staging step, so the DW output never goes to HBM.
+ * x: [n][c_in][h][w]; dw_weight: [c_in][3][3]; dw_bias: [c_in] or NULL;
+ * weight / bias: the SCC layer's (as scc_forward_f32);
+ * y: [n][c_out][h_out][w_out], h_out = (h - 1) / stride + 1 (same for w). */
+scc_status_t scc_dsc_forward_f32(const scc_plan_t* plan, int64_t n, int64_t h, int64_t w,
+                                 int64_t stride, const float* x, const float* dw_weight,
+                                 const float* dw_bias, const float* weight, const float* bias,
+                                 float* y, void* stream);
+
+/* ---- depthwise 3x3 stage of a dsc_block (model.cpp:213-220) -------------- */
+/* groups = c, kernel 3, padding 1, stride 1 or 2 (conv_forward_impl,
+ * reference.cpp:74-123).  x: [n][c][h][w]; weight: [c][3][3]; bias: [c] or
+ * NULL; y / dy: [n][c][h_out][w_out] with h_out = (h - 1) / stride + 1.
+ * Backward-weight needs scc_dw3x3_workspace_size() bytes of workspace and is
+ * deterministic (fixed-order reduction, no atomics). */
+scc_status_t scc_dw3x3_forward_f32(int64_t n, int64_t c, int64_t h, int64_t w, int64_t stride,
+                                   const float* x, const float* weight, const float* bias,
+                                   float* y, void* stream);
+scc_status_t scc_dw3x3_backward_data_f32(int64_t n, int64_t c, int64_t h, int64_t w,
+                                         int64_t stride, const float* dy, const float* weight,
+                                         float* dx, void* stream);
+scc_status_t scc_dw3x3_workspace_size(int64_t c, size_t* bytes);
+scc_status_t scc_dw3x3_backward_weight_f32(int64_t n, int64_t c, int64_t h, int64_t w,
+                                           int64_t stride, const float* dy, const float* x,
+                                           float* dweight, float* dbias, void* workspace,
+                                           size_t workspace_bytes, void* stream);
+
 #ifdef __cplusplus
 }  /* extern "C" */
 #endif

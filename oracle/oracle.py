@@ -113,6 +113,20 @@ class _Base:
         return dw, (db if cfg.has_bias else None)
 
 
+    def dw_forward(self, x, wt, bias, k=3, stride=1):
+        """Depthwise k x k conv of a dsc_block (model.cpp:213-220; padding k/2,
+        reference.cpp:74-123).  wt: [c][k][k]; bias: [c] or None."""
+        x = _d(x)
+        n, c, h, wd = x.shape
+        pad = k // 2
+        ho, wo = (h + 2 * pad - k) // stride + 1, (wd + 2 * pad - k) // stride + 1
+        y = np.empty((n, c, ho, wo), np.float64)
+        wt = _d(wt)
+        b = _d(bias) if bias is not None else None
+        self._dw(n, c, h, wd, k, stride, _ptr(x), _ptr(wt), _ptr(b) if b is not None else None, _ptr(y))
+        return y
+
+
 class PortOracle(_Base):
     """oracle/scc_oracle.c (plain-C restatement, single thread)."""
 
@@ -138,6 +152,8 @@ class PortOracle(_Base):
         L.scc_oracle_forward_macs.argtypes = [C.POINTER(_Cfg), _i64, _i64, _i64]
         L.scc_oracle_forward_macs.restype = C.c_uint64
         self._fwd = L.scc_oracle_forward
+        L.scc_oracle_dw_forward.argtypes = [_i64] * 6 + [_dp, _dp, _dp, _dp]
+        self._dw = L.scc_oracle_dw_forward
         self._bwd_in = L.scc_oracle_backward_input
         self._bwd_p = L.scc_oracle_backward_params
 
@@ -203,6 +219,8 @@ class RefOracle(_Base):
         L.ref_problem_step.restype = C.c_double
         L.ref_problem_free.argtypes = [C.c_void_p]
         self._fwd = self._checked(L.ref_forward)
+        L.sccl_ref_dw_forward.argtypes = [_i64] * 6 + [_dp, _dp, _dp, _dp]
+        self._dw = self._checked(L.sccl_ref_dw_forward)
         self._bwd_in = self._checked(L.ref_backward_input)
         self._bwd_p = self._checked(L.ref_backward_params)
 

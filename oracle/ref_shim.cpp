@@ -17,6 +17,7 @@
 #include "sccl/errors.hpp"
 #include "sccl/kernel.hpp"
 #include "sccl/parallel.hpp"
+#include "sccl/reference.hpp"
 #include "sccl/tensor.hpp"
 
 namespace {
@@ -277,3 +278,30 @@ double ref_problem_step(void* handle) {
 void ref_problem_free(void* handle) { delete static_cast<ref_problem*>(handle); }
 
 }  // extern "C"
+
+// grouped_conv_forward (reference.hpp:71, reference.cpp:145) as the
+// depthwise stage of a dsc_block (model.cpp:213-220: groups = c_in,
+// padding = kernel / 2).  bias may be null (empty ConvWeights::bias).
+extern "C" int sccl_ref_dw_forward(int64_t n, int64_t c, int64_t h, int64_t w, int64_t k,
+                                   int64_t stride, const double* x, const double* wt,
+                                   const double* bias, double* y) {
+  try {
+    sccl::ConvSpec spec;
+    spec.c_in = c;
+    spec.c_out = c;
+    spec.kernel = k;
+    spec.stride = stride;
+    spec.padding = k / 2;
+    spec.groups = c;
+    sccl::ConvWeights wts;
+    wts.weight.assign(wt, wt + c * k * k);
+    if (bias) wts.bias.assign(bias, bias + c);
+    sccl::Tensor4 in(n, c, h, w);
+    std::memcpy(in.data(), x, sizeof(double) * static_cast<size_t>(in.size()));
+    const sccl::Tensor4 out = sccl::grouped_conv_forward(in, wts, spec);
+    std::memcpy(y, out.data(), sizeof(double) * static_cast<size_t>(out.size()));
+    return 0;
+  } catch (...) {
+    return map_exception();
+  }
+}

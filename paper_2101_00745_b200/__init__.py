@@ -21,6 +21,10 @@ from .scc import (  # noqa: F401
     ShapeError,
     compute_channel_cycle,
     covering_filters,
+    dsc_forward,
+    dw3x3_backward_data,
+    dw3x3_backward_weight,
+    dw3x3_forward,
     launch_count,
     scc_backward,
     scc_backward_input,
@@ -32,6 +36,6 @@ from .scc import (  # noqa: F401
     scc_weights_init,
     window_of,
 )
-from .module import SCC2d, scc2d  # noqa: F401
+from .module import DSC2d, SCC2d, dsc2d, scc2d  # noqa: F401
 
 __all__ = [n for n in dir() if not n.startswith("_")]

@@ -874,6 +874,122 @@ scc_status_t scc_backward_f32(const scc_plan_t* plan, int64_t n, int64_t h, int6
   });
 }
 
+scc_status_t scc_dsc_forward_f32(const scc_plan_t* plan, int64_t n, int64_t h, int64_t w,
+                                 int64_t stride, const float* x, const float* dw_weight,
+                                 const float* dw_bias, const float* weight, const float* bias,
+                                 float* y, void* stream) {
+  return guard([&] {
+    scc::check_ptr(plan, "plan");
+    scc::check_extents(n, h, w);
+    scc::check_ptr(x, "x");
+    scc::check_ptr(dw_weight, "dw_weight");
+    scc::check_ptr(weight, "weight");
+    scc::check_ptr(y, "y");
+    auto& p = *const_cast<scc_plan_t*>(plan);
+    scc::check_bias(p, bias, "bias");
+    if (stride != 1 && stride != 2) {
+      scc::fail(SCC_ERR_ARGUMENT, "depthwise stride must be 1 or 2, got " + std::to_string(stride));
+    }
+    const int64_t ho = (h - 1) / stride + 1, wo = (w - 1) / stride + 1;
+    if (n * p.cfg.c_in * h * w >= (int64_t(1) << 31) || n * ho * wo >= (int64_t(1) << 31)) {
+      scc::fail(SCC_ERR_SHAPE, "dsc forward: tensor too large for 32-bit plane indexing");
+    }
+    const scc::DeviceTables& t = scc::tables(p);
+    scc::BandLaunch a = scc::band_args(p, t, false, n, ho * wo, x, y, weight, bias);
+    a.dw_w = dw_weight;
+    a.dw_b = dw_bias;
+    a.dw_stride = static_cast<int32_t>(stride);
+    a.h_in = static_cast<int32_t>(h);
+    a.w_in = static_cast<int32_t>(w);
+    a.w_out = static_cast<int32_t>(wo);
+    scc::cuda_check(scc::launch_band_cc(a, static_cast<cudaStream_t>(stream)), "dsc forward launch");
+  });
+}
+
+namespace scc {
+namespace {
+DwArgs dw_args(int64_t n, int64_t c, int64_t h, int64_t w, int64_t stride) {
+  check_extents(n, h, w);
+  if (c < 1) fail(SCC_ERR_SHAPE, "depthwise channel count must be >= 1, got " + std::to_string(c));
+  if (stride != 1 && stride != 2) {
+    fail(SCC_ERR_ARGUMENT, "depthwise stride must be 1 or 2, got " + std::to_string(stride));
+  }
+  if (n * c * h * w >= (int64_t(1) << 31)) fail(SCC_ERR_SHAPE, "depthwise tensor too large (>= 2^31 elements)");
+  current_device();
+  DwArgs a;
+  a.n = n;
+  a.c = c;
+  a.h = static_cast<int32_t>(h);
+  a.w = static_cast<int32_t>(w);
+  a.ho = static_cast<int32_t>((h - 1) / stride + 1);
+  a.wo = static_cast<int32_t>((w - 1) / stride + 1);
+  a.stride = static_cast<int32_t>(stride);
+  return a;
+}
+}  // namespace
+}  // namespace scc
+
+scc_status_t scc_dw3x3_forward_f32(int64_t n, int64_t c, int64_t h, int64_t w, int64_t stride,
+                                   const float* x, const float* weight, const float* bias,
+                                   float* y, void* stream) {
+  return guard([&] {
+    scc::DwArgs a = scc::dw_args(n, c, h, w, stride);
+    scc::check_ptr(x, "x");
+    scc::check_ptr(weight, "weight");
+    scc::check_ptr(y, "y");
+    a.x = x;
+    a.wt = weight;
+    a.b = bias;
+    a.y = y;
+    scc::cuda_check(scc::launch_dw(a, 0, static_cast<cudaStream_t>(stream)), "depthwise forward launch");
+  });
+}
+
+scc_status_t scc_dw3x3_backward_data_f32(int64_t n, int64_t c, int64_t h, int64_t w,
+                                         int64_t stride, const float* dy, const float* weight,
+                                         float* dx, void* stream) {
+  return guard([&] {
+    scc::DwArgs a = scc::dw_args(n, c, h, w, stride);
+    scc::check_ptr(dy, "dy");
+    scc::check_ptr(weight, "weight");
+    scc::check_ptr(dx, "dx");
+    a.dy = dy;
+    a.wt = weight;
+    a.dx = dx;
+    scc::cuda_check(scc::launch_dw(a, 1, static_cast<cudaStream_t>(stream)),
+                    "depthwise backward-data launch");
+  });
+}
+
+scc_status_t scc_dw3x3_workspace_size(int64_t c, size_t* bytes) {
+  return guard([&] {
+    scc::check_ptr(bytes, "bytes");
+    *bytes = scc::dw_workspace_bytes(c);
+  });
+}
+
+scc_status_t scc_dw3x3_backward_weight_f32(int64_t n, int64_t c, int64_t h, int64_t w,
+                                           int64_t stride, const float* dy, const float* x,
+                                           float* dweight, float* dbias, void* workspace,
+                                           size_t workspace_bytes, void* stream) {
+  return guard([&] {
+    scc::DwArgs a = scc::dw_args(n, c, h, w, stride);
+    scc::check_ptr(dy, "dy");
+    scc::check_ptr(x, "x");
+    scc::check_ptr(dweight, "dweight");
+    if (workspace == nullptr || workspace_bytes < scc::dw_workspace_bytes(c)) {
+      scc::fail(SCC_ERR_ARGUMENT, "workspace too small: need " + std::to_string(scc::dw_workspace_bytes(c)) + " bytes");
+    }
+    a.dy = dy;
+    a.x = x;
+    a.dw = dweight;
+    a.db = dbias;
+    a.part = static_cast<float*>(workspace);
+    scc::cuda_check(scc::launch_dw(a, 2, static_cast<cudaStream_t>(stream)),
+                    "depthwise backward-weight launch");
+  });
+}
+
 scc_status_t scc_forward_host_f32(scc_plan_t* plan, int64_t n, int64_t h, int64_t w,
                                   const float* x, const float* weight, const float* bias,
                                   float* y) {

@@ -56,7 +56,47 @@ __device__ __forceinline__ int64_t pix_offset(int64_t q, int64_t plane, int64_t 
   return n * c_t * plane + p;
 }
 
-template <bool VEC>
+// Fused depthwise prologue.  A staging thread owns 4 fixed DW-output pixels
+// for the whole chunk loop, so their input offsets and 3x3 tap masks are
+// computed once (DwPix); each staged element is then 9 predicated loads and
+// 9 FMAs in the order of conv_forward_impl (bias, then taps i, j ascending,
+// reference.cpp:94-106; out-of-plane taps contribute nothing where the
+// reference multiplies an explicit 0.0, reference.cpp:67-72).
+struct DwPix {
+  int64_t base;   // element offset of (n, channel 0, iy0, ix0) in x, iy0 = oy*s - 1
+  uint32_t mask;  // bit 3i+j: tap (i, j) inside the input plane
+};
+
+__device__ __forceinline__ DwPix dw_pix(const BandLaunch& a, int64_t q, bool valid) {
+  DwPix d{0, 0u};
+  if (!valid) return d;
+  int64_t n, p;
+  pix_np(q, a.plane, n, p);
+  const int oy = static_cast<int>(p / a.w_out), ox = static_cast<int>(p - static_cast<int64_t>(oy) * a.w_out);
+  const int iy0 = oy * a.dw_stride - 1, ix0 = ox * a.dw_stride - 1;
+  d.base = n * a.c_in_t * static_cast<int64_t>(a.h_in) * a.w_in + static_cast<int64_t>(iy0) * a.w_in + ix0;
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j)
+      if (iy0 + i >= 0 && iy0 + i < a.h_in && ix0 + j >= 0 && ix0 + j < a.w_in) d.mask |= 1u << (3 * i + j);
+  return d;
+}
+
+__device__ __forceinline__ float dw_value(const BandLaunch& a, const float (&wk)[9], float b,
+                                          const float* chan, const DwPix& d) {
+  float sum = b;
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      const float v = (d.mask >> (3 * i + j)) & 1u ? __ldg(chan + d.base + i * a.w_in + j) : 0.f;
+      sum = fmaf(wk[3 * i + j], v, sum);
+    }
+  return sum;
+}
+
+template <bool VEC, bool DW = false>
 __global__ void __launch_bounds__(kThreads) band_cc_kernel(const BandLaunch a) {
   __shared__ __align__(16) float xs[KC][TQ];
   __shared__ __align__(16) float ws[kBlocksPerGroup][KC][kRowsPerBlock];
@@ -106,6 +146,11 @@ __global__ void __launch_bounds__(kThreads) band_cc_kernel(const BandLaunch a) {
       poff[e] = pval[e] ? pix_offset(qv + e, a.plane, a.c_in_t) : 0;
     }
   }
+  DwPix dwp[4];
+  if (DW) {
+#pragma unroll
+    for (int e = 0; e < 4; ++e) dwp[e] = dw_pix(a, qv + e, qv + e < qend);
+  }
   // Weight-staging role: (r, j) fixed, one entry per block of the group.
   const int wr = threadIdx.x >> 3, wj = threadIdx.x & 7;
 
@@ -115,7 +160,20 @@ __global__ void __launch_bounds__(kThreads) band_cc_kernel(const BandLaunch a) {
     for (int k = 0; k < KC / (kThreads / (TQ / 4)); ++k) {
       const int r = (threadIdx.x >> 5) + k * (kThreads / (TQ / 4));
       float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (r < kc) {
+      if (r < kc && DW) {
+        // fused dsc_block: stage DW3x3(x) rows instead of x rows; the DW
+        // output never goes to HBM (forward ring = input channels)
+        const int ch = wrap(gstart + c0 + r, a.ring);
+        const float* chan = a.in + static_cast<int64_t>(ch) * a.h_in * a.w_in;
+        float wk[9];
+#pragma unroll
+        for (int t = 0; t < 9; ++t) wk[t] = __ldg(a.dw_w + ch * 9 + t);
+        const float b = a.dw_b != nullptr ? __ldg(a.dw_b + ch) : 0.f;
+        v.x = dw_value(a, wk, b, chan, dwp[0]);
+        v.y = dw_value(a, wk, b, chan, dwp[1]);
+        v.z = dw_value(a, wk, b, chan, dwp[2]);
+        v.w = dw_value(a, wk, b, chan, dwp[3]);
+      } else if (r < kc) {
         const int pos = wrap(gstart + c0 + r, a.ring);
         const int ch = a.ring_map ? __ldg(a.ring_map + pos) : pos;
         const float* src = a.in + static_cast<int64_t>(ch) * a.plane;
@@ -420,7 +478,9 @@ cudaError_t launch_band_cc(const BandLaunch& a, cudaStream_t s) {
   const int64_t grid = tiles * a.ngrp;
   if (grid <= 0) return cudaSuccess;
   if (grid > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
-  if (a.plane % 4 == 0) {
+  if (a.dw_w != nullptr) {
+    band_cc_kernel<false, true><<<static_cast<unsigned>(grid), kThreads, 0, s>>>(a);
+  } else if (a.plane % 4 == 0) {
     band_cc_kernel<true><<<static_cast<unsigned>(grid), kThreads, 0, s>>>(a);
   } else {
     band_cc_kernel<false><<<static_cast<unsigned>(grid), kThreads, 0, s>>>(a);

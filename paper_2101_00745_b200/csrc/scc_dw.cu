@@ -1,0 +1,184 @@
+// Depthwise 3x3 stage of a dsc_block (model.cpp:213-220: groups = c, kernel
+// 3, padding 1, stride 1 or 2), sm_100a CUDA-core kernels.  HBM-bound
+// (9 MACs per output element): thread per element, taps through L1, so every
+// input element is read from HBM about once.
+//
+//   dw_fwd_kernel   y[n,c,oy,ox] = b[c] + sum_{i,j} w[c][i][j] * x[n,c,oy*s-1+i,ox*s-1+j]
+//                   (conv_forward_impl, reference.cpp:74-123; taps i, j ascending)
+//   dw_bwd_data_kernel  dx[n,c,iy,ix] = sum_{i,j : (iy+1-i)%s==0, (ix+1-j)%s==0}
+//                   w[c][i][j] * dy[n,c,(iy+1-i)/s,(ix+1-j)/s]
+//   dw_bwd_weight_kernel + dw_bwd_weight_finalize
+//                   dw[c][i][j] = sum_{n,oy,ox} dy * x[...tap...], db[c] = sum dy:
+//                   per (c, sample slice) partials in a fixed order, then a fixed
+//                   order sum over slices (deterministic, no atomics).
+#include <algorithm>
+
+#include "scc_kernels.hpp"
+
+namespace scc {
+namespace {
+
+constexpr int kDwThreads = 256;
+constexpr int kDwMaxSlices = 32;  // sample slices of the weight gradient
+
+// Thread per output element, straight from global memory: neighbouring
+// threads read neighbouring pixels, so the 9 taps of a warp hit the same few
+// L1 lines and every input element comes from HBM about once.  The stride is
+// a template parameter so the tap arithmetic has no runtime division.
+// The host guarantees n*c*h*w < 2^31 (32-bit index math: a 64-bit division
+// per element cost more than the element's memory traffic).
+template <int S>
+__global__ void __launch_bounds__(kDwThreads) dw_fwd_kernel(DwArgs a) {
+  const int hi = a.h, wi = a.w, ho = a.ho, wo = a.wo;
+  const uint32_t plane = static_cast<uint32_t>(ho * wo), nc = static_cast<uint32_t>(a.c);
+  const uint32_t total = static_cast<uint32_t>(a.n * a.c) * plane;
+  for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
+    const uint32_t pl = e / plane;
+    const int o = static_cast<int>(e - pl * plane);
+    const int c = static_cast<int>(pl % nc);
+    const int oy = o / wo, ox = o - oy * wo;
+    const float* src = a.x + static_cast<size_t>(pl) * hi * wi;
+    const float* wk = a.wt + c * 9;
+    float sum = a.b != nullptr ? __ldg(a.b + c) : 0.f;
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      const int iy = oy * S - 1 + i;
+#pragma unroll
+      for (int j = 0; j < 3; ++j) {
+        const int ix = ox * S - 1 + j;
+        const float v = (iy >= 0 && iy < hi && ix >= 0 && ix < wi) ? __ldg(src + iy * wi + ix) : 0.f;
+        sum = fmaf(__ldg(wk + 3 * i + j), v, sum);
+      }
+    }
+    a.y[e] = sum;
+  }
+}
+
+// Thread per input element: dx[iy, ix] gathers the outputs whose taps cover
+// it (oy*S - 1 + i == iy), taps i, j ascending.
+template <int S>
+__global__ void __launch_bounds__(kDwThreads) dw_bwd_data_kernel(DwArgs a) {
+  const int hi = a.h, wi = a.w, ho = a.ho, wo = a.wo;
+  const uint32_t plane = static_cast<uint32_t>(hi * wi), nc = static_cast<uint32_t>(a.c);
+  const uint32_t total = static_cast<uint32_t>(a.n * a.c) * plane;
+  for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
+    const uint32_t pl = e / plane;
+    const int q = static_cast<int>(e - pl * plane);
+    const int c = static_cast<int>(pl % nc);
+    const int iy = q / wi, ix = q - iy * wi;
+    const float* src = a.dy + static_cast<size_t>(pl) * ho * wo;
+    const float* wk = a.wt + c * 9;
+    float sum = 0.f;
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      const int ty = iy + 1 - i;
+      if (ty < 0 || ty % S != 0 || ty / S >= ho) continue;
+#pragma unroll
+      for (int j = 0; j < 3; ++j) {
+        const int tx = ix + 1 - j;
+        if (tx < 0 || tx % S != 0 || tx / S >= wo) continue;
+        sum = fmaf(__ldg(wk + 3 * i + j), __ldg(src + (ty / S) * wo + tx / S), sum);
+      }
+    }
+    a.dx[e] = sum;
+  }
+}
+
+// Block (c, slice): samples n = slice, slice + S, ... ascending, pixels
+// strided by the block; then a fixed shuffle tree and fixed warp order.
+template <int S>
+__global__ void __launch_bounds__(kDwThreads) dw_bwd_weight_kernel(DwArgs a) {
+  const int hi = a.h, wi = a.w, ho = a.ho, wo = a.wo;
+  const int c = blockIdx.x, slice = blockIdx.y;
+  float acc[10];
+#pragma unroll
+  for (int t = 0; t < 10; ++t) acc[t] = 0.f;
+  // flattened (sample of the slice, pixel) index, so small planes keep every
+  // thread busy; the per-thread order is fixed by the shape
+  const int P = ho * wo;
+  const int cnt = static_cast<int>((a.n - slice + gridDim.y - 1) / gridDim.y);
+  for (int k = threadIdx.x; k < cnt * P; k += blockDim.x) {
+    const int kn = k / P, o = k - kn * P;
+    const int64_t n = slice + static_cast<int64_t>(kn) * gridDim.y;
+    const float* xp = a.x + (n * a.c + c) * hi * wi;
+    const float* gp = a.dy + (n * a.c + c) * ho * wo;
+    {
+      const int oy = o / wo, ox = o - oy * wo;
+      const float g = __ldg(gp + o);
+      acc[9] += g;
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        const int iy = oy * S - 1 + i;
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+          const int ix = ox * S - 1 + j;
+          if (iy >= 0 && iy < hi && ix >= 0 && ix < wi) acc[3 * i + j] = fmaf(g, __ldg(xp + iy * wi + ix), acc[3 * i + j]);
+        }
+      }
+    }
+  }
+  __shared__ float red[kDwThreads / 32][10];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int t = 0; t < 10; ++t) {
+    float v = acc[t];
+#pragma unroll
+    for (int m = 16; m >= 1; m >>= 1) v += __shfl_xor_sync(0xffffffffu, v, m);
+    if (lane == 0) red[warp][t] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < 10) {
+    float v = 0.f;
+    for (int w = 0; w < kDwThreads / 32; ++w) v += red[w][threadIdx.x];
+    a.part[(static_cast<int64_t>(c) * gridDim.y + slice) * 10 + threadIdx.x] = v;
+  }
+}
+
+__global__ void dw_bwd_weight_finalize(DwArgs a, int slices) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= a.c * 10) return;
+  const int c = i / 10, t = i - c * 10;
+  float v = 0.f;
+  for (int s = 0; s < slices; ++s) v += a.part[(static_cast<int64_t>(c) * slices + s) * 10 + t];
+  if (t < 9) a.dw[c * 9 + t] = v;
+  else if (a.db != nullptr) a.db[c] = v;
+}
+
+int dw_grid(int64_t elements) {
+  return static_cast<int>(std::min<int64_t>((elements + kDwThreads - 1) / kDwThreads, 148 * 16));
+}
+
+}  // namespace
+
+size_t dw_workspace_bytes(int64_t c) { return static_cast<size_t>(c) * kDwMaxSlices * 10 * sizeof(float); }
+
+cudaError_t launch_dw(DwArgs a, int op, cudaStream_t s) {
+  const int64_t planes = a.n * a.c;
+  if (planes <= 0) return cudaSuccess;
+  const bool s2 = a.stride == 2;
+  if (op == 0) {
+    const int g = dw_grid(planes * a.ho * a.wo);
+    if (s2) dw_fwd_kernel<2><<<g, kDwThreads, 0, s>>>(a);
+    else dw_fwd_kernel<1><<<g, kDwThreads, 0, s>>>(a);
+    note_launches(1);
+  } else if (op == 1) {
+    const int g = dw_grid(planes * a.h * a.w);
+    if (s2) dw_bwd_data_kernel<2><<<g, kDwThreads, 0, s>>>(a);
+    else dw_bwd_data_kernel<1><<<g, kDwThreads, 0, s>>>(a);
+    note_launches(1);
+  } else {
+    // enough (channel, slice) blocks to fill the chip; the slice count depends
+    // only on the shape, so the summation order is fixed per shape
+    const int64_t want = (148 * 8 + a.c - 1) / a.c;
+    const int slices = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>({want, a.n, kDwMaxSlices})));
+    dim3 grid(static_cast<unsigned>(a.c), static_cast<unsigned>(slices));
+    if (s2) dw_bwd_weight_kernel<2><<<grid, kDwThreads, 0, s>>>(a);
+    else dw_bwd_weight_kernel<1><<<grid, kDwThreads, 0, s>>>(a);
+    const int fb = static_cast<int>((a.c * 10 + 255) / 256);
+    dw_bwd_weight_finalize<<<fb, 256, 0, s>>>(a, slices);
+    note_launches(2);
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace scc

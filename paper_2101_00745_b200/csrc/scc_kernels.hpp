@@ -26,6 +26,13 @@ struct BandLaunch {
   int64_t shift;
   int64_t n, plane;         // batch, H*W
   bool backward_data;       // weight lookup orientation
+  // Fused depthwise prologue (dsc_block, model.cpp:213-220): when dw_w is set
+  // the staged "input" rows are DW3x3(x) computed on the fly from x of
+  // [N][c_in][h_in][w_in] (stride dw_stride, padding 1); `plane` is then the
+  // DW output plane h_out * w_out.
+  const float* dw_w = nullptr;  // [c_in][3][3]
+  const float* dw_b = nullptr;  // [c_in] or nullptr
+  int32_t dw_stride = 1, h_in = 0, w_in = 0, w_out = 0;
 };
 
 struct WeightLaunch {
@@ -135,5 +142,24 @@ bool tc_bwd_supported(const TcWeightPlan& tw, int64_t plane, int32_t c_in, int32
 size_t tc_bwd_workspace_bytes(int32_t c_out, int32_t gw, int64_t n, int64_t plane);
 cudaError_t launch_tc_bwd(const TcWeightPlan& tw, const TcBwdCall& call, cudaStream_t s);
 int tc_bwd_trace(unsigned long long* out, int n);
+
+// Depthwise 3x3 stage of a dsc_block (scc_dw.cu).  op 0 forward, 1
+// backward-data, 2 backward-weight (+ bias; part = workspace partials).
+struct DwArgs {
+  const float* x = nullptr;   // [n][c][h][w]
+  const float* wt = nullptr;  // [c][3][3]
+  const float* b = nullptr;   // [c] or nullptr (forward)
+  float* y = nullptr;         // [n][c][ho][wo]
+  const float* dy = nullptr;  // [n][c][ho][wo]
+  float* dx = nullptr;        // [n][c][h][w]
+  float* dw = nullptr;        // [c][3][3]
+  float* db = nullptr;        // [c] or nullptr
+  float* part = nullptr;      // workspace
+  int64_t n = 0, c = 0;
+  int32_t h = 0, w = 0, ho = 0, wo = 0, stride = 1;
+  int32_t staged = 0;
+};
+size_t dw_workspace_bytes(int64_t c);
+cudaError_t launch_dw(DwArgs a, int op, cudaStream_t s);
 
 }  // namespace scc

@@ -10,8 +10,9 @@ parameter counts:
     every 3x3 conv except the stem -> DW3x3(stride s) + SCC(cg=2, co=50%),
     1x1 shortcut convs stay dense, BN + ReLU after the SCC.
 
-The SCC layers run the libscc_b200 kernels (``SCC2d``); depthwise convs, BN,
-pooling and the head are stock PyTorch (library ops on the non-hot path).
+The DW3x3 + SCC pairs run the libscc_b200 kernels (``DSC2d``: depthwise
+kernels of scc_dw.cu, SCC tensor-core kernels); BN, pooling, the stem, 1x1
+shortcuts and the head are stock PyTorch (library ops off the hot path).
 The DW -> SCC pair keeps the reference's ordering (no BN between them), which
 is what a fused DW+SCC kernel needs.
 """
@@ -22,19 +23,16 @@ from typing import List
 import torch
 from torch import nn
 
-from .module import SCC2d
+from .module import DSC2d, SCC2d
 
 
-class DSC(nn.Module):
-    """dsc_block (model.cpp:213-220): depthwise 3x3 (stride s) then SCC."""
+class DSC(DSC2d):
+    """dsc_block (model.cpp:213-220): depthwise 3x3 (stride s) then SCC, both
+    stages on the libscc_b200 kernels (module.DSC2d; no bias on either stage,
+    BN follows)."""
 
     def __init__(self, cin: int, cout: int, stride: int = 1, cg: int = 2, co="50%", device=None):
-        super().__init__()
-        self.dw = nn.Conv2d(cin, cin, 3, stride=stride, padding=1, groups=cin, bias=False, device=device)
-        self.scc = SCC2d(cin, cout, cg, co, bias=False, device=device)
-
-    def forward(self, x):
-        return self.scc(self.dw(x))
+        super().__init__(cin, cout, stride, cg, co, dw_bias=False, bias=False, fused=False, device=device)
 
 
 class BasicBlock(nn.Module):
@@ -105,10 +103,11 @@ MODELS = {"resnet18": SCCResNet18, "vgg16": SCCVGG16}
 
 
 def scc_layers(model: nn.Module):
-    return [m for m in model.modules() if isinstance(m, SCC2d)]
+    """Every SCC stage (standalone SCC2d or the SCC half of a DSC2d block)."""
+    return [m for m in model.modules() if isinstance(m, (SCC2d, DSC2d))]
 
 
 def param_counts(model: nn.Module):
-    scc = sum(p.numel() for m in scc_layers(model) for p in m.parameters())
+    scc = sum(m.weight.numel() + (m.bias.numel() if m.bias is not None else 0) for m in scc_layers(model))
     total = sum(p.numel() for p in model.parameters())
     return {"total": total, "scc": scc}

@@ -275,6 +275,79 @@ def scc_forward(input: torch.Tensor, wts: SccWeights, cfg: SccConfig) -> torch.T
     return y
 
 
+def dsc_forward(input: torch.Tensor, dw_weight: torch.Tensor, dw_bias: Optional[torch.Tensor],
+                wts: SccWeights, cfg: SccConfig, stride: int = 1) -> torch.Tensor:
+    """Fused dsc_block forward (model.cpp:213-220): SCC(DW3x3(input)), the
+    depthwise output computed inside the SCC kernel (never written to HBM).
+    dw_weight: [c_in, 3, 3] (or [c_in, 1, 3, 3]); dw_bias: [c_in] or None;
+    padding 1, stride 1 or 2 (conv_forward_impl, reference.cpp:74-123)."""
+    x = _dev4(input, "input")
+    if x.shape[1] != cfg.c_in:
+        raise ShapeError(f"input has {x.shape[1]} channels, config expects {cfg.c_in}")
+    if dw_weight.numel() != cfg.c_in * 9:
+        raise ShapeError(f"depthwise weight has {dw_weight.numel()} entries, needs {cfg.c_in * 9}")
+    if dw_bias is not None and dw_bias.numel() != cfg.c_in:
+        raise ShapeError(f"depthwise bias has {dw_bias.numel()} entries, needs {cfg.c_in}")
+    _check_weights(wts, cfg)
+    n, _, h, w = x.shape
+    ho, wo = (h - 1) // stride + 1, (w - 1) // stride + 1
+    y = torch.empty((n, cfg.c_out, ho, wo), dtype=torch.float32, device=x.device)
+    dww = dw_weight.contiguous().float()
+    dwb = dw_bias.contiguous().float() if dw_bias is not None else None
+    wt = wts.weight.contiguous()
+    b = wts.bias.contiguous() if wts.bias is not None else None
+    check(lib().scc_dsc_forward_f32(cfg.handle, n, h, w, stride, x.data_ptr(), dww.data_ptr(),
+                                    _ptr(dwb), wt.data_ptr(), _ptr(b), y.data_ptr(), _stream(x)))
+    return y
+
+
+def _dw_out(h: int, w: int, stride: int):
+    return (h - 1) // stride + 1, (w - 1) // stride + 1
+
+
+def dw3x3_forward(x: torch.Tensor, weight: torch.Tensor, bias: Optional[torch.Tensor],
+                  stride: int = 1) -> torch.Tensor:
+    """Depthwise 3x3 stage of a dsc_block (groups = c, padding 1;
+    conv_forward_impl, reference.cpp:74-123) on the B200 kernels."""
+    x = _dev4(x, "input")
+    n, c, h, w = x.shape
+    if weight.numel() != c * 9:
+        raise ShapeError(f"depthwise weight has {weight.numel()} entries, needs {c * 9}")
+    ho, wo = _dw_out(h, w, stride)
+    y = torch.empty((n, c, ho, wo), dtype=torch.float32, device=x.device)
+    wt = weight.contiguous()
+    b = bias.contiguous() if bias is not None else None
+    check(lib().scc_dw3x3_forward_f32(n, c, h, w, stride, x.data_ptr(), wt.data_ptr(), _ptr(b),
+                                      y.data_ptr(), _stream(x)))
+    return y
+
+
+def dw3x3_backward_data(grad_out: torch.Tensor, weight: torch.Tensor, in_hw, stride: int = 1) -> torch.Tensor:
+    g = _dev4(grad_out, "grad_out")
+    n, c, _, _ = g.shape
+    h, w = in_hw
+    dx = torch.empty((n, c, h, w), dtype=torch.float32, device=g.device)
+    wt = weight.contiguous()
+    check(lib().scc_dw3x3_backward_data_f32(n, c, h, w, stride, g.data_ptr(), wt.data_ptr(),
+                                            dx.data_ptr(), _stream(g)))
+    return dx
+
+
+def dw3x3_backward_weight(grad_out: torch.Tensor, x: torch.Tensor, stride: int = 1,
+                          with_bias: bool = False):
+    g, x = _dev4(grad_out, "grad_out"), _dev4(x, "input")
+    n, c, h, w = x.shape
+    dw = torch.empty((c, 3, 3), dtype=torch.float32, device=x.device)
+    db = torch.empty(c, dtype=torch.float32, device=x.device) if with_bias else None
+    nb = C.c_size_t()
+    check(lib().scc_dw3x3_workspace_size(c, C.byref(nb)))
+    ws = torch.empty(max(nb.value, 4), dtype=torch.uint8, device=x.device)
+    check(lib().scc_dw3x3_backward_weight_f32(n, c, h, w, stride, g.data_ptr(), x.data_ptr(),
+                                              dw.data_ptr(), _ptr(db), ws.data_ptr(), ws.numel(),
+                                              _stream(x)))
+    return dw, db
+
+
 def scc_backward_input(grad_out: torch.Tensor, wts: SccWeights, cfg: SccConfig) -> torch.Tensor:
     """scc_backward_input (kernel.hpp:56-61)."""
     g = _dev4(grad_out, "grad_out")

@@ -1,0 +1,162 @@
+"""Fused dsc_block (model.cpp:213-220: depthwise 3x3 then SCC) on the B200.
+
+Forward: scc_dsc_forward_f32 against the CPU oracle composition
+port.dw_forward (restating reference.cpp:74-123, pinned to the compiled
+reference in test_oracle.py) -> port.forward (kernel.cpp:29-69), fp64 on the
+same fp32 inputs, norm-relative <= 1e-5.  Backward (DSC2d autograd): against
+float64 torch autograd of the same composition (depthwise conv + the SCC
+band as a dense 1x1 conv), <= 1e-4."""
+import numpy as np
+import pytest
+
+from conftest import norm_rel
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+FWD_TOL = 1e-5
+GRAD_TOL = 1e-4
+
+CASES = [  # c_in, c_out, cg, co, n, h, w, stride, dw_bias, bias
+    (64, 128, 2, "50%", 2, 8, 8, 1, False, True),
+    (64, 128, 2, "50%", 3, 9, 9, 2, True, True),
+    (48, 80, 3, 1, 2, 7, 5, 1, True, False),
+    (32, 32, 4, "25%", 1, 1, 1, 1, False, True),
+    (16, 24, 2, "75%", 2, 6, 6, 2, False, False),
+    (128, 256, 2, "50%", 2, 16, 16, 2, False, True),
+]
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    torch.cuda.set_device(0)
+
+
+def _problem(case, seed=0):
+    ci, co, cg, ov, n, h, w, s, dwb, hb = case
+    rng = np.random.default_rng(seed)
+    x = rng.standard_normal((n, ci, h, w)).astype(np.float32)
+    dww = rng.uniform(-1 / 3, 1 / 3, (ci, 3, 3)).astype(np.float32)
+    dwbias = rng.uniform(-0.5, 0.5, ci).astype(np.float32) if dwb else None
+    return x, dww, dwbias
+
+
+@pytest.mark.parametrize("case", CASES, ids=lambda c: f"{c[0]}-{c[1]}-cg{c[2]}-{c[3]}-{c[5]}x{c[6]}-s{c[7]}")
+def test_fused_forward_matches_oracle(port, case):
+    import paper_2101_00745_b200 as scc
+    ci, co, cg, ov, n, h, w, s, dwb, hb = case
+    cfg = scc.scc_config_new(ci, co, cg, ov if isinstance(ov, str) else scc.Overlap.channels(ov), hb)
+    x, dww, dwbias = _problem(case)
+    rng = np.random.default_rng(1)
+    gw = cfg.group_width
+    wt = rng.uniform(-(1 / gw) ** 0.5, (1 / gw) ** 0.5, co * gw).astype(np.float32)
+    b = rng.uniform(-0.5, 0.5, co).astype(np.float32) if hb else None
+    wts = scc.SccWeights(torch.from_numpy(wt).cuda(), torch.from_numpy(b).cuda() if hb else None)
+    y = scc.dsc_forward(torch.from_numpy(x).cuda(), torch.from_numpy(dww).cuda(),
+                        torch.from_numpy(dwbias).cuda() if dwb else None, wts, cfg, s)
+    t = port.dw_forward(x, dww, dwbias, 3, s)
+    o = port.config(ci, co, cg, ("ratio", float(ov[:-1]) / 100) if isinstance(ov, str) else ("channels", ov), hb)
+    ref = port.forward(o, t, wt, b)
+    assert y.shape == ref.shape
+    assert norm_rel(y.cpu().numpy(), ref) <= FWD_TOL
+    y2 = scc.dsc_forward(torch.from_numpy(x).cuda(), torch.from_numpy(dww).cuda(),
+                         torch.from_numpy(dwbias).cuda() if dwb else None, wts, cfg, s)
+    assert torch.equal(y, y2)  # deterministic
+
+
+@pytest.mark.parametrize("fused", [False, True], ids=["dw+scc", "fused"])
+@pytest.mark.parametrize("case", [CASES[0], CASES[1], CASES[2]], ids=["s1", "s2-bias", "ragged"])
+def test_dsc2d_autograd_matches_fp64(case, fused):
+    import paper_2101_00745_b200 as scc
+    ci, co, cg, ov, n, h, w, s, dwb, hb = case
+    torch.manual_seed(0)
+    layer = scc.DSC2d(ci, co, s, cg, ov if isinstance(ov, str) else scc.Overlap.channels(ov),
+                      dw_bias=dwb, bias=hb, fused=fused, device="cuda")
+    if hb:
+        with torch.no_grad():
+            layer.bias.uniform_(-0.5, 0.5)
+    x = torch.randn(n, ci, h, w, device="cuda", requires_grad=True)
+    y = layer(x)
+    gy = torch.randn_like(y)
+    y.backward(gy)
+    cfg = layer.cfg
+    # float64 reference: depthwise conv, then the SCC band as a dense 1x1 conv
+    xd = x.detach().double().cpu().requires_grad_(True)
+    dwd = layer.dw_weight.detach().double().cpu().requires_grad_(True)
+    dbd = layer.dw_bias.detach().double().cpu().requires_grad_(True) if dwb else None
+    wd = layer.weight.detach().double().cpu().requires_grad_(True)
+    bd = layer.bias.detach().double().cpu().requires_grad_(True) if hb else None
+    dense = torch.zeros(co, ci, dtype=torch.float64)
+    rows, cols, slots = [], [], []
+    for oc in range(co):
+        st = (oc * cfg.shift) % ci
+        for k in range(cfg.group_width):
+            rows.append(oc); cols.append((st + k) % ci); slots.append(oc * cfg.group_width + k)
+    dense = dense.index_put((torch.tensor(rows), torch.tensor(cols)), wd.reshape(-1)[torch.tensor(slots)])
+    t = torch.nn.functional.conv2d(xd, dwd, dbd, s, 1, 1, ci)
+    yd = torch.nn.functional.conv2d(t, dense.view(co, ci, 1, 1), bd)
+    yd.backward(gy.double().cpu())
+    assert norm_rel(y.detach().cpu().numpy(), yd.detach().numpy()) <= FWD_TOL
+    assert norm_rel(x.grad.cpu().numpy(), xd.grad.numpy()) <= GRAD_TOL
+    assert norm_rel(layer.dw_weight.grad.cpu().numpy(), dwd.grad.numpy()) <= GRAD_TOL
+    assert norm_rel(layer.weight.grad.cpu().numpy(), wd.grad.numpy()) <= GRAD_TOL
+    if dwb:
+        assert norm_rel(layer.dw_bias.grad.cpu().numpy(), dbd.grad.numpy()) <= GRAD_TOL
+    if hb:
+        assert norm_rel(layer.bias.grad.cpu().numpy(), bd.grad.numpy()) <= GRAD_TOL
+
+
+def test_dsc_argument_errors():
+    import paper_2101_00745_b200 as scc
+    cfg = scc.scc_config_new(8, 8, 2, "50%", True)
+    wts = scc.scc_weights_init(cfg)
+    x = torch.randn(1, 8, 4, 4, device="cuda")
+    dww = torch.randn(8, 3, 3, device="cuda")
+    with pytest.raises(scc.ArgumentError):
+        scc.dsc_forward(x, dww, None, wts, cfg, 3)
+    with pytest.raises(scc.ShapeError):
+        scc.dsc_forward(x, dww[:4], None, wts, cfg, 1)
+    with pytest.raises(scc.ShapeError):
+        scc.dsc_forward(torch.randn(1, 4, 4, 4, device="cuda"), dww, None, wts, cfg, 1)
+
+
+DW_SHAPES = [(2, 5, 7, 6, 1), (3, 4, 9, 9, 2), (1, 3, 1, 1, 1), (2, 8, 32, 32, 2), (1, 2, 112, 112, 1),
+             (1, 2, 111, 113, 2)]
+
+
+@pytest.mark.parametrize("shape", DW_SHAPES, ids=lambda s: f"{s[2]}x{s[3]}-s{s[4]}")
+def test_dw3x3_forward_matches_oracle(port, shape):
+    """The depthwise kernel against the C restatement of conv_forward_impl
+    (pinned bit-exact to the compiled reference in test_oracle.py), including
+    planes too large to stage in shared memory (112x112)."""
+    import paper_2101_00745_b200 as scc
+    n, c, h, w, s = shape
+    rng = np.random.default_rng(5)
+    x = rng.standard_normal((n, c, h, w)).astype(np.float32)
+    wt = rng.uniform(-1 / 3, 1 / 3, (c, 3, 3)).astype(np.float32)
+    b = rng.uniform(-0.5, 0.5, c).astype(np.float32)
+    y = scc.dw3x3_forward(torch.from_numpy(x).cuda(), torch.from_numpy(wt).cuda(), torch.from_numpy(b).cuda(), s)
+    assert norm_rel(y.cpu().numpy(), port.dw_forward(x, wt, b, 3, s)) <= FWD_TOL
+
+
+@pytest.mark.parametrize("shape", DW_SHAPES, ids=lambda s: f"{s[2]}x{s[3]}-s{s[4]}")
+def test_dw3x3_backward_matches_fp64(shape):
+    import paper_2101_00745_b200 as scc
+    n, c, h, w, s = shape
+    g = torch.Generator().manual_seed(3)
+    x = torch.randn(n, c, h, w, generator=g)
+    wt = torch.rand(c, 1, 3, 3, generator=g) - 0.5
+    b = torch.rand(c, generator=g) - 0.5
+    xd, wd, bd = (t.double().requires_grad_(True) for t in (x, wt, b))
+    yd = torch.nn.functional.conv2d(xd, wd, bd, s, 1, 1, c)
+    gy = torch.randn(yd.shape, generator=g)
+    yd.backward(gy.double())
+    dx = scc.dw3x3_backward_data(gy.cuda(), wt.cuda(), (h, w), s)
+    dw, db = scc.dw3x3_backward_weight(gy.cuda(), x.cuda(), s, True)
+    assert norm_rel(dx.cpu().numpy(), xd.grad.numpy()) <= GRAD_TOL
+    assert norm_rel(dw.cpu().numpy(), wd.grad.view(c, 3, 3).numpy()) <= GRAD_TOL
+    assert norm_rel(db.cpu().numpy(), bd.grad.numpy()) <= GRAD_TOL
+    dw2, _ = scc.dw3x3_backward_weight(gy.cuda(), x.cuda(), s, True)
+    assert torch.equal(dw, dw2)  # fixed-order reduction

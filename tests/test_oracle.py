@@ -198,3 +198,25 @@ def test_adjoint_identity_port(port):  # kernel_test.cpp:172-207
         lhs = float(np.sum(g * port.forward(cfg, x, w, None)))
         rhs = float(np.sum(port.backward_input(cfg, g, w) * x))
         assert norm_rel(lhs, rhs) < 1e-10
+
+
+@pytest.mark.parametrize("shape", [(2, 5, 7, 6, 3, 1), (1, 8, 8, 8, 3, 2), (3, 4, 9, 5, 3, 2),
+                                   (1, 3, 1, 1, 3, 1), (2, 6, 4, 4, 1, 1)])
+@pytest.mark.parametrize("with_bias", [True, False])
+def test_dw_port_matches_compiled_reference(port, ref, shape, with_bias):
+    """The depthwise stage of a dsc_block: the C restatement equals the
+    reference's grouped_conv_forward bit for bit (padding, stride 2, 1x1
+    planes, kernel 1)."""
+    n, c, h, w, k, s = shape
+    rng = np.random.default_rng(7)
+    x = rng.standard_normal((n, c, h, w))
+    wt = rng.uniform(-1, 1, (c, k, k))
+    b = rng.uniform(-0.5, 0.5, c) if with_bias else None
+    assert np.array_equal(port.dw_forward(x, wt, b, k, s), ref.dw_forward(x, wt, b, k, s))
+
+
+def test_dw_port_known_answer(port):
+    """All-ones 3x3 depthwise on a 3x3 plane of ones: interior 9, edges 6,
+    corners 4 (zero padding counts as explicit zeros, reference.cpp:67-72)."""
+    y = port.dw_forward(np.ones((1, 1, 3, 3)), np.ones((1, 3, 3)), None)
+    assert y[0, 0].tolist() == [[4, 6, 4], [6, 9, 6], [4, 6, 4]]
