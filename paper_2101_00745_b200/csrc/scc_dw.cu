@@ -25,10 +25,58 @@ constexpr int kDwMaxSlices = 32;  // sample slices of the weight gradient
 // threads read neighbouring pixels, so the 9 taps of a warp hit the same few
 // L1 lines and every input element comes from HBM about once.  The stride is
 // a template parameter so the tap arithmetic has no runtime division.
-// The host guarantees n*c*h*w < 2^31 (32-bit index math: a 64-bit division
-// per element cost more than the element's memory traffic).
-template <int S>
+// Thread per 4 consecutive outputs of a row: the 3 x ((4-1)*S + 3) input
+// window is loaded once into registers and reused by the 4 outputs (18 loads
+// instead of 36 at stride 1).  The host guarantees n*c*h*w < 2^31, so index
+// math is 32-bit (a 64-bit division per element cost more than its traffic).
+// FLIP: the 3x3 taps reversed -- at stride 1 backward-data is exactly this
+// kernel applied to dy (dx[iy,ix] = sum w[i][j] dy[iy+1-i, ix+1-j]).
+template <int S, bool FLIP = false>
 __global__ void __launch_bounds__(kDwThreads) dw_fwd_kernel(DwArgs a) {
+  constexpr int V = 4, NW = (V - 1) * S + 3;
+  const int hi = a.h, wi = a.w, ho = a.ho, wo = a.wo;
+  const int wq = (wo + V - 1) / V;  // 4-wide groups per output row
+  const uint32_t rows = static_cast<uint32_t>(a.n * a.c) * ho, nc = static_cast<uint32_t>(a.c);
+  const uint32_t total = rows * wq;
+  for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
+    const uint32_t r = e / wq;
+    const int ox0 = static_cast<int>(e - r * wq) * V;
+    const uint32_t pl = r / ho;
+    const int oy = static_cast<int>(r - pl * ho);
+    const int c = static_cast<int>(pl % nc);
+    const float* src = a.x + static_cast<size_t>(pl) * hi * wi;
+    float wk[9];
+#pragma unroll
+    for (int t = 0; t < 9; ++t) wk[t] = __ldg(a.wt + c * 9 + (FLIP ? 8 - t : t));
+    const float b = a.b != nullptr ? __ldg(a.b + c) : 0.f;
+    float out[V];
+#pragma unroll
+    for (int v = 0; v < V; ++v) out[v] = b;
+    const int ix0 = ox0 * S - 1;
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      const int iy = oy * S - 1 + i;
+      float win[NW];
+#pragma unroll
+      for (int k = 0; k < NW; ++k) {
+        const int ix = ix0 + k;
+        win[k] = (iy >= 0 && iy < hi && ix >= 0 && ix < wi) ? __ldg(src + iy * wi + ix) : 0.f;
+      }
+#pragma unroll
+      for (int v = 0; v < V; ++v)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) out[v] = fmaf(wk[3 * i + j], win[v * S + j], out[v]);
+    }
+    float* dst = a.y + static_cast<size_t>(r) * wo + ox0;
+#pragma unroll
+    for (int v = 0; v < V; ++v)
+      if (ox0 + v < wo) dst[v] = out[v];
+  }
+}
+
+// Stride 2: thread per output element (the 4-wide register window measured
+// slower there: the strided window doubles its loads and the rows are short).
+__global__ void __launch_bounds__(kDwThreads) dw_fwd_s2_kernel(DwArgs a) {
   const int hi = a.h, wi = a.w, ho = a.ho, wo = a.wo;
   const uint32_t plane = static_cast<uint32_t>(ho * wo), nc = static_cast<uint32_t>(a.c);
   const uint32_t total = static_cast<uint32_t>(a.n * a.c) * plane;
@@ -42,10 +90,10 @@ __global__ void __launch_bounds__(kDwThreads) dw_fwd_kernel(DwArgs a) {
     float sum = a.b != nullptr ? __ldg(a.b + c) : 0.f;
 #pragma unroll
     for (int i = 0; i < 3; ++i) {
-      const int iy = oy * S - 1 + i;
+      const int iy = oy * 2 - 1 + i;
 #pragma unroll
       for (int j = 0; j < 3; ++j) {
-        const int ix = ox * S - 1 + j;
+        const int ix = ox * 2 - 1 + j;
         const float v = (iy >= 0 && iy < hi && ix >= 0 && ix < wi) ? __ldg(src + iy * wi + ix) : 0.f;
         sum = fmaf(__ldg(wk + 3 * i + j), v, sum);
       }
@@ -157,14 +205,19 @@ cudaError_t launch_dw(DwArgs a, int op, cudaStream_t s) {
   if (planes <= 0) return cudaSuccess;
   const bool s2 = a.stride == 2;
   if (op == 0) {
-    const int g = dw_grid(planes * a.ho * a.wo);
-    if (s2) dw_fwd_kernel<2><<<g, kDwThreads, 0, s>>>(a);
-    else dw_fwd_kernel<1><<<g, kDwThreads, 0, s>>>(a);
+    if (s2) dw_fwd_s2_kernel<<<dw_grid(planes * a.ho * a.wo), kDwThreads, 0, s>>>(a);
+    else dw_fwd_kernel<1><<<dw_grid(planes * a.ho * ((a.wo + 3) / 4)), kDwThreads, 0, s>>>(a);
     note_launches(1);
   } else if (op == 1) {
-    const int g = dw_grid(planes * a.h * a.w);
-    if (s2) dw_bwd_data_kernel<2><<<g, kDwThreads, 0, s>>>(a);
-    else dw_bwd_data_kernel<1><<<g, kDwThreads, 0, s>>>(a);
+    if (s2) {
+      dw_bwd_data_kernel<2><<<dw_grid(planes * a.h * a.w), kDwThreads, 0, s>>>(a);
+    } else {
+      DwArgs f = a;  // stride 1: the flipped-tap forward over dy
+      f.x = a.dy;
+      f.y = a.dx;
+      f.b = nullptr;
+      dw_fwd_kernel<1, true><<<dw_grid(planes * a.ho * ((a.wo + 3) / 4)), kDwThreads, 0, s>>>(f);
+    }
     note_launches(1);
   } else {
     // enough (channel, slice) blocks to fill the chip; the slice count depends
