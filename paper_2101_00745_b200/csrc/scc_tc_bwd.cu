@@ -668,11 +668,14 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 // Fixed-order reduction of the per-slice partials, PDL-chained behind the main
 // kernel (its CTAs launch while the main kernel runs and wait for it).  Block
-// = 32 consecutive partial elements; warp w sums slices w, w+8, ... in order
-// (each load a coalesced 128 B row piece), then warp 0 adds the 8 warp sums
-// in order.  Bitwise reproducible.
-__global__ void __launch_bounds__(256) tc_bwd_reduce(const __grid_constant__ BArgs a) {
-  __shared__ float red[8][33];
+// = 32 consecutive partial elements x 16 warps; warp w sums slices w, w+16,
+// ... in order (each load a coalesced 128 B row piece; <= 10 loads per thread,
+// all in flight at once -- 8 warps with 19 dependent-register loads each ran
+// latency bound at 0.17 eligible warps), then warp 0 adds the 16 warp sums in
+// order.  Bitwise reproducible.
+constexpr int kRedWarps = 16;  // 512 threads x 32 regs: still resident next to a main CTA (118 regs x 384)
+__global__ void __launch_bounds__(32 * kRedWarps) tc_bwd_reduce(const __grid_constant__ BArgs a) {
+  __shared__ float red[kRedWarps][33];
   cudaGridDependencySynchronize();
   // the next kernel may start its prologue (it waits for this grid)
   cudaTriggerProgrammaticLaunchCompletion();
@@ -680,11 +683,11 @@ __global__ void __launch_bounds__(256) tc_bwd_reduce(const __grid_constant__ BAr
   const int e = blockIdx.x * 32 + l;
   float acc = 0.f;
   if (e < a.elems) {
-    constexpr int kPer = (kSlices + 7) / 8;
+    constexpr int kPer = (kSlices + kRedWarps - 1) / kRedWarps;
     float v[kPer];
 #pragma unroll
     for (int m = 0; m < kPer; ++m) {
-      const int k = w + 8 * m;
+      const int k = w + kRedWarps * m;
       v[m] = k < a.slices ? __ldcg(a.part + static_cast<int64_t>(k) * a.elems + e) : 0.f;
     }
 #pragma unroll
@@ -695,7 +698,7 @@ __global__ void __launch_bounds__(256) tc_bwd_reduce(const __grid_constant__ BAr
   if (w == 0 && e < a.elems) {
     float t = red[0][l];
 #pragma unroll
-    for (int q = 1; q < 8; ++q) t += red[q][l];
+    for (int q = 1; q < kRedWarps; ++q) t += red[q][l];
     const int nw = a.c_out * a.gw;
     if (e < nw) {
       const int i = e / a.gw;
@@ -842,7 +845,7 @@ cudaError_t launch_tc_bwd(const TcWeightPlan& tw, const TcBwdCall& call, cudaStr
   if (a.do_dw) {
     cudaLaunchConfig_t rc{};
     rc.gridDim = dim3(static_cast<unsigned>((a.elems + 31) / 32));
-    rc.blockDim = dim3(256);
+    rc.blockDim = dim3(32 * kRedWarps);
     rc.stream = s;
     rc.attrs = attr;
     rc.numAttrs = 1;
