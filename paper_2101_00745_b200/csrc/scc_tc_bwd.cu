@@ -668,12 +668,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 // Fixed-order reduction of the per-slice partials, PDL-chained behind the main
 // kernel (its CTAs launch while the main kernel runs and wait for it).  Block
-// = 32 consecutive partial elements x 16 warps; warp w sums slices w, w+16,
-// ... in order (each load a coalesced 128 B row piece; <= 10 loads per thread,
+// = 32 consecutive partial elements x 32 warps; warp w sums slices w, w+32,
+// ... in order (each load a coalesced 128 B row piece; <= 5 loads per thread,
 // all in flight at once -- 8 warps with 19 dependent-register loads each ran
-// latency bound at 0.17 eligible warps), then warp 0 adds the 16 warp sums in
+// latency bound at 0.17 eligible warps), then warp 0 adds the 32 warp sums in
 // order.  Bitwise reproducible.
-constexpr int kRedWarps = 16;  // 512 threads x 32 regs: still resident next to a main CTA (118 regs x 384)
+constexpr int kRedWarps = 32;  // 1024 threads: <= 5 in-flight loads per thread (16 warps measured 0.7 us slower)
 __global__ void __launch_bounds__(32 * kRedWarps) tc_bwd_reduce(const __grid_constant__ BArgs a) {
   __shared__ float red[kRedWarps][33];
   cudaGridDependencySynchronize();
