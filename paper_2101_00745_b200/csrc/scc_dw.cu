@@ -141,11 +141,45 @@ __global__ void __launch_bounds__(kDwThreads) dw_bwd_weight_kernel(DwArgs a) {
   float acc[10];
 #pragma unroll
   for (int t = 0; t < 10; ++t) acc[t] = 0.f;
+  const int cnt = static_cast<int>((a.n - slice + gridDim.y - 1) / gridDim.y);
+  if (S == 1) {
+    // stride 1: a thread takes 4 consecutive outputs of a row and a 3 x 6
+    // register window of x (22 loads for 40 MACs instead of 40 loads)
+    constexpr int V = 4;
+    const int wq = (wo + V - 1) / V;
+    const int per = ho * wq;
+    for (int k = threadIdx.x; k < cnt * per; k += blockDim.x) {
+      const int kn = k / per, r = k - kn * per;
+      const int oy = r / wq, ox0 = (r - oy * wq) * V;
+      const int64_t n = slice + static_cast<int64_t>(kn) * gridDim.y;
+      const float* xp = a.x + (n * a.c + c) * hi * wi;
+      const float* gp = a.dy + (n * a.c + c) * ho * wo + oy * wo;
+      float g[V];
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        g[v] = ox0 + v < wo ? __ldg(gp + ox0 + v) : 0.f;
+        acc[9] += g[v];
+      }
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        const int iy = oy - 1 + i;
+        float win[V + 2];
+#pragma unroll
+        for (int q = 0; q < V + 2; ++q) {
+          const int ix = ox0 - 1 + q;
+          win[q] = (iy >= 0 && iy < hi && ix >= 0 && ix < wi) ? __ldg(xp + iy * wi + ix) : 0.f;
+        }
+#pragma unroll
+        for (int j = 0; j < 3; ++j)
+#pragma unroll
+          for (int v = 0; v < V; ++v) acc[3 * i + j] = fmaf(g[v], win[v + j], acc[3 * i + j]);
+      }
+    }
+  }
   // flattened (sample of the slice, pixel) index, so small planes keep every
   // thread busy; the per-thread order is fixed by the shape
   const int P = ho * wo;
-  const int cnt = static_cast<int>((a.n - slice + gridDim.y - 1) / gridDim.y);
-  for (int k = threadIdx.x; k < cnt * P; k += blockDim.x) {
+  for (int k = threadIdx.x; S != 1 && k < cnt * P; k += blockDim.x) {
     const int kn = k / P, o = k - kn * P;
     const int64_t n = slice + static_cast<int64_t>(kn) * gridDim.y;
     const float* xp = a.x + (n * a.c + c) * hi * wi;
