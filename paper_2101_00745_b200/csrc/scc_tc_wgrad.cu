@@ -385,40 +385,37 @@ __global__ void __launch_bounds__(256) tc_weight_finalize_wide(const FArgs a) {
   }
 }
 
-// Warp per output (few outputs, many splits): lane l sums splits l, l+32, ...
-// in order, then a fixed butterfly combines the lanes.
-__global__ void __launch_bounds__(256) tc_weight_finalize(const FArgs a) {
+// Few outputs, many splits: block = 32 consecutive outputs x 32 warps; warp w
+// sums splits w, w+32, ... in order (each load a coalesced row piece of one
+// split plane -- the former warp-per-output scheme touched 32 split planes per
+// load, ~8x the sectors), then warp 0 adds the 32 warp sums in order.
+constexpr int kFinWarps = 32;
+__global__ void __launch_bounds__(32 * kFinWarps) tc_weight_finalize(const FArgs a) {
+  __shared__ float red[kFinWarps][33];
   const int64_t nw_out = static_cast<int64_t>(a.c_out) * a.gw;
   const int64_t total = nw_out + (a.dbias ? a.c_out : 0);
-  const int lane = threadIdx.x & 31;
-  const int64_t warps = static_cast<int64_t>(gridDim.x) * (blockDim.x / 32);
-  for (int64_t o = blockIdx.x * static_cast<int64_t>(blockDim.x / 32) + (threadIdx.x >> 5); o < total;
-       o += warps) {
-    float s = 0.f;
-    if (o < nw_out) {
-      const int oc = static_cast<int>(o / a.gw);
-      const int k = static_cast<int>(o - static_cast<int64_t>(oc) * a.gw);
-      const int pos = a.inv_perm[oc];
-      const int rt = pos >> 7, row = pos & 127;
-      int col = a.starts[oc] + k - a.rt_info[2 * rt];
-      while (col < 0) col += a.c_in;
-      while (col >= a.c_in) col -= a.c_in;
-      const int nc = col / a.nw, c = col - nc * a.nw;
-      const int64_t base = ((static_cast<int64_t>(rt) * a.n_nc + nc) * 128 + row) * a.nw + c;
-      const int64_t stride = static_cast<int64_t>(a.n_rt) * a.n_nc * 128 * a.nw;
-      for (int sp = lane; sp < a.splits; sp += 32) s += a.part[base + sp * stride];
-    } else {
-      const int oc = static_cast<int>(o - nw_out);
-      const int pos = a.inv_perm[oc];
-      const int rt = pos >> 7, row = pos & 127;
-      for (int sp = lane; sp < a.splits; sp += 32) s += a.pbias[(static_cast<int64_t>(sp) * a.n_rt + rt) * 128 + row];
-    }
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  const int64_t o = blockIdx.x * 32ll + l;
+  float s = 0.f;
+  if (o < nw_out) {
+    const int oc = static_cast<int>(o / a.gw);
+    const int64_t base = fin_base(a, oc, static_cast<int>(o - static_cast<int64_t>(oc) * a.gw));
+    const int64_t stride = static_cast<int64_t>(a.n_rt) * a.n_nc * 128 * a.nw;
+    for (int sp = w; sp < a.splits; sp += kFinWarps) s += a.part[base + sp * stride];
+  } else if (o < total) {
+    const int oc = static_cast<int>(o - nw_out);
+    const int pos = a.inv_perm[oc];
+    const int rt = pos >> 7, row = pos & 127;
+    for (int sp = w; sp < a.splits; sp += kFinWarps) s += a.pbias[(static_cast<int64_t>(sp) * a.n_rt + rt) * 128 + row];
+  }
+  red[w][l] = s;
+  __syncthreads();
+  if (w == 0 && o < total) {
+    float t = red[0][l];
 #pragma unroll
-    for (int m = 16; m >= 1; m >>= 1) s += __shfl_xor_sync(0xffffffffu, s, m);
-    if (lane == 0) {
-      if (o < nw_out) a.dweight[o] = s;
-      else a.dbias[o - nw_out] = s;
-    }
+    for (int q = 1; q < kFinWarps; ++q) t += red[q][l];
+    if (o < nw_out) a.dweight[o] = t;
+    else a.dbias[o - nw_out] = t;
   }
 }
 
@@ -579,8 +576,7 @@ cudaError_t launch_weight_tc(const TcWeightPlan& tw, const TcWeightCall& call, c
     const int fgrid = static_cast<int>(std::min<int64_t>((outs + 255) / 256, 148 * 8));
     tc_weight_finalize_wide<<<fgrid, 256, 0, s>>>(f);
   } else {
-    const int fgrid = static_cast<int>(std::min<int64_t>((outs + 7) / 8, 148 * 16));
-    tc_weight_finalize<<<fgrid, 256, 0, s>>>(f);
+    tc_weight_finalize<<<static_cast<unsigned>((outs + 31) / 32), 32 * kFinWarps, 0, s>>>(f);
   }
   note_launches(2);
   return cudaGetLastError();
