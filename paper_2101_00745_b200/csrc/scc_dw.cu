@@ -132,6 +132,46 @@ __global__ void __launch_bounds__(kDwThreads) dw_bwd_data_kernel(DwArgs a) {
   }
 }
 
+// Stride-2 backward-data: a thread owns a 2x2 input block (2a.., 2b..), which
+// gathers from the 2x2 output window (a.., b..): input row 2a takes tap row 1
+// of output row a, row 2a+1 takes tap row 0 of output row a+1 and tap row 2
+// of output row a (same for columns).  4 loads for 4 outputs, no divergence
+// (the per-element form branched on the parity of each lane's column).
+__global__ void __launch_bounds__(kDwThreads) dw_bwd_data_s2_kernel(DwArgs a) {
+  const int hi = a.h, wi = a.w, ho = a.ho, wo = a.wo;
+  const int bh = (hi + 1) / 2, bw = (wi + 1) / 2;
+  const uint32_t per = static_cast<uint32_t>(bh * bw), nc = static_cast<uint32_t>(a.c);
+  const uint32_t total = static_cast<uint32_t>(a.n * a.c) * per;
+  for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
+    const uint32_t pl = e / per;
+    const int q = static_cast<int>(e - pl * per);
+    const int c = static_cast<int>(pl % nc);
+    const int ya = q / bw, xb = q - ya * bw;
+    const float* gp = a.dy + static_cast<size_t>(pl) * ho * wo;
+    float w[9];
+#pragma unroll
+    for (int t = 0; t < 9; ++t) w[t] = __ldg(a.wt + c * 9 + t);
+    const bool y1 = ya + 1 < ho, x1 = xb + 1 < wo;
+    const float g00 = __ldg(gp + ya * wo + xb);
+    const float g01 = x1 ? __ldg(gp + ya * wo + xb + 1) : 0.f;
+    const float g10 = y1 ? __ldg(gp + (ya + 1) * wo + xb) : 0.f;
+    const float g11 = (y1 && x1) ? __ldg(gp + (ya + 1) * wo + xb + 1) : 0.f;
+    // taps in ascending (i, j) order per output
+    const float d00 = w[4] * g00;
+    const float d01 = fmaf(w[5], g00, w[3] * g01);
+    const float d10 = fmaf(w[7], g00, w[1] * g10);
+    const float d11 = fmaf(w[8], g00, fmaf(w[6], g01, fmaf(w[2], g10, w[0] * g11)));
+    float* dst = a.dx + static_cast<size_t>(pl) * hi * wi;
+    const int iy = 2 * ya, ix = 2 * xb;
+    dst[iy * wi + ix] = d00;
+    if (ix + 1 < wi) dst[iy * wi + ix + 1] = d01;
+    if (iy + 1 < hi) {
+      dst[(iy + 1) * wi + ix] = d10;
+      if (ix + 1 < wi) dst[(iy + 1) * wi + ix + 1] = d11;
+    }
+  }
+}
+
 // Block (c, slice): samples n = slice, slice + S, ... ascending, pixels
 // strided by the block; then a fixed shuffle tree and fixed warp order.
 template <int S>
@@ -244,7 +284,7 @@ cudaError_t launch_dw(DwArgs a, int op, cudaStream_t s) {
     note_launches(1);
   } else if (op == 1) {
     if (s2) {
-      dw_bwd_data_kernel<2><<<dw_grid(planes * a.h * a.w), kDwThreads, 0, s>>>(a);
+      dw_bwd_data_s2_kernel<<<dw_grid(planes * ((a.h + 1) / 2) * ((a.w + 1) / 2)), kDwThreads, 0, s>>>(a);
     } else {
       DwArgs f = a;  // stride 1: the flipped-tap forward over dy
       f.x = a.dy;
