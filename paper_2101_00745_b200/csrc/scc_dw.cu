@@ -25,52 +25,65 @@ constexpr int kDwMaxSlices = 32;  // sample slices of the weight gradient
 // threads read neighbouring pixels, so the 9 taps of a warp hit the same few
 // L1 lines and every input element comes from HBM about once.  The stride is
 // a template parameter so the tap arithmetic has no runtime division.
-// Thread per 4 consecutive outputs of a row: the 3 x ((4-1)*S + 3) input
-// window is loaded once into registers and reused by the 4 outputs (18 loads
-// instead of 36 at stride 1).  The host guarantees n*c*h*w < 2^31, so index
-// math is 32-bit (a 64-bit division per element cost more than its traffic).
+// Stride 1: a thread computes an R x 4 output block from an (R+2) x 6 register
+// window of the input (R=2: 24 loads for 8 outputs; per element needed 72).
+// The host guarantees n*c*h*w < 2^31, so index math is 32-bit (a 64-bit
+// division per element cost more than the element's traffic).
 // FLIP: the 3x3 taps reversed -- at stride 1 backward-data is exactly this
 // kernel applied to dy (dx[iy,ix] = sum w[i][j] dy[iy+1-i, ix+1-j]).
-template <int S, bool FLIP = false>
+// R = 2 pays on large planes (32x32: 27 -> 20 us); on small planes the halved
+// thread count costs more than the saved loads, so R = 1 there.
+template <int S, bool FLIP = false, int R = 2>
 __global__ void __launch_bounds__(kDwThreads) dw_fwd_kernel(DwArgs a) {
-  constexpr int V = 4, NW = (V - 1) * S + 3;
+  static_assert(S == 1, "the register-window kernel is stride 1");
+  constexpr int V = 4;
   const int hi = a.h, wi = a.w, ho = a.ho, wo = a.wo;
-  const int wq = (wo + V - 1) / V;  // 4-wide groups per output row
-  const uint32_t rows = static_cast<uint32_t>(a.n * a.c) * ho, nc = static_cast<uint32_t>(a.c);
-  const uint32_t total = rows * wq;
+  const int wq = (wo + V - 1) / V, hq = (ho + R - 1) / R;
+  const uint32_t per = static_cast<uint32_t>(hq * wq), nc = static_cast<uint32_t>(a.c);
+  const uint32_t total = static_cast<uint32_t>(a.n * a.c) * per;
   for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
-    const uint32_t r = e / wq;
-    const int ox0 = static_cast<int>(e - r * wq) * V;
-    const uint32_t pl = r / ho;
-    const int oy = static_cast<int>(r - pl * ho);
+    const uint32_t pl = e / per;
+    const int q = static_cast<int>(e - pl * per);
     const int c = static_cast<int>(pl % nc);
+    const int oy0 = (q / wq) * R, ox0 = (q - (q / wq) * wq) * V;
     const float* src = a.x + static_cast<size_t>(pl) * hi * wi;
     float wk[9];
 #pragma unroll
     for (int t = 0; t < 9; ++t) wk[t] = __ldg(a.wt + c * 9 + (FLIP ? 8 - t : t));
     const float b = a.b != nullptr ? __ldg(a.b + c) : 0.f;
-    float out[V];
+    float out[R][V];
 #pragma unroll
-    for (int v = 0; v < V; ++v) out[v] = b;
-    const int ix0 = ox0 * S - 1;
+    for (int r = 0; r < R; ++r)
 #pragma unroll
-    for (int i = 0; i < 3; ++i) {
-      const int iy = oy * S - 1 + i;
-      float win[NW];
+      for (int v = 0; v < V; ++v) out[r][v] = b;
 #pragma unroll
-      for (int k = 0; k < NW; ++k) {
-        const int ix = ix0 + k;
+    for (int yy = 0; yy < R + 2; ++yy) {
+      const int iy = oy0 - 1 + yy;
+      float win[V + 2];
+#pragma unroll
+      for (int k = 0; k < V + 2; ++k) {
+        const int ix = ox0 - 1 + k;
         win[k] = (iy >= 0 && iy < hi && ix >= 0 && ix < wi) ? __ldg(src + iy * wi + ix) : 0.f;
       }
+      // input row yy feeds output row r through tap row i = yy - r
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int i = yy - r;
+        if (i < 0 || i > 2) continue;
+#pragma unroll
+        for (int v = 0; v < V; ++v)
+#pragma unroll
+          for (int j = 0; j < 3; ++j) out[r][v] = fmaf(wk[3 * i + j], win[v + j], out[r][v]);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      if (oy0 + r >= ho) break;
+      float* dst = a.y + (static_cast<size_t>(pl) * ho + oy0 + r) * wo + ox0;
 #pragma unroll
       for (int v = 0; v < V; ++v)
-#pragma unroll
-        for (int j = 0; j < 3; ++j) out[v] = fmaf(wk[3 * i + j], win[v * S + j], out[v]);
+        if (ox0 + v < wo) dst[v] = out[r][v];
     }
-    float* dst = a.y + static_cast<size_t>(r) * wo + ox0;
-#pragma unroll
-    for (int v = 0; v < V; ++v)
-      if (ox0 + v < wo) dst[v] = out[v];
   }
 }
 
@@ -280,7 +293,10 @@ cudaError_t launch_dw(DwArgs a, int op, cudaStream_t s) {
   const bool s2 = a.stride == 2;
   if (op == 0) {
     if (s2) dw_fwd_s2_kernel<<<dw_grid(planes * a.ho * a.wo), kDwThreads, 0, s>>>(a);
-    else dw_fwd_kernel<1><<<dw_grid(planes * a.ho * ((a.wo + 3) / 4)), kDwThreads, 0, s>>>(a);
+    else if (a.ho * a.wo >= 1024)
+      dw_fwd_kernel<1, false, 2><<<dw_grid(planes * ((a.ho + 1) / 2) * ((a.wo + 3) / 4)), kDwThreads, 0, s>>>(a);
+    else
+      dw_fwd_kernel<1, false, 1><<<dw_grid(planes * a.ho * ((a.wo + 3) / 4)), kDwThreads, 0, s>>>(a);
     note_launches(1);
   } else if (op == 1) {
     if (s2) {
@@ -290,7 +306,10 @@ cudaError_t launch_dw(DwArgs a, int op, cudaStream_t s) {
       f.x = a.dy;
       f.y = a.dx;
       f.b = nullptr;
-      dw_fwd_kernel<1, true><<<dw_grid(planes * a.ho * ((a.wo + 3) / 4)), kDwThreads, 0, s>>>(f);
+      if (a.ho * a.wo >= 1024)
+        dw_fwd_kernel<1, true, 2><<<dw_grid(planes * ((a.ho + 1) / 2) * ((a.wo + 3) / 4)), kDwThreads, 0, s>>>(f);
+      else
+        dw_fwd_kernel<1, true, 1><<<dw_grid(planes * a.ho * ((a.wo + 3) / 4)), kDwThreads, 0, s>>>(f);
     }
     note_launches(1);
   } else {
