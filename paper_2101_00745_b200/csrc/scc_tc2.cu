@@ -119,13 +119,35 @@ struct Band2Args {
 };
 
 // Contiguous run of blocks owned by this CTA, cut into tiles of <= 4 blocks
-// that never straddle a sample.
+// that never straddle a sample.  A tile costs one pass of the load / convert /
+// MMA / store pipeline whatever its width, so when there are at least as many
+// CTAs as samples the runs are cut inside samples (each sample gets
+// floor(grid / n) or one more runs): on config 1 every CTA then has <= 2
+// tiles (7-8 blocks), where an even split of the flat block range gave 22 % of
+// the CTAs a run across a sample boundary and 3 tiles.
 struct TileIter {
   int32_t u, u1, nbps;
   int32_t n, b0, cnt;
   __device__ explicit TileIter(const Band2Args& a) {
-    // 32-bit division when the products fit (the 64-bit one is a slow call)
-    if (a.units < (1 << 22)) {
+    const int32_t ns = a.nbps > 0 ? a.units / a.nbps : 0;  // samples
+    if (ns > 0 && static_cast<int32_t>(gridDim.x) >= ns) {
+      const int32_t g = static_cast<int32_t>(gridDim.x), i = static_cast<int32_t>(blockIdx.x);
+      const int32_t base = g / ns, extra = g % ns;
+      int32_t smp, r, nr;
+      if (i < extra * (base + 1)) {
+        smp = i / (base + 1);
+        r = i - smp * (base + 1);
+        nr = base + 1;
+      } else {
+        const int32_t i2 = i - extra * (base + 1);
+        smp = extra + i2 / base;
+        r = i2 - (smp - extra) * base;
+        nr = base;
+      }
+      u = smp * a.nbps + (r * a.nbps) / nr;
+      u1 = smp * a.nbps + ((r + 1) * a.nbps) / nr;
+    } else if (a.units < (1 << 22)) {
+      // 32-bit division when the products fit (the 64-bit one is a slow call)
       u = static_cast<int32_t>((blockIdx.x * static_cast<uint32_t>(a.units)) / gridDim.x);
       u1 = static_cast<int32_t>(((blockIdx.x + 1) * static_cast<uint32_t>(a.units)) / gridDim.x);
     } else {
