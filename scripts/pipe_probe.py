@@ -37,3 +37,29 @@ for k in (1, 2, 4, 8):
         t0 = time.perf_counter()
         for _ in range(20): run(k, co_)
         print(k, "copies_only" if co_ else "with_kernels", round((time.perf_counter() - t0) / 20 * 1e3, 3), "ms", flush=True)
+
+# variant: x / dy (and y / dx) copies on separate streams (more copy engines)
+s_in2, s_out2 = torch.cuda.Stream(), torch.cuda.Stream()
+def run2(k):
+    m = n // k
+    for i in range(k):
+        sl = slice(i * m, (i + 1) * m)
+        with torch.cuda.stream(s_in):
+            xd[sl].copy_(xh[sl], non_blocking=True)
+            e = torch.cuda.Event(); e.record(s_in)
+        with torch.cuda.stream(s_in2):
+            dyd[sl].copy_(dyh[sl], non_blocking=True)
+            e1 = torch.cuda.Event(); e1.record(s_in2)
+        s_c.wait_event(e); s_c.wait_event(e1)
+        e2 = torch.cuda.Event(); e2.record(s_c)
+        s_out.wait_event(e2); s_out2.wait_event(e2)
+        with torch.cuda.stream(s_out):
+            yh[sl].copy_(yd[sl], non_blocking=True)
+        with torch.cuda.stream(s_out2):
+            dxh[sl].copy_(dxd[sl], non_blocking=True)
+    torch.cuda.synchronize()
+for k in (2, 4, 8):
+    run2(k)
+    t0 = time.perf_counter()
+    for _ in range(20): run2(k)
+    print(k, "copies_only 4 streams", round((time.perf_counter() - t0) / 20 * 1e3, 3), "ms", flush=True)
