@@ -200,6 +200,12 @@ void build_tc_side(const Plan& p, bool bwd, TcBandPlan& tp) {
       best = nt;
     }
   }
+  // gw = 64: 64-row tiles measured 2-6 % faster at 14x14 and 56x56
+  // (scripts/band_ab.py: each CTA keeps one row tile's panel resident and the
+  // band padding halves); for gw >= 256 they lose up to 40 % (every tile
+  // re-streams the wide activation arc), for gw = 32 / 128 it is shape
+  // dependent, so those keep the widest tile.
+  if (c.group_width == 64 && rows_total % 64 == 0) best = 64;
   if (const char* e = getenv("SCC_TC_NT")) {  // experiment override
     const int v = atoi(e);
     if (v == 64 || v == 128) best = v;

@@ -70,7 +70,7 @@ struct TcCfg {
 // Shared-memory plan of one launch (host computes, kernel re-derives).
 struct BandSmem {
   int a_stages;     // raw activation ring depth (16 KB each)
-  int b_resident;   // 1: whole panel in smem, loaded once
+  int b_resident;   // 1: whole panel in smem, loaded once; 2: this CTA's row tile's panel
   int b_stages;     // streamed panel ring depth
   int b_bytes;      // resident panel bytes, or one chunk image
   int total;        // dynamic smem bytes
@@ -221,10 +221,17 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                         __ldg(a.class_d + cl), tc.n * a.rows_per_sample_3d + j);
           }
           advance(sa, pa, SA);
-          if (a.sm.b_resident && t == blockIdx.x && c == 0) {
+          if (a.sm.b_resident == 1 && t == blockIdx.x && c == 0) {
             panel_ready();
             mbar_expect_tx(&b_full[0], a.panel_floats * 4);
             bulk_load(b_base, a.panel, a.panel_floats * 4, &b_full[0]);
+          } else if (a.sm.b_resident == 2 && t == blockIdx.x && c == 0) {
+            // every tile of this CTA has row tile blockIdx.x % n_rt (the grid
+            // is a multiple of n_rt): only that row tile's panel is resident
+            panel_ready();
+            const uint32_t bytes = static_cast<uint32_t>(nch) * C::kBBytes;
+            mbar_expect_tx(&b_full[0], bytes);
+            bulk_load(b_base, a.panel + a.rt_info[4 * tc.rt + 2], bytes, &b_full[0]);
           }
         }
       }
@@ -272,8 +279,10 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       for (int c = 0; c < nch; ++c) {
         mbar_wait_tag(&conv[st], ps, 5);
         uint8_t* bimg;
-        if (a.sm.b_resident) {
+        if (a.sm.b_resident == 1) {
           bimg = b_base + (a.rt_info[4 * rt + 2] + c * (C::kBBytes / 4)) * 4;
+        } else if (a.sm.b_resident == 2) {
+          bimg = b_base + c * C::kBBytes;
         } else {
           mbar_wait_tag(&b_full[sb], pb, 6);
           bimg = b_base + sb * C::kBBytes;
@@ -564,8 +573,18 @@ static cudaError_t launch_tc_nt(const TcBandPlan& tp, const TcDeviceTables& dt,
   ka.ptiles = static_cast<int32_t>((call.plane + TM - 1) / TM);
   ka.plane = call.plane;
   ka.n = call.n;
+  const int64_t tiles = call.n * ka.ptiles * tp.n_rt;
+  int nsm = 148;
+  {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  }
+  int64_t grid = std::min<int64_t>(tiles, nsm);
   // Shared memory: resident weight panel when it fits next to a >= 5-deep
-  // activation ring, else a streamed 2-deep panel ring.
+  // activation ring; else, when a grid that is a multiple of n_rt gives each
+  // CTA a single row tile, that row tile's panel resident; else a streamed
+  // panel ring on its own producer warp.
   {
     constexpr int kBudget = 227 * 1024 - 1024 /*align*/ - 2048 /*barriers + static*/;
     const int panel_bytes = static_cast<int>(tc_panel_bytes(tp));
@@ -576,23 +595,29 @@ static cudaError_t launch_tc_nt(const TcBandPlan& tp, const TcDeviceTables& dt,
       sm.b_bytes = panel_bytes;
       sm.b_stages = 1;
     } else {
-      sm.b_resident = 0;
-      sm.b_bytes = C::kBBytes;
-      sm.b_stages = 3;
-      if (const char* e = getenv("SCC_BAND_BSTAGES")) sm.b_stages = std::max(2, std::min(C::kMaxBStages, atoi(e)));
+      int max_rt = 0;
+      for (int rt = 0; rt < tp.n_rt; ++rt) max_rt = std::max(max_rt, tp.rt_info[4 * rt + 3]);
+      const int64_t grid_rt = grid / tp.n_rt * tp.n_rt;
+      const char* no_rt_env = getenv("SCC_BAND_NO_RT_PANEL");  // A/B knob
+      const bool no_rt = no_rt_env != nullptr && no_rt_env[0] == '1';
+      if (!no_rt && grid_rt >= tp.n_rt && grid_rt >= grid - grid / 16 &&
+          max_rt * C::kBBytes + 5 * kABytes <= rest) {
+        sm.b_resident = 2;
+        sm.b_bytes = max_rt * C::kBBytes;
+        sm.b_stages = 1;
+        grid = grid_rt;
+      } else {
+        sm.b_resident = 0;
+        sm.b_bytes = C::kBBytes;
+        sm.b_stages = 3;
+        if (const char* e = getenv("SCC_BAND_BSTAGES")) sm.b_stages = std::max(2, std::min(C::kMaxBStages, atoi(e)));
+      }
     }
     const int b_total = sm.b_resident ? sm.b_bytes : sm.b_stages * C::kBBytes;
     sm.a_stages = std::min(C::kMaxAStages, (rest - b_total) / kABytes);
     sm.total = sm.a_stages * kABytes + b_total + C::kStoreBytes + 1024 + 512;
   }
   ka.panel_floats = static_cast<int32_t>(tc_panel_bytes(tp) / 4);
-  const int64_t tiles = call.n * ka.ptiles * tp.n_rt;
-  int nsm = 148;
-  {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  }
   {
     static bool attr_set[64] = {false};  // per device, per template instance
     int dev = 0;
@@ -605,7 +630,7 @@ static cudaError_t launch_tc_nt(const TcBandPlan& tp, const TcDeviceTables& dt,
     }
   }
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(static_cast<unsigned>(std::min<int64_t>(tiles, nsm)));
+  cfg.gridDim = dim3(static_cast<unsigned>(grid));
   cfg.blockDim = dim3(kTcThreads);
   cfg.dynamicSmemBytes = ka.sm.total;
   cfg.stream = s;
