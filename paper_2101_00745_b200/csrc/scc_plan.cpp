@@ -200,12 +200,25 @@ void build_tc_side(const Plan& p, bool bwd, TcBandPlan& tp) {
       best = nt;
     }
   }
-  // gw = 64: 64-row tiles measured 2-6 % faster at 14x14 and 56x56
-  // (scripts/band_ab.py: each CTA keeps one row tile's panel resident and the
-  // band padding halves); for gw >= 256 they lose up to 40 % (every tile
-  // re-streams the wide activation arc), for gw = 32 / 128 it is shape
-  // dependent, so those keep the widest tile.
-  if (c.group_width == 64 && rows_total % 64 == 0) best = 64;
+  // gw = 64 with tight 64-row arcs (<= 96 ring rows, i.e. co = 50 %): 64-row
+  // tiles measured 2-10 % faster at 14x14 and 56x56 (scripts/band_ab.py: each
+  // CTA keeps one row tile's panel resident, the band padding halves).  With
+  // wider arcs (co = 25 / 75 %: more, shorter class runs) every extra
+  // activation row re-read costs more than that (measured 5-15 % slower), and
+  // for gw >= 256 they lose up to 40 %, so those keep the widest tile.
+  if (c.group_width == 64 && rows_total % 64 == 0) {
+    int32_t max_arc = 0;
+    for (int32_t t0 = 0; t0 < rows_total; t0 += 64) {
+      std::vector<Arc> arcs;
+      for (int32_t i = t0; i < std::min(t0 + 64, rows_total); ++i) {
+        arcs.push_back(bwd ? p.ic_arcs[static_cast<size_t>(i)]
+                           : Arc{static_cast<int32_t>(p.start_of(p.perm[static_cast<size_t>(i)])),
+                                 static_cast<int32_t>(c.group_width)});
+      }
+      max_arc = std::max(max_arc, cover_arcs(arcs, tp.ring).len);
+    }
+    if (max_arc <= 96) best = 64;
+  }
   if (const char* e = getenv("SCC_TC_NT")) {  // experiment override
     const int v = atoi(e);
     if (v == 64 || v == 128) best = v;
