@@ -45,6 +45,13 @@ for _c in (256, 512, 1024):
 METRIC = "SCC fwd+bwd GB/s (% HBM roofline)"
 
 
+def workload_desc(name):
+    """config.workload, identical in both arms (the driver compares them)."""
+    ci, co, cg, ov, n, h, w = WORKLOADS[name]
+    return (f"{name}: SCC layer fwd+bwd fp32 NCHW, N={n}/GPU C_in={ci} C_out={co} "
+            f"H=W={h} cg={cg} co={ov}")
+
+
 def algo_bytes(ci, co, n, h, w):
     """Compulsory fp32 bytes of fwd + bwd."""
     p = n * h * w
@@ -207,7 +214,7 @@ def run_reference_arm(args):
         "n_gpus": args.gpus, "steps": r["steps"], "warmup": args.warmup,
         "ms_per_step": round(r["ms_per_step"], 3), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{args.workload}: N={n} C_in={ci} C_out={co} H=W={h} cg={cg} co={ov}",
+        "config": {"workload": workload_desc(args.workload),
                    "device": "host CPU", "parallelism": "host threads"},
         "cpu_baseline": {"value": round(r["value"], 4), "unit": "GB/s", "cores": r["cores"],
                          "kind": r["kind"], "sample": r["sample"]},
@@ -222,12 +229,36 @@ def run_reference_arm(args):
 # our arm
 
 
+def measure_traffic(workload, timeout=240):
+    """roofline.traffic, measured in this run: scripts/traffic_probe.py under
+    ncu (dram__bytes_read + dram__bytes_write of the step's kernels, plus the
+    dirty lines they leave in L2, evicted by a read-only flush that follows).
+    A separate process: no number here is timed under the profiler."""
+    import tempfile
+    csv_path = os.path.join(tempfile.mkdtemp(prefix="scc_traffic_"), "t.csv")
+    cmd = ["ncu", "--metrics", "dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum",
+           "--clock-control", "none", "--print-units", "base", "--csv", "--log-file", csv_path,
+           sys.executable, os.path.join(ROOT, "scripts", "traffic_probe.py"), "--workload", workload]
+    try:
+        subprocess.run(cmd, stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL, timeout=timeout,
+                       env=dict(os.environ, CUDA_VISIBLE_DEVICES=os.environ.get("CUDA_VISIBLE_DEVICES", "0")))
+        sys.path.insert(0, os.path.join(ROOT, "scripts"))
+        from traffic_probe import parse
+        d = parse(csv_path)
+        d["method"] = ("ncu dram__bytes_read.sum + dram__bytes_write.sum of the phase's kernels "
+                       "+ dram__bytes_write.sum of the read-only L2 flush that follows (scripts/traffic_probe.py)")
+        return d
+    except Exception as ex:  # reported, never required
+        return {"error": f"traffic pass failed: {str(ex)[:160]}"}
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
 
     import paper_2101_00745_b200 as scc
     from paper_2101_00745_b200 import _lib
+    from paper_2101_00745_b200.dist import allreduce_grads
 
     ws, rank, local = dist_env()
     if ws > 1:
@@ -294,7 +325,9 @@ def run_ours(args):
         fwd(i)
         bwd(i)
         if ws > 1:
-            dist.all_reduce(grads)  # data-parallel exchange of dW/db (north_star)
+            # data-parallel exchange of dW|db (north_star): one flat bucket,
+            # reduced in place (dist.py, the same call train.py makes)
+            allreduce_grads([grads], average=True)
 
     def barrier():
         if ws > 1:
@@ -407,17 +440,14 @@ def run_ours(args):
         kms[name] = a.elapsed_time(b) / reps
     dominant = max(("forward", "backward"), key=kms.get)
     achieved = nbytes[dominant] / (kms[dominant] * 1e-3) / 1e9
-    traffic = None
-    prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(prof):
-        try:
-            with open(prof) as f:
-                tr = json.load(f)
-            traffic = tr.get(args.workload, {}).get(dominant)
-        except Exception:
-            traffic = None
+    traffic, traffic_detail = None, None
+    if rank == 0 and ws == 1 and not args.no_traffic:
+        traffic_detail = measure_traffic(args.workload)
+        if traffic_detail and dominant in traffic_detail:
+            traffic = int(traffic_detail[dominant]["total"])
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
                 "frac": round(achieved / hbm_peak, 4), "traffic": traffic,
+                "traffic_detail": traffic_detail,
                 "kernel": dominant, "peak_kind": peak_kind,
                 "algorithmic_bytes_per_launch": nbytes[dominant],
                 "kernel_ms": {k: round(v, 5) for k, v in kms.items()},
@@ -481,8 +511,7 @@ def run_ours(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 5),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f32", "data": "synthetic",
-            "config": {"workload": (f"{args.workload}: SCC layer fwd+bwd N={n}/GPU C_in={ci} "
-                                    f"C_out={co} H=W={h} cg={cg} co={ov} (gw={gw}, shift={cfg.shift})"),
+            "config": {"workload": workload_desc(args.workload), "gw": gw, "shift": cfg.shift,
                        "global_batch": n * ws, "parallelism": f"dp{ws}",
                        "l2": f"inputs rotate over {nsets} buffer sets "
                              f"({nsets * per_set / 2**20:.0f} MiB > 3x L2 {l2 / 2**20:.0f} MiB)",
@@ -516,6 +545,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-models", action="store_true", help="skip the SCC-ResNet-18/VGG16 images/sec")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--no-traffic", action="store_true", help="skip the ncu DRAM-traffic pass")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

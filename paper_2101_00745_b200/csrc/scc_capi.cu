@@ -297,7 +297,7 @@ void do_forward(Plan& p, int64_t n, int64_t h, int64_t w, const float* x, const 
   check_ptr(y, "y");
   check_bias(p, b, "bias");
   const DeviceTables& t = tables(p);
-  if (choose_path(p, n, h, w, 0) == SCC_PATH_TENSOR) {
+  if (aligned16(x) && aligned16(y) && choose_path(p, n, h, w, 0) == SCC_PATH_TENSOR) {
     TcBandCall c = tc_call(p, false, n, h * w, x, y, wt, b);
     if (p.path != SCC_PATH_TENSOR_V1 && tc_band2_supported(p.tc_fwd, h * w, static_cast<int32_t>(p.cfg.c_out))) {
       cuda_check(launch_band_tc2(p.tc_fwd, t.tc_fwd, c, p.cfg.shift, static_cast<int32_t>(p.cfg.c_out), s),
@@ -311,7 +311,9 @@ void do_forward(Plan& p, int64_t n, int64_t h, int64_t w, const float* x, const 
   cuda_check(launch_band_cc(band_args(p, t, false, n, h * w, x, y, wt, b), s), "forward launch");
 }
 
-bool use_fused(Plan& p, int64_t n, int64_t h, int64_t w) {
+bool use_fused(Plan& p, int64_t n, int64_t h, int64_t w, std::initializer_list<const void*> ptrs) {
+  for (const void* q : ptrs)
+    if (q != nullptr && !aligned16(q)) return false;
   return choose_path(p, n, h, w, 2) == SCC_PATH_TENSOR && fused_bwd_supported(p, h * w);
 }
 
@@ -344,12 +346,12 @@ void do_backward_data(Plan& p, int64_t n, int64_t h, int64_t w, const float* dy,
   check_ptr(dy, "dy");
   check_ptr(wt, "weight");
   check_ptr(dx, "dx");
-  if (use_fused(p, n, h, w)) {
+  if (use_fused(p, n, h, w, {dy, dx})) {
     launch_fused(p, n, h, w, dy, nullptr, wt, dx, nullptr, nullptr, nullptr, 0, s);
     return;
   }
   const DeviceTables& t = tables(p);
-  if (choose_path(p, n, h, w, 1) == SCC_PATH_TENSOR) {
+  if (aligned16(dy) && aligned16(dx) && choose_path(p, n, h, w, 1) == SCC_PATH_TENSOR) {
     TcBandCall c = tc_call(p, true, n, h * w, dy, dx, wt, nullptr);
     c.max_ctas = max_ctas;
     if (p.path != SCC_PATH_TENSOR_V1 && tc_band2_supported(p.tc_bwd, h * w, static_cast<int32_t>(p.cfg.c_out))) {
@@ -377,12 +379,12 @@ void do_backward_weight(Plan& p, int64_t n, int64_t h, int64_t w, const float* d
   if (ws_bytes < need || (need > 0 && ws == nullptr)) {
     fail(SCC_ERR_ARGUMENT, "workspace too small: need " + std::to_string(need) + " bytes");
   }
-  if (use_fused(p, n, h, w)) {
+  if (use_fused(p, n, h, w, {dy, x})) {
     launch_fused(p, n, h, w, dy, x, nullptr, nullptr, dw, db, ws, ws_bytes, s);
     return;
   }
   const DeviceTables& t = tables(p);
-  if (choose_path(p, n, h, w, 2) == SCC_PATH_TENSOR) {
+  if (aligned16(dy) && aligned16(x) && choose_path(p, n, h, w, 2) == SCC_PATH_TENSOR) {
     TcWeightCall c{};
     c.dy = dy;
     c.x = x;
@@ -441,7 +443,7 @@ void do_backward(Plan& p, int64_t n, int64_t h, int64_t w, const float* dy, cons
                  const float* wt, float* dx, float* dw, float* db, void* ws, size_t ws_bytes,
                  cudaStream_t s) {
   const int64_t plane = h * w;
-  if (use_fused(p, n, h, w)) {
+  if (use_fused(p, n, h, w, {dy, x, dx})) {
     check_extents(n, h, w);
     check_ptr(dy, "dy");
     check_ptr(x, "x");
@@ -456,7 +458,8 @@ void do_backward(Plan& p, int64_t n, int64_t h, int64_t w, const float* dy, cons
     launch_fused(p, n, h, w, dy, x, wt, dx, dw, db, ws, ws_bytes, s);
     return;
   }
-  const bool both2 = p.path != SCC_PATH_TENSOR_V1 && p.path != SCC_PATH_CUDA_CORE &&
+  const bool both2 = aligned16(dy) && aligned16(x) && aligned16(dx) &&
+                     p.path != SCC_PATH_TENSOR_V1 && p.path != SCC_PATH_CUDA_CORE &&
                      choose_path(p, n, h, w, 1) == SCC_PATH_TENSOR &&
                      choose_path(p, n, h, w, 2) == SCC_PATH_TENSOR &&
                      tc_band2_supported(p.tc_bwd, plane, static_cast<int32_t>(p.cfg.c_out)) &&

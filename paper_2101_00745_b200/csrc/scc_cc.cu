@@ -480,7 +480,7 @@ cudaError_t launch_band_cc(const BandLaunch& a, cudaStream_t s) {
   if (grid > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
   if (a.dw_w != nullptr) {
     band_cc_kernel<false, true><<<static_cast<unsigned>(grid), kThreads, 0, s>>>(a);
-  } else if (a.plane % 4 == 0) {
+  } else if (a.plane % 4 == 0 && aligned16(a.in) && aligned16(a.out)) {
     band_cc_kernel<true><<<static_cast<unsigned>(grid), kThreads, 0, s>>>(a);
   } else {
     band_cc_kernel<false><<<static_cast<unsigned>(grid), kThreads, 0, s>>>(a);
@@ -500,7 +500,7 @@ cudaError_t launch_weight_cc(const WeightLaunch& a, size_t ws_bytes, cudaStream_
   if (static_cast<size_t>(g.split_stride) * g.splits * sizeof(float) > ws_bytes)
     return cudaErrorInvalidValue;
   const int64_t grid = static_cast<int64_t>(a.nblk) * g.nkt * g.splits;
-  const bool vec = a.plane % 4 == 0;
+  const bool vec = a.plane % 4 == 0 && aligned16(a.dy) && aligned16(a.x);
   if (g.kt_size == 32) {
     if (vec) weight_cc_kernel<32, true><<<static_cast<unsigned>(grid), kThreads, 0, s>>>(a, g);
     else weight_cc_kernel<32, false><<<static_cast<unsigned>(grid), kThreads, 0, s>>>(a, g);

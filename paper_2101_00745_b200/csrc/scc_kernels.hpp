@@ -8,6 +8,10 @@
 
 namespace scc {
 
+// Vector (float4) and TMA paths need 16-byte aligned activation pointers; a
+// caller's view with an odd storage offset takes the scalar CUDA-core path.
+inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
 // Geometry + tables one band launch needs (all device pointers).
 struct BandLaunch {
   const float* in;          // [N][c_in_t][P]  (x for forward, dy for backward-data)

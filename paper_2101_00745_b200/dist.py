@@ -58,11 +58,19 @@ class GradBucket:
 
 def allreduce_grads(grads: List[torch.Tensor], group=None, average: bool = True,
                     bucket: Optional[GradBucket] = None) -> None:
-    """Sum (or mean) `grads` across the process group in ONE collective."""
+    """Sum (or mean) `grads` across the process group in ONE collective.  A
+    single contiguous tensor (an already-flat bucket, as bench.py's dW|db
+    buffer) is reduced in place with no pack / unpack copies."""
     if not grads:
         return
     world = dist.get_world_size(group)
     if world == 1:
+        return
+    if len(grads) == 1 and grads[0].is_contiguous():
+        flat = grads[0]
+        dist.all_reduce(flat, op=dist.ReduceOp.SUM, group=group)
+        if average:
+            flat.div_(world)
         return
     bucket = bucket or GradBucket(grads)
     flat = bucket.pack(grads)
@@ -73,28 +81,55 @@ def allreduce_grads(grads: List[torch.Tensor], group=None, average: bool = True,
 
 
 def scc_parameters(module: torch.nn.Module) -> Iterable[torch.nn.Parameter]:
-    from .module import SCC2d
+    """The parameters of every SCC stage: SCC2d layers and both halves of the
+    DSC2d (depthwise 3x3 + SCC) blocks the model zoo is built from."""
+    from .module import DSC2d, SCC2d
     for m in module.modules():
-        if isinstance(m, SCC2d):
-            yield m.weight
-            if m.bias is not None:
-                yield m.bias
+        if isinstance(m, (SCC2d, DSC2d)):
+            for name in ("dw_weight", "dw_bias", "weight", "bias"):
+                p = getattr(m, name, None)
+                if p is not None:
+                    yield p
 
 
-class SccGradSync:
-    """Call after loss.backward(): one bucketed all-reduce of every SCC
-    parameter gradient of `module` (other parameters are left to the caller's
-    DDP wrapper)."""
+class GradSync:
+    """Data-parallel gradient exchange of a whole model: after
+    loss.backward(), ONE bucketed all-reduce (mean) of every parameter
+    gradient.  All tensors live in fixed buffers, so the call can be captured
+    in the same CUDA graph as the step (NCCL collectives are graph-capturable)
+    and the N-GPU step replays exactly like the 1-GPU one.  World size 1 is a
+    no-op.  `params` defaults to every trainable parameter of `module`."""
 
-    def __init__(self, module: torch.nn.Module, group=None, average: bool = True):
-        self.params = [p for p in scc_parameters(module) if p.requires_grad]
+    def __init__(self, module: torch.nn.Module, group=None, average: bool = True,
+                 params: Optional[Sequence[torch.nn.Parameter]] = None):
+        self.params = [p for p in (params if params is not None else module.parameters())
+                       if p.requires_grad]
         self.group, self.average = group, average
-        self._bucket = None
+        self._bucket = GradBucket(self.params) if self.params else None
+
+    def broadcast_parameters(self, src: int = 0) -> None:
+        """Start every rank from rank `src`'s weights (one collective)."""
+        if not self.params or dist.get_world_size(self.group) == 1:
+            return
+        flat = self._bucket.pack([p.detach() for p in self.params])
+        dist.broadcast(flat, src=src, group=self.group)
+        with torch.no_grad():
+            self._bucket.unpack([p.data for p in self.params])
 
     def __call__(self) -> None:
-        grads = [p.grad for p in self.params if p.grad is not None]
-        if not grads:
+        if not self.params:
             return
-        if self._bucket is None or len(self._bucket.params) != len(grads):
-            self._bucket = GradBucket(grads)
+        grads = []
+        for p in self.params:
+            if p.grad is None:  # a parameter this step did not reach: zero, so every rank reduces alike
+                p.grad = torch.zeros_like(p)
+            grads.append(p.grad)
         allreduce_grads(grads, self.group, self.average, self._bucket)
+
+
+class SccGradSync(GradSync):
+    """GradSync over the SCC stages only (SCC2d, and DSC2d's depthwise + SCC
+    parameters), for callers that leave the other parameters to DDP."""
+
+    def __init__(self, module: torch.nn.Module, group=None, average: bool = True):
+        super().__init__(module, group, average, params=list(scc_parameters(module)))

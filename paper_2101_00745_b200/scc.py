@@ -100,6 +100,7 @@ class SccConfig:
     def set_path(self, path: int) -> None:
         """Force the kernel family (_lib.SCC_PATH_*) for this layer."""
         check(lib().scc_plan_set_path(self._h, int(path)))
+        self._ws_cache.clear()  # the workspace size depends on the family
 
     def path_for(self, n: int, h: int, w: int) -> int:
         out = C.c_int32()
@@ -245,8 +246,23 @@ def _dev4(t: torch.Tensor, name: str) -> torch.Tensor:
     return t.contiguous()
 
 
-def _check_weights(wts: SccWeights, cfg: SccConfig) -> None:
-    """check_weights (kernel.cpp:14-25)."""
+def _check_param(t: Optional[torch.Tensor], name: str, device: Optional[torch.device]) -> None:
+    """Parameters are handed to the kernels as raw device pointers: they must be
+    float32 CUDA tensors on the activations' device (else ArgumentError)."""
+    if t is None:
+        return
+    if not isinstance(t, torch.Tensor) or not t.is_cuda or t.dtype != torch.float32:
+        raise ArgumentError(f"{name} must be a float32 CUDA tensor (got "
+                            f"{getattr(t, 'dtype', type(t))} on {getattr(t, 'device', '?')})")
+    if device is not None and t.device != device:
+        raise ArgumentError(f"{name} is on {t.device}, the activations on {device}")
+
+
+def _check_weights(wts: SccWeights, cfg: SccConfig, device: Optional[torch.device] = None) -> None:
+    """check_weights (kernel.cpp:14-25), plus the device / dtype contract of the
+    raw-pointer C ABI."""
+    _check_param(wts.weight, "weight", device)
+    _check_param(wts.bias, "bias", device)
     want_w = cfg.c_out * cfg.group_width
     if wts.weight.numel() != want_w:
         raise ShapeError(f"weight array has {wts.weight.numel()} entries, config needs {want_w}")
@@ -265,7 +281,7 @@ def scc_forward(input: torch.Tensor, wts: SccWeights, cfg: SccConfig) -> torch.T
     x = _dev4(input, "input")
     if x.shape[1] != cfg.c_in:
         raise ShapeError(f"input has {x.shape[1]} channels, config expects {cfg.c_in}")
-    _check_weights(wts, cfg)
+    _check_weights(wts, cfg, x.device)
     n, _, h, w = x.shape
     y = torch.empty((n, cfg.c_out, h, w), dtype=torch.float32, device=x.device)
     wt = wts.weight.contiguous()
@@ -288,7 +304,9 @@ def dsc_forward(input: torch.Tensor, dw_weight: torch.Tensor, dw_bias: Optional[
         raise ShapeError(f"depthwise weight has {dw_weight.numel()} entries, needs {cfg.c_in * 9}")
     if dw_bias is not None and dw_bias.numel() != cfg.c_in:
         raise ShapeError(f"depthwise bias has {dw_bias.numel()} entries, needs {cfg.c_in}")
-    _check_weights(wts, cfg)
+    _check_param(dw_weight, "dw_weight", x.device)
+    _check_param(dw_bias, "dw_bias", x.device)
+    _check_weights(wts, cfg, x.device)
     n, _, h, w = x.shape
     ho, wo = (h - 1) // stride + 1, (w - 1) // stride + 1
     y = torch.empty((n, cfg.c_out, ho, wo), dtype=torch.float32, device=x.device)
@@ -353,7 +371,7 @@ def scc_backward_input(grad_out: torch.Tensor, wts: SccWeights, cfg: SccConfig) 
     g = _dev4(grad_out, "grad_out")
     if g.shape[1] != cfg.c_out:
         raise ShapeError(f"grad_out has {g.shape[1]} channels, config expects {cfg.c_out}")
-    _check_weights(wts, cfg)
+    _check_weights(wts, cfg, g.device)
     n, _, h, w = g.shape
     dx = torch.empty((n, cfg.c_in, h, w), dtype=torch.float32, device=g.device)
     wt = wts.weight.contiguous()
@@ -388,7 +406,7 @@ def scc_backward(grad_out: torch.Tensor, input: torch.Tensor, wts: SccWeights,
     """scc_backward (kernel.hpp:70-72)."""
     g, x = _dev4(grad_out, "grad_out"), _dev4(input, "input")
     _check_pair(g, x, cfg)
-    _check_weights(wts, cfg)
+    _check_weights(wts, cfg, x.device)
     n, _, h, w = x.shape
     dx = torch.empty_like(x)
     dw = torch.empty(cfg.c_out * cfg.group_width, dtype=torch.float32, device=x.device)

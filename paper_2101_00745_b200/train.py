@@ -1,10 +1,16 @@
 """Synthetic-data training throughput of the SCC models (images/sec), one
-process per GPU, data parallel over NCCL (DistributedDataParallel: one
-bucketed all-reduce of the gradients, SCC weights included, per step).
+process per GPU, data parallel over NCCL.
+
+Every world size runs the same step: forward, cross-entropy, backward, ONE
+bucketed all-reduce (mean) of all gradients through ``dist.GradSync`` (a
+no-op at world size 1), momentum SGD update -- captured once as a CUDA graph
+and replayed, collective included.  ``tests/test_dist.py`` runs this same
+``make_train_step`` / ``GradSync`` code with 2 gloo ranks on CPU.
 
 The reference trains its sequential networks on one CPU thread pool
-(train.cpp:66-125); this is the B200 harness for BASELINE configs C2/C3
-(SCC-VGG16 / SCC-ResNet-18 on CIFAR-shaped synthetic data).
+(train.cpp:66-125); this is the B200 harness for BASELINE configs C2-C4
+(SCC-VGG16 / SCC-ResNet-18 on CIFAR-shaped and SCC-ResNet-50 on
+ImageNet-shaped synthetic data).
 """
 from __future__ import annotations
 
@@ -12,38 +18,45 @@ import torch
 import torch.distributed as dist
 from torch import nn
 
+from .dist import GradSync
 from .models import MODELS
+
+
+def make_train_step(model: nn.Module, opt: torch.optim.Optimizer, loss_fn, x: torch.Tensor,
+                    y: torch.Tensor, sync: GradSync):
+    """One data-parallel SGD step over this rank's shard (x, y)."""
+
+    def step():
+        opt.zero_grad(set_to_none=False)
+        loss = loss_fn(model(x), y)
+        loss.backward()
+        sync()
+        opt.step()
+        return loss
+
+    return step
 
 
 def train_throughput(model_name: str = "resnet18", batch: int = 128, steps: int = 20, warmup: int = 5,
                      image: int = 32, num_classes: int = 10, seed: int = 0, graph: bool = True):
-    """Time `steps` SGD steps (forward, cross-entropy, backward, all-reduce
-    when distributed, momentum SGD update) after `warmup` steps.  Returns
-    per-rank images/sec x world size (max-over-ranks device time).
+    """Time `steps` SGD steps after `warmup` steps.  Returns images/sec over
+    all ranks (per-rank batch x world size / max-over-ranks device time).
 
-    On one GPU the whole step is captured once as a CUDA graph and replayed
-    (a CIFAR-size step is ~300 small kernels, so eager launches make it host
+    The whole step is captured once as a CUDA graph and replayed (a
+    CIFAR-size step is ~300 small kernels, so eager launches make it host
     bound); the warm-up runs on the capture stream so every per-stream
-    resource of the SCC plans exists before capture.  Under torchrun (DDP)
-    the step runs eagerly."""
+    resource of the SCC plans (and NCCL's) exists before capture."""
     dev = torch.device("cuda", torch.cuda.current_device())
     ws = dist.get_world_size() if dist.is_available() and dist.is_initialized() else 1
     torch.manual_seed(seed)
     model = MODELS[model_name](num_classes=num_classes, device=dev)
-    if ws > 1:
-        model = nn.parallel.DistributedDataParallel(model, device_ids=[dev.index])
+    sync = GradSync(model)
+    sync.broadcast_parameters()
     opt = torch.optim.SGD(model.parameters(), lr=0.05, momentum=0.9, weight_decay=5e-4)
     gen = torch.Generator(device=dev).manual_seed(seed + (dist.get_rank() if ws > 1 else 0))
     x = torch.randn(batch, 3, image, image, device=dev, generator=gen)
     y = torch.randint(0, num_classes, (batch,), device=dev, generator=gen)
-    loss_fn = nn.CrossEntropyLoss()
-
-    def step():
-        opt.zero_grad(set_to_none=True)
-        loss = loss_fn(model(x), y)
-        loss.backward()
-        opt.step()
-        return loss
+    step = make_train_step(model, opt, nn.CrossEntropyLoss(), x, y, sync)
 
     launch = "eager"
     stream = torch.cuda.Stream(dev)
@@ -51,7 +64,7 @@ def train_throughput(model_name: str = "resnet18", batch: int = 128, steps: int 
     with torch.cuda.stream(stream):
         losses = [float(step().item()) for _ in range(max(warmup, 1))]
         run = step
-        if graph and ws == 1:
+        if graph:
             try:
                 g = torch.cuda.CUDAGraph()
                 with torch.cuda.graph(g, stream=stream):
