@@ -130,6 +130,8 @@ scc_status_t scc_forward_macs(const scc_plan_t* plan, int64_t n, int64_t h,
                               int64_t w, uint64_t* macs);
 
 /* Force a kernel family for this plan (tests/bench); AUTO by default.
+ * Set it before issuing work: calls already in flight on other threads may
+ * run with either the old or the new family.
  * SCC_PATH_TENSOR is a preference: directions (or calls) the tensor-core
  * band GEMM cannot express run on the CUDA-core kernels.  SCC_ERR_ARGUMENT for
  * an unknown value. */
@@ -181,7 +183,19 @@ scc_status_t scc_forward_host_f32(scc_plan_t* plan, int64_t n, int64_t h, int64_
 scc_status_t scc_backward_host_f32(scc_plan_t* plan, int64_t n, int64_t h, int64_t w,
                                    const float* dy, const float* x, const float* weight,
                                    float* dx, float* dweight, float* dbias);
-/* One training step of the layer (forward then backward) with host buffers. */
+/* scc_backward_input (kernel.hpp:56-61) with host buffers: moves dy in and dx
+ * out only (backward-data never sees x, kernel.cpp:98-138). */
+scc_status_t scc_backward_data_host_f32(scc_plan_t* plan, int64_t n, int64_t h, int64_t w,
+                                        const float* dy, const float* weight, float* dx);
+/* scc_backward_params (kernel.hpp:62-68) with host buffers: dy and x in,
+ * dweight / dbias out (dbias NULL iff !has_bias). */
+scc_status_t scc_backward_weight_host_f32(scc_plan_t* plan, int64_t n, int64_t h, int64_t w,
+                                          const float* dy, const float* x, float* dweight,
+                                          float* dbias);
+/* One training step of the layer (forward then backward) with host buffers.
+ * All host entry points pipeline H2D / kernels / D2H over batch chunks; when
+ * every buffer is page-locked the pipeline is captured once per (extents,
+ * buffers) as a CUDA graph and replayed on later calls with the same buffers. */
 scc_status_t scc_fwd_bwd_host_f32(scc_plan_t* plan, int64_t n, int64_t h, int64_t w,
                                   const float* x, const float* weight, const float* bias,
                                   const float* dy, float* y, float* dx, float* dweight,

@@ -283,22 +283,40 @@ inline SccGradients scc_backward(const HostTensor4& grad_out, const HostTensor4&
   return out;
 }
 
-// scc_backward_input (kernel.hpp:56-61).  Runs the joint host call with a
-// zero input, which leaves the input gradient unaffected.
+// scc_backward_input (kernel.hpp:56-61): dy in, dx out (backward-data never
+// sees x, kernel.cpp:98-138).
 inline HostTensor4 scc_backward_input(const HostTensor4& grad_out, const SccWeights& wts,
                                       const SccConfig& cfg) {
   if (grad_out.c() != cfg.c_out)
     throw ShapeError("grad_out has " + std::to_string(grad_out.c()) + " channels, config expects " +
                      std::to_string(cfg.c_out));
-  HostTensor4 zero(grad_out.n(), cfg.c_in, grad_out.h(), grad_out.w());
-  return scc_backward(grad_out, zero, wts, cfg).grad_input;
+  detail::check_weights(wts, cfg);
+  const auto g = detail::narrow(grad_out.data(), grad_out.size());
+  const auto w = detail::narrow(wts.weight.data(), static_cast<std::int64_t>(wts.weight.size()));
+  HostTensor4 out(grad_out.n(), cfg.c_in, grad_out.h(), grad_out.w());
+  std::vector<float> dx(static_cast<size_t>(out.size()));
+  check(scc_backward_data_host_f32(cfg.plan(), grad_out.n(), grad_out.h(), grad_out.w(), g.data(),
+                                   w.data(), dx.data()));
+  detail::widen(dx, out.data());
+  return out;
 }
 
-// scc_backward_params (kernel.hpp:62-68).
+// scc_backward_params (kernel.hpp:62-68): dy and x in, dW / db out.
 inline SccParamGradients scc_backward_params(const HostTensor4& grad_out, const HostTensor4& input,
                                              const SccConfig& cfg) {
-  SccWeights zero = scc_weights_filled(cfg, 0.0, 0.0);
-  return scc_backward(grad_out, input, zero, cfg).params;
+  if (grad_out.c() != cfg.c_out || input.c() != cfg.c_in || grad_out.n() != input.n() ||
+      grad_out.h() != input.h() || grad_out.w() != input.w())
+    throw ShapeError("grad_out/input shapes inconsistent with config");
+  const auto g = detail::narrow(grad_out.data(), grad_out.size());
+  const auto x = detail::narrow(input.data(), input.size());
+  std::vector<float> dw(static_cast<size_t>(cfg.c_out * cfg.group_width)),
+      db(static_cast<size_t>(cfg.has_bias ? cfg.c_out : 0));
+  check(scc_backward_weight_host_f32(cfg.plan(), input.n(), input.h(), input.w(), g.data(), x.data(),
+                                     dw.data(), cfg.has_bias ? db.data() : nullptr));
+  SccParamGradients out;
+  out.grad_weight.assign(dw.begin(), dw.end());
+  out.grad_bias.assign(db.begin(), db.end());
+  return out;
 }
 
 // ---- device fp32 views (asynchronous on a caller stream) ----

@@ -127,6 +127,21 @@ class _Base:
         return y
 
 
+    def dw_backward(self, dy, x, wt, k=3, stride=1, with_bias=False):
+        """grouped_conv_backward of the depthwise stage (groups = c, padding
+        k/2; reference.cpp:155-247): (dx, dW [c][k][k], db or None)."""
+        if not hasattr(self, "_dwb"):
+            raise NotImplementedError("depthwise backward: compiled reference only")
+        dy, x, wt = _d(dy), _d(x), _d(wt)
+        n, c, h, wd = x.shape
+        dx = np.empty_like(x)
+        dwt = np.empty(c * k * k, np.float64)
+        db = np.empty(c, np.float64) if with_bias else None
+        self._dwb(n, c, h, wd, k, stride, _ptr(dy), _ptr(x), _ptr(wt), _ptr(dx), _ptr(dwt),
+                  _ptr(db) if db is not None else None)
+        return dx, dwt.reshape(c, k, k), db
+
+
 class PortOracle(_Base):
     """oracle/scc_oracle.c (plain-C restatement, single thread)."""
 
@@ -221,6 +236,8 @@ class RefOracle(_Base):
         self._fwd = self._checked(L.ref_forward)
         L.sccl_ref_dw_forward.argtypes = [_i64] * 6 + [_dp, _dp, _dp, _dp]
         self._dw = self._checked(L.sccl_ref_dw_forward)
+        L.sccl_ref_dw_backward.argtypes = [_i64] * 6 + [_dp] * 6
+        self._dwb = self._checked(L.sccl_ref_dw_backward)
         self._bwd_in = self._checked(L.ref_backward_input)
         self._bwd_p = self._checked(L.ref_backward_params)
 

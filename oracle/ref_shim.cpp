@@ -305,3 +305,34 @@ extern "C" int sccl_ref_dw_forward(int64_t n, int64_t c, int64_t h, int64_t w, i
     return map_exception();
   }
 }
+
+// grouped_conv_backward (reference.hpp:83, reference.cpp:155-247) of the
+// depthwise stage: dx (input-centric), dW [c][k][k], db [c] (db may be null).
+extern "C" int sccl_ref_dw_backward(int64_t n, int64_t c, int64_t h, int64_t w, int64_t k,
+                                    int64_t stride, const double* dy, const double* x,
+                                    const double* wt, double* dx, double* dwt, double* db) {
+  try {
+    sccl::ConvSpec spec;
+    spec.c_in = c;
+    spec.c_out = c;
+    spec.kernel = k;
+    spec.stride = stride;
+    spec.padding = k / 2;
+    spec.groups = c;
+    sccl::ConvWeights wts;
+    wts.weight.assign(wt, wt + c * k * k);
+    if (db) wts.bias.assign(static_cast<size_t>(c), 0.0);
+    const int64_t ho = sccl::conv_output_extent(h, k, stride, k / 2);
+    const int64_t wo = sccl::conv_output_extent(w, k, stride, k / 2);
+    sccl::Tensor4 in(n, c, h, w), g(n, c, ho, wo);
+    std::memcpy(in.data(), x, sizeof(double) * static_cast<size_t>(in.size()));
+    std::memcpy(g.data(), dy, sizeof(double) * static_cast<size_t>(g.size()));
+    const sccl::ConvGradients r = sccl::grouped_conv_backward(g, in, wts, spec);
+    std::memcpy(dx, r.grad_input.data(), sizeof(double) * static_cast<size_t>(r.grad_input.size()));
+    std::memcpy(dwt, r.grad_weight.data(), sizeof(double) * r.grad_weight.size());
+    if (db) std::memcpy(db, r.grad_bias.data(), sizeof(double) * r.grad_bias.size());
+    return 0;
+  } catch (...) {
+    return map_exception();
+  }
+}

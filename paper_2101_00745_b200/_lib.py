@@ -44,6 +44,7 @@ EXPORTS = (
     "scc_dw3x3_forward_f32", "scc_dw3x3_backward_data_f32", "scc_dw3x3_workspace_size",
     "scc_dw3x3_backward_weight_f32",
     "scc_forward_host_f32", "scc_backward_host_f32", "scc_fwd_bwd_host_f32",
+    "scc_backward_data_host_f32", "scc_backward_weight_host_f32",
 )
 
 
@@ -144,6 +145,8 @@ def _declare(L):
         "scc_forward_host_f32": ([vp, i64, i64, i64, fp, fp, fp, fp], C.c_int),
         "scc_backward_host_f32": ([vp, i64, i64, i64, fp, fp, fp, fp, fp, fp], C.c_int),
         "scc_fwd_bwd_host_f32": ([vp, i64, i64, i64, fp, fp, fp, fp, fp, fp, fp, fp], C.c_int),
+        "scc_backward_data_host_f32": ([vp, i64, i64, i64, fp, fp, fp], C.c_int),
+        "scc_backward_weight_host_f32": ([vp, i64, i64, i64, fp, fp, fp, fp], C.c_int),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)

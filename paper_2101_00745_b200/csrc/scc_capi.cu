@@ -282,7 +282,10 @@ size_t weight_ws_bytes(const Plan& p, int64_t n, int64_t plane) {
                          ? tc_wgrad2_workspace_bytes(static_cast<int32_t>(p.cfg.c_out),
                                                      static_cast<int32_t>(p.cfg.group_width), 74)
                          : 0;
-  const size_t tc3 = fused_bwd_supported(p, plane)
+  // (independent of the forced path, so a size queried before set_path stays
+  // large enough after it)
+  const size_t tc3 = tc_bwd_supported(p.tc_wgt, plane, static_cast<int32_t>(p.cfg.c_in),
+                                      static_cast<int32_t>(p.cfg.c_out), static_cast<int32_t>(p.cfg.group_width))
                          ? tc_bwd_workspace_bytes(static_cast<int32_t>(p.cfg.c_out),
                                                   static_cast<int32_t>(p.cfg.group_width), n, plane)
                          : 0;
@@ -530,8 +533,11 @@ Staged stage(Plan& p, int64_t n, int64_t h, int64_t wd) {
       mk(&st->ev_done[i]);
     }
     mk(&st->ev_out);
+    mk(&st->ev_fork);
   }
   if (st->bytes < total) {
+    for (HostStaging::Graph& e : st->graphs) cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(e.exec));
+    st->graphs.clear();
     if (st->buf) cuda_check(cudaFree(st->buf), "cudaFree(staging)");
     st->buf = nullptr;
     cuda_check(cudaMalloc(&st->buf, total), "cudaMalloc(staging)");
@@ -577,29 +583,46 @@ void d2h(void* h, const void* d, size_t bytes, cudaStream_t s) {
 //   copy-out stream: per chunk y_c / dx_c; dW / db last
 // Forward and backward-data are per sample (kernel.cpp:45-60, :107-137) and
 // the kernels' per-element arithmetic does not depend on n, so chunked
-// results are bitwise equal to one full-batch call.
+// results are bitwise equal to one full-batch call.  Any subset of the three
+// passes runs (y: forward, dx: backward-data, dw: backward-weight), so the
+// reference's separate scc_backward_input / scc_backward_params calls move
+// only their own bytes.
 struct HostIo {
   const float *x = nullptr, *w = nullptr, *b = nullptr, *dy = nullptr;
   float *y = nullptr, *dx = nullptr, *dw = nullptr, *db = nullptr;
 };
 
 int host_chunks(int64_t n, size_t bytes_per_sample) {
-  // >= ~1 MB of traffic per chunk keeps each copy near full PCIe speed
-  const int64_t by_size = static_cast<int64_t>(bytes_per_sample * n / (1u << 20));
-  int64_t k = std::min<int64_t>({n, kMaxHostChunks / 4, std::max<int64_t>(by_size, 1)});
+  // >= ~2 MB of traffic per chunk keeps each copy near full PCIe speed; more
+  // chunks shorten the un-overlapped first H2D / last D2H
+  const int64_t by_size = static_cast<int64_t>(bytes_per_sample * n / (2u << 20));
+  int64_t k = std::min<int64_t>({n, kMaxHostChunks / 2, std::max<int64_t>(by_size, 1)});
   if (const char* e = getenv("SCC_HOST_CHUNKS")) k = std::max<int64_t>(1, std::min<int64_t>({atoi(e), n, kMaxHostChunks}));
   return static_cast<int>(k);
 }
 
-void run_host(Plan& p, int64_t n, int64_t h, int64_t wd, const HostIo& io) {
+bool pinned(const void* q) {
+  if (q == nullptr) return true;
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, q) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeHost;
+}
+
+void issue_host(Plan& p, int64_t n, int64_t h, int64_t wd, const HostIo& io, const Staged& g, int k) {
   const scc_config_t& c = p.cfg;
   const int64_t P = h * wd;
-  Staged g = stage(p, n, h, wd);
-  const bool fwd = io.y != nullptr, bwd = io.dx != nullptr;
+  const bool fwd = io.y != nullptr, bdata = io.dx != nullptr, bwt = io.dw != nullptr;
+  const bool need_x = fwd || bwt, need_dy = bdata || bwt;
   const size_t sx = static_cast<size_t>(c.c_in * P) * 4, sy = static_cast<size_t>(c.c_out * P) * 4;
   const size_t nw = static_cast<size_t>(c.c_out * c.group_width) * 4, nb = static_cast<size_t>(c.c_out) * 4;
-  const int k = host_chunks(n, (fwd ? sx + sy : 0) + (bwd ? sx + sy : 0) + (bwd && !fwd ? sx : 0));
-  h2d(g.w, io.w, nw, g.s_in);
+  // fork the copy streams off the compute stream (also makes the sequence capturable)
+  cuda_check(cudaEventRecord(static_cast<cudaEvent_t>(g.st->ev_fork), g.s), "cudaEventRecord");
+  cuda_check(cudaStreamWaitEvent(g.s_in, static_cast<cudaEvent_t>(g.st->ev_fork), 0), "cudaStreamWaitEvent");
+  cuda_check(cudaStreamWaitEvent(g.s_out, static_cast<cudaEvent_t>(g.st->ev_fork), 0), "cudaStreamWaitEvent");
+  if (fwd || bdata) h2d(g.w, io.w, nw, g.s_in);
   if (fwd && io.b) h2d(g.b, io.b, nb, g.s_in);
   int64_t n0 = 0;
   for (int i = 0; i < k; ++i) {
@@ -607,25 +630,90 @@ void run_host(Plan& p, int64_t n, int64_t h, int64_t wd, const HostIo& io) {
     const size_t ox = static_cast<size_t>(n0) * sx / 4, oy = static_cast<size_t>(n0) * sy / 4;
     cudaEvent_t ein = static_cast<cudaEvent_t>(g.st->ev_in[i]);
     cudaEvent_t edone = static_cast<cudaEvent_t>(g.st->ev_done[i]);
-    h2d(g.x + ox, io.x + ox, m * sx, g.s_in);
-    if (bwd) h2d(g.dy + oy, io.dy + oy, m * sy, g.s_in);
+    if (need_x) h2d(g.x + ox, io.x + ox, m * sx, g.s_in);
+    if (need_dy) h2d(g.dy + oy, io.dy + oy, m * sy, g.s_in);
     cuda_check(cudaEventRecord(ein, g.s_in), "cudaEventRecord");
     cuda_check(cudaStreamWaitEvent(g.s, ein, 0), "cudaStreamWaitEvent");
     if (fwd) do_forward(p, m, h, wd, g.x + ox, g.w, io.b ? g.b : nullptr, g.y + oy, g.s);
-    if (bwd) do_backward_data(p, m, h, wd, g.dy + oy, g.w, g.dx + ox, g.s);
-    cuda_check(cudaEventRecord(edone, g.s), "cudaEventRecord");
-    cuda_check(cudaStreamWaitEvent(g.s_out, edone, 0), "cudaStreamWaitEvent");
-    if (fwd) d2h(io.y + oy, g.y + oy, m * sy, g.s_out);
-    if (bwd) d2h(io.dx + ox, g.dx + ox, m * sx, g.s_out);
+    if (bdata) do_backward_data(p, m, h, wd, g.dy + oy, g.w, g.dx + ox, g.s);
+    if (fwd || bdata) {
+      cuda_check(cudaEventRecord(edone, g.s), "cudaEventRecord");
+      cuda_check(cudaStreamWaitEvent(g.s_out, edone, 0), "cudaStreamWaitEvent");
+      if (fwd) d2h(io.y + oy, g.y + oy, m * sy, g.s_out);
+      if (bdata) d2h(io.dx + ox, g.dx + ox, m * sx, g.s_out);
+    }
     n0 += m;
   }
-  if (bwd) {
+  if (bwt) {
     do_backward_weight(p, n, h, wd, g.dy, g.x, g.dw, io.db ? g.db : nullptr, g.ws, g.ws_bytes, g.s);
     d2h(io.dw, g.dw, nw, g.s);
     if (io.db) d2h(io.db, g.db, nb, g.s);
   }
   cuda_check(cudaEventRecord(static_cast<cudaEvent_t>(g.st->ev_out), g.s_out), "cudaEventRecord");
   cuda_check(cudaStreamWaitEvent(g.s, static_cast<cudaEvent_t>(g.st->ev_out), 0), "cudaStreamWaitEvent");
+}
+
+constexpr size_t kMaxHostGraphs = 8;
+
+void run_host(Plan& p, int64_t n, int64_t h, int64_t wd, const HostIo& io) {
+  const scc_config_t& c = p.cfg;
+  const int64_t P = h * wd;
+  Staged g = stage(p, n, h, wd);
+  const bool fwd = io.y != nullptr, bdata = io.dx != nullptr, bwt = io.dw != nullptr;
+  const size_t sx = static_cast<size_t>(c.c_in * P) * 4, sy = static_cast<size_t>(c.c_out * P) * 4;
+  const size_t per_sample = ((fwd || bwt) ? sx : 0) + ((bdata || bwt) ? sy : 0) + (fwd ? sy : 0) + (bdata ? sx : 0);
+  const int k = host_chunks(n, per_sample);
+  HostStaging& st = *g.st;
+  const int64_t key[14] = {n, h, wd, k, p.path.load(),
+                           reinterpret_cast<int64_t>(io.x), reinterpret_cast<int64_t>(io.w),
+                           reinterpret_cast<int64_t>(io.b), reinterpret_cast<int64_t>(io.dy),
+                           reinterpret_cast<int64_t>(io.y), reinterpret_cast<int64_t>(io.dx),
+                           reinterpret_cast<int64_t>(io.dw), reinterpret_cast<int64_t>(io.db),
+                           reinterpret_cast<int64_t>(st.buf)};
+  for (HostStaging::Graph& e : st.graphs) {
+    if (std::equal(key, key + 14, e.key)) {
+      e.used = ++st.tick;
+      cuda_check(cudaGraphLaunch(static_cast<cudaGraphExec_t>(e.exec), g.s), "cudaGraphLaunch(host pipeline)");
+      cuda_check(cudaStreamSynchronize(g.s), "cudaStreamSynchronize");
+      return;
+    }
+  }
+  const bool replayable = getenv("SCC_HOST_NO_GRAPH") == nullptr &&
+                          pinned(io.x) && pinned(io.w) && pinned(io.b) && pinned(io.dy) && pinned(io.y) &&
+                          pinned(io.dx) && pinned(io.dw) && pinned(io.db);
+  if (replayable) {
+    // first call with these buffers: run it eagerly (creates every lazily
+    // built per-stream resource), then capture the same sequence for replays
+    issue_host(p, n, h, wd, io, g, k);
+    cuda_check(cudaStreamSynchronize(g.s), "cudaStreamSynchronize");
+    cudaGraph_t graph = nullptr;
+    cuda_check(cudaStreamBeginCapture(g.s, cudaStreamCaptureModeThreadLocal), "cudaStreamBeginCapture");
+    try {
+      issue_host(p, n, h, wd, io, g, k);
+    } catch (...) {
+      cudaStreamEndCapture(g.s, &graph);
+      if (graph) cudaGraphDestroy(graph);
+      throw;
+    }
+    cuda_check(cudaStreamEndCapture(g.s, &graph), "cudaStreamEndCapture");
+    cudaGraphExec_t exec = nullptr;
+    const cudaError_t e = cudaGraphInstantiate(&exec, graph, 0);
+    cudaGraphDestroy(graph);
+    cuda_check(e, "cudaGraphInstantiate(host pipeline)");
+    if (st.graphs.size() >= kMaxHostGraphs) {
+      auto lru = std::min_element(st.graphs.begin(), st.graphs.end(),
+                                  [](const HostStaging::Graph& a, const HostStaging::Graph& b) { return a.used < b.used; });
+      cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(lru->exec));
+      st.graphs.erase(lru);
+    }
+    HostStaging::Graph ge;
+    std::copy(key, key + 14, ge.key);
+    ge.exec = exec;
+    ge.used = ++st.tick;
+    st.graphs.push_back(ge);
+    return;
+  }
+  issue_host(p, n, h, wd, io, g, k);
   cuda_check(cudaStreamSynchronize(g.s), "cudaStreamSynchronize");
 }
 
@@ -729,6 +817,8 @@ scc_status_t scc_plan_destroy(scc_plan_t* plan) {
         if (s.ev_done[i]) cudaEventDestroy(static_cast<cudaEvent_t>(s.ev_done[i]));
       }
       if (s.ev_out) cudaEventDestroy(static_cast<cudaEvent_t>(s.ev_out));
+      if (s.ev_fork) cudaEventDestroy(static_cast<cudaEvent_t>(s.ev_fork));
+      for (const scc::HostStaging::Graph& e : s.graphs) cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(e.exec));
     }
     for (const scc::ForkJoin& f : plan->forks) {
       cudaSetDevice(f.device);
@@ -1031,6 +1121,43 @@ scc_status_t scc_backward_host_f32(scc_plan_t* plan, int64_t n, int64_t h, int64
     io.w = weight;
     io.dy = dy;
     io.dx = dx;
+    io.dw = dweight;
+    io.db = dbias;
+    scc::run_host(*plan, n, h, w, io);
+  });
+}
+
+scc_status_t scc_backward_data_host_f32(scc_plan_t* plan, int64_t n, int64_t h, int64_t w,
+                                        const float* dy, const float* weight, float* dx) {
+  return guard([&] {
+    scc::check_ptr(plan, "plan");
+    scc::check_extents(n, h, w);
+    scc::check_ptr(dy, "dy");
+    scc::check_ptr(weight, "weight");
+    scc::check_ptr(dx, "dx");
+    std::lock_guard<std::mutex> lk(plan->host_mu);
+    scc::HostIo io;
+    io.w = weight;
+    io.dy = dy;
+    io.dx = dx;
+    scc::run_host(*plan, n, h, w, io);
+  });
+}
+
+scc_status_t scc_backward_weight_host_f32(scc_plan_t* plan, int64_t n, int64_t h, int64_t w,
+                                          const float* dy, const float* x, float* dweight,
+                                          float* dbias) {
+  return guard([&] {
+    scc::check_ptr(plan, "plan");
+    scc::check_extents(n, h, w);
+    scc::check_ptr(dy, "dy");
+    scc::check_ptr(x, "x");
+    scc::check_ptr(dweight, "dweight");
+    scc::check_bias(*plan, dbias, "dbias");
+    std::lock_guard<std::mutex> lk(plan->host_mu);
+    scc::HostIo io;
+    io.x = x;
+    io.dy = dy;
     io.dw = dweight;
     io.db = dbias;
     scc::run_host(*plan, n, h, w, io);

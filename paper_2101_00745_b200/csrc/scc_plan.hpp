@@ -15,6 +15,7 @@
 //     exactly that arc, so no kernel ever touches channels outside the band.
 #pragma once
 
+#include <atomic>
 #include <cstdint>
 #include <deque>
 #include <mutex>
@@ -133,6 +134,17 @@ struct HostStaging {
   void* ev_in[kMaxHostChunks] = {};    // cudaEvent_t: chunk inputs resident
   void* ev_done[kMaxHostChunks] = {};  // cudaEvent_t: chunk outputs written
   void* ev_out = nullptr;              // cudaEvent_t: all D2H issued
+  void* ev_fork = nullptr;             // cudaEvent_t: capture fork into the copy streams
+  // Replayable pipelines: one CUDA graph per (extents, host pointers, chunking)
+  // when every host buffer is page-locked (a repeated call with the same
+  // buffers -- a training loop -- replays instead of re-issuing ~20 calls).
+  struct Graph {
+    int64_t key[14] = {};
+    void* exec = nullptr;  // cudaGraphExec_t
+    uint64_t used = 0;
+  };
+  std::vector<Graph> graphs;
+  uint64_t tick = 0;
 };
 
 // Per (device, stream, direction) scratch for the tensor-core weight panels,
@@ -163,7 +175,9 @@ struct Plan {
   std::vector<Arc> ic_arcs;          // covering arc of each input channel (sorted order)
   TcBandPlan tc_fwd, tc_bwd;
   TcWeightPlan tc_wgt;
-  int32_t path = SCC_PATH_AUTO;
+  // forced kernel family (scc_plan_set_path); atomic so a concurrent set_path
+  // is not a data race (calls already in flight may still see either value)
+  std::atomic<int32_t> path{SCC_PATH_AUTO};
 
   std::mutex dev_mu;
   std::deque<DeviceTables> dev;  // deque: references stay valid

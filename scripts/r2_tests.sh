@@ -1,0 +1,5 @@
+#!/bin/bash
+# GPU test pass + a short bench (with the in-run traffic pass).
+mkdir -p gpurun_out
+timeout 1500 python -m pytest tests -m gpu -q -x --durations=15 > gpurun_out/gpu_tests.log 2>&1; tail -25 gpurun_out/gpu_tests.log
+timeout 600 python bench.py --steps 50 --warmup 5 --no-models > gpurun_out/bench.json 2> gpurun_out/bench.err; tail -1 gpurun_out/bench.json | cut -c1-3000

@@ -159,16 +159,40 @@ Tensor4 scc_backward_input(const Tensor4& grad_out, const SccWeights& wts, const
                      " channels, config expects " + std::to_string(cfg.c_out));
   }
   check_weights(wts, cfg);
-  // backward-data never sees X (kernel.cpp:120); the host entry point wants
-  // one, so pass zeros and keep dx only.
-  Tensor4 zeros(grad_out.n(), cfg.c_in, grad_out.h(), grad_out.w());
-  return scc_backward(grad_out, zeros, wts, cfg).grad_input;
+  // backward-data never sees X (kernel.cpp:120): dy in, dx out
+  Tensor4 dx(grad_out.n(), cfg.c_in, grad_out.h(), grad_out.w());
+  const std::vector<float> dy = narrow(grad_out.data(), static_cast<std::size_t>(grad_out.size()));
+  const std::vector<float> w = narrow(wts.weight.data(), wts.weight.size());
+  std::vector<float> out(static_cast<std::size_t>(dx.size()));
+  check(scc_backward_data_host_f32(plan_for(cfg), grad_out.n(), grad_out.h(), grad_out.w(), dy.data(),
+                                   w.data(), out.data()));
+  widen(out, dx.data());
+  return dx;
 }
 
 SccParamGradients scc_backward_params(const Tensor4& grad_out, const Tensor4& input,
                                       const SccConfig& cfg) {
-  SccWeights zeros = scc_weights_filled(cfg, 0.0, 0.0);
-  return scc_backward(grad_out, input, zeros, cfg).params;
+  if (grad_out.c() != cfg.c_out) {
+    throw ShapeError("grad_out has " + std::to_string(grad_out.c()) +
+                     " channels, config expects " + std::to_string(cfg.c_out));
+  }
+  if (input.c() != cfg.c_in) {
+    throw ShapeError("input has " + std::to_string(input.c()) + " channels, config expects " +
+                     std::to_string(cfg.c_in));
+  }
+  if (grad_out.n() != input.n() || grad_out.h() != input.h() || grad_out.w() != input.w()) {
+    throw ShapeError("grad_out and input disagree on batch or spatial extents");
+  }
+  const std::vector<float> dy = narrow(grad_out.data(), static_cast<std::size_t>(grad_out.size()));
+  const std::vector<float> x = narrow(input.data(), static_cast<std::size_t>(input.size()));
+  std::vector<float> dw(static_cast<std::size_t>(cfg.c_out * cfg.group_width));
+  std::vector<float> db(static_cast<std::size_t>(cfg.has_bias ? cfg.c_out : 0));
+  check(scc_backward_weight_host_f32(plan_for(cfg), input.n(), input.h(), input.w(), dy.data(), x.data(),
+                                     dw.data(), cfg.has_bias ? db.data() : nullptr));
+  SccParamGradients g;
+  g.grad_weight.assign(dw.begin(), dw.end());
+  g.grad_bias.assign(db.begin(), db.end());
+  return g;
 }
 
 }  // namespace sccl

@@ -3,9 +3,11 @@
 Forward: scc_dsc_forward_f32 against the CPU oracle composition
 port.dw_forward (restating reference.cpp:74-123, pinned to the compiled
 reference in test_oracle.py) -> port.forward (kernel.cpp:29-69), fp64 on the
-same fp32 inputs, norm-relative <= 1e-5.  Backward (DSC2d autograd): against
-float64 torch autograd of the same composition (depthwise conv + the SCC
-band as a dense 1x1 conv), <= 1e-4."""
+same fp32 inputs, norm-relative <= 1e-5.  Backward: the depthwise kernels and
+the whole DSC2d composition against the compiled reference's own
+grouped_conv_backward (reference.cpp:155-247, via oracle/ref_shim.cpp) and
+scc_backward_input / scc_backward_params (kernel.cpp:98-181), <= 1e-4; plus
+float64 torch autograd of the same composition as a second check."""
 import numpy as np
 import pytest
 
@@ -142,21 +144,63 @@ def test_dw3x3_forward_matches_oracle(port, shape):
 
 
 @pytest.mark.parametrize("shape", DW_SHAPES, ids=lambda s: f"{s[2]}x{s[3]}-s{s[4]}")
-def test_dw3x3_backward_matches_fp64(shape):
+def test_dw3x3_backward_matches_reference(ref, shape):
+    """Depthwise backward-data / backward-weight / bias kernels against the
+    reference's grouped_conv_backward (reference.cpp:155-247, groups = c)."""
     import paper_2101_00745_b200 as scc
     n, c, h, w, s = shape
     g = torch.Generator().manual_seed(3)
     x = torch.randn(n, c, h, w, generator=g)
     wt = torch.rand(c, 1, 3, 3, generator=g) - 0.5
-    b = torch.rand(c, generator=g) - 0.5
-    xd, wd, bd = (t.double().requires_grad_(True) for t in (x, wt, b))
-    yd = torch.nn.functional.conv2d(xd, wd, bd, s, 1, 1, c)
-    gy = torch.randn(yd.shape, generator=g)
-    yd.backward(gy.double())
+    ho, wo = (h - 1) // s + 1, (w - 1) // s + 1
+    gy = torch.randn(n, c, ho, wo, generator=g)
+    rdx, rdw, rdb = ref.dw_backward(gy.numpy(), x.numpy(), wt.view(c, 3, 3).numpy(), 3, s, True)
     dx = scc.dw3x3_backward_data(gy.cuda(), wt.cuda(), (h, w), s)
     dw, db = scc.dw3x3_backward_weight(gy.cuda(), x.cuda(), s, True)
-    assert norm_rel(dx.cpu().numpy(), xd.grad.numpy()) <= GRAD_TOL
-    assert norm_rel(dw.cpu().numpy(), wd.grad.view(c, 3, 3).numpy()) <= GRAD_TOL
-    assert norm_rel(db.cpu().numpy(), bd.grad.numpy()) <= GRAD_TOL
+    assert norm_rel(dx.cpu().numpy(), rdx) <= GRAD_TOL
+    assert norm_rel(dw.cpu().numpy(), rdw) <= GRAD_TOL
+    assert norm_rel(db.cpu().numpy(), rdb) <= GRAD_TOL
     dw2, _ = scc.dw3x3_backward_weight(gy.cuda(), x.cuda(), s, True)
     assert torch.equal(dw, dw2)  # fixed-order reduction
+
+
+@pytest.mark.parametrize("fused", [False, True], ids=["dw+scc", "fused"])
+@pytest.mark.parametrize("case", CASES, ids=lambda c: f"{c[0]}-{c[1]}-cg{c[2]}-{c[3]}-{c[5]}x{c[6]}-s{c[7]}")
+def test_dsc2d_matches_reference_composition(ref, case, fused):
+    """The whole dsc_block (model.cpp:213-220) forward and backward against
+    the reference's own stages: grouped_conv_forward/_backward for the
+    depthwise 3x3 and scc_forward / scc_backward_input / scc_backward_params."""
+    import paper_2101_00745_b200 as scc
+    ci, co, cg, ov, n, h, w, s, dwb, hb = case
+    torch.manual_seed(1)
+    layer = scc.DSC2d(ci, co, s, cg, ov if isinstance(ov, str) else scc.Overlap.channels(ov),
+                      dw_bias=dwb, bias=hb, fused=fused, device="cuda")
+    with torch.no_grad():
+        if hb:
+            layer.bias.uniform_(-0.5, 0.5)
+        if dwb:
+            layer.dw_bias.uniform_(-0.5, 0.5)
+    x = torch.randn(n, ci, h, w, device="cuda", requires_grad=True)
+    y = layer(x)
+    gy = torch.randn_like(y)
+    y.backward(gy)
+    xn = x.detach().cpu().numpy()
+    dww = layer.dw_weight.detach().cpu().numpy().reshape(ci, 3, 3)
+    dwbn = layer.dw_bias.detach().cpu().numpy() if dwb else None
+    wn = layer.weight.detach().cpu().numpy().reshape(-1)
+    bn = layer.bias.detach().cpu().numpy() if hb else None
+    o = ref.config(ci, co, cg, ov if isinstance(ov, str) else ("channels", ov), hb)
+    t = ref.dw_forward(xn, dww, dwbn, 3, s)
+    ry = ref.forward(o, t, wn, bn)
+    gyn = gy.cpu().numpy()
+    dt = ref.backward_input(o, gyn, wn)
+    rdw, rdb = ref.backward_params(o, gyn, t)
+    rdx, rddw, rddb = ref.dw_backward(dt, xn, dww, 3, s, dwb)
+    assert norm_rel(y.detach().cpu().numpy(), ry) <= FWD_TOL
+    assert norm_rel(x.grad.cpu().numpy(), rdx) <= GRAD_TOL
+    assert norm_rel(layer.weight.grad.cpu().numpy().reshape(-1), rdw) <= GRAD_TOL
+    assert norm_rel(layer.dw_weight.grad.cpu().numpy().reshape(ci, 3, 3), rddw) <= GRAD_TOL
+    if hb:
+        assert norm_rel(layer.bias.grad.cpu().numpy(), rdb) <= GRAD_TOL
+    if dwb:
+        assert norm_rel(layer.dw_bias.grad.cpu().numpy(), rddb) <= GRAD_TOL

@@ -220,3 +220,29 @@ def test_dw_port_known_answer(port):
     corners 4 (zero padding counts as explicit zeros, reference.cpp:67-72)."""
     y = port.dw_forward(np.ones((1, 1, 3, 3)), np.ones((1, 3, 3)), None)
     assert y[0, 0].tolist() == [[4, 6, 4], [6, 9, 6], [4, 6, 4]]
+
+
+def test_fp64_class_gemm_reference_matches_oracle(port):
+    """tests/fp64_ref.py (the full-batch checker of the GPU sweep parity test)
+    equals the oracle to fp64 round-off on random geometries, including
+    wrap-around windows, ragged c_out, cg=1, ov=0 and uncovered channels."""
+    import torch
+    from fp64_ref import scc_fp64
+    from conftest import norm_rel
+    rng = np.random.default_rng(21)
+    cases = [(64, 128, 2, 16), (24, 40, 3, 2), (8, 5, 4, 1), (12, 12, 1, 5), (16, 20, 4, 0),
+             (32, 48, 8, 3), (60, 64, 3, 15)]
+    for ci, co, cg, ov in cases:
+        o = port.config(ci, co, cg, ("channels", ov), True)
+        gw = ci // cg
+        shift = gw - ov
+        x = rng.standard_normal((3, ci, 5, 4))
+        dy = rng.standard_normal((3, co, 5, 4))
+        w = rng.uniform(-1, 1, co * gw)
+        b = rng.uniform(-0.5, 0.5, co)
+        y, dx, dw, db = scc_fp64(ci, co, gw, shift, torch.from_numpy(x), torch.from_numpy(w),
+                                 torch.from_numpy(b), torch.from_numpy(dy))
+        assert norm_rel(y.numpy(), port.forward(o, x, w, b)) <= 1e-13
+        assert norm_rel(dx.numpy(), port.backward_input(o, dy, w)) <= 1e-13
+        rdw, rdb = port.backward_params(o, dy, x)
+        assert norm_rel(dw.numpy(), rdw) <= 1e-13 and norm_rel(db.numpy(), rdb) <= 1e-13
