@@ -237,7 +237,7 @@ def measure_traffic(workload, timeout=240):
     import tempfile
     csv_path = os.path.join(tempfile.mkdtemp(prefix="scc_traffic_"), "t.csv")
     cmd = ["ncu", "--metrics", "dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum",
-           "--clock-control", "none", "--print-units", "base", "--csv", "--log-file", csv_path,
+           "--clock-control", "none", "--cache-control", "none", "--print-units", "base", "--csv", "--log-file", csv_path,
            sys.executable, os.path.join(ROOT, "scripts", "traffic_probe.py"), "--workload", workload]
     try:
         subprocess.run(cmd, stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL, timeout=timeout,

@@ -56,6 +56,13 @@ class GradBucket:
             off += n
 
 
+def _world(group=None) -> int:
+    """World size, 1 when no process group is initialised (single process)."""
+    if not (dist.is_available() and dist.is_initialized()):
+        return 1
+    return dist.get_world_size(group)
+
+
 def allreduce_grads(grads: List[torch.Tensor], group=None, average: bool = True,
                     bucket: Optional[GradBucket] = None) -> None:
     """Sum (or mean) `grads` across the process group in ONE collective.  A
@@ -63,7 +70,7 @@ def allreduce_grads(grads: List[torch.Tensor], group=None, average: bool = True,
     buffer) is reduced in place with no pack / unpack copies."""
     if not grads:
         return
-    world = dist.get_world_size(group)
+    world = _world(group)
     if world == 1:
         return
     if len(grads) == 1 and grads[0].is_contiguous():
@@ -109,7 +116,7 @@ class GradSync:
 
     def broadcast_parameters(self, src: int = 0) -> None:
         """Start every rank from rank `src`'s weights (one collective)."""
-        if not self.params or dist.get_world_size(self.group) == 1:
+        if not self.params or _world(self.group) == 1:
             return
         flat = self._bucket.pack([p.detach() for p in self.params])
         dist.broadcast(flat, src=src, group=self.group)
@@ -117,7 +124,7 @@ class GradSync:
             self._bucket.unpack([p.data for p in self.params])
 
     def __call__(self) -> None:
-        if not self.params:
+        if not self.params or _world(self.group) == 1:
             return
         grads = []
         for p in self.params:

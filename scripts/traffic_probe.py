@@ -1,10 +1,10 @@
 """DRAM traffic of the bench step's kernels, writes included (run under ncu).
 
-    ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum \
+    ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --cache-control none \
         --clock-control none --csv --log-file T.csv python scripts/traffic_probe.py --workload c1
     python scripts/traffic_probe.py --parse T.csv
 
-A kernel's output usually still sits in the 126 MB L2 when it ends, so its
+With ncu's cache control off, a kernel's output usually still sits in the 126 MB L2 when it ends, so its
 own dram__bytes_write reads ~0.  The probe therefore brackets each phase with
 READ-ONLY L2 flushes (a sum over a buffer 2x the L2): the flush before leaves
 only clean lines (so the phase's own counters hold its reads and any evictions
