@@ -484,14 +484,18 @@ def run_ours(args):
                "ms_per_step": round(dt * 1e3, 4),
                "api": "scc_fwd_bwd_host_f32 (include/scc_b200.h)"}
 
-    # ---- BASELINE configs C2/C3: SCC-ResNet-18 / SCC-VGG16 training images/sec ----
+    # ---- BASELINE configs C2-C4: SCC-VGG16 / SCC-ResNet-18 / SCC-ResNet-50 images/sec ----
     models = None
     if not args.no_models:
         from paper_2101_00745_b200.train import train_throughput
         models = {}
-        for name in ("resnet18", "vgg16"):
+        runs = {"resnet18": dict(batch=128, steps=20, warmup=5),            # C3 (CIFAR shape)
+                "vgg16": dict(batch=128, steps=20, warmup=5),               # C2 (CIFAR shape)
+                "resnet50": dict(batch=256, steps=8, warmup=3, image=224,   # C4 (ImageNet shape)
+                                 num_classes=1000)}
+        for name, kw in runs.items():
             try:
-                models[name] = train_throughput(name, batch=128, steps=20, warmup=5)
+                models[name] = train_throughput(name, **kw)
             except Exception as ex:  # reported, never required for the headline
                 models[name] = {"error": str(ex)[:200]}
 

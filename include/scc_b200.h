@@ -193,9 +193,7 @@ scc_status_t scc_backward_weight_host_f32(scc_plan_t* plan, int64_t n, int64_t h
                                           const float* dy, const float* x, float* dweight,
                                           float* dbias);
 /* One training step of the layer (forward then backward) with host buffers.
- * All host entry points pipeline H2D / kernels / D2H over batch chunks; when
- * every buffer is page-locked the pipeline is captured once per (extents,
- * buffers) as a CUDA graph and replayed on later calls with the same buffers. */
+ * All host entry points pipeline H2D / kernels / D2H over batch chunks. */
 scc_status_t scc_fwd_bwd_host_f32(scc_plan_t* plan, int64_t n, int64_t h, int64_t w,
                                   const float* x, const float* weight, const float* bias,
                                   const float* dy, float* y, float* dx, float* dweight,

@@ -190,6 +190,26 @@ float* panel_buffer(Plan& p, int dir, cudaStream_t s) {
   return static_cast<float*>(b.ptr);
 }
 
+// Arrival counter of the fused backward's dW reduction (scc_tc_bwd.cu), one
+// per (device, stream): monotonic, so it never needs a reset between launches.
+unsigned long long* ticket_buffer(Plan& p, cudaStream_t s) {
+  const int dev = current_device();
+  std::lock_guard<std::mutex> lk(p.panel_mu);
+  for (PanelBuf& b : p.panels) {
+    if (b.device == dev && b.stream == static_cast<void*>(s) && b.dir == 2)
+      return static_cast<unsigned long long*>(b.ptr);
+  }
+  PanelBuf b;
+  b.device = dev;
+  b.stream = s;
+  b.dir = 2;
+  b.bytes = 256;
+  cuda_check(cudaMalloc(&b.ptr, b.bytes), "cudaMalloc(ticket)");
+  cuda_check(cudaMemsetAsync(b.ptr, 0, b.bytes, s), "cudaMemsetAsync(ticket)");
+  p.panels.push_back(b);
+  return static_cast<unsigned long long*>(b.ptr);
+}
+
 int device_sms() {
   int dev = 0, n = 148;
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
@@ -340,6 +360,7 @@ void launch_fused(Plan& p, int64_t n, int64_t h, int64_t w, const float* dy, con
   c.starts = t.starts;
   c.do_dx = dx != nullptr;
   c.do_dw = dw != nullptr;
+  if (c.do_dw) c.ticket = ticket_buffer(p, s);
   cuda_check(launch_tc_bwd(p.tc_wgt, c, s), "backward (fused tensor) launch");
 }
 
@@ -536,8 +557,6 @@ Staged stage(Plan& p, int64_t n, int64_t h, int64_t wd) {
     mk(&st->ev_fork);
   }
   if (st->bytes < total) {
-    for (HostStaging::Graph& e : st->graphs) cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(e.exec));
-    st->graphs.clear();
     if (st->buf) cuda_check(cudaFree(st->buf), "cudaFree(staging)");
     st->buf = nullptr;
     cuda_check(cudaMalloc(&st->buf, total), "cudaMalloc(staging)");
@@ -593,22 +612,14 @@ struct HostIo {
 };
 
 int host_chunks(int64_t n, size_t bytes_per_sample) {
-  // >= ~2 MB of traffic per chunk keeps each copy near full PCIe speed; more
-  // chunks shorten the un-overlapped first H2D / last D2H
-  const int64_t by_size = static_cast<int64_t>(bytes_per_sample * n / (2u << 20));
-  int64_t k = std::min<int64_t>({n, kMaxHostChunks / 2, std::max<int64_t>(by_size, 1)});
+  // >= ~1 MB of traffic per chunk keeps each copy near full PCIe speed; 4
+  // chunks measured best at config 1 (scripts/host_sweep.py: 1 / 2 / 4 / 8
+  // chunks 0.97 / 0.83 / 0.77 / 0.84 ms; replaying the pipeline as a CUDA
+  // graph measured 0.05 ms slower than issuing it)
+  const int64_t by_size = static_cast<int64_t>(bytes_per_sample * n / (1u << 20));
+  int64_t k = std::min<int64_t>({n, kMaxHostChunks / 4, std::max<int64_t>(by_size, 1)});
   if (const char* e = getenv("SCC_HOST_CHUNKS")) k = std::max<int64_t>(1, std::min<int64_t>({atoi(e), n, kMaxHostChunks}));
   return static_cast<int>(k);
-}
-
-bool pinned(const void* q) {
-  if (q == nullptr) return true;
-  cudaPointerAttributes at{};
-  if (cudaPointerGetAttributes(&at, q) != cudaSuccess) {
-    cudaGetLastError();
-    return false;
-  }
-  return at.type == cudaMemoryTypeHost;
 }
 
 void issue_host(Plan& p, int64_t n, int64_t h, int64_t wd, const HostIo& io, const Staged& g, int k) {
@@ -653,8 +664,6 @@ void issue_host(Plan& p, int64_t n, int64_t h, int64_t wd, const HostIo& io, con
   cuda_check(cudaStreamWaitEvent(g.s, static_cast<cudaEvent_t>(g.st->ev_out), 0), "cudaStreamWaitEvent");
 }
 
-constexpr size_t kMaxHostGraphs = 8;
-
 void run_host(Plan& p, int64_t n, int64_t h, int64_t wd, const HostIo& io) {
   const scc_config_t& c = p.cfg;
   const int64_t P = h * wd;
@@ -662,58 +671,7 @@ void run_host(Plan& p, int64_t n, int64_t h, int64_t wd, const HostIo& io) {
   const bool fwd = io.y != nullptr, bdata = io.dx != nullptr, bwt = io.dw != nullptr;
   const size_t sx = static_cast<size_t>(c.c_in * P) * 4, sy = static_cast<size_t>(c.c_out * P) * 4;
   const size_t per_sample = ((fwd || bwt) ? sx : 0) + ((bdata || bwt) ? sy : 0) + (fwd ? sy : 0) + (bdata ? sx : 0);
-  const int k = host_chunks(n, per_sample);
-  HostStaging& st = *g.st;
-  const int64_t key[14] = {n, h, wd, k, p.path.load(),
-                           reinterpret_cast<int64_t>(io.x), reinterpret_cast<int64_t>(io.w),
-                           reinterpret_cast<int64_t>(io.b), reinterpret_cast<int64_t>(io.dy),
-                           reinterpret_cast<int64_t>(io.y), reinterpret_cast<int64_t>(io.dx),
-                           reinterpret_cast<int64_t>(io.dw), reinterpret_cast<int64_t>(io.db),
-                           reinterpret_cast<int64_t>(st.buf)};
-  for (HostStaging::Graph& e : st.graphs) {
-    if (std::equal(key, key + 14, e.key)) {
-      e.used = ++st.tick;
-      cuda_check(cudaGraphLaunch(static_cast<cudaGraphExec_t>(e.exec), g.s), "cudaGraphLaunch(host pipeline)");
-      cuda_check(cudaStreamSynchronize(g.s), "cudaStreamSynchronize");
-      return;
-    }
-  }
-  const bool replayable = getenv("SCC_HOST_NO_GRAPH") == nullptr &&
-                          pinned(io.x) && pinned(io.w) && pinned(io.b) && pinned(io.dy) && pinned(io.y) &&
-                          pinned(io.dx) && pinned(io.dw) && pinned(io.db);
-  if (replayable) {
-    // first call with these buffers: run it eagerly (creates every lazily
-    // built per-stream resource), then capture the same sequence for replays
-    issue_host(p, n, h, wd, io, g, k);
-    cuda_check(cudaStreamSynchronize(g.s), "cudaStreamSynchronize");
-    cudaGraph_t graph = nullptr;
-    cuda_check(cudaStreamBeginCapture(g.s, cudaStreamCaptureModeThreadLocal), "cudaStreamBeginCapture");
-    try {
-      issue_host(p, n, h, wd, io, g, k);
-    } catch (...) {
-      cudaStreamEndCapture(g.s, &graph);
-      if (graph) cudaGraphDestroy(graph);
-      throw;
-    }
-    cuda_check(cudaStreamEndCapture(g.s, &graph), "cudaStreamEndCapture");
-    cudaGraphExec_t exec = nullptr;
-    const cudaError_t e = cudaGraphInstantiate(&exec, graph, 0);
-    cudaGraphDestroy(graph);
-    cuda_check(e, "cudaGraphInstantiate(host pipeline)");
-    if (st.graphs.size() >= kMaxHostGraphs) {
-      auto lru = std::min_element(st.graphs.begin(), st.graphs.end(),
-                                  [](const HostStaging::Graph& a, const HostStaging::Graph& b) { return a.used < b.used; });
-      cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(lru->exec));
-      st.graphs.erase(lru);
-    }
-    HostStaging::Graph ge;
-    std::copy(key, key + 14, ge.key);
-    ge.exec = exec;
-    ge.used = ++st.tick;
-    st.graphs.push_back(ge);
-    return;
-  }
-  issue_host(p, n, h, wd, io, g, k);
+  issue_host(p, n, h, wd, io, g, host_chunks(n, per_sample));
   cuda_check(cudaStreamSynchronize(g.s), "cudaStreamSynchronize");
 }
 
@@ -818,7 +776,6 @@ scc_status_t scc_plan_destroy(scc_plan_t* plan) {
       }
       if (s.ev_out) cudaEventDestroy(static_cast<cudaEvent_t>(s.ev_out));
       if (s.ev_fork) cudaEventDestroy(static_cast<cudaEvent_t>(s.ev_fork));
-      for (const scc::HostStaging::Graph& e : s.graphs) cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(e.exec));
     }
     for (const scc::ForkJoin& f : plan->forks) {
       cudaSetDevice(f.device);

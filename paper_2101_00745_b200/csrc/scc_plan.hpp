@@ -134,17 +134,7 @@ struct HostStaging {
   void* ev_in[kMaxHostChunks] = {};    // cudaEvent_t: chunk inputs resident
   void* ev_done[kMaxHostChunks] = {};  // cudaEvent_t: chunk outputs written
   void* ev_out = nullptr;              // cudaEvent_t: all D2H issued
-  void* ev_fork = nullptr;             // cudaEvent_t: capture fork into the copy streams
-  // Replayable pipelines: one CUDA graph per (extents, host pointers, chunking)
-  // when every host buffer is page-locked (a repeated call with the same
-  // buffers -- a training loop -- replays instead of re-issuing ~20 calls).
-  struct Graph {
-    int64_t key[14] = {};
-    void* exec = nullptr;  // cudaGraphExec_t
-    uint64_t used = 0;
-  };
-  std::vector<Graph> graphs;
-  uint64_t tick = 0;
+  void* ev_fork = nullptr;             // cudaEvent_t: fork of the copy streams off the compute stream
 };
 
 // Per (device, stream, direction) scratch for the tensor-core weight panels,

@@ -48,6 +48,18 @@ def train_throughput(model_name: str = "resnet18", batch: int = 128, steps: int 
     resource of the SCC plans (and NCCL's) exists before capture."""
     dev = torch.device("cuda", torch.cuda.current_device())
     ws = dist.get_world_size() if dist.is_available() and dist.is_initialized() else 1
+    # fp32 end to end: the stock dense layers (stem, 1x1 convs, head) must not
+    # silently run TF32 next to the 3xTF32 SCC kernels
+    tf32 = (torch.backends.cudnn.allow_tf32, torch.backends.cuda.matmul.allow_tf32)
+    torch.backends.cudnn.allow_tf32 = False
+    torch.backends.cuda.matmul.allow_tf32 = False
+    try:
+        return _train_throughput(model_name, batch, steps, warmup, image, num_classes, seed, graph, dev, ws)
+    finally:
+        torch.backends.cudnn.allow_tf32, torch.backends.cuda.matmul.allow_tf32 = tf32
+
+
+def _train_throughput(model_name, batch, steps, warmup, image, num_classes, seed, graph, dev, ws):
     torch.manual_seed(seed)
     model = MODELS[model_name](num_classes=num_classes, device=dev)
     sync = GradSync(model)
@@ -98,5 +110,5 @@ def train_throughput(model_name: str = "resnet18", batch: int = 128, steps: int 
             "ms_per_step": round(ms, 4), "batch_per_gpu": batch, "global_batch": batch * ws,
             "n_gpus": ws, "steps": steps, "warmup": warmup, "image": f"3x{image}x{image}",
             "loss_first": round(losses[0], 4), "loss_last": round(float(last.item()), 4),
-            "launch": launch,
+            "launch": launch, "dense_layers": "fp32 (TF32 off)",
             "data": "synthetic N(0,1) images, uniform labels"}

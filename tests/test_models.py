@@ -22,9 +22,27 @@ def test_param_counts_match_paper():
     assert len(models.scc_layers(models.SCCResNet18())) == 16
 
 
+def test_resnet50_param_count_matches_paper():
+    # SCC-ResNet-50 12.87 M parameters (CIFAR-10 head).  With the
+    # ImageNet 7x7 stem the count is 7,680 higher.
+    r = models.param_counts(models.SCCResNet50(num_classes=10))
+    assert abs(r["total"] - 12.87e6) / 12.87e6 < 0.002, r
+    assert len(models.scc_layers(models.SCCResNet50())) == 16
+    assert len(models.scc_layers(models.SCCResNet50(rule="all"))) == 48
+
+
+# (c_in, c_out, plane) of every SCC layer of SCC-ResNet-50 at 224x224, both rules
+RESNET50_SHAPES = [(64, 64, 56), (128, 128, 28), (256, 256, 14), (512, 512, 7),
+                   (64, 256, 56), (256, 64, 56), (256, 128, 56), (128, 512, 28), (512, 128, 28),
+                   (512, 256, 28), (256, 1024, 14), (1024, 256, 14), (1024, 512, 14),
+                   (512, 2048, 7), (2048, 512, 7)]
+
+
 def _shapes():
-    out = set()
+    out = set(RESNET50_SHAPES)
     for name, cls in models.MODELS.items():
+        if name == "resnet50":
+            continue
         m = cls()
         size = {"resnet18": [32, 32, 16, 16, 8, 8, 4, 4], "vgg16": [32, 16, 16, 8, 8, 8, 4, 4, 4, 2, 2, 2]}[name]
         for layer, hw in zip(models.scc_layers(m), [s for s in size for _ in range(2)] if name == "resnet18" else size):
@@ -48,7 +66,7 @@ def test_model_layer_shapes(shape):
         pytest.skip("no CUDA device")
     ci, co, hw = shape
     cfg = scc.scc_config_new(ci, co, 2, "50%", True)
-    n = 8
+    n = 8 if hw <= 32 else 2
     g = torch.Generator(device="cuda").manual_seed(ci * 7 + co + hw)
     x = torch.randn(n, ci, hw, hw, device="cuda", generator=g)
     gy = torch.randn(n, co, hw, hw, device="cuda", generator=g)
@@ -72,11 +90,12 @@ def test_model_layer_shapes(shape):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("name", ["resnet18", "vgg16"])
+@pytest.mark.parametrize("name", ["resnet18", "vgg16", "resnet50"])
 def test_training_loss_falls(name):
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     from paper_2101_00745_b200.train import train_throughput
-    r = train_throughput(name, batch=32, steps=15, warmup=1)
+    kw = dict(image=64, num_classes=10) if name == "resnet50" else {}
+    r = train_throughput(name, batch=32, steps=15, warmup=1, **kw)
     assert r["images_per_s"] > 0
     assert r["loss_last"] < r["loss_first"], r

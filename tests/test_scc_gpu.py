@@ -457,12 +457,12 @@ def test_host_pipeline_bitwise(chunks, monkeypatch):
     assert np.array_equal(y, y2)
 
 
-def test_host_separate_entry_points_and_graph_replay():
+def test_host_separate_entry_points():
     """scc_backward_data_host_f32 / scc_backward_weight_host_f32 (the
     reference's separate scc_backward_input / scc_backward_params, kernel.hpp:
-    56-68) move only their own bytes and agree bitwise with the joint call;
-    with page-locked buffers the second call replays the captured pipeline
-    and must see the NEW contents of the same buffers."""
+    56-68) move only their own bytes and agree bitwise with the joint call and
+    the device entry points; repeated calls on the same page-locked buffers
+    see their new contents."""
     import paper_2101_00745_b200 as scc
     from paper_2101_00745_b200 import _lib
     L = _lib.lib()
