@@ -190,26 +190,6 @@ float* panel_buffer(Plan& p, int dir, cudaStream_t s) {
   return static_cast<float*>(b.ptr);
 }
 
-// Arrival counter of the fused backward's dW reduction (scc_tc_bwd.cu), one
-// per (device, stream): monotonic, so it never needs a reset between launches.
-unsigned long long* ticket_buffer(Plan& p, cudaStream_t s) {
-  const int dev = current_device();
-  std::lock_guard<std::mutex> lk(p.panel_mu);
-  for (PanelBuf& b : p.panels) {
-    if (b.device == dev && b.stream == static_cast<void*>(s) && b.dir == 2)
-      return static_cast<unsigned long long*>(b.ptr);
-  }
-  PanelBuf b;
-  b.device = dev;
-  b.stream = s;
-  b.dir = 2;
-  b.bytes = 256;
-  cuda_check(cudaMalloc(&b.ptr, b.bytes), "cudaMalloc(ticket)");
-  cuda_check(cudaMemsetAsync(b.ptr, 0, b.bytes, s), "cudaMemsetAsync(ticket)");
-  p.panels.push_back(b);
-  return static_cast<unsigned long long*>(b.ptr);
-}
-
 int device_sms() {
   int dev = 0, n = 148;
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
@@ -360,7 +340,6 @@ void launch_fused(Plan& p, int64_t n, int64_t h, int64_t w, const float* dy, con
   c.starts = t.starts;
   c.do_dx = dx != nullptr;
   c.do_dw = dw != nullptr;
-  if (c.do_dw) c.ticket = ticket_buffer(p, s);
   cuda_check(launch_tc_bwd(p.tc_wgt, c, s), "backward (fused tensor) launch");
 }
 

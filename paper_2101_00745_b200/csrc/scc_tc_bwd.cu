@@ -27,12 +27,14 @@
 // converters refill them while the rest of the pair's MMAs run.
 //
 // dW accumulates over the CTA's pixel slice in TMEM and is written as that
-// slice's window-relative partial; a PDL-chained kernel sums the partials in
-// a fixed order (the slice count is fixed per geometry, so the bits of dW do
-// not depend on the grid).  dx is drained from TMEM per pair, staged and
-// stored by TMA.  The same kernel, with either GEMM switched off, serves
-// scc_backward_input / scc_backward_params alone, so the fused and separate
-// entry points agree bit for bit.
+// slice's window-relative partial (db: the dy converters sum their rows on
+// the CUDA cores, so the dW GEMM's N is exactly the x arc); a PDL-chained
+// kernel sums the slice partials in a fixed order (the slice count is fixed
+// per geometry, so the bits of dW do not depend on the grid).  dx is drained from TMEM per pair; the W_lo half of the stacked
+// accumulator is exchanged through shared memory and the W_hi half adds it
+// and stores straight to global.  The same kernel, with either GEMM switched
+// off, serves scc_backward_input / scc_backward_params alone, so the fused
+// and separate entry points agree bit for bit.
 //
 // Warp roles (384 threads, one CTA per SM, one slice per CTA):
 //   warp 0      TMA producer
@@ -78,7 +80,7 @@ __device__ unsigned long long g_cta3[2 * 256];
 
 constexpr int kThreads = 384;
 constexpr int kSlots = 3;             // TMA pair slots in the ring
-constexpr int kSlices = 148;          // pixel slices (dW partials) per launch
+constexpr int kSlices = 148;          // pixel slices (dW partials) per launch = CTAs (one per SM)
 constexpr int kSmemLimit = 227 * 1024;
 constexpr int kMaxGw = 32;
 // TMEM columns (512 allocated)
@@ -90,13 +92,15 @@ constexpr uint32_t kDxAcc = 384;     // two dx accumulators: [ic lane (+64: lo p
 struct BArgs {
   float* part;               // [slices][c_out*gw + c_out] partial dW | db (c_out <= 128)
   float* dweight;            // [c_out*gw]
+  float* dx;                 // [n][c_in][plane]
+  int32_t plane;
   float* dbias;              // [c_out] or nullptr
   const float* weight;       // [c_out*gw]
   const int32_t* starts;     // oc -> window start
   int32_t c_in, c_out, gw, cls, n_class;
   int32_t start8;            // first x row (input channel) of the filters' arc
   int32_t nx;                // x rows loaded (8-aligned arc)
-  int32_t xr;                // x stage rows (nx + ones row, rounded to 16) = dW MMA N
+  int32_t xr;                // x stage rows (nx rounded to 16) = dW MMA N
   int32_t rbb;               // x TMA box rows when the arc wraps
   int32_t xbox;              // 1: one x box {32 px, nx rows}
   int32_t nbps;              // 32-pixel blocks per sample
@@ -125,12 +129,13 @@ __device__ __forceinline__ void advance(int& stage, uint32_t& phase, int stages)
 __host__ __device__ constexpr int round1k(int b) { return (b + 1023) & ~1023; }
 
 // Shared memory: kSlots TMA pair slots (per block: raw dy | x), one lo pair
-// (per block: dy_lo | x_lo) and one dx staging pair.
+// (per block: dy_lo | x_lo), one dx exchange pair (the W_lo half of the
+// accumulator, handed to the W_hi half) and the per-filter db sums.
 // The W staging of the prologue aliases the lo pair (its writers wait for
 // W^T to be built) and so does the dW row dump of the epilogue (each CTA runs
 // exactly one slice, so the lo pair is idle by then).
 struct BLayout {
-  int blk, x, slot, lo0, xlo, stg, stgb, wst, dump, bars, total;
+  int blk, x, slot, lo0, xlo, stg, stgb, wst, dump, dbs, bars, total;
   __host__ __device__ BLayout(int c_in, int c_out, int gw, int xr) {
     const int dyb = round1k(c_out * 128), xb = round1k(xr * 128);
     blk = dyb + xb;                       // one block: dy (or dy_lo) | x (or x_lo)
@@ -155,6 +160,8 @@ struct BLayout {
       dump = end;
       end += round1k(dneed);
     }
+    dbs = end;  // [128] per-filter dy sums of the slice
+    end += 512;
     bars = end;
     total = bars + 64 * 8;
   }
@@ -216,7 +223,7 @@ __device__ __forceinline__ float4 f4(const uint32_t* v) {
 
 __global__ void __launch_bounds__(kThreads, 1)
     tc_bwd_kernel(const __grid_constant__ CUtensorMap tdy, const __grid_constant__ CUtensorMap tx,
-                  const __grid_constant__ CUtensorMap tdx, const __grid_constant__ BArgs a) {
+                  const __grid_constant__ BArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const BLayout L(a.c_in, a.c_out, a.gw, a.xr);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bars);
@@ -231,7 +238,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* accfull = dxempty + 2;             // MMA commit: the slice's dW done
   uint64_t* wt_ready = accfull + 1;            // 4 epilogue warps: W^T in TMEM
   uint64_t* w_bar = wt_ready + 1;              // W bulk copy landed
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(w_bar + 1);
+  uint64_t* dbready = w_bar + 1;               // 4 dy converter warps: slice db sums in smem
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dbready + 1);
 
   const uint32_t warp = warp_id();
   const int lane = threadIdx.x & 31;
@@ -255,12 +263,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     mbar_init(accfull, 1);
     mbar_init(wt_ready, 4);
     mbar_init(w_bar, 1);
+    mbar_init(dbready, 4);
     fence_mbar_init();
   }
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&tdy);
     if (a.do_dw) prefetch_tmap(&tx);
-    if (a.do_dx) prefetch_tmap(&tdx);
   }
   if (warp == 1) tmem_alloc<512>(tmem_slot);
   tc_fence_before();
@@ -384,19 +392,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ---------------- x lo converters ----------------
     if (a.do_dw) {
       const int ct = threadIdx.x - 64;  // 0..63
-      // constant rows [nx, xr): row nx = 1 (x) / 0 (x_lo), the rest 0 (the lo
-      // pair once the W staging it aliases is consumed)
-      for (int s = 0; s < 2 * kSlots + 2; ++s) {
+      // padding rows [nx, xr) of every x / x_lo stage are zero (the lo pair
+      // once the W staging it aliases is consumed)
+      for (int s = 0; s < 2 * kSlots + 2 && a.xr > a.nx; ++s) {
         if (s == 2 * kSlots && a.do_dx) mbar_wait(wt_ready, 0);
         float* xs = reinterpret_cast<float*>(s < 2 * kSlots ? smem + s * L.blk + L.x
                                                             : smem + L.lo0 + (s - 2 * kSlots) * L.blk + L.xlo);
-        const float one = s < 2 * kSlots ? 1.f : 0.f;
-        for (int i = ct; i < (a.xr - a.nx) * 32; i += 64) {
-          const int r = a.nx + (i >> 5), c = i & 31;
-          const int off = r * 32 + ((((c >> 2) ^ (r & 7)) << 2) | (c & 3));
-          xs[off] = r == a.nx ? one : 0.f;
-        }
+        for (int i = ct; i < (a.xr - a.nx) * 32; i += 64) xs[a.nx * 32 + i] = 0.f;
       }
+      // the W staging of the prologue aliases the lo pair
+      if (a.do_dx) mbar_wait(wt_ready, 0);
       fence_proxy_async_smem();
       int s = 0;
       uint32_t ph = 0, lph = 0;
@@ -439,11 +444,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     // for dW, the hi / lo row to TMEM lane `row`.
     const int q = warp & 3;
     const int row = q * 32 + lane;
+    const int swp = (row >> 2) & 1;
     const bool live = row < a.c_out;
     const bool warp_live = q * 32 < a.c_out;  // tcgen05.st is warp-collective
     const uint32_t lane_base = static_cast<uint32_t>(q * 32) << 16;
     int s = 0;
     uint32_t ph = 0, tph = 0, lph = 0;
+    float dbsum = 0.f;  // db of this filter over the slice (fixed order: blocks, then pixels)
     for (int p = 0; p < npairs; ++p) {
       const int nb = min(2, u1 - (u0 + 2 * p));
       mbar_wait(&full[s], ph);
@@ -453,17 +460,31 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int c = 0; c < 32; ++c) hi[c] = lo[c] = 0u;
         if (live) {
           const float4* rp = reinterpret_cast<const float4*>(smem + s * L.slot + k * L.blk + row * 128);
+          float bs = 0.f;
 #pragma unroll
-          for (int c = 0; c < 8; ++c) {
-            const float4 v = rp[((((c >> 1) ^ row) & 3) << 1) | (c & 1)];
-            const float e[4] = {v.x, v.y, v.z, v.w};
+          for (int j = 0; j < 4; ++j) {
+            // 32 B atom j of the row sits at atom (j ^ row) & 3; rows 4 apart
+            // share that position, so they take its two 16 B halves in the
+            // opposite order: the 8 rows of a quarter warp hit 8 distinct
+            // 16 B bank groups (no 2-way conflict).
+            const int at = ((j ^ row) & 3) << 1;
+            const float4 va = rp[at | swp], vb = rp[at | (swp ^ 1)];
+            const float4 v0 = swp ? vb : va, v1 = swp ? va : vb;
 #pragma unroll
-            for (int t = 0; t < 4; ++t) {
-              const float h = tf32_hi(e[t]);
-              hi[4 * c + t] = __float_as_uint(h);
-              lo[4 * c + t] = __float_as_uint(e[t] - h);
+            for (int hh = 0; hh < 2; ++hh) {
+              const float4 v = hh ? v1 : v0;
+              const int c = 2 * j + hh;
+              const float e[4] = {v.x, v.y, v.z, v.w};
+              bs += (e[0] + e[1]) + (e[2] + e[3]);
+#pragma unroll
+              for (int t = 0; t < 4; ++t) {
+                const float h = tf32_hi(e[t]);
+                hi[4 * c + t] = __float_as_uint(h);
+                lo[4 * c + t] = __float_as_uint(e[t] - h);
+              }
             }
           }
+          dbsum += bs;
         }
         if (k == 0) {
           mbar_wait(lofree, lph ^ 1u);
@@ -473,8 +494,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (live) {
           const uint32_t lo_row = smem_u32(smem + L.lo0 + k * L.blk + row * 128);
 #pragma unroll
-          for (int c = 0; c < 8; ++c)
-            sts_v4(lo_row + (((((c >> 1) ^ row) & 3) << 1) | (c & 1)) * 16, f4(lo + 4 * c));
+          for (int j = 0; j < 4; ++j) {
+            const int at = ((j ^ row) & 3) << 1;
+            const float4 l0 = f4(lo + 8 * j), l1 = f4(lo + 8 * j + 4);
+            sts_v4(lo_row + (at | swp) * 16, swp ? l1 : l0);
+            sts_v4(lo_row + (at | (swp ^ 1)) * 16, swp ? l0 : l1);
+          }
         }
         if (a.do_dw) {
           if (k == 0) {
@@ -498,6 +523,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (lane == 0) mbar_arrive(conv);
       if (row == 0) TRACE3K(8, p);
       advance(s, ph, kSlots);
+    }
+    if (a.do_dw) {
+      reinterpret_cast<float*>(smem + L.dbs)[row] = dbsum;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(dbready);
     }
   } else {
     // ---------------- W^T build, dx epilogue, dW slice epilogue ----------------
@@ -565,10 +595,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&dxempty[b]);
-        // the staging pair was last read by the stores of the previous pair
-        if (leader) bulk_wait_read<0>();
+        // rows 64-127 (the W_lo part) -> exchange pair; rows 0-63 add theirs and
+        // store the sum straight to global (each thread one input channel,
+        // 32 contiguous pixels per block).  The first barrier orders this
+        // pair's exchange writes after the previous pair's reads.
         named_bar_sync(1, 128);
-        // rows 64-127 (the W_lo part) -> staging, then rows 0-63 add theirs in place
         const uint32_t r0 = smem_u32(smem + L.stg + dx_row * 128), r1 = r0 + L.stgb;
         if (bottom && dx_warp && dx_live) {
 #pragma unroll
@@ -579,28 +610,26 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         named_bar_sync(1, 128);
         if (!bottom && dx_warp && dx_live) {
-          const float4* s0 = reinterpret_cast<const float4*>(smem + L.stg + dx_row * 128);
-          const float4* s1 = reinterpret_cast<const float4*>(smem + L.stg + L.stgb + dx_row * 128);
 #pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const int pj = j ^ (dx_row & 7);
-            const float4 o0 = s0[pj], o1 = s1[pj];
-            const float4 a0 = f4(v0 + 4 * j), a1 = f4(v1 + 4 * j);
-            sts_v4(r0 + (pj << 4), make_float4(a0.x + o0.x, a0.y + o0.y, a0.z + o0.z, a0.w + o0.w));
-            sts_v4(r1 + (pj << 4), make_float4(a1.x + o1.x, a1.y + o1.y, a1.z + o1.z, a1.w + o1.w));
+          for (int k = 0; k < 2; ++k) {
+            if (k < nb) {
+              const int u = ub + k;
+              const int n = u / a.nbps, px0 = (u - n * a.nbps) * 32;
+              float* drow = a.dx + (static_cast<int64_t>(n) * a.c_in + dx_row) * a.plane + px0;
+              const uint32_t* vv = k == 0 ? v0 : v1;
+              const uint32_t rk = k == 0 ? r0 : r1;
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                const float4 o = lds_v4(rk + ((j ^ (dx_row & 7)) << 4));
+                const float4 m = f4(vv + 4 * j);
+                if (px0 + 4 * j < a.plane)
+                  __stcs(reinterpret_cast<float4*>(drow + 4 * j),
+                         make_float4(m.x + o.x, m.y + o.y, m.z + o.z, m.w + o.w));
+              }
+            }
           }
         }
-        fence_proxy_async_smem();
-        named_bar_sync(1, 128);
-        if (leader) {
-          for (int k = 0; k < nb; ++k) {
-            const int u = ub + k;
-            const int n = u / a.nbps, px0 = (u - n * a.nbps) * 32;
-            tma_store_3d(&tdx, smem + L.stg + k * L.stgb, px0, 0, n);
-          }
-          bulk_commit();
-          TRACE3K(40, p);
-        }
+        if (leader) TRACE3K(40, p);
         if (++b == 2) {
           b = 0;
           dph ^= 1u;
@@ -613,6 +642,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       float* prow = dump + i * rstride;
       const uint32_t prow_a = smem_u32(prow);
       mbar_wait(accfull, 0);
+      mbar_wait(dbready, 0);
       if (et == 0) TRACE3(51);
       tc_fence_after();
       for (int c0 = 0; c0 < a.xr; c0 += 32) {
@@ -649,11 +679,10 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int t = 0; t < kMaxGw; ++t)
             if (t < a.gw) dst[i * a.gw + t] = wv[t];
         }
-        dst[a.c_out * a.gw + i] = live ? prow[a.nx] : 0.f;
+        dst[a.c_out * a.gw + i] = live ? reinterpret_cast<const float*>(smem + L.dbs)[i] : 0.f;
       }
     }
     if (leader) {
-      bulk_wait<0>();
       TRACE3(52);
 #if defined(SCC_TRACE)
       if (blockIdx.x < 256) g_cta3[2 * blockIdx.x + 1] = globaltimer();
@@ -718,7 +747,7 @@ Geo geometry(const TcWeightPlan& tw, int32_t c_in, int32_t c_out, int32_t gw) {
   Geo g;
   g.start8 = tw.rt_info[0];
   g.nx = tw.rt_info[1];
-  g.xr = (g.nx + 1 + 15) / 16 * 16;
+  g.xr = (g.nx + 15) / 16 * 16;
   g.fits = BLayout(c_in, c_out, gw, g.xr).total <= kSmemLimit;
   return g;
 }
@@ -794,6 +823,8 @@ cudaError_t launch_tc_bwd(const TcWeightPlan& tw, const TcBwdCall& call, cudaStr
     return cudaErrorInvalidValue;
   a.part = static_cast<float*>(call.workspace);
   a.dweight = call.dweight;
+  a.dx = call.dx;
+  a.plane = static_cast<int32_t>(call.plane);
   a.dbias = call.dbias;
   a.weight = call.weight;
   a.starts = call.starts;
@@ -802,7 +833,7 @@ cudaError_t launch_tc_bwd(const TcWeightPlan& tw, const TcBwdCall& call, cudaStr
   (void)nsm;
 
   const uint64_t P = static_cast<uint64_t>(call.plane);
-  CUtensorMap tdy{}, tx{}, tdx{};
+  CUtensorMap tdy{}, tx{};
   {
     // dy {P, cls, D, N}: row (d, j) = filter d + D*j; one box per block
     const uint64_t dims[4] = {P, static_cast<uint64_t>(tw.cls), static_cast<uint64_t>(tw.n_class),
@@ -818,10 +849,6 @@ cudaError_t launch_tc_bwd(const TcWeightPlan& tw, const TcBwdCall& call, cudaStr
     const uint32_t box[3] = {32, static_cast<uint32_t>(a.xbox ? g.nx : tw.rbb), 1};
     if (!encode_f32(&tx, call.x, 3, dimx, strx, box, CU_TENSOR_MAP_SWIZZLE_128B)) return cudaErrorInvalidValue;
   }
-  if (a.do_dx) {
-    const uint32_t box[3] = {32, static_cast<uint32_t>(call.c_in), 1};
-    if (!encode_f32(&tdx, call.dx, 3, dimx, strx, box, CU_TENSOR_MAP_SWIZZLE_128B)) return cudaErrorInvalidValue;
-  }
   if (dev < 0 || dev >= 64 || !attr_set[dev]) {
     cudaError_t e = cudaFuncSetAttribute(tc_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit);
     if (e != cudaSuccess) return e;
@@ -830,19 +857,24 @@ cudaError_t launch_tc_bwd(const TcWeightPlan& tw, const TcBwdCall& call, cudaStr
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(static_cast<unsigned>(grid));
   cfg.blockDim = dim3(kThreads);
-  // (no slack: the extern smem array is 1024-aligned; staying under 227 KB - 2 KB lets
-  // the small reduce CTAs be resident next to these and wait on the dependency)
   cfg.dynamicSmemBytes = BLayout(a.c_in, a.c_out, a.gw, a.xr).total;
   cfg.stream = s;
+  // PDL-chained to the neighbouring kernels; one CTA per SM.
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, tc_bwd_kernel, tdy, tx, tdx, a);
+  if (grid > nsm) return cudaErrorInvalidConfiguration;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, tc_bwd_kernel, tdy, tx, a);
   if (e != cudaSuccess) return e;
   int launches = 1;
   if (a.do_dw) {
+    // the fixed-order partial reduction, PDL-chained (its CTAs launch while
+    // this grid runs and wait on it).  Measured against alternatives without
+    // a second launch (cooperative grid barrier; the last CTAs to arrive
+    // reducing behind a ticket counter): +1.7 us for this kernel vs +2.5 /
+    // +4.1 us for those (scripts/bwd_timing.py, config 1).
     cudaLaunchConfig_t rc{};
     rc.gridDim = dim3(static_cast<unsigned>((a.elems + 31) / 32));
     rc.blockDim = dim3(32 * kRedWarps);
