@@ -536,6 +536,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int i = q * 32 + lane;       // TMEM lane: input channel (+64: lo part) / filter row (dW)
     const uint32_t lane_base = static_cast<uint32_t>(q * 32) << 16;
     float* wst = reinterpret_cast<float*>(smem + L.wst);
+    // window start of filter row i for the dW epilogue (a plan table, never
+    // written by a preceding kernel: loaded before the dependency wait, so
+    // the epilogue does not pay a cold load at the end)
+    const int start_i = (a.do_dw && i < a.c_out) ? __ldg(a.starts + row_oc(a, i)) : 0;
     cudaGridDependencySynchronize();
     if (et == 0) TRACE3(53);
     if (a.do_dx) {
@@ -657,7 +661,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const bool live = i < a.c_out && u0 < u1;
       int j0 = 0;
       if (live) {
-        j0 = __ldg(a.starts + row_oc(a, i)) - a.start8;
+        j0 = start_i - a.start8;
         j0 += j0 < 0 ? a.c_in : 0;
       }
       float* dst = a.part + static_cast<int64_t>(sl) * a.elems;
