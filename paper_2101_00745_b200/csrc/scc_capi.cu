@@ -275,7 +275,14 @@ bool fused_bwd_supported(const Plan& p, int64_t plane) {
                           static_cast<int32_t>(p.cfg.group_width));
 }
 
+size_t weight_ws_bytes_plane(const Plan& p, int64_t n, int64_t plane);
 size_t weight_ws_bytes(const Plan& p, int64_t n, int64_t plane) {
+  // the padded-plane path (do_forward_padded) runs the kernels on P4 planes
+  size_t b = weight_ws_bytes_plane(p, n, plane);
+  if (plane % 4 != 0) b = std::max(b, weight_ws_bytes_plane(p, n, (plane + 3) & ~int64_t(3)));
+  return b;
+}
+size_t weight_ws_bytes_plane(const Plan& p, int64_t n, int64_t plane) {
   const size_t cc = weight_cc_workspace_bytes(p.fwd.nblk(), p.fwd.max_block_len, n, plane);
   const size_t tc = tc_weight_supported(p.tc_wgt, plane) ? tc_weight_workspace_bytes(p.tc_wgt, n, plane) : 0;
   const size_t tc2 = tc_wgrad2_supported(p.tc_wgt, plane, static_cast<int32_t>(p.cfg.group_width))
@@ -292,6 +299,67 @@ size_t weight_ws_bytes(const Plan& p, int64_t n, int64_t plane) {
   return std::max(std::max(cc, tc), std::max(tc2, tc3));
 }
 
+// Planes with P % 4 != 0 (7x7 in ResNet-50 stage 4, ...) cannot be described
+// to TMA (16 B strides).  For windows wide enough that the CUDA-core kernels
+// are compute-bound (gw >= 64), the operands are copied into zero-padded
+// [rows][P4] planes and the tensor-core kernels run on those: a 1x1
+// convolution does not care about the spatial shape, the padded pixels are
+// zeros (they add nothing to dW / db) and their outputs are dropped.
+constexpr int64_t kPadMinGw = 64;
+int64_t round4(int64_t v) { return (v + 3) & ~int64_t(3); }
+
+bool pad_tc(const Plan& p, int64_t n, int64_t h, int64_t w, int dir) {
+  const int64_t P = h * w;
+  if (P % 4 == 0 || p.path == SCC_PATH_CUDA_CORE || p.cfg.group_width < kPadMinGw) return false;
+  if (round4(P) > (int64_t(1) << 30)) return false;
+  return choose_path(p, n, 1, round4(P), dir) == SCC_PATH_TENSOR;
+}
+
+float* pad_buffer(Plan& p, cudaStream_t s, size_t bytes) {
+  const int dev = current_device();
+  std::lock_guard<std::mutex> lk(p.panel_mu);
+  PadBuf* b = nullptr;
+  for (PadBuf& e : p.pads) {
+    if (e.device == dev && e.stream == static_cast<void*>(s)) b = &e;
+  }
+  if (b == nullptr) {
+    p.pads.push_back(PadBuf{});
+    b = &p.pads.back();
+    b->device = dev;
+    b->stream = s;
+  }
+  if (b->bytes < bytes) {
+    if (b->ptr) b->retired.push_back(b->ptr);
+    b->ptr = nullptr;
+    cuda_check(cudaMalloc(&b->ptr, bytes), "cudaMalloc(pad scratch)");
+    b->bytes = bytes;
+  }
+  return static_cast<float*>(b->ptr);
+}
+
+void pad(const float* in, float* out, int64_t rows, int64_t P, cudaStream_t s) {
+  cuda_check(launch_pad_planes(in, out, rows, static_cast<int32_t>(P), static_cast<int32_t>(round4(P)), false, s),
+             "pad launch");
+}
+void unpad(const float* in, float* out, int64_t rows, int64_t P, cudaStream_t s) {
+  cuda_check(launch_pad_planes(in, out, rows, static_cast<int32_t>(P), static_cast<int32_t>(round4(P)), true, s),
+             "unpad launch");
+}
+
+void do_forward(Plan& p, int64_t n, int64_t h, int64_t w, const float* x, const float* wt,
+                const float* b, float* y, cudaStream_t s);
+
+void do_forward_padded(Plan& p, int64_t n, int64_t h, int64_t w, const float* x, const float* wt,
+                       const float* b, float* y, cudaStream_t s) {
+  const int64_t P = h * w, P4 = round4(P);
+  const int64_t ci = p.cfg.c_in, co = p.cfg.c_out;
+  float* xp = pad_buffer(p, s, static_cast<size_t>(n * (ci + co) * P4) * sizeof(float));
+  float* yp = xp + n * ci * P4;
+  pad(x, xp, n * ci, P, s);
+  do_forward(p, n, 1, P4, xp, wt, b, yp, s);
+  unpad(yp, y, n * co, P, s);
+}
+
 void do_forward(Plan& p, int64_t n, int64_t h, int64_t w, const float* x, const float* wt,
                 const float* b, float* y, cudaStream_t s) {
   check_extents(n, h, w);
@@ -299,6 +367,10 @@ void do_forward(Plan& p, int64_t n, int64_t h, int64_t w, const float* x, const 
   check_ptr(wt, "weight");
   check_ptr(y, "y");
   check_bias(p, b, "bias");
+  if (pad_tc(p, n, h, w, 0)) {
+    do_forward_padded(p, n, h, w, x, wt, b, y, s);
+    return;
+  }
   const DeviceTables& t = tables(p);
   if (aligned16(x) && aligned16(y) && choose_path(p, n, h, w, 0) == SCC_PATH_TENSOR) {
     TcBandCall c = tc_call(p, false, n, h * w, x, y, wt, b);
@@ -349,6 +421,15 @@ void do_backward_data(Plan& p, int64_t n, int64_t h, int64_t w, const float* dy,
   check_ptr(dy, "dy");
   check_ptr(wt, "weight");
   check_ptr(dx, "dx");
+  if (pad_tc(p, n, h, w, 1)) {
+    const int64_t P = h * w, P4 = round4(P), ci = p.cfg.c_in, co = p.cfg.c_out;
+    float* dyp = pad_buffer(p, s, static_cast<size_t>(n * (ci + co) * P4) * sizeof(float));
+    float* dxp = dyp + n * co * P4;
+    pad(dy, dyp, n * co, P, s);
+    do_backward_data(p, n, 1, P4, dyp, wt, dxp, s, max_ctas);
+    unpad(dxp, dx, n * ci, P, s);
+    return;
+  }
   if (use_fused(p, n, h, w, {dy, dx})) {
     launch_fused(p, n, h, w, dy, nullptr, wt, dx, nullptr, nullptr, nullptr, 0, s);
     return;
@@ -382,6 +463,15 @@ void do_backward_weight(Plan& p, int64_t n, int64_t h, int64_t w, const float* d
   if (ws_bytes < need || (need > 0 && ws == nullptr)) {
     fail(SCC_ERR_ARGUMENT, "workspace too small: need " + std::to_string(need) + " bytes");
   }
+  if (pad_tc(p, n, h, w, 2)) {
+    const int64_t P = h * w, P4 = round4(P), ci = p.cfg.c_in, co = p.cfg.c_out;
+    float* dyp = pad_buffer(p, s, static_cast<size_t>(n * (ci + co) * P4) * sizeof(float));
+    float* xp = dyp + n * co * P4;
+    pad(dy, dyp, n * co, P, s);
+    pad(x, xp, n * ci, P, s);
+    do_backward_weight(p, n, 1, P4, dyp, xp, dw, db, ws, ws_bytes, s, max_ctas);
+    return;
+  }
   if (use_fused(p, n, h, w, {dy, x})) {
     launch_fused(p, n, h, w, dy, x, nullptr, nullptr, dw, db, ws, ws_bytes, s);
     return;
@@ -402,6 +492,7 @@ void do_backward_weight(Plan& p, int64_t n, int64_t h, int64_t w, const float* d
     c.gw = static_cast<int32_t>(p.cfg.group_width);
     c.starts = t.starts;
     c.inv_perm = t.inv_perm;
+    c.perm = t.perm;
     c.rt_info = t.tcw_rt_info;
     c.class_d = t.tcw_class_d;
     c.max_ctas = max_ctas;
@@ -446,6 +537,21 @@ void do_backward(Plan& p, int64_t n, int64_t h, int64_t w, const float* dy, cons
                  const float* wt, float* dx, float* dw, float* db, void* ws, size_t ws_bytes,
                  cudaStream_t s) {
   const int64_t plane = h * w;
+  if (pad_tc(p, n, h, w, 1) && pad_tc(p, n, h, w, 2)) {
+    check_extents(n, h, w);
+    check_ptr(dy, "dy");
+    check_ptr(x, "x");
+    check_ptr(dx, "dx");
+    const int64_t P4 = round4(plane), ci = p.cfg.c_in, co = p.cfg.c_out;
+    float* dyp = pad_buffer(p, s, static_cast<size_t>(n * (2 * ci + co) * P4) * sizeof(float));
+    float* xp = dyp + n * co * P4;
+    float* dxp = xp + n * ci * P4;
+    pad(dy, dyp, n * co, plane, s);
+    pad(x, xp, n * ci, plane, s);
+    do_backward(p, n, 1, P4, dyp, xp, wt, dxp, dw, db, ws, ws_bytes, s);
+    unpad(dxp, dx, n * ci, plane, s);
+    return;
+  }
   if (use_fused(p, n, h, w, {dy, x, dx})) {
     check_extents(n, h, w);
     check_ptr(dy, "dy");
@@ -756,6 +862,12 @@ scc_status_t scc_plan_destroy(scc_plan_t* plan) {
       if (s.ev_out) cudaEventDestroy(static_cast<cudaEvent_t>(s.ev_out));
       if (s.ev_fork) cudaEventDestroy(static_cast<cudaEvent_t>(s.ev_fork));
     }
+    for (const scc::PadBuf& b : plan->pads) {
+      cudaSetDevice(b.device);
+      cudaStreamSynchronize(static_cast<cudaStream_t>(b.stream));
+      if (b.ptr) cudaFree(b.ptr);
+      for (void* q : b.retired) cudaFree(q);
+    }
     for (const scc::ForkJoin& f : plan->forks) {
       cudaSetDevice(f.device);
       cudaStreamSynchronize(static_cast<cudaStream_t>(f.side));
@@ -847,7 +959,7 @@ scc_status_t scc_plan_get_path(const scc_plan_t* plan, int64_t n, int64_t h, int
   return guard([&] {
     scc::check_ptr(plan, "plan");
     scc::check_ptr(path, "path");
-    *path = scc::choose_path(*plan, n, h, w);
+    *path = scc::pad_tc(*plan, n, h, w, 0) ? SCC_PATH_TENSOR : scc::choose_path(*plan, n, h, w);
   });
 }
 

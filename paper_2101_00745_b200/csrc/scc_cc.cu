@@ -470,7 +470,32 @@ __global__ void __launch_bounds__(kThreads) weight_finalize_kernel(const WeightL
   }
 }
 
+// Plane padding for the tensor-core path on planes with P % 4 != 0 (TMA
+// strides must be 16 B multiples): out[r][p] = p < P ? in[r][p] : 0 over
+// P4 = P rounded up to 4 (pad), or the inverse copy (unpad).
+__global__ void __launch_bounds__(256) pad_planes_kernel(const float* __restrict__ in, float* __restrict__ out,
+                                                         int64_t rows, int32_t P, int32_t P4, int32_t unpad) {
+  const int32_t src_w = unpad ? P4 : P, dst_w = unpad ? P : P4;
+  const int64_t total = rows * dst_w;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = i / dst_w;
+    const int32_t c = static_cast<int32_t>(i - r * dst_w);
+    out[i] = c < P ? __ldg(in + r * src_w + c) : 0.f;
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_pad_planes(const float* in, float* out, int64_t rows, int32_t P, int32_t P4, bool unpad,
+                              cudaStream_t s) {
+  const int64_t total = rows * (unpad ? P : P4);
+  if (total <= 0) return cudaSuccess;
+  const unsigned grid = static_cast<unsigned>(std::min<int64_t>((total + 255) / 256, 148 * 16));
+  pad_planes_kernel<<<grid, 256, 0, s>>>(in, out, rows, P, P4, unpad ? 1 : 0);
+  note_launches(1);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_band_cc(const BandLaunch& a, cudaStream_t s) {
   const int64_t q = a.n * a.plane;

@@ -87,6 +87,7 @@ struct TcWeightCall {
   int32_t c_in, c_out, gw;
   const int32_t* starts;    // oc -> window start
   const int32_t* inv_perm;  // oc -> sorted position
+  const int32_t* perm = nullptr;  // sorted position -> oc
   const int32_t* rt_info;   // TcWeightPlan::rt_info (device)
   const int32_t* class_d;
   int32_t max_ctas = 0;     // grid cap (0 = one CTA per SM)
@@ -103,6 +104,10 @@ void note_launches(uint64_t k);
 
 // CUDA-core family -----------------------------------------------------------
 cudaError_t launch_band_cc(const BandLaunch& a, cudaStream_t s);
+// Zero-padded copy [rows][P] -> [rows][P4] (or back, unpad) for the
+// tensor-core path on planes with P % 4 != 0.
+cudaError_t launch_pad_planes(const float* in, float* out, int64_t rows, int32_t P, int32_t P4, bool unpad,
+                              cudaStream_t s);
 size_t weight_cc_workspace_bytes(int32_t nblk, int32_t max_block_len, int64_t n,
                                  int64_t plane);
 cudaError_t launch_weight_cc(const WeightLaunch& a, size_t ws_bytes, cudaStream_t s);

@@ -157,6 +157,17 @@ struct ForkJoin {
   void* ev_join = nullptr;
 };
 
+// Scratch for the padded-plane tensor-core path, per (device, stream).
+// Grown on demand; outgrown buffers are kept until the plan is destroyed
+// (work queued earlier on the stream may still reference them).
+struct PadBuf {
+  int device = -1;
+  void* stream = nullptr;
+  void* ptr = nullptr;
+  size_t bytes = 0;
+  std::vector<void*> retired;
+};
+
 struct Plan {
   scc_config_t cfg{};
   std::vector<int64_t> cycle_starts;  // compute_channel_cycle order
@@ -176,6 +187,7 @@ struct Plan {
   std::mutex host_mu;
   std::deque<HostStaging> staging;
   std::deque<ForkJoin> forks;  // guarded by panel_mu
+  std::deque<PadBuf> pads;     // guarded by panel_mu
 
   int64_t start_of(int64_t oc) const { return (oc * cfg.shift) % cfg.c_in; }
   // Forward-band weight of output channel oc on input channel ic (0 outside

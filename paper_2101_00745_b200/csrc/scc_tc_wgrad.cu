@@ -48,9 +48,11 @@ constexpr int kMaxT = 3;               // TMEM / x stage depth cap
 struct WArgs {
   const int32_t* rt_info;  // per row tile: start8, ncols
   const int32_t* class_d;
-  float* part;             // [split][rt][nc][128][nw]
+  const int32_t* perm;     // sorted position -> oc
+  const int32_t* starts;   // oc -> window start
+  float* part;             // [split][rt][nc][128][nw] (only each row's window columns are written)
   float* pbias;            // [split][rt][128]
-  int32_t n_rt, n_nc, nw, cls, c_in, c_out;
+  int32_t n_rt, n_nc, nw, cls, c_in, c_out, gw;
   int32_t rba, rbb;        // TMA box rows (dy, x)
   int32_t blk;             // 32-pixel atoms per stage (1 or 2)
   int32_t a_stages, t_stages;
@@ -126,6 +128,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   if (threadIdx.x == 0) WTRACE(1);
+  // PDL: the prologue above overlaps the previous kernel's tail; every global
+  // read (dy, x) and write (the partials, which a previous call's finalize
+  // may still read) comes after its completion.
+  cudaGridDependencySynchronize();
+  cudaTriggerProgrammaticLaunchCompletion();
 
   // Row r (0..127) of a dy stage: quarter q = r/32 holds boxes of rba rows,
   // each box [NB atoms][rba rows][128 B].
@@ -316,6 +323,28 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int row = quarter * 32 + lane;
     float* dst = a.part + ((static_cast<int64_t>(split) * a.n_rt + rt) * a.n_nc + nc) * 128 * a.nw +
                  static_cast<int64_t>(row) * a.nw;
+    // Only the float4 groups that overlap this filter's window are written:
+    // the finalize reads nothing else (the band is gw of the tile's nw
+    // columns, so this cuts the partial traffic by nw / gw).
+    // (window start in tile columns; a tile spanning the whole ring starts at
+    // column 0 and its windows may wrap)
+    int j0 = -1;
+    const int pos = rt * 128 + row;
+    if (pos < a.c_out) {
+      j0 = __ldg(a.starts + __ldg(a.perm + pos)) - start8;
+      j0 += j0 < 0 ? a.c_in : 0;
+    }
+    auto in_window = [&](int c4) {  // float4 group at chunk column c4 touches the window
+      if (j0 < 0) return false;
+      const int col = nc * a.nw + c4;
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        int d = col + t - j0;
+        d += d < 0 ? a.c_in : 0;
+        if (d < a.gw) return true;
+      }
+      return false;
+    };
     if (nchunks > 0) {
       mbar_wait_tag(tfull, 0, 25);
       tc_fence_after();
@@ -325,11 +354,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         tmem_ld16(taddr + c0, v);
 #pragma unroll
         for (int j = 0; j < 16; j += 4) {
-          *reinterpret_cast<float4*>(dst + c0 + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+          if (in_window(c0 + j))
+            *reinterpret_cast<float4*>(dst + c0 + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
         }
       }
     } else {
-      for (int c0 = 0; c0 < a.nw; c0 += 4) *reinterpret_cast<float4*>(dst + c0) = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int c0 = 0; c0 < a.nw; c0 += 4)
+        if (in_window(c0)) *reinterpret_cast<float4*>(dst + c0) = make_float4(0.f, 0.f, 0.f, 0.f);
     }
     if (row == 0) WTRACE(26);
   }
@@ -364,6 +395,8 @@ __device__ __forceinline__ int64_t fin_base(const FArgs& a, int oc, int k) {
 // in ascending order; neighbouring threads read neighbouring window slots, so
 // every split plane is read coalesced.
 __global__ void __launch_bounds__(256) tc_weight_finalize_wide(const FArgs a) {
+  cudaGridDependencySynchronize();
+  cudaTriggerProgrammaticLaunchCompletion();
   const int64_t nw_out = static_cast<int64_t>(a.c_out) * a.gw;
   const int64_t total = nw_out + (a.dbias ? a.c_out : 0);
   const int64_t stride = static_cast<int64_t>(a.n_rt) * a.n_nc * 128 * a.nw;
@@ -392,6 +425,8 @@ __global__ void __launch_bounds__(256) tc_weight_finalize_wide(const FArgs a) {
 constexpr int kFinWarps = 32;
 __global__ void __launch_bounds__(32 * kFinWarps) tc_weight_finalize(const FArgs a) {
   __shared__ float red[kFinWarps][33];
+  cudaGridDependencySynchronize();
+  cudaTriggerProgrammaticLaunchCompletion();
   const int64_t nw_out = static_cast<int64_t>(a.c_out) * a.gw;
   const int64_t total = nw_out + (a.dbias ? a.c_out : 0);
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
@@ -521,6 +556,9 @@ cudaError_t launch_weight_tc(const TcWeightPlan& tw, const TcWeightCall& call, c
   WArgs a{};
   a.rt_info = call.rt_info;
   a.class_d = call.class_d;
+  a.perm = call.perm;
+  a.starts = call.starts;
+  a.gw = call.gw;
   a.part = part;
   a.pbias = pbias;
   a.n_rt = tw.n_rt;
@@ -553,8 +591,17 @@ cudaError_t launch_weight_tc(const TcWeightPlan& tw, const TcWeightCall& call, c
     }
   }
   const unsigned grid = static_cast<unsigned>(g.splits) * tw.n_rt * tw.n_nc;
-  tc_weight_kernel<<<grid, kThreads, g.smem, s>>>(tdy, tx, a);
-  cudaError_t e = cudaGetLastError();
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = g.smem;
+  cfg.stream = s;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, tc_weight_kernel, tdy, tx, a);
   if (e != cudaSuccess) return e;
   FArgs f{};
   f.part = part;
@@ -572,14 +619,21 @@ cudaError_t launch_weight_tc(const TcWeightPlan& tw, const TcWeightCall& call, c
   f.c_out = call.c_out;
   f.gw = call.gw;
   const int64_t outs = static_cast<int64_t>(call.c_out) * call.gw + (call.dbias ? call.c_out : 0);
+  cudaLaunchConfig_t fc{};
+  fc.stream = s;
+  fc.attrs = attr;
+  fc.numAttrs = 1;
   if (outs >= 65536) {
-    const int fgrid = static_cast<int>(std::min<int64_t>((outs + 255) / 256, 148 * 8));
-    tc_weight_finalize_wide<<<fgrid, 256, 0, s>>>(f);
+    fc.gridDim = dim3(static_cast<unsigned>(std::min<int64_t>((outs + 255) / 256, 148 * 8)));
+    fc.blockDim = dim3(256);
+    e = cudaLaunchKernelEx(&fc, tc_weight_finalize_wide, f);
   } else {
-    tc_weight_finalize<<<static_cast<unsigned>((outs + 31) / 32), 32 * kFinWarps, 0, s>>>(f);
+    fc.gridDim = dim3(static_cast<unsigned>((outs + 31) / 32));
+    fc.blockDim = dim3(32 * kFinWarps);
+    e = cudaLaunchKernelEx(&fc, tc_weight_finalize, f);
   }
   note_launches(2);
-  return cudaGetLastError();
+  return e;
 }
 
 }  // namespace scc

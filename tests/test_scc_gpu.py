@@ -523,3 +523,19 @@ def test_non_finite_inputs_contract(port, path):
         assert fin[1].all(), f"{name}: sample 1 has no non-finite input"
         scale = np.abs(r[np.isfinite(r)]).max()
         assert np.abs(g[fin] - r[fin]).max() <= tol * scale, name
+
+
+@pytest.mark.parametrize("shape", [(512, 512, 2, "50%", 4, 7, 7), (256, 128, 2, "25%", 3, 5, 5),
+                                   (128, 256, 2, "50%", 5, 3, 3), (256, 256, 4, "75%", 2, 9, 9)],
+                         ids=lambda s: f"{s[0]}to{s[1]}_cg{s[2]}_{s[5]}x{s[6]}")
+def test_padded_plane_tensor_path(port, shape):
+    """Planes with P % 4 != 0 (ResNet-50 stage 4: 7x7) and gw >= 64 run the
+    tensor-core kernels on zero-padded [rows][P4] copies; parity against the
+    oracle, fused == separate backward, and the path is reported as tensor."""
+    from paper_2101_00745_b200 import _lib
+    ci, co, cg, ov, n, h, w = shape
+    cfg = make_cfg(ci, co, cg, ov, True, _lib.SCC_PATH_AUTO)
+    assert cfg.path_for(n, h, w) == _lib.SCC_PATH_TENSOR
+    rng = np.random.default_rng(7)
+    x, wt, b, dy = rand_problem(rng, ci, co, cfg.group_width, n, h, w, True)
+    check_against_oracle(port, cfg, x, wt, b, dy)
