@@ -30,7 +30,7 @@ SCC_OVERLAP_RATIO = 1
 SCC_PATH_AUTO = 0
 SCC_PATH_CUDA_CORE = 1
 SCC_PATH_TENSOR = 2
-SCC_PATH_TENSOR_V1 = 3
+SCC_PATH_TENSOR_STREAMED = 3
 
 # Every symbol include/scc_b200.h declares (tests assert the .so exports them).
 EXPORTS = (

@@ -265,12 +265,7 @@ WeightLaunch weight_args(const Plan& p, const DeviceTables& t, int64_t n, int64_
 // that fused and separate calls agree bitwise, the separate backward-data and
 // backward-weight entry points too, whenever its geometry fits.
 bool fused_bwd_supported(const Plan& p, int64_t plane) {
-  if (p.path == SCC_PATH_TENSOR_V1 || p.path == SCC_PATH_CUDA_CORE) return false;
-  static const bool off = [] {
-    const char* e = getenv("SCC_NO_FUSED_BWD");
-    return e != nullptr && e[0] == '1';
-  }();
-  if (off) return false;
+  if (p.path == SCC_PATH_TENSOR_STREAMED || p.path == SCC_PATH_CUDA_CORE) return false;
   return tc_bwd_supported(p.tc_wgt, plane, static_cast<int32_t>(p.cfg.c_in), static_cast<int32_t>(p.cfg.c_out),
                           static_cast<int32_t>(p.cfg.group_width));
 }
@@ -374,7 +369,7 @@ void do_forward(Plan& p, int64_t n, int64_t h, int64_t w, const float* x, const 
   const DeviceTables& t = tables(p);
   if (aligned16(x) && aligned16(y) && choose_path(p, n, h, w, 0) == SCC_PATH_TENSOR) {
     TcBandCall c = tc_call(p, false, n, h * w, x, y, wt, b);
-    if (p.path != SCC_PATH_TENSOR_V1 && tc_band2_supported(p.tc_fwd, h * w, static_cast<int32_t>(p.cfg.c_out))) {
+    if (p.path != SCC_PATH_TENSOR_STREAMED && tc_band2_supported(p.tc_fwd, h * w, static_cast<int32_t>(p.cfg.c_out))) {
       cuda_check(launch_band_tc2(p.tc_fwd, t.tc_fwd, c, p.cfg.shift, static_cast<int32_t>(p.cfg.c_out), s),
                  "forward (tensor) launch");
       return;
@@ -438,7 +433,7 @@ void do_backward_data(Plan& p, int64_t n, int64_t h, int64_t w, const float* dy,
   if (aligned16(dy) && aligned16(dx) && choose_path(p, n, h, w, 1) == SCC_PATH_TENSOR) {
     TcBandCall c = tc_call(p, true, n, h * w, dy, dx, wt, nullptr);
     c.max_ctas = max_ctas;
-    if (p.path != SCC_PATH_TENSOR_V1 && tc_band2_supported(p.tc_bwd, h * w, static_cast<int32_t>(p.cfg.c_out))) {
+    if (p.path != SCC_PATH_TENSOR_STREAMED && tc_band2_supported(p.tc_bwd, h * w, static_cast<int32_t>(p.cfg.c_out))) {
       cuda_check(launch_band_tc2(p.tc_bwd, t.tc_bwd, c, p.cfg.shift, static_cast<int32_t>(p.cfg.c_out), s),
                  "backward-data (tensor) launch");
       return;
@@ -496,7 +491,7 @@ void do_backward_weight(Plan& p, int64_t n, int64_t h, int64_t w, const float* d
     c.rt_info = t.tcw_rt_info;
     c.class_d = t.tcw_class_d;
     c.max_ctas = max_ctas;
-    if (p.path != SCC_PATH_TENSOR_V1 && tc_wgrad2_supported(p.tc_wgt, h * w, c.gw)) {
+    if (p.path != SCC_PATH_TENSOR_STREAMED && tc_wgrad2_supported(p.tc_wgt, h * w, c.gw)) {
       cuda_check(launch_wgrad2(p.tc_wgt, c, t.perm, s), "backward-weight (tensor) launch");
       return;
     }
@@ -568,20 +563,18 @@ void do_backward(Plan& p, int64_t n, int64_t h, int64_t w, const float* dy, cons
     return;
   }
   const bool both2 = aligned16(dy) && aligned16(x) && aligned16(dx) &&
-                     p.path != SCC_PATH_TENSOR_V1 && p.path != SCC_PATH_CUDA_CORE &&
+                     p.path != SCC_PATH_TENSOR_STREAMED && p.path != SCC_PATH_CUDA_CORE &&
                      choose_path(p, n, h, w, 1) == SCC_PATH_TENSOR &&
                      choose_path(p, n, h, w, 2) == SCC_PATH_TENSOR &&
                      tc_band2_supported(p.tc_bwd, plane, static_cast<int32_t>(p.cfg.c_out)) &&
                      tc_wgrad2_supported(p.tc_wgt, plane, static_cast<int32_t>(p.cfg.group_width));
-  const char* env = getenv("SCC_SERIAL_BACKWARD");
-  if (!both2 || (env != nullptr && env[0] == '1')) {
+  if (!both2) {
     do_backward_data(p, n, h, w, dy, wt, dx, s);
     do_backward_weight(p, n, h, w, dy, x, dw, db, ws, ws_bytes, s);
     return;
   }
   const int nsm = device_sms();
-  int32_t half = nsm / 2;
-  if (const char* sp = getenv("SCC_BWD_SPLIT")) half = atoi(sp);
+  const int32_t half = nsm / 2;
   ForkJoin& f = fork_join(p, s);
   cudaStream_t side = static_cast<cudaStream_t>(f.side);
   cuda_check(cudaEventRecord(static_cast<cudaEvent_t>(f.ev_fork), s), "cudaEventRecord(fork)");
@@ -947,7 +940,7 @@ scc_status_t scc_plan_set_path(scc_plan_t* plan, int32_t path) {
   return guard([&] {
     scc::check_ptr(plan, "plan");
     if (path != SCC_PATH_AUTO && path != SCC_PATH_CUDA_CORE && path != SCC_PATH_TENSOR &&
-        path != SCC_PATH_TENSOR_V1) {
+        path != SCC_PATH_TENSOR_STREAMED) {
       scc::fail(SCC_ERR_ARGUMENT, "unknown path " + std::to_string(path));
     }
     plan->path = path;

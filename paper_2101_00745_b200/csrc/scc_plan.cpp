@@ -219,10 +219,6 @@ void build_tc_side(const Plan& p, bool bwd, TcBandPlan& tp) {
     }
     if (max_arc <= 96) best = 64;
   }
-  if (const char* e = getenv("SCC_TC_NT")) {  // experiment override
-    const int v = atoi(e);
-    if (v == 64 || v == 128) best = v;
-  }
   tp.nt = best;
   tp.n_rt = (rows_total + tp.nt - 1) / tp.nt;
   tp.rows.assign(static_cast<size_t>(tp.n_rt) * tp.nt, -1);

@@ -598,9 +598,7 @@ static cudaError_t launch_tc_nt(const TcBandPlan& tp, const TcDeviceTables& dt,
       int max_rt = 0;
       for (int rt = 0; rt < tp.n_rt; ++rt) max_rt = std::max(max_rt, tp.rt_info[4 * rt + 3]);
       const int64_t grid_rt = grid / tp.n_rt * tp.n_rt;
-      const char* no_rt_env = getenv("SCC_BAND_NO_RT_PANEL");  // A/B knob
-      const bool no_rt = no_rt_env != nullptr && no_rt_env[0] == '1';
-      if (!no_rt && grid_rt >= tp.n_rt && grid_rt >= grid - grid / 16 &&
+      if (grid_rt >= tp.n_rt && grid_rt >= grid - grid / 16 &&
           max_rt * C::kBBytes + 5 * kABytes <= rest) {
         sm.b_resident = 2;
         sm.b_bytes = max_rt * C::kBBytes;
@@ -610,7 +608,6 @@ static cudaError_t launch_tc_nt(const TcBandPlan& tp, const TcDeviceTables& dt,
         sm.b_resident = 0;
         sm.b_bytes = C::kBBytes;
         sm.b_stages = 3;
-        if (const char* e = getenv("SCC_BAND_BSTAGES")) sm.b_stages = std::max(2, std::min(C::kMaxBStages, atoi(e)));
       }
     }
     const int b_total = sm.b_resident ? sm.b_bytes : sm.b_stages * C::kBBytes;

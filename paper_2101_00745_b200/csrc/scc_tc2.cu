@@ -772,7 +772,6 @@ cudaError_t launch_tc2_nt(const TcBandPlan& tp, const TcDeviceTables& dt, const 
     a.fwd4 = (!BWD && a.w_staged && call.gw % 4 == 0 && call.c_in % 4 == 0 && shift % 4 == 0) ? 1 : 0;
   }
   a.stages = band2_stages<NT>(tp, a.store_mode, 0, a.scratch);
-  if (const char* e = getenv("SCC_TC2_MAXSTAGES")) a.stages = std::max(2, std::min(a.stages, atoi(e)));
   a.plane = P;
   const int64_t units = call.n * a.nbps;
   if (units > (1ll << 30)) return cudaErrorInvalidValue;

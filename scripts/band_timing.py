@@ -20,10 +20,10 @@ def fwd(i, s):
     _lib.check(L.scc_forward_f32(cfg.handle, N, H, W, xs[i].data_ptr(), wts.weight.data_ptr(), wts.bias.data_ptr(), ys[i].data_ptr(), s))
 def bwdd(i, s):
     _lib.check(L.scc_backward_data_f32(cfg.handle, N, H, W, dys[i].data_ptr(), wts.weight.data_ptr(), dxs[i].data_ptr(), s))
-for path, name in ((_lib.SCC_PATH_TENSOR_V1, "gen1"), (_lib.SCC_PATH_TENSOR, "gen2")):
+for path, name in ((_lib.SCC_PATH_TENSOR_STREAMED, "gen1"), (_lib.SCC_PATH_TENSOR, "gen2")):
     cfg.set_path(path)
     for op, f, nbytes in (("fwd", fwd, 4 * N * H * W * (CI + CO)), ("bwd_data", bwdd, 4 * N * H * W * (CI + CO))):
-        if path == _lib.SCC_PATH_TENSOR_V1 and len(sys.argv) > 7: continue
+        if path == _lib.SCC_PATH_TENSOR_STREAMED and len(sys.argv) > 7: continue
         st = torch.cuda.Stream()
         with torch.cuda.stream(st):
             for i in range(R): f(i, st.cuda_stream)

@@ -1,7 +1,7 @@
 """Panel-build micro-benchmark (tests/cuda/build_probe.cu)."""
 import ctypes as C, os
 import torch
-HERE = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HERE = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 lib = C.CDLL(os.path.join(HERE, "tests", "cuda", "_build", "build_probe.so"))
 lib.build_probe.argtypes = [C.c_void_p, C.c_int, C.c_int]
 for warm in (0, 1):

@@ -1,7 +1,7 @@
 """Epilogue cost probe (tests/cuda/epi_probe.cu): cycles per 32-column group."""
 import ctypes as C, os
 import torch
-HERE = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HERE = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 lib = C.CDLL(os.path.join(HERE, "tests", "cuda", "_build", "epi_probe.so"))
 lib.epi_probe.argtypes = [C.c_void_p, C.c_int, C.c_int]
 names = {0: "LDTM x32 + wait", 1: "LDTM + 32 STS", 2: "32 STS only", 3: "LDTM + 32 STS with MMAs running"}

@@ -1,7 +1,7 @@
 """Shared-memory latency / STS throughput probe (tests/cuda/lds_probe.cu)."""
 import ctypes as C, os
 import torch
-HERE = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HERE = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 lib = C.CDLL(os.path.join(HERE, "tests", "cuda", "_build", "lds_probe.so"))
 lib.lds_probe.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int]
 for smem in (65536, 226 * 1024):

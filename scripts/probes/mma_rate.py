@@ -3,7 +3,7 @@ cycles per MMA, M=128 K=8, for N in 32..256, A in TMEM or SMEM, B MN- or
 K-major; one CTA per SM, median over CTAs."""
 import ctypes as C, os, subprocess, sys
 import torch
-HERE = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HERE = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 so = os.path.join(HERE, "tests", "cuda", "_build", "mma_rate_probe.so")
 lib = C.CDLL(so)
 out = torch.zeros(148, dtype=torch.int64, device="cuda")

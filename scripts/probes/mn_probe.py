@@ -2,7 +2,7 @@
 assignment makes a TMA SWIZZLE_128B_ATOM_32B tile a valid MN-major operand."""
 import ctypes as C, os, sys
 import numpy as np, torch
-HERE = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HERE = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 lib = C.CDLL(os.path.join(HERE, "tests", "cuda", "_build", "mn_probe.so"))
 lib.mn_probe.argtypes = [C.c_void_p] * 3 + [C.c_int] * 3
 def trunc(a):

@@ -1,7 +1,7 @@
 """Run one SCC op a few times on config 1 or $SCC_SHAPE (for ncu captures).
 usage: one_op.py fwd|bwd_data|bwd_weight|bwd [path]"""
 import os, sys
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import torch
 import paper_2101_00745_b200 as scc
 from paper_2101_00745_b200 import _lib

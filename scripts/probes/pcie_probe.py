@@ -2,7 +2,7 @@
 config-1 step's bytes (25.2 MB each way), alone and concurrently on two
 streams, plus scc_fwd_bwd_host_f32 at 1..8 chunks."""
 import os, sys, time, json
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import torch
 torch.cuda.set_device(0)
 nb = 25182720 // 4

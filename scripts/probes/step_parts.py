@@ -2,7 +2,7 @@
 concurrent scc_backward_f32), forward+backward -- config 1, inputs rotated
 over 8 buffer sets."""
 import os, sys
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import torch
 import paper_2101_00745_b200 as scc
 from paper_2101_00745_b200 import _lib

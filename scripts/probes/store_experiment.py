@@ -1,6 +1,6 @@
 """Diagnostic: epilogue store throughput vs output allocation type."""
 import ctypes as C, os, sys, time
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import torch
 import paper_2101_00745_b200 as scc
 from paper_2101_00745_b200 import _lib

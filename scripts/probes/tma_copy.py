@@ -2,7 +2,7 @@
 read once, written twice into y [32][128][1024]; us per launch (back to back)."""
 import ctypes as C, os
 import torch
-root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+root = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 L = C.CDLL(os.path.join(root, "tests/cuda/_build/tma_copy_probe.so")); L.tma_copy.restype = C.c_float
 L.tma_copy.argtypes = [C.c_void_p, C.c_void_p] + [C.c_int] * 5
 x = torch.randn(32, 64, 1024, device="cuda"); y = torch.empty(32, 128, 1024, device="cuda")

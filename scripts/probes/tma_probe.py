@@ -1,5 +1,5 @@
 import ctypes as C, os, subprocess, sys, torch
-root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+root = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 so = os.path.join(root, "tests/cuda/_build/tma_probe.so")
 if not os.path.exists(so):
     subprocess.check_call(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O2", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",

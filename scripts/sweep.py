@@ -96,7 +96,7 @@ def run_shape(c, cg, co, hw, n, L, st):
     parts = {}
     if PARTS:
         parts = {"bwd_data": round(time_graph(bdata, sets, st), 2), "bwd_weight": round(time_graph(bweight, sets, st), 2)}
-    path = {0: "auto", 1: "cuda_core", 2: "tensor", 3: "tensor_v1"}.get(cfg.path_for(n, hw, hw), "?") \
+    path = {0: "auto", 1: "cuda_core", 2: "tensor", 3: "tensor_streamed"}.get(cfg.path_for(n, hw, hw), "?") \
         if hasattr(cfg, "path_for") else None
     del xs, dys, ys, dxs
     byt = {"fwd": 4 * n * P * 2 * c, "bwd": 4 * n * P * 3 * c, "step": 4 * n * P * 5 * c}

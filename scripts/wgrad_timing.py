@@ -15,7 +15,7 @@ ws = torch.empty(cfg.workspace_bytes(N, H, W), dtype=torch.uint8, device="cuda")
 dw = torch.empty(CO * 32, device="cuda"); db = torch.empty(CO, device="cuda")
 def bw(i, s):
     _lib.check(L.scc_backward_weight_f32(cfg.handle, N, H, W, dys[i].data_ptr(), xs[i].data_ptr(), dw.data_ptr(), db.data_ptr(), ws.data_ptr(), ws.numel(), s))
-for path, name in ((_lib.SCC_PATH_TENSOR_V1, "gen1"), (_lib.SCC_PATH_TENSOR, "gen2")):
+for path, name in ((_lib.SCC_PATH_TENSOR_STREAMED, "gen1"), (_lib.SCC_PATH_TENSOR, "gen2")):
     cfg.set_path(path)
     st = torch.cuda.Stream()
     with torch.cuda.stream(st):

@@ -37,15 +37,15 @@ def _paths():
     try:
         cfg.set_path(_lib.SCC_PATH_TENSOR)
         out.append(_lib.SCC_PATH_TENSOR)
-        cfg.set_path(_lib.SCC_PATH_TENSOR_V1)
-        out.append(_lib.SCC_PATH_TENSOR_V1)
+        cfg.set_path(_lib.SCC_PATH_TENSOR_STREAMED)
+        out.append(_lib.SCC_PATH_TENSOR_STREAMED)
     except scc.ArgumentError:
         pass
     return out
 
 
 PATHS = _paths() if torch.cuda.is_available() else [1]
-PATH_IDS = {1: "cuda_core", 2: "tensor", 3: "tensor_v1"}
+PATH_IDS = {1: "cuda_core", 2: "tensor", 3: "tensor_streamed"}
 
 
 def make_cfg(ci, co, cg, ov, hb, path):
