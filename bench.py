@@ -491,8 +491,10 @@ def run_ours(args):
         models = {}
         runs = {"resnet18": dict(batch=128, steps=20, warmup=5),            # C3 (CIFAR shape)
                 "vgg16": dict(batch=128, steps=20, warmup=5),               # C2 (CIFAR shape)
-                "resnet50": dict(batch=256, steps=8, warmup=3, image=224,   # C4 (ImageNet shape)
-                                 num_classes=1000)}
+                "resnet50": dict(batch=256, steps=8, warmup=3, image=224,   # C4 (ImageNet shape;
+                                 num_classes=1000),                         # paper rule, 12.87 M)
+                "resnet50_all": dict(batch=256, steps=8, warmup=3, image=224,  # every 1x1 -> SCC
+                                     num_classes=1000)}
         for name, kw in runs.items():
             try:
                 models[name] = train_throughput(name, **kw)

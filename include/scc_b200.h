@@ -24,6 +24,14 @@
  * across streams and plans, and deterministic (no floating-point atomics), so
  * repeated calls are bitwise identical — the GPU analogue of the reference's
  * thread-count invariance (kernel.hpp:43-48, kernel_test.cpp:209-241).
+ *
+ * Activation pointers should be 16-byte aligned: the vector / TMA kernels
+ * need it, and a misaligned buffer takes the scalar CUDA-core kernels.
+ * Non-finite activations: the banded tensor-core kernels multiply explicit
+ * zero weights outside each window, so an Inf/NaN input reaches every output
+ * sharing its pixel and row tile -- a superset of the outputs the reference
+ * makes non-finite (kernel.cpp:45-60 only touches in-window channels);
+ * finite inputs are unaffected.
  */
 #ifndef SCC_B200_H_
 #define SCC_B200_H_

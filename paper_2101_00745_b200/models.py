@@ -167,7 +167,11 @@ class SCCResNet50(nn.Module):
         return self.fc(torch.flatten(nn.functional.adaptive_avg_pool2d(y, 1), 1))
 
 
-MODELS = {"resnet18": SCCResNet18, "vgg16": SCCVGG16, "resnet50": SCCResNet50}
+def _resnet50_all(num_classes: int = 1000, cg: int = 2, co="50%", device=None):
+    return SCCResNet50(num_classes, cg, co, device, rule="all")
+
+
+MODELS = {"resnet18": SCCResNet18, "vgg16": SCCVGG16, "resnet50": SCCResNet50, "resnet50_all": _resnet50_all}
 
 
 def scc_layers(model: nn.Module):

@@ -1,0 +1,11 @@
+#!/bin/bash
+# Round-2 measurement: tests, bench (+ reference arm), launch list, full ncu of
+# the c1 forward and fused backward kernels.
+mkdir -p gpurun_out
+timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/gpu_tests.log 2>&1; tail -1 gpurun_out/gpu_tests.log
+timeout 900 python bench.py --steps 200 --warmup 10 > gpurun_out/bench.json 2> gpurun_out/bench.err; tail -1 gpurun_out/bench.json | cut -c1-400
+timeout 300 python bench.py --impl reference --steps 10 --warmup 3 > gpurun_out/bench_ref.json 2>&1; tail -1 gpurun_out/bench_ref.json | cut -c1-300
+scripts/ncu_launches.sh gpurun_out/launches.csv --no-graph > gpurun_out/launches.txt 2>&1; cat gpurun_out/launches.txt
+for k in tc_bwd_kernel "tc_band2_kernel"; do
+  timeout 300 ncu --set full --clock-control none --import-source on -k regex:"$k" -s 3 -c 1 -o gpurun_out/prof_$k -f python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu-baseline --no-models --no-graph --no-traffic > /dev/null 2>&1; ls -la gpurun_out/prof_$k.ncu-rep
+done

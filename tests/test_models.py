@@ -41,7 +41,7 @@ RESNET50_SHAPES = [(64, 64, 56), (128, 128, 28), (256, 256, 14), (512, 512, 7),
 def _shapes():
     out = set(RESNET50_SHAPES)
     for name, cls in models.MODELS.items():
-        if name == "resnet50":
+        if name.startswith("resnet50"):
             continue
         m = cls()
         size = {"resnet18": [32, 32, 16, 16, 8, 8, 4, 4], "vgg16": [32, 16, 16, 8, 8, 8, 4, 4, 4, 2, 2, 2]}[name]
