@@ -190,7 +190,11 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 
   if (warp == 0) {
     // ---------------- producer: activation ring (+ streamed weight panel) ----------------
-    if (elect_one()) {
+    // The lanes issue a stage's boxes in parallel (one box each): a TMA
+    // instruction holds its issuing thread ~0.1-0.3 us and short class runs
+    // cut a stage into up to 4 boxes.
+    {
+      const int lane = threadIdx.x & 31;
       int sa = 0;
       uint32_t pa = 0;
       int sb = 0;
@@ -212,15 +216,21 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           // activations: [32 ring rows][128 px], boxes of rb rows
           mbar_wait_tag(&a_free[sa], pa ^ 1u, 1);
           const int steps = min(4, nk8 - 4 * c);
-          mbar_expect_tx(&a_full[sa], steps * 8 * TM * 4);
-          for (int r = 0; r < steps * 8; r += a.rb) {
-            int pos = start8 + 32 * c + r;
-            while (pos >= a.ring) pos -= a.ring;
-            const int cl = pos / a.cls, j = pos - cl * a.cls;
-            tma_load_3d(a_ring + sa * kABytes + r * (TM * 4), &tmap, &a_full[sa], tc.p0,
-                        __ldg(a.class_d + cl), tc.n * a.rows_per_sample_3d + j);
+          if (lane == 0) mbar_expect_tx(&a_full[sa], steps * 8 * TM * 4);
+          __syncwarp();
+          {
+            const int r = lane * a.rb;
+            if (r < steps * 8) {
+              int pos = start8 + 32 * c + r;
+              while (pos >= a.ring) pos -= a.ring;
+              const int cl = pos / a.cls, j = pos - cl * a.cls;
+              tma_load_3d(a_ring + sa * kABytes + r * (TM * 4), &tmap, &a_full[sa], tc.p0,
+                          __ldg(a.class_d + cl), tc.n * a.rows_per_sample_3d + j);
+            }
           }
+          __syncwarp();
           advance(sa, pa, SA);
+          if (lane != 0) continue;
           if (a.sm.b_resident == 1 && t == blockIdx.x && c == 0) {
             panel_ready();
             mbar_expect_tx(&b_full[0], a.panel_floats * 4);

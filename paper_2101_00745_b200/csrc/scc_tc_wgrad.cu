@@ -150,60 +150,71 @@ __global__ void __launch_bounds__(kThreads, 1)
   const bool dy_role = warp == 0;
   const bool x_role = warp == 10;
   if (dy_role) {
-    if (elect_one()) {
-      int sa = 0;
-      uint32_t pa = 0;
-      const int rows_a = min(128, a.c_out - rt * 128);
-      const int a_boxes_rows = (rows_a + a.rba - 1) / a.rba * a.rba;
-      for (int64_t qc = q_begin; qc < q_end; ++qc) {
-        const int n = static_cast<int>(qc / a.pcs);
-        const int p0 = static_cast<int>(qc - static_cast<int64_t>(n) * a.pcs) * kpix;
-        if (qc - q_begin == 1) WTRACE(27);
-        mbar_wait_tag(&a_free[sa], pa ^ 1u, 20);
+    // All 32 lanes issue the stage's boxes (one box per lane): a TMA
+    // instruction holds its issuing thread ~0.1-0.3 us, and short class runs
+    // (co = 25 / 75 %, cg = 8) give up to 16 boxes per stage.  (All lanes
+    // poll the ring barrier: polling from one lane measured slower.)
+    int sa = 0;
+    uint32_t pa = 0;
+    const int rows_a = min(128, a.c_out - rt * 128);
+    const int a_boxes_rows = (rows_a + a.rba - 1) / a.rba * a.rba;
+    const int nbox = a_boxes_rows / a.rba;
+    for (int64_t qc = q_begin; qc < q_end; ++qc) {
+      const int n = static_cast<int>(qc / a.pcs);
+      const int p0 = static_cast<int>(qc - static_cast<int64_t>(n) * a.pcs) * kpix;
+      if (lane == 0 && qc - q_begin == 1) WTRACE(27);
+      mbar_wait_tag(&a_free[sa], pa ^ 1u, 20);
+      if (lane == 0) {
         if (qc - q_begin == 1) WTRACE(28);
         mbar_expect_tx(&a_full[sa], a_boxes_rows * NB * 128);
-        uint8_t* ad = a_ring + sa * a_stage_bytes;
-        for (int r = 0; r < a_boxes_rows; r += a.rba) {
-          const int i0 = rt * 128 + r;
-          const int cl = i0 / a.cls, j = i0 - cl * a.cls;
-          const int d = __ldg(a.class_d + cl);
-          if (a.dy4d) {
-            tma_load_4d(ad + a_row_off(r, 0), &tdy, &a_full[sa], 0, d, n * a.cls + j, p0 / kAtom);
-          } else {
-            for (int b = 0; b < NB; ++b) {
-              tma_load_3d(ad + a_row_off(r, b), &tdy, &a_full[sa], p0 + b * kAtom, d, n * a.cls + j);
-            }
+      }
+      __syncwarp();
+      uint8_t* ad = a_ring + sa * a_stage_bytes;
+      for (int bi = lane; bi < nbox; bi += 32) {
+        const int r = bi * a.rba;
+        const int i0 = rt * 128 + r;
+        const int cl = i0 / a.cls, j = i0 - cl * a.cls;
+        const int d = __ldg(a.class_d + cl);
+        if (a.dy4d) {
+          tma_load_4d(ad + a_row_off(r, 0), &tdy, &a_full[sa], 0, d, n * a.cls + j, p0 / kAtom);
+        } else {
+          for (int b = 0; b < NB; ++b) {
+            tma_load_3d(ad + a_row_off(r, b), &tdy, &a_full[sa], p0 + b * kAtom, d, n * a.cls + j);
           }
         }
-        advance(sa, pa, SA);
+      }
+      __syncwarp();
+      advance(sa, pa, SA);
+      if (lane == 0) {
         if (qc - q_begin == 1) WTRACE(29);
         if (qc - q_begin < 8) WTRACE(2 + (qc - q_begin));
       }
     }
   } else if (x_role) {
-    if (elect_one()) {
-      int sb = 0;
-      uint32_t pb = 0;
-      const int cols_b = min(a.nw, ncols - nc * a.nw);
-      const int b_boxes_rows = (cols_b + a.rbb - 1) / a.rbb * a.rbb;
-      for (int64_t qc = q_begin; qc < q_end; ++qc) {
-        const int n = static_cast<int>(qc / a.pcs);
-        const int p0 = static_cast<int>(qc - static_cast<int64_t>(n) * a.pcs) * kpix;
-        mbar_wait_tag(&t_free[sb], pb ^ 1u, 21);
+    int sb = 0;
+    uint32_t pb = 0;
+    const int cols_b = min(a.nw, ncols - nc * a.nw);
+    const int b_boxes_rows = (cols_b + a.rbb - 1) / a.rbb * a.rbb;
+    const int nbr = b_boxes_rows / a.rbb;
+    for (int64_t qc = q_begin; qc < q_end; ++qc) {
+      const int n = static_cast<int>(qc / a.pcs);
+      const int p0 = static_cast<int>(qc - static_cast<int64_t>(n) * a.pcs) * kpix;
+      mbar_wait_tag(&t_free[sb], pb ^ 1u, 21);
+      if (lane == 0) {
         if (qc - q_begin == 1) WTRACE(30);
         mbar_expect_tx(&b_full[sb], b_boxes_rows * NB * 128);
-        uint8_t* bd = b_ring + sb * b_stage_bytes;
-        for (int b = 0; b < NB; ++b) {
-          for (int r = 0; r < b_boxes_rows; r += a.rbb) {
-            int pos = start8 + nc * a.nw + r;
-            while (pos >= a.c_in) pos -= a.c_in;
-            tma_load_3d(bd + b * b_blk_bytes + r * 128, &tx, &b_full[sb], p0 + b * kAtom, 0,
-                        n * a.c_in + pos);
-          }
-        }
-        if (qc - q_begin == 1) WTRACE(31);
-        advance(sb, pb, ST);
       }
+      __syncwarp();
+      uint8_t* bd = b_ring + sb * b_stage_bytes;
+      for (int bi = lane; bi < NB * nbr; bi += 32) {
+        const int b = bi / nbr, r = (bi - b * nbr) * a.rbb;
+        int pos = start8 + nc * a.nw + r;
+        while (pos >= a.c_in) pos -= a.c_in;
+        tma_load_3d(bd + b * b_blk_bytes + r * 128, &tx, &b_full[sb], p0 + b * kAtom, 0, n * a.c_in + pos);
+      }
+      __syncwarp();
+      if (lane == 0 && qc - q_begin == 1) WTRACE(31);
+      advance(sb, pb, ST);
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer (dy hi/lo from TMEM, x from SMEM) ----------------
