@@ -79,15 +79,17 @@ __device__ unsigned long long g_cta3[2 * 256];
 #endif
 
 constexpr int kThreads = 384;
-constexpr int kSlots = 3;             // TMA pair slots in the ring
+constexpr int kSlots = 3;             // raw TMA pair slots (dy | x per block); x_lo is written in place
+constexpr int kStages = 2;            // dy_lo pairs and TMEM dW A stages
 constexpr int kSlices = 148;          // pixel slices (dW partials) per launch = CTAs (one per SM)
 constexpr int kSmemLimit = 227 * 1024;
 constexpr int kMaxGw = 32;
+constexpr int kMaxXr = 64;            // dW accumulator columns
 // TMEM columns (512 allocated)
 constexpr uint32_t kWt = 0;          // W^T: [ic lane (hi) | 64 + ic lane (lo)][oc column]
-constexpr uint32_t kDwAcc = 128;     // dW accumulator: [filter lane][x row column]
-constexpr uint32_t kDwA = 256;       // dy hi | lo of the pair's two blocks: [filter lane][px]
-constexpr uint32_t kDxAcc = 384;     // two dx accumulators: [ic lane (+64: lo part)][64 px]
+constexpr uint32_t kDwAcc = 128;     // dW accumulator: [filter lane][x row column] (xr <= 64)
+constexpr uint32_t kDxAcc = 192;     // dx accumulator: [ic lane (+64: lo part)][64 px]
+constexpr uint32_t kDwA = 256;       // per stage: dy hi | lo of the pair's two blocks [filter lane][px]
 
 struct BArgs {
   float* part;               // [slices][c_out*gw + c_out] partial dW | db (c_out <= 128)
@@ -111,60 +113,58 @@ struct BArgs {
   int32_t w_bulk;            // 1: W staged by one bulk copy (16 B aligned, size % 16 == 0)
 };
 
+
 // Filter of class-major dy row `i` (row (d, j) = oc d + D*j).
 __device__ __forceinline__ int row_oc(const BArgs& a, int i) {
   const int d = i / a.cls;
   return d + a.n_class * (i - d * a.cls);
 }
-__device__ __forceinline__ int slice_u(const BArgs& a, int k) {
-  return static_cast<int>((static_cast<int64_t>(k) * a.units) / a.slices);
+// Slice `sl` owns blocks sl, sl + slices, sl + 2*slices, ... (interleaved: at
+// any moment the CTAs fetch a contiguous window of blocks, i.e. whole channel
+// planes, instead of 148 scattered 128 B pieces of them -- measured faster
+// than contiguous slices); a pair is any two consecutive blocks of the slice.
+__device__ __forceinline__ int slice_blocks(const BArgs& a, int sl) {
+  return (a.units - sl + a.slices - 1) / a.slices;
 }
-__device__ __forceinline__ void advance(int& stage, uint32_t& phase, int stages) {
-  if (++stage == stages) {
-    stage = 0;
-    phase ^= 1u;
-  }
-}
+__device__ __forceinline__ int blk_u(const BArgs& a, int sl, int m) { return sl + a.slices * m; }
+
 
 __host__ __device__ constexpr int round1k(int b) { return (b + 1023) & ~1023; }
 
-// Shared memory: kSlots TMA pair slots (per block: raw dy | x), one lo pair
-// (per block: dy_lo | x_lo), one dx exchange pair (the W_lo half of the
-// accumulator, handed to the W_hi half) and the per-filter db sums.
-// The W staging of the prologue aliases the lo pair (its writers wait for
-// W^T to be built) and so does the dW row dump of the epilogue (each CTA runs
-// exactly one slice, so the lo pair is idle by then).
+// Shared memory: kSlots raw TMA pair slots (per block: dy | x; x is turned
+// into x_lo in place once the MMAs that read raw x are done), kStages dy_lo
+// pairs (the dx GEMM's B lo), one dx exchange pair (the W_lo half of the
+// accumulator, handed to the W_hi half), the per-filter (oc*gw - start,
+// start) table.  The W staging of the prologue
+// aliases the exchange pair when it fits (its first use follows the dx MMAs,
+// which wait for W^T); the dW row dump of the epilogue aliases slot 0 (every
+// MMA has completed by then).
 struct BLayout {
-  int blk, x, slot, lo0, xlo, stg, stgb, wst, dump, dbs, bars, total;
+  int blk, x, slot, dlo, dlob, stg, stgb, wst, kt, dump, bars, total;
   __host__ __device__ BLayout(int c_in, int c_out, int gw, int xr) {
     const int dyb = round1k(c_out * 128), xb = round1k(xr * 128);
-    blk = dyb + xb;                       // one block: dy (or dy_lo) | x (or x_lo)
+    blk = dyb + xb;                       // one block: dy | x
     x = dyb;
     slot = 2 * blk;
-    lo0 = kSlots * slot;
-    xlo = dyb;
+    dlob = 2 * dyb;                       // one dy_lo pair
+    dlo = kSlots * slot;
     stgb = round1k(c_in * 128);           // one block's dx [c_in rows][32 px] (SWIZZLE_128B)
-    stg = lo0 + 2 * blk;                  // one staging pair
+    stg = dlo + kStages * dlob;
     int end = stg + 2 * stgb;
-    const int wneed = c_out * gw * 4 + c_out * 8;  // W + (oc*gw - start, start) table
-    if (wneed <= 2 * blk) {
-      wst = lo0;
+    const int wneed = c_out * gw * 4;
+    if (wneed <= 2 * stgb) {
+      wst = stg;
     } else {
       wst = end;
       end += round1k(wneed);
     }
-    const int dneed = 128 * (xr + 4) * 4;  // dW row dump [128][xr + 4]
-    if (dneed <= 2 * blk) {
-      dump = lo0;
-    } else {
-      dump = end;
-      end += round1k(dneed);
-    }
-    dbs = end;  // [128] per-filter dy sums of the slice
-    end += 512;
+    kt = end;                             // [c_out] int2
+    end += round1k(c_out * 8);
+    dump = 0;                             // [128][xr + 4] over slot 0
     bars = end;
     total = bars + 64 * 8;
   }
+  __host__ __device__ bool dump_fits(int xr) const { return 128 * (xr + 4) * 4 <= slot; }
 };
 
 // Row `L` (this thread's TMEM lane) of the resident stacked W^T operand:
@@ -172,9 +172,7 @@ struct BLayout {
 // columns, zero outside each filter's window; built from W and the
 // (oc*gw - start, start) table staged in shared memory.
 __device__ __forceinline__ void build_wt(const BArgs& a, uint32_t tmem, uint32_t lane_base, int L,
-                                         const float* wst) {
-  const float* ws = wst;
-  const int2* kt = reinterpret_cast<const int2*>(wst + a.c_out * a.gw);
+                                         const float* ws, const int2* kt) {
   const int ic = L & 63;
   const bool lo_lane = L >= 64;
   const bool live = ic < a.c_in;
@@ -221,6 +219,15 @@ __device__ __forceinline__ float4 f4(const uint32_t* v) {
   return make_float4(__uint_as_float(v[0]), __uint_as_float(v[1]), __uint_as_float(v[2]), __uint_as_float(v[3]));
 }
 
+// Pipeline (pair p: raw slot p % 3, dy_lo pair and TMEM dW A stage p % 2):
+//   MMA  dW raw (dy_hi * x, dy_lo * x)  -> commit xraw   (x converters: x -> x_lo in place)
+//        dx (W^T * dy, W^T * dy_lo)     -> commit dxfull (single accumulator; epilogue drains it)
+//        dW lo (dy_hi * x_lo)           -> commit pfree (dy_lo pair + TMEM A), sfree (raw slot)
+// so three pairs of raw data are in flight from the start (round 1 kept one
+// lo pair and one TMEM A: conversion and MMA alternated, ~2 us per pair
+// against 1.1 us of tensor work), the dy converters of pair p+1 run under the
+// MMAs of pair p, and the in-place x_lo conversion runs under the dx MMAs.
+// The first pair's dW MMAs do not need W^T, so they start while it is built.
 __global__ void __launch_bounds__(kThreads, 1)
     tc_bwd_kernel(const __grid_constant__ CUtensorMap tdy, const __grid_constant__ CUtensorMap tx,
                   const __grid_constant__ BArgs a) {
@@ -228,22 +235,24 @@ __global__ void __launch_bounds__(kThreads, 1)
   const BLayout L(a.c_in, a.c_out, a.gw, a.xr);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bars);
   uint64_t* full = bars;                       // [slot] TMA landed
-  uint64_t* sfree = full + kSlots;             // [slot] MMA commit: slot consumed
-  uint64_t* xlo = sfree + kSlots;              // 2 x-lo warps: x_lo of the pair written
-  uint64_t* conv = xlo + 1;                    // 4 dy converter warps: dy_lo + dW A written
-  uint64_t* lofree = conv + 1;                 // MMA commit: lo pair consumed
-  uint64_t* tfree = lofree + 1;                // MMA commit: dW A (TMEM) consumed
-  uint64_t* dxfull = tfree + 1;                // [2] MMA commit
-  uint64_t* dxempty = dxfull + 2;              // [2] 4 epilogue warps
-  uint64_t* accfull = dxempty + 2;             // MMA commit: the slice's dW done
+  uint64_t* sfree = full + kSlots;             // [slot] MMA commit: raw slot consumed
+  uint64_t* pfree = sfree + kSlots;            // [stage] MMA commit: dy_lo pair + TMEM A consumed
+  uint64_t* conv = pfree + kStages;            // [stage] 4 dy converter warps: dy_lo + dW A written
+  uint64_t* xraw = conv + kStages;             // [stage] MMA commit: raw x consumed
+  uint64_t* xlo = xraw + kStages;              // [stage] 2 x warps: x_lo written in place
+  uint64_t* dxfull = xlo + kStages;            // MMA commit
+  uint64_t* dxempty = dxfull + 1;              // 4 epilogue warps
+  uint64_t* accfull = dxempty + 1;             // MMA commit: the slice's dW done
   uint64_t* wt_ready = accfull + 1;            // 4 epilogue warps: W^T in TMEM
   uint64_t* w_bar = wt_ready + 1;              // W bulk copy landed
-  uint64_t* dbready = w_bar + 1;               // 4 dy converter warps: slice db sums in smem
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(dbready + 1);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(w_bar + 1);
 
   const uint32_t warp = warp_id();
   const int lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
+#if defined(SCC_TRACE)
+    if (blockIdx.x == 0) g_trace3[59] = g_trace3[62];  // the previous call's reduce end
+#endif
     TRACE3(48);
 #if defined(SCC_TRACE)
     if (blockIdx.x < 256) g_cta3[2 * blockIdx.x] = globaltimer();
@@ -252,18 +261,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&full[s], 1);
       mbar_init(&sfree[s], 1);
     }
-    mbar_init(xlo, 2);
-    mbar_init(conv, 4);
-    mbar_init(lofree, 1);
-    mbar_init(tfree, 1);
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&dxfull[i], 1);
-      mbar_init(&dxempty[i], 4);
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&pfree[s], 1);
+      mbar_init(&conv[s], 4);
+      mbar_init(&xraw[s], 1);
+      mbar_init(&xlo[s], 2);
     }
+    mbar_init(dxfull, 1);
+    mbar_init(dxempty, 4);
     mbar_init(accfull, 1);
     mbar_init(wt_ready, 4);
     mbar_init(w_bar, 1);
-    mbar_init(dbready, 4);
     fence_mbar_init();
   }
   if (warp == 0 && lane == 0) {
@@ -282,142 +290,144 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   // this CTA's slice (exactly one, see the launch) and its block pairs
   const int sl = blockIdx.x;
-  const int u0 = slice_u(a, sl), u1 = slice_u(a, sl + 1);
-  const int npairs = (u1 - u0 + 1) >> 1;
+  const int nblk = slice_blocks(a, sl);
+  const int npairs = (nblk + 1) >> 1;
 
   if (warp == 0) {
     // ---------------- producer ----------------
+    // A pair is 2 dy boxes + 2 x boxes (more when the x arc wraps); the lanes
+    // issue them in parallel (one TMA instruction holds its thread ~0.1-0.3 us).
     cudaGridDependencySynchronize();
-    if (elect_one()) {
-      if (a.do_dx && a.w_bulk) {
-        // W first: the dx GEMM's operand is built from it
-        const uint32_t wb = 4u * a.c_out * a.gw;
-        mbar_expect_tx(w_bar, wb);
-        bulk_load(smem + L.wst, a.weight, wb, w_bar);
-      }
-      int s = 0;
-      uint32_t ph = 0;
-      const uint32_t bytes = a.c_out * 128 + (a.do_dw ? a.nx * 128 : 0);
-      for (int p = 0; p < npairs; ++p) {
-        const int ub = u0 + 2 * p, nb = min(2, u1 - ub);
-        mbar_wait(&sfree[s], ph ^ 1u);
+    if (a.do_dx && a.w_bulk && lane == 0) {
+      // W first: the dx GEMM's operand is built from it
+      const uint32_t wb = 4u * a.c_out * a.gw;
+      mbar_expect_tx(w_bar, wb);
+      bulk_load(smem + L.wst, a.weight, wb, w_bar);
+    }
+    const int nxb = a.do_dw ? (a.xbox ? 1 : a.nx / a.rbb) : 0;
+    const int per_blk = 1 + nxb;
+    const uint32_t bytes = a.c_out * 128 + (a.do_dw ? a.nx * 128 : 0);
+    for (int p = 0; p < npairs; ++p) {
+      const int s = p % kSlots;
+      const int nb = min(2, nblk - 2 * p);
+      if (p >= kSlots) mbar_wait(&sfree[s], (p / kSlots - 1) & 1);
+      if (lane == 0) {
         TRACE3K(0, p);
         mbar_expect_tx(&full[s], bytes * nb);
-        for (int k = 0; k < nb; ++k) {
-          const int u = ub + k;
-          const int n = u / a.nbps, px0 = (u - n * a.nbps) * 32;
-          uint8_t* st = smem + s * L.slot + k * L.blk;
-          tma_load_4d(st, &tdy, &full[s], px0, 0, 0, n);
-          if (a.do_dw) {
-            if (a.xbox) {
-              tma_load_3d(st + L.x, &tx, &full[s], px0, a.start8, n);
-            } else {
-              for (int r = 0; r < a.nx; r += a.rbb) {
-                int ic = a.start8 + r;
-                ic -= ic >= a.c_in ? a.c_in : 0;
-                tma_load_3d(st + L.x + r * 128, &tx, &full[s], px0, ic, n);
-              }
-            }
-          }
-        }
-        advance(s, ph, kSlots);
       }
+      __syncwarp();
+      for (int bi = lane; bi < nb * per_blk; bi += 32) {
+        const int k = bi / per_blk, j = bi - k * per_blk;
+        const int u = blk_u(a, sl, 2 * p + k);
+        const int n = u / a.nbps, px0 = (u - n * a.nbps) * 32;
+        uint8_t* st = smem + s * L.slot + k * L.blk;
+        if (j == 0) {
+          tma_load_4d(st, &tdy, &full[s], px0, 0, 0, n);
+        } else if (a.xbox) {
+          tma_load_3d(st + L.x, &tx, &full[s], px0, a.start8, n);
+        } else {
+          const int r = (j - 1) * a.rbb;
+          int ic = a.start8 + r;
+          ic -= ic >= a.c_in ? a.c_in : 0;
+          tma_load_3d(st + L.x + r * 128, &tx, &full[s], px0, ic, n);
+        }
+      }
+      __syncwarp();
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer ----------------
     const uint32_t idw = idesc_tf32(128, static_cast<uint32_t>(a.xr), 0, 0);
     const uint32_t idx = idesc_tf32(128, 64, 0, 1);  // B = dy of the pair, MN-major (pixels contiguous)
     const int ksteps = a.c_out >> 3;
-    const uint32_t lbo = static_cast<uint32_t>(L.blk);  // the pair's second 32-px atom
-    int s = 0, b = 0;
-    uint32_t ph = 0, dph = 0, cph = 0;
-    if (a.do_dx) mbar_wait(wt_ready, 0);
+    const uint32_t lbo = static_cast<uint32_t>(L.blk);   // the pair's second 32-px atom (raw)
+    const uint32_t lbol = static_cast<uint32_t>(L.dlob / 2);  // ... (dy_lo)
+    uint32_t dph = 0;
     for (int p = 0; p < npairs; ++p) {
-      const int nb = min(2, u1 - (u0 + 2 * p));
-      mbar_wait(conv, cph);
-      if (a.do_dw) mbar_wait(xlo, cph);
-      cph ^= 1u;
-      if (a.do_dx) mbar_wait(&dxempty[b], dph ^ 1u);
+      const int s = p % kSlots, e = p & 1;
+      const uint32_t ph = (p >> 1) & 1;
+      const int nb = min(2, nblk - 2 * p);
+      mbar_wait(&conv[e], ph);
       tc_fence_after();
       const uint32_t st = smem_u32(smem + s * L.slot);
-      const uint32_t lb = smem_u32(smem + L.lo0);
-      const uint32_t d = tmem + kDxAcc + 64 * b;
-      if (elect_one()) {
-        // 1. everything that reads the lo pair
-        if (a.do_dw) {
+      const uint32_t lb = smem_u32(smem + L.dlo + e * L.dlob);
+      const uint32_t aw = tmem + kDwA + 128 * e;
+      if (a.do_dw) {
+        // dW with raw x (x_hi): dy_hi * x, dy_lo * x
+        if (elect_one()) {
           for (int k = 0; k < nb; ++k) {
-            const uint32_t ah = tmem + kDwA + 64 * k;
-            for (int q = 0; q < 4; ++q)
-              mma_tf32_ts(tmem + kDwAcc, ah + 8 * q, desc_sw128(lb + k * L.blk + L.xlo + q * 32, 16, 1024), idw,
-                          (p == 0 && k == 0 && q == 0) ? 0u : 1u);
-          }
-        }
-        if (a.do_dx) {
-          for (int q = 0; q < ksteps; ++q)
-            mma_tf32_ts(d, tmem + kWt + 8 * q, desc_mn32(lb + q * 1024, lbo, 512), idx, q == 0 ? 0u : 1u);
-        }
-        mma_commit(lofree);
-        // 2. the rest of dW (frees the TMEM A pair), then dx * dy
-        if (a.do_dw) {
-          for (int k = 0; k < nb; ++k) {
-            const uint32_t ah = tmem + kDwA + 64 * k, al = ah + 32;
+            const uint32_t ah = aw + 64 * k, al = ah + 32;
             for (int q = 0; q < 4; ++q) {
               const uint64_t dbx = desc_sw128(st + k * L.blk + L.x + q * 32, 16, 1024);
-              mma_tf32_ts(tmem + kDwAcc, ah + 8 * q, dbx, idw, 1);
+              mma_tf32_ts(tmem + kDwAcc, ah + 8 * q, dbx, idw, (p == 0 && k == 0 && q == 0) ? 0u : 1u);
               mma_tf32_ts(tmem + kDwAcc, al + 8 * q, dbx, idw, 1);
             }
           }
-          mma_commit(tfree);
+          mma_commit(&xraw[e]);
           TRACE3K(16, p);
         }
-        if (a.do_dx) {
-          for (int q = 0; q < ksteps; ++q)
-            mma_tf32_ts(d, tmem + kWt + 8 * q, desc_mn32(st + q * 1024, lbo, 512), idx, 1);
-          mma_commit(&dxfull[b]);
+        __syncwarp();
+      }
+      if (a.do_dx) {
+        if (p == 0) mbar_wait(wt_ready, 0);
+        mbar_wait(dxempty, dph ^ 1u);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint32_t d = tmem + kDxAcc;
+          for (int q = 0; q < ksteps; ++q) {
+            mma_tf32_ts(d, tmem + kWt + 8 * q, desc_mn32(st + q * 1024, lbo, 512), idx, q == 0 ? 0u : 1u);
+            mma_tf32_ts(d, tmem + kWt + 8 * q, desc_mn32(lb + q * 1024, lbol, 512), idx, 1);
+          }
+          mma_commit(dxfull);
           TRACE3K(24, p);
         }
+        __syncwarp();
+        dph ^= 1u;
+      }
+      if (a.do_dw) {
+        // dW with x_lo (converted in place under the dx MMAs): dy_hi * x_lo
+        mbar_wait(&xlo[e], ph);
+        tc_fence_after();
+        if (elect_one()) {
+          for (int k = 0; k < nb; ++k) {
+            const uint32_t ah = aw + 64 * k;
+            for (int q = 0; q < 4; ++q)
+              mma_tf32_ts(tmem + kDwAcc, ah + 8 * q, desc_sw128(st + k * L.blk + L.x + q * 32, 16, 1024), idw, 1);
+          }
+        }
+        __syncwarp();
+      }
+      if (elect_one()) {
+        mma_commit(&pfree[e]);
         mma_commit(&sfree[s]);
       }
       __syncwarp();
-      if (a.do_dx && ++b == 2) {
-        b = 0;
-        dph ^= 1u;
-      }
-      advance(s, ph, kSlots);
     }
     // (an empty slice accumulates nothing; the epilogue writes zeros)
     if (a.do_dw && elect_one()) mma_commit(accfull);
     __syncwarp();
   } else if (warp < 4) {
-    // ---------------- x lo converters ----------------
+    // ---------------- x lo converters (in place) ----------------
     if (a.do_dw) {
       const int ct = threadIdx.x - 64;  // 0..63
-      // padding rows [nx, xr) of every x / x_lo stage are zero (the lo pair
-      // once the W staging it aliases is consumed)
-      for (int s = 0; s < 2 * kSlots + 2 && a.xr > a.nx; ++s) {
-        if (s == 2 * kSlots && a.do_dx) mbar_wait(wt_ready, 0);
-        float* xs = reinterpret_cast<float*>(s < 2 * kSlots ? smem + s * L.blk + L.x
-                                                            : smem + L.lo0 + (s - 2 * kSlots) * L.blk + L.xlo);
+      // padding rows [nx, xr) of every x block are zero (TMA never writes
+      // them; lo of zero is zero)
+      for (int b = 0; b < 2 * kSlots && a.xr > a.nx; ++b) {
+        float* xs = reinterpret_cast<float*>(smem + (b >> 1) * L.slot + (b & 1) * L.blk + L.x);
         for (int i = ct; i < (a.xr - a.nx) * 32; i += 64) xs[a.nx * 32 + i] = 0.f;
       }
-      // the W staging of the prologue aliases the lo pair
-      if (a.do_dx) mbar_wait(wt_ready, 0);
       fence_proxy_async_smem();
-      int s = 0;
-      uint32_t ph = 0, lph = 0;
       const int words = a.nx * 8;  // float4 per x block
       for (int p = 0; p < npairs; ++p) {
-        const int nb = min(2, u1 - (u0 + 2 * p));
-        mbar_wait(&full[s], ph);
-        mbar_wait(lofree, lph ^ 1u);
-        lph ^= 1u;
+        const int s = p % kSlots, e = p & 1;
+        const int nb = min(2, nblk - 2 * p);
+        // the MMAs that read raw x are done (and so the data had landed)
+        mbar_wait(&xraw[e], (p >> 1) & 1);
         for (int k = 0; k < nb; ++k) {
-          const float4* src = reinterpret_cast<const float4*>(smem + s * L.slot + k * L.blk + L.x);
-          const uint32_t dst = smem_u32(smem + L.lo0 + k * L.blk + L.xlo);
+          const uint32_t base = smem_u32(smem + s * L.slot + k * L.blk + L.x);
           for (int i0 = ct; i0 < words; i0 += 64 * 4) {
             float4 v[4];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) v[q] = src[min(i0 + 64 * q, words - 1)];
+            for (int q = 0; q < 4; ++q) v[q] = lds_v4(base + min(i0 + 64 * q, words - 1) * 16);
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
               if (i0 + 64 * q < words) {
@@ -426,34 +436,36 @@ __global__ void __launch_bounds__(kThreads, 1)
                 o.y = v[q].y - tf32_hi(v[q].y);
                 o.z = v[q].z - tf32_hi(v[q].z);
                 o.w = v[q].w - tf32_hi(v[q].w);
-                sts_v4(dst + (i0 + 64 * q) * 16, o);
+                sts_v4(base + (i0 + 64 * q) * 16, o);
               }
             }
           }
         }
         fence_proxy_async_smem();
         __syncwarp();
-        if (lane == 0) mbar_arrive(xlo);
-        advance(s, ph, kSlots);
+        if (lane == 0) mbar_arrive(&xlo[e]);
       }
     }
   } else if (warp < 8) {
     // ---------------- dy row converters ----------------
     // Row `row` of a block: 128 B, 32 B chunk c at physical chunk c ^ (row % 4)
-    // (SWIZZLE_128B_BASE32B).  Writes the lo row to the lo pair (dx B lo) and,
-    // for dW, the hi / lo row to TMEM lane `row`.
+    // (SWIZZLE_128B_BASE32B).  Writes the lo row to the stage's lo pair (dx B
+    // lo) and, for dW, the hi / lo row to TMEM lane `row`.
     const int q = warp & 3;
     const int row = q * 32 + lane;
     const int swp = (row >> 2) & 1;
     const bool live = row < a.c_out;
     const bool warp_live = q * 32 < a.c_out;  // tcgen05.st is warp-collective
     const uint32_t lane_base = static_cast<uint32_t>(q * 32) << 16;
-    int s = 0;
-    uint32_t ph = 0, tph = 0, lph = 0;
+    // window start of filter row `row` (a plan table: no dependency wait)
+    const int start_i = (a.do_dw && live) ? __ldg(a.starts + row_oc(a, row)) : 0;
     float dbsum = 0.f;  // db of this filter over the slice (fixed order: blocks, then pixels)
     for (int p = 0; p < npairs; ++p) {
-      const int nb = min(2, u1 - (u0 + 2 * p));
-      mbar_wait(&full[s], ph);
+      const int s = p % kSlots, e = p & 1;
+      const int nb = min(2, nblk - 2 * p);
+      mbar_wait(&full[s], (p / kSlots) & 1);
+      if (p >= kStages) mbar_wait(&pfree[e], ((p >> 1) - 1) & 1);  // dy_lo pair + TMEM A of pair p-2
+      tc_fence_after();
       for (int k = 0; k < nb; ++k) {
         uint32_t hi[32], lo[32];
 #pragma unroll
@@ -485,14 +497,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
           dbsum += bs;
-        }
-        if (k == 0) {
-          mbar_wait(lofree, lph ^ 1u);
-          lph ^= 1u;
-          if (p == 0 && a.do_dx) mbar_wait(wt_ready, 0);  // the W staging aliases the lo pair
-        }
-        if (live) {
-          const uint32_t lo_row = smem_u32(smem + L.lo0 + k * L.blk + row * 128);
+          const uint32_t lo_row = smem_u32(smem + L.dlo + e * L.dlob + k * (L.dlob / 2) + row * 128);
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
             const int at = ((j ^ row) & 3) << 1;
@@ -501,17 +506,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             sts_v4(lo_row + (at | (swp ^ 1)) * 16, swp ? l0 : l1);
           }
         }
-        if (a.do_dw) {
-          if (k == 0) {
-            mbar_wait(tfree, tph ^ 1u);
-            tph ^= 1u;
-            tc_fence_after();
-          }
-          if (warp_live) {
-            const uint32_t col = tmem + kDwA + 64 * k + lane_base;
-            tmem_st32(col, hi);
-            tmem_st32(col + 32, lo);
-          }
+        if (a.do_dw && warp_live) {
+          const uint32_t col = tmem + kDwA + 128 * e + 64 * k + lane_base;
+          tmem_st32(col, hi);
+          tmem_st32(col + 32, lo);
         }
       }
       fence_proxy_async_smem();
@@ -520,14 +518,56 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_before();
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(conv);
+      if (lane == 0) mbar_arrive(&conv[e]);
       if (row == 0) TRACE3K(8, p);
-      advance(s, ph, kSlots);
     }
     if (a.do_dw) {
-      reinterpret_cast<float*>(smem + L.dbs)[row] = dbsum;
+      // dW slice epilogue (these warps are idle once the last pair is
+      // converted; the epilogue warps may still be draining dx): TMEM row
+      // `row` -> smem dump over slot 0 (every MMA has completed) -> the
+      // window-relative values -> this slice's partial
+      const int i = row;
+      float* prow = reinterpret_cast<float*>(smem + L.dump) + i * (a.xr + 4);
+      const uint32_t prow_a = smem_u32(prow);
+      mbar_wait(accfull, 0);
+      if (row == 0) TRACE3(51);
+      tc_fence_after();
+      for (int c0 = 0; c0 < a.xr; c0 += 32) {
+        uint32_t v[32];
+        tmem_ld32_nowait(tmem + kDwAcc + c0 + lane_base, v);
+        tmem_ld_wait();
+#pragma unroll
+        for (int t = 0; t < 32; t += 4)
+          if (c0 + t < a.xr) sts_v4(prow_a + (c0 + t) * 4, f4(v + t));
+      }
       __syncwarp();
-      if (lane == 0) mbar_arrive(dbready);
+      const bool wlive = i < a.c_out && nblk > 0;
+      int j0 = 0;
+      if (wlive) {
+        j0 = start_i - a.start8;
+        j0 += j0 < 0 ? a.c_in : 0;
+      }
+      float* dst = a.part + static_cast<int64_t>(sl) * a.elems;
+      float wv[kMaxGw];
+#pragma unroll
+      for (int t = 0; t < kMaxGw; ++t) {
+        int j = j0 + t;
+        j -= j >= a.c_in ? a.c_in : 0;
+        wv[t] = (wlive && t < a.gw) ? prow[j] : 0.f;
+      }
+      if (i < a.c_out) {
+        if ((a.gw & 3) == 0) {
+#pragma unroll
+          for (int t = 0; t < kMaxGw; t += 4)
+            if (t < a.gw)
+              *reinterpret_cast<float4*>(dst + i * a.gw + t) = make_float4(wv[t], wv[t + 1], wv[t + 2], wv[t + 3]);
+        } else {
+#pragma unroll
+          for (int t = 0; t < kMaxGw; ++t)
+            if (t < a.gw) dst[i * a.gw + t] = wv[t];
+        }
+        dst[a.c_out * a.gw + i] = wlive ? dbsum : 0.f;
+      }
     }
   } else {
     // ---------------- W^T build, dx epilogue, dW slice epilogue ----------------
@@ -536,23 +576,20 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int i = q * 32 + lane;       // TMEM lane: input channel (+64: lo part) / filter row (dW)
     const uint32_t lane_base = static_cast<uint32_t>(q * 32) << 16;
     float* wst = reinterpret_cast<float*>(smem + L.wst);
-    // window start of filter row i for the dW epilogue (a plan table, never
-    // written by a preceding kernel: loaded before the dependency wait, so
-    // the epilogue does not pay a cold load at the end)
-    const int start_i = (a.do_dw && i < a.c_out) ? __ldg(a.starts + row_oc(a, i)) : 0;
+    int2* kt = reinterpret_cast<int2*>(smem + L.kt);
+    // plan table, never written by a preceding kernel: loaded before the
+    // dependency wait
+    if (a.do_dx && et < a.c_out) {
+      const int oc = row_oc(a, et);
+      const int st = __ldg(a.starts + oc);
+      kt[et] = make_int2(oc * a.gw - st, st);
+    }
     cudaGridDependencySynchronize();
     if (et == 0) TRACE3(53);
     if (a.do_dx) {
-      // W (bulk copy by the producer, or loads here, all in flight at once)
-      // and per class-major column k the (oc*gw - start, start) pair; then
-      // this lane's row of W^T -> TMEM
-      int2* kt = reinterpret_cast<int2*>(wst + a.c_out * a.gw);
+      // W (bulk copy by the producer, or loads here, all in flight at once);
+      // then this lane's row of W^T -> TMEM
       const int nw = a.c_out * a.gw;
-      if (et < a.c_out) {
-        const int oc = row_oc(a, et);
-        const int st = __ldg(a.starts + oc);
-        kt[et] = make_int2(oc * a.gw - st, st);
-      }
       if (!a.w_bulk) {
         for (int k0 = 0; k0 < nw; k0 += 128 * 32) {
           float v[32];
@@ -571,7 +608,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       named_bar_sync(1, 128);
       if (a.w_bulk) mbar_wait(w_bar, 0);
       if (et == 0) TRACE3(55);
-      build_wt(a, tmem, lane_base, i, wst);
+      build_wt(a, tmem, lane_base, i, wst, kt);
       __syncwarp();
       if (lane == 0) mbar_arrive(wt_ready);
       if (et == 0) TRACE3(50);
@@ -582,27 +619,28 @@ __global__ void __launch_bounds__(kThreads, 1)
     const bool dx_live = dx_row < a.c_in;
     const bool dx_warp = (q & 1) * 32 < a.c_in;
     const bool leader = et == 0;
-    int b = 0;
     uint32_t dph = 0;
     if (a.do_dx) {
       for (int p = 0; p < npairs; ++p) {
-        const int ub = u0 + 2 * p, nb = min(2, u1 - ub);
-        mbar_wait(&dxfull[b], dph);
+        const int nb = min(2, nblk - 2 * p);
+        mbar_wait(dxfull, dph);
+        dph ^= 1u;
         if (et == 0) TRACE3K(32, p);
         tc_fence_after();
         uint32_t v0[32], v1[32];
         if (dx_warp) {
-          tmem_ld32_nowait(tmem + kDxAcc + 64 * b + lane_base, v0);
-          tmem_ld32_nowait(tmem + kDxAcc + 64 * b + 32 + lane_base, v1);
+          tmem_ld32_nowait(tmem + kDxAcc + lane_base, v0);
+          tmem_ld32_nowait(tmem + kDxAcc + 32 + lane_base, v1);
           tmem_ld_wait();
         }
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&dxempty[b]);
+        if (lane == 0) mbar_arrive(dxempty);
         // rows 64-127 (the W_lo part) -> exchange pair; rows 0-63 add theirs and
         // store the sum straight to global (each thread one input channel,
         // 32 contiguous pixels per block).  The first barrier orders this
-        // pair's exchange writes after the previous pair's reads.
+        // pair's exchange writes after the previous pair's reads (and, on the
+        // first pair, after every lane's last read of the W staging).
         named_bar_sync(1, 128);
         const uint32_t r0 = smem_u32(smem + L.stg + dx_row * 128), r1 = r0 + L.stgb;
         if (bottom && dx_warp && dx_live) {
@@ -617,7 +655,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int k = 0; k < 2; ++k) {
             if (k < nb) {
-              const int u = ub + k;
+              const int u = blk_u(a, sl, 2 * p + k);
               const int n = u / a.nbps, px0 = (u - n * a.nbps) * 32;
               float* drow = a.dx + (static_cast<int64_t>(n) * a.c_in + dx_row) * a.plane + px0;
               const uint32_t* vv = k == 0 ? v0 : v1;
@@ -634,56 +672,6 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
         if (leader) TRACE3K(40, p);
-        if (++b == 2) {
-          b = 0;
-          dph ^= 1u;
-        }
-      }
-    }
-    if (a.do_dw) {
-      float* dump = reinterpret_cast<float*>(smem + L.dump);
-      const int rstride = a.xr + 4;
-      float* prow = dump + i * rstride;
-      const uint32_t prow_a = smem_u32(prow);
-      mbar_wait(accfull, 0);
-      mbar_wait(dbready, 0);
-      if (et == 0) TRACE3(51);
-      tc_fence_after();
-      for (int c0 = 0; c0 < a.xr; c0 += 32) {
-        uint32_t v[32];
-        tmem_ld32_nowait(tmem + kDwAcc + c0 + lane_base, v);
-        tmem_ld_wait();
-#pragma unroll
-        for (int t = 0; t < 32; t += 4)
-          if (c0 + t < a.xr) sts_v4(prow_a + (c0 + t) * 4, f4(v + t));
-      }
-      // window-relative values of filter row i -> the slice's partial
-      const bool live = i < a.c_out && u0 < u1;
-      int j0 = 0;
-      if (live) {
-        j0 = start_i - a.start8;
-        j0 += j0 < 0 ? a.c_in : 0;
-      }
-      float* dst = a.part + static_cast<int64_t>(sl) * a.elems;
-      float wv[kMaxGw];
-#pragma unroll
-      for (int t = 0; t < kMaxGw; ++t) {
-        int j = j0 + t;
-        j -= j >= a.c_in ? a.c_in : 0;
-        wv[t] = (live && t < a.gw) ? prow[j] : 0.f;
-      }
-      if (i < a.c_out) {
-        if ((a.gw & 3) == 0) {
-#pragma unroll
-          for (int t = 0; t < kMaxGw; t += 4)
-            if (t < a.gw)
-              *reinterpret_cast<float4*>(dst + i * a.gw + t) = make_float4(wv[t], wv[t + 1], wv[t + 2], wv[t + 3]);
-        } else {
-#pragma unroll
-          for (int t = 0; t < kMaxGw; ++t)
-            if (t < a.gw) dst[i * a.gw + t] = wv[t];
-        }
-        dst[a.c_out * a.gw + i] = live ? reinterpret_cast<const float*>(smem + L.dbs)[i] : 0.f;
       }
     }
     if (leader) {
@@ -709,7 +697,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 constexpr int kRedWarps = 32;  // 1024 threads: <= 5 in-flight loads per thread (16 warps measured 0.7 us slower)
 __global__ void __launch_bounds__(32 * kRedWarps) tc_bwd_reduce(const __grid_constant__ BArgs a) {
   __shared__ float red[kRedWarps][33];
+  if (threadIdx.x == 0) TRACE3(60);
   cudaGridDependencySynchronize();
+  if (threadIdx.x == 0) TRACE3(61);
   // the next kernel may start its prologue (it waits for this grid)
   cudaTriggerProgrammaticLaunchCompletion();
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
@@ -740,6 +730,7 @@ __global__ void __launch_bounds__(32 * kRedWarps) tc_bwd_reduce(const __grid_con
       a.dbias[row_oc(a, e - nw)] = t;
     }
   }
+  if (threadIdx.x == 0) TRACE3(62);
 }
 
 struct Geo {
@@ -752,7 +743,8 @@ Geo geometry(const TcWeightPlan& tw, int32_t c_in, int32_t c_out, int32_t gw) {
   g.start8 = tw.rt_info[0];
   g.nx = tw.rt_info[1];
   g.xr = (g.nx + 15) / 16 * 16;
-  g.fits = BLayout(c_in, c_out, gw, g.xr).total <= kSmemLimit;
+  const BLayout L(c_in, c_out, gw, g.xr);
+  g.fits = L.total <= kSmemLimit && L.dump_fits(g.xr) && g.xr <= kMaxXr;
   return g;
 }
 

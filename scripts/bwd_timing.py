@@ -39,19 +39,23 @@ for name, f in (("bwd", bwd), ("bwd_data", bdata), ("bwd_weight", bweight)):
         e1.record(st); e1.synchronize()
     print(f"{name}: {e0.elapsed_time(e1) * 1e3 / 160:.2f} us per call", flush=True)
 for name, f in (("bwd_data", bdata), ("bwd", bwd)):
-    f(0, torch.cuda.current_stream().cuda_stream); torch.cuda.synchronize()
+    with torch.cuda.stream(st):
+        gr = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gr, stream=st):
+            for k in range(4): f(k % R, st.cuda_stream)
+        gr.replay(); st.synchronize()
     n = 64 + 512
     buf = (C.c_uint64 * n)()
     L.scc_debug_trace_fused(buf, n)
     t = [buf[i] for i in range(64)]
     t0 = t[48]
-    print("raw", t[48:53], t[62:64])
+    print("raw", t[48:53], t[60:63])
     if t0 == 0:
         print("(no trace: build with SCC_EXTRA=-DSCC_TRACE)"); break
-    lab = {48: "start", 49: "tmem", 50: "wt_ready", 51: "accfull", 52: "end", 53: "e_dep", 55: "e_bar", 62: "red_start", 63: "red_end"}
+    lab = {48: "start", 49: "tmem", 50: "wt_ready", 51: "accfull", 52: "end", 53: "e_dep", 55: "e_bar", 60: "red_entry", 61: "red_dep", 62: "red_end", 59: "prev_red_end"}
     for k in range(8):
         lab[k] = f"tma{k}"; lab[8 + k] = f"conv{k}"; lab[16 + k] = f"mdw{k}"; lab[24 + k] = f"mdx{k}"; lab[32 + k] = f"dxfull{k}"; lab[40 + k] = f"store{k}"  # k = block pair
-    print(name, " ".join(f"{lab[i]}={(t[i] - t0) / 1e3:.2f}" for i in sorted(lab) if t[i] >= t0 and t[i] - t0 < 1e8))
+    print(name, " ".join(f"{lab[i]}={(t[i] - t0) / 1e3:.2f}" for i in sorted(lab) if t[i] > 0 and abs(t[i] - t0) < 1e8))
     cs = [buf[64 + 2 * i] for i in range(148)]; ce = [buf[64 + 2 * i + 1] for i in range(148)]
     m0 = min(cs)
     s_ = sorted((x - m0) / 1e3 for x in cs); e_ = sorted((x - m0) / 1e3 for x in ce)
