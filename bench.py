@@ -423,21 +423,40 @@ def run_ours(args):
     # The step launches forward + scc_backward_f32; the dominant of those two
     # is the roofline kernel.  backward-data / backward-weight alone are
     # reported for reference (kernel_ms) but are not what the step runs.
+    # Each part is replayed from a CUDA graph of 16 calls (rotating over the
+    # buffer sets, like the step), so host launch overhead is not timed.
     parts = {"forward": fwd, "backward": bwd, "backward_data": bwd_data, "backward_weight": bwd_weight}
     kms = {}
-    reps = max(args.steps, 20)
-    for name, fn in parts.items():
-        for i in range(3):
-            fn(i)
-        torch.cuda.synchronize()
-        a = torch.cuda.Event(enable_timing=True)
-        b = torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        for i in range(reps):
-            fn(i)
-        b.record(stream)
-        b.synchronize()
-        kms[name] = a.elapsed_time(b) / reps
+    reps = max(args.steps // 16, 4)
+    pstream = cap if graphs is not None else stream
+    sp_saved = sp
+    sp = pstream.cuda_stream
+    with torch.cuda.stream(pstream):
+        for name, fn in parts.items():
+            for i in range(3):
+                fn(i)
+            torch.cuda.synchronize()
+            pg = None
+            if graphs is not None:
+                pg = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(pg, stream=pstream):
+                    for i in range(16):
+                        fn(i)
+                pg.replay()
+            torch.cuda.synchronize()
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(pstream)
+            for r in range(reps):
+                if pg is None:
+                    for i in range(16):
+                        fn(i)
+                else:
+                    pg.replay()
+            b.record(pstream)
+            b.synchronize()
+            kms[name] = a.elapsed_time(b) / (16 * reps)
+    sp = sp_saved
     dominant = max(("forward", "backward"), key=kms.get)
     achieved = nbytes[dominant] / (kms[dominant] * 1e-3) / 1e9
     traffic, traffic_detail = None, None

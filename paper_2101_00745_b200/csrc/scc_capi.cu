@@ -12,6 +12,8 @@
 #include <exception>
 #include <mutex>
 #include <string>
+#include <vector>
+#include <cmath>
 
 #include "scc_b200.h"
 #include "scc_kernels.hpp"
@@ -672,12 +674,15 @@ void d2h(void* h, const void* d, size_t bytes, cudaStream_t s) {
 }
 
 // Host-buffer operator, pipelined over batch chunks so PCIe H2D, the kernels
-// and PCIe D2H overlap (the link is full duplex):
-//   copy-in stream : w, b, then per chunk x_c / dy_c          -> ev_in[c]
-//   compute stream : per chunk forward and backward-data      -> ev_done[c]
-//                    then backward-weight over the whole batch (it reduces
-//                    over n, so its bits equal the device entry point's)
-//   copy-out stream: per chunk y_c / dx_c; dW / db last
+// and PCIe D2H overlap (the link is full duplex).  All x chunks go first, so
+// the forward and the y read-back start after one x chunk has landed and y
+// (the largest output) drains while dy comes in; dx trails dy by one chunk:
+//   copy-in stream : w, b, x_0..x_k-1 (-> ev_in[c]), dy_0..dy_k-1 (-> ev_in[8+c])
+//   compute stream : forward of chunk c after x_c (-> ev_done[c]); backward-data
+//                    of chunk c after dy_c (-> ev_done[8+c]); then
+//                    backward-weight over the whole batch (it reduces over n,
+//                    so its bits equal the device entry point's)
+//   copy-out stream: y_0..y_k-1, dx_0..dx_k-1; dW / db last (compute stream)
 // Forward and backward-data are per sample (kernel.cpp:45-60, :107-137) and
 // the kernels' per-element arithmetic does not depend on n, so chunked
 // results are bitwise equal to one full-batch call.  Any subset of the three
@@ -689,14 +694,50 @@ struct HostIo {
   float *y = nullptr, *dx = nullptr, *dw = nullptr, *db = nullptr;
 };
 
+// Chunk boundaries (sample counts) of one pipelined pass.  The schedule may
+// differ between the x pass and the dy pass (SCC_HOST_XCH / SCC_HOST_DYCH:
+// comma-separated relative weights, for the sweep in scripts/host_sweep.py).
+int host_split(int64_t n, int k, const char* env, int64_t* bounds) {
+  std::vector<double> wts;
+  if (const char* e = getenv(env)) {
+    for (const char* q = e; *q;) {
+      wts.push_back(atof(q));
+      while (*q && *q != ',') ++q;
+      if (*q == ',') ++q;
+    }
+  }
+  if (wts.empty()) {
+    // measured best at config 1 (scripts/host_sweep.py, profiles/r02_host_sweep.txt):
+    // x in a quarter then three quarters (y -- twice x -- starts draining
+    // early), dy in three equal chunks
+    // (an explicit SCC_HOST_CHUNKS asks for k equal chunks instead)
+    const bool tuned = k >= 3 && getenv("SCC_HOST_CHUNKS") == nullptr;
+    if (tuned && std::strcmp(env, "SCC_HOST_XCH") == 0) wts = {1.0, 3.0};
+    else if (tuned) wts = {1.0, 1.0, 1.0};
+    else wts.assign(static_cast<size_t>(k), 1.0);
+  }
+  int m = static_cast<int>(std::min<size_t>(wts.size(), static_cast<size_t>(std::min<int64_t>(n, kMaxHostChunks / 2))));
+  double tot = 0;
+  for (int i = 0; i < m; ++i) tot += wts[i];
+  bounds[0] = 0;
+  double acc = 0;
+  int c = 0;
+  for (int i = 0; i < m; ++i) {
+    acc += wts[i];
+    int64_t b = i == m - 1 ? n : static_cast<int64_t>(std::llround(acc / tot * static_cast<double>(n)));
+    b = std::max<int64_t>(b, bounds[c] + 1);
+    b = std::min<int64_t>(b, n - (m - 1 - i));
+    if (b > bounds[c]) bounds[++c] = b;
+  }
+  return c;
+}
+
 int host_chunks(int64_t n, size_t bytes_per_sample) {
-  // >= ~1 MB of traffic per chunk keeps each copy near full PCIe speed; 4
-  // chunks measured best at config 1 (scripts/host_sweep.py: 1 / 2 / 4 / 8
-  // chunks 0.97 / 0.83 / 0.77 / 0.84 ms; replaying the pipeline as a CUDA
-  // graph measured 0.05 ms slower than issuing it)
+  // >= ~1 MB of traffic per chunk keeps each copy near full PCIe speed
+  // (scripts/host_sweep.py sweeps the depth)
   const int64_t by_size = static_cast<int64_t>(bytes_per_sample * n / (1u << 20));
-  int64_t k = std::min<int64_t>({n, kMaxHostChunks / 4, std::max<int64_t>(by_size, 1)});
-  if (const char* e = getenv("SCC_HOST_CHUNKS")) k = std::max<int64_t>(1, std::min<int64_t>({atoi(e), n, kMaxHostChunks}));
+  int64_t k = std::min<int64_t>({n, 4, std::max<int64_t>(by_size, 1)});
+  if (const char* e = getenv("SCC_HOST_CHUNKS")) k = std::max<int64_t>(1, std::min<int64_t>({atoi(e), n, kMaxHostChunks / 2}));
   return static_cast<int>(k);
 }
 
@@ -707,39 +748,55 @@ void issue_host(Plan& p, int64_t n, int64_t h, int64_t wd, const HostIo& io, con
   const bool need_x = fwd || bwt, need_dy = bdata || bwt;
   const size_t sx = static_cast<size_t>(c.c_in * P) * 4, sy = static_cast<size_t>(c.c_out * P) * 4;
   const size_t nw = static_cast<size_t>(c.c_out * c.group_width) * 4, nb = static_cast<size_t>(c.c_out) * 4;
+  constexpr int kHalf = kMaxHostChunks / 2;
+  auto ev = [](void* e) { return static_cast<cudaEvent_t>(e); };
+  auto rec = [](cudaEvent_t e, cudaStream_t s) { cuda_check(cudaEventRecord(e, s), "cudaEventRecord"); };
+  auto wait = [](cudaStream_t s, cudaEvent_t e) { cuda_check(cudaStreamWaitEvent(s, e, 0), "cudaStreamWaitEvent"); };
+  int64_t xb[kHalf + 1], yb[kHalf + 1];
+  const int kx = host_split(n, k, "SCC_HOST_XCH", xb);
+  const int ky = host_split(n, k, "SCC_HOST_DYCH", yb);
   // fork the copy streams off the compute stream (also makes the sequence capturable)
-  cuda_check(cudaEventRecord(static_cast<cudaEvent_t>(g.st->ev_fork), g.s), "cudaEventRecord");
-  cuda_check(cudaStreamWaitEvent(g.s_in, static_cast<cudaEvent_t>(g.st->ev_fork), 0), "cudaStreamWaitEvent");
-  cuda_check(cudaStreamWaitEvent(g.s_out, static_cast<cudaEvent_t>(g.st->ev_fork), 0), "cudaStreamWaitEvent");
+  rec(ev(g.st->ev_fork), g.s);
+  wait(g.s_in, ev(g.st->ev_fork));
+  wait(g.s_out, ev(g.st->ev_fork));
   if (fwd || bdata) h2d(g.w, io.w, nw, g.s_in);
   if (fwd && io.b) h2d(g.b, io.b, nb, g.s_in);
-  int64_t n0 = 0;
-  for (int i = 0; i < k; ++i) {
-    const int64_t m = n / k + (i < n % k ? 1 : 0);  // parallel_chunks split (parallel.cpp:36-66)
-    const size_t ox = static_cast<size_t>(n0) * sx / 4, oy = static_cast<size_t>(n0) * sy / 4;
-    cudaEvent_t ein = static_cast<cudaEvent_t>(g.st->ev_in[i]);
-    cudaEvent_t edone = static_cast<cudaEvent_t>(g.st->ev_done[i]);
-    if (need_x) h2d(g.x + ox, io.x + ox, m * sx, g.s_in);
-    if (need_dy) h2d(g.dy + oy, io.dy + oy, m * sy, g.s_in);
-    cuda_check(cudaEventRecord(ein, g.s_in), "cudaEventRecord");
-    cuda_check(cudaStreamWaitEvent(g.s, ein, 0), "cudaStreamWaitEvent");
-    if (fwd) do_forward(p, m, h, wd, g.x + ox, g.w, io.b ? g.b : nullptr, g.y + oy, g.s);
-    if (bdata) do_backward_data(p, m, h, wd, g.dy + oy, g.w, g.dx + ox, g.s);
-    if (fwd || bdata) {
-      cuda_check(cudaEventRecord(edone, g.s), "cudaEventRecord");
-      cuda_check(cudaStreamWaitEvent(g.s_out, edone, 0), "cudaStreamWaitEvent");
-      if (fwd) d2h(io.y + oy, g.y + oy, m * sy, g.s_out);
-      if (bdata) d2h(io.dx + ox, g.dx + ox, m * sx, g.s_out);
+  if (need_x) {
+    for (int i = 0; i < kx; ++i) {
+      const int64_t m = xb[i + 1] - xb[i];
+      const size_t ox = static_cast<size_t>(xb[i]) * sx / 4, oy = static_cast<size_t>(xb[i]) * sy / 4;
+      h2d(g.x + ox, io.x + ox, m * sx, g.s_in);
+      rec(ev(g.st->ev_in[i]), g.s_in);
+      if (!fwd) continue;
+      wait(g.s, ev(g.st->ev_in[i]));
+      do_forward(p, m, h, wd, g.x + ox, g.w, io.b ? g.b : nullptr, g.y + oy, g.s);
+      rec(ev(g.st->ev_done[i]), g.s);
+      wait(g.s_out, ev(g.st->ev_done[i]));
+      d2h(io.y + oy, g.y + oy, m * sy, g.s_out);
     }
-    n0 += m;
+  }
+  if (need_dy) {
+    for (int i = 0; i < ky; ++i) {
+      const int64_t m = yb[i + 1] - yb[i];
+      const size_t ox = static_cast<size_t>(yb[i]) * sx / 4, oy = static_cast<size_t>(yb[i]) * sy / 4;
+      h2d(g.dy + oy, io.dy + oy, m * sy, g.s_in);
+      rec(ev(g.st->ev_in[kHalf + i]), g.s_in);
+      wait(g.s, ev(g.st->ev_in[kHalf + i]));
+      if (!bdata) continue;
+      do_backward_data(p, m, h, wd, g.dy + oy, g.w, g.dx + ox, g.s);
+      rec(ev(g.st->ev_done[kHalf + i]), g.s);
+      wait(g.s_out, ev(g.st->ev_done[kHalf + i]));
+      d2h(io.dx + ox, g.dx + ox, m * sx, g.s_out);
+    }
   }
   if (bwt) {
+    // after the last x and dy chunk (the compute stream waited for both)
     do_backward_weight(p, n, h, wd, g.dy, g.x, g.dw, io.db ? g.db : nullptr, g.ws, g.ws_bytes, g.s);
     d2h(io.dw, g.dw, nw, g.s);
     if (io.db) d2h(io.db, g.db, nb, g.s);
   }
-  cuda_check(cudaEventRecord(static_cast<cudaEvent_t>(g.st->ev_out), g.s_out), "cudaEventRecord");
-  cuda_check(cudaStreamWaitEvent(g.s, static_cast<cudaEvent_t>(g.st->ev_out), 0), "cudaStreamWaitEvent");
+  rec(ev(g.st->ev_out), g.s_out);
+  wait(g.s, ev(g.st->ev_out));
 }
 
 void run_host(Plan& p, int64_t n, int64_t h, int64_t wd, const HostIo& io) {

@@ -421,16 +421,24 @@ def test_host_buffer_entry_points(port):
     assert np.array_equal(y, y2)
 
 
-@pytest.mark.parametrize("chunks", ["1", "3", "8"])
+@pytest.mark.parametrize("chunks", ["1", "3", "8", "1,3|1,1,1", "5,1,2|3,1", "1|7,1,1,1"])
 def test_host_pipeline_bitwise(chunks, monkeypatch):
     """The host-buffer entry points pipeline H2D / kernels / D2H over batch
-    chunks (ragged split of n=10 here); forward and backward-data are per
-    sample and backward-weight runs once over the whole batch, so every output
-    is bitwise equal to the device-buffer entry points' on the same inputs."""
+    chunks (ragged split of n=10 here; "x|dy" cases give the x pass and the dy
+    pass different chunk schedules, as the default does); forward and
+    backward-data are per sample and backward-weight runs once over the whole
+    batch, so every output is bitwise equal to the device-buffer entry
+    points' on the same inputs."""
     import ctypes as C
     import paper_2101_00745_b200 as scc
     from paper_2101_00745_b200 import _lib
-    monkeypatch.setenv("SCC_HOST_CHUNKS", chunks)
+    if "|" in chunks:
+        xs, ds = chunks.split("|")
+        monkeypatch.setenv("SCC_HOST_CHUNKS", "4")
+        monkeypatch.setenv("SCC_HOST_XCH", xs)
+        monkeypatch.setenv("SCC_HOST_DYCH", ds)
+    else:
+        monkeypatch.setenv("SCC_HOST_CHUNKS", chunks)
     rng = np.random.default_rng(11)
     n = 10
     cfg = scc.scc_config_new(64, 128, 2, "50%", True)
