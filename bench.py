@@ -520,6 +520,17 @@ def run_ours(args):
             except Exception as ex:  # reported, never required for the headline
                 models[name] = {"error": str(ex)[:200]}
 
+    # ---- the paper's Base vs Opt on this GPU: one layer step through the
+    # stock-operator compositions (reference.cpp:335-490) vs the SCC kernels
+    compositions = None
+    if rank == 0 and ws == 1 and not args.no_compositions and args.workload == "c1":
+        try:
+            sys.path.insert(0, os.path.join(ROOT, "scripts"))
+            from compose_bench import SHAPES, run_shape
+            compositions = run_shape("c1", *SHAPES["c1"])
+        except Exception as ex:  # reported, never required for the headline
+            compositions = {"error": str(ex)[:200]}
+
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
         try:
@@ -549,6 +560,7 @@ def run_ours(args):
             "e2e": e2e,
             "gpu_launches": int(launches),
             "models": models,
+            "compositions": compositions,
             "clocks": clocks,
         }
         print(json.dumps(line), flush=True)
@@ -569,6 +581,8 @@ def main():
     ap.add_argument("--no-graph", action="store_true", help="launch each step eagerly")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-models", action="store_true", help="skip the SCC-ResNet-18/VGG16 images/sec")
+    ap.add_argument("--no-compositions", action="store_true",
+                    help="skip the stock-operator (paper 'Base') composition timings")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--no-traffic", action="store_true", help="skip the ncu DRAM-traffic pass")
     args = ap.parse_args()

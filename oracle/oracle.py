@@ -25,7 +25,7 @@ _i64p = C.POINTER(C.c_int64)
 
 class OracleError(RuntimeError):
     """Raised with the reference's status code (1 shape, 2 index, 3 config,
-    4 argument; sccl/errors.hpp:9-55)."""
+    4 argument, 8 format (fixture files); sccl/errors.hpp:9-55)."""
 
     def __init__(self, code: int, msg: str = ""):
         super().__init__(f"oracle status {code}: {msg}")
@@ -238,6 +238,13 @@ class RefOracle(_Base):
         self._dw = self._checked(L.sccl_ref_dw_forward)
         L.sccl_ref_dw_backward.argtypes = [_i64] * 6 + [_dp] * 6
         self._dwb = self._checked(L.sccl_ref_dw_backward)
+        L.ref_fixture_write.argtypes = [C.c_char_p, _i64, _i64, _i64, _i64, _dp]
+        L.ref_fixture_read.argtypes = [C.c_char_p, _i64p, _dp, _i64]
+        L.ref_fixture_probes.argtypes = [C.c_char_p, C.c_uint64]
+        L.ref_compose_forward.argtypes = [C.POINTER(_Cfg), _i32, _i32, _i64, _i64, _i64, _dp, _dp,
+                                          _dp, _dp, _i64p]
+        L.ref_compose_backward.argtypes = [C.POINTER(_Cfg), _i32, _i32, _i64, _i64, _i64, _dp,
+                                           _dp, _dp, _dp, _dp, _dp]
         self._bwd_in = self._checked(L.ref_backward_input)
         self._bwd_p = self._checked(L.ref_backward_params)
 
@@ -302,6 +309,47 @@ class RefOracle(_Base):
                                                _ptr(w), w.size, _ptr(b) if b.size else
                                                _ptr(np.zeros(1)), b.size, _ptr(y))
         return y
+
+    # --- DSX1 fixtures (fixture.cpp:29-97) ---
+    def fixture_write(self, t, path: str) -> None:
+        t = _d(t)
+        n, c, h, w = t.shape
+        self._checked(self.lib.ref_fixture_write)(path.encode(), n, c, h, w, _ptr(t))
+
+    def fixture_read(self, path: str) -> np.ndarray:
+        dims = (C.c_int64 * 4)()
+        self._checked(self.lib.ref_fixture_read)(path.encode(), dims, None, 0)
+        out = np.empty(tuple(dims), np.float64)
+        self._checked(self.lib.ref_fixture_read)(path.encode(), dims, _ptr(out), out.size)
+        return out
+
+    def fixture_probes(self, directory: str, seed: int) -> None:
+        """The reference CLI's golden probes (tools/scc/main.cpp:98-132), plus
+        each probe's input / weight / bias."""
+        self._checked(self.lib.ref_fixture_probes)(directory.encode(), seed)
+
+    # --- composition routes (reference.cpp:335-490) ---
+    def compose_forward(self, cfg: OracleConfig, route: str, use_cc: bool, x, w, b):
+        x, w = _d(x), _d(w)
+        b = _d(b) if b is not None else np.zeros(max(cfg.c_out, 1))
+        n, _, h, wd = x.shape
+        y = np.empty((n, cfg.c_out, h, wd), np.float64)
+        aux = _i64()
+        self._checked(self.lib.ref_compose_forward)(C.byref(cfg._c()), int(route == "conv"),
+                                                    int(use_cc), n, h, wd, _ptr(x), _ptr(w),
+                                                    _ptr(b), _ptr(y), C.byref(aux))
+        return y, int(aux.value)
+
+    def compose_backward(self, cfg: OracleConfig, route: str, use_cc: bool, dy, x, w):
+        dy, x, w = _d(dy), _d(x), _d(w)
+        n, _, h, wd = x.shape
+        dx = np.empty_like(x)
+        dw = np.empty(cfg.c_out * cfg.group_width, np.float64)
+        db = np.zeros(max(cfg.c_out, 1), np.float64)
+        self._checked(self.lib.ref_compose_backward)(C.byref(cfg._c()), int(route == "conv"),
+                                                     int(use_cc), n, h, wd, _ptr(dy), _ptr(x),
+                                                     _ptr(w), _ptr(dx), _ptr(dw), _ptr(db))
+        return dx, dw, (db[: cfg.c_out] if cfg.has_bias else None)
 
     # --- timed baseline (bench.py --impl reference / cpu_baseline) ---
     def problem(self, cfg: OracleConfig, x, w, b, dy):

@@ -15,6 +15,8 @@
 #include "sccl/config.hpp"
 #include "sccl/cycle.hpp"
 #include "sccl/errors.hpp"
+#include "sccl/fixture.hpp"
+#include "sccl/rng.hpp"
 #include "sccl/kernel.hpp"
 #include "sccl/parallel.hpp"
 #include "sccl/reference.hpp"
@@ -40,6 +42,9 @@ int map_exception() {
   } catch (const sccl::ArgumentError& e) {
     g_err = e.what();
     return 4;
+  } catch (const sccl::FormatError& e) {
+    g_err = e.what();
+    return 8;  // shim-local: the GPU C ABI has no file I/O
   } catch (const std::exception& e) {
     g_err = e.what();
     return 7;
@@ -331,6 +336,119 @@ extern "C" int sccl_ref_dw_backward(int64_t n, int64_t c, int64_t h, int64_t w, 
     std::memcpy(dx, r.grad_input.data(), sizeof(double) * static_cast<size_t>(r.grad_input.size()));
     std::memcpy(dwt, r.grad_weight.data(), sizeof(double) * r.grad_weight.size());
     if (db) std::memcpy(db, r.grad_bias.data(), sizeof(double) * r.grad_bias.size());
+    return 0;
+  } catch (...) {
+    return map_exception();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// DSX1 fixtures (fixture.cpp:29-97) and the golden probes of the reference
+// CLI (tools/scc/main.cpp:98-132: same configs, seeds and calls), plus the
+// probe inputs / weights so a GPU test can rerun them.
+extern "C" int ref_fixture_write(const char* path, int64_t n, int64_t c, int64_t h, int64_t w,
+                                 const double* data) {
+  try {
+    sccl::fixture_write(load(data, n, c, h, w), path);
+    return 0;
+  } catch (...) {
+    return map_exception();
+  }
+}
+
+// dims[4] out; data (capacity `cap` doubles) may be null to query the extents.
+extern "C" int ref_fixture_read(const char* path, int64_t* dims, double* data, int64_t cap) {
+  try {
+    const sccl::Tensor4 t = sccl::fixture_read(path);
+    dims[0] = t.n();
+    dims[1] = t.c();
+    dims[2] = t.h();
+    dims[3] = t.w();
+    if (data != nullptr) {
+      if (cap < t.size()) throw sccl::ArgumentError("buffer too small");
+      std::memcpy(data, t.data(), sizeof(double) * static_cast<size_t>(t.size()));
+    }
+    return 0;
+  } catch (...) {
+    return map_exception();
+  }
+}
+
+extern "C" int ref_fixture_probes(const char* dir, uint64_t seed) {
+  try {
+    struct Probe {
+      int64_t c_in, c_out, cg;
+      const char* co;
+    };
+    const Probe probes[] = {{4, 4, 2, "1"}, {6, 6, 2, "33%"}, {8, 16, 4, "50%"}, {12, 12, 3, "2"}};
+    int index = 0;
+    for (const Probe& p : probes) {
+      const sccl::SccConfig cfg =
+          sccl::scc_config_new(p.c_in, p.c_out, p.cg, sccl::Overlap::parse(p.co), true);
+      sccl::Rng rng(seed + static_cast<uint64_t>(index));
+      const sccl::Tensor4 input = sccl::tensor_normal(2, cfg.c_in, 5, 5, rng);
+      sccl::SccWeights wts = sccl::scc_weights_init(cfg, rng);
+      const sccl::Tensor4 out = sccl::scc_forward(input, wts, cfg);
+      const std::string base = std::string(dir) + "/probe_" + std::to_string(index);
+      sccl::fixture_write(out, base + ".dsx");
+      sccl::fixture_write(input, base + "_input.dsx");
+      sccl::Tensor4 w(1, cfg.c_out, 1, cfg.group_width), b(1, 1, 1, cfg.c_out);
+      std::memcpy(w.data(), wts.weight.data(), sizeof(double) * wts.weight.size());
+      std::memcpy(b.data(), wts.bias.data(), sizeof(double) * wts.bias.size());
+      sccl::fixture_write(w, base + "_weight.dsx");
+      sccl::fixture_write(b, base + "_bias.dsx");
+      ++index;
+    }
+    return 0;
+  } catch (...) {
+    return map_exception();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// The composition routes (reference.cpp:335-490): channel stack / conv stack,
+// with or without the channel-cyclic (CC) sharing -- the paper's "Base"
+// implementations of SCC from stock operators.
+namespace {
+sccl::SccWeights make_wts(const sccl::SccConfig& cfg, const double* wt, const double* bias) {
+  sccl::SccWeights wts;
+  wts.weight.assign(wt, wt + cfg.c_out * cfg.group_width);
+  if (cfg.has_bias) wts.bias.assign(bias, bias + cfg.c_out);
+  return wts;
+}
+}  // namespace
+
+extern "C" int ref_compose_forward(const ref_cfg* c, int32_t route, int32_t use_cc, int64_t n,
+                                   int64_t h, int64_t w, const double* x, const double* wt,
+                                   const double* bias, double* y, int64_t* aux_channels) {
+  try {
+    const sccl::SccConfig cfg = to_cfg(c);
+    const sccl::SccWeights wts = make_wts(cfg, wt, bias);
+    const sccl::Tensor4 in = load(x, n, cfg.c_in, h, w);
+    const sccl::CompositionResult r = route == 0 ? sccl::scc_channel_stack_forward(in, wts, cfg, use_cc != 0)
+                                                 : sccl::scc_conv_stack_forward(in, wts, cfg, use_cc != 0);
+    std::memcpy(y, r.output.data(), sizeof(double) * static_cast<size_t>(r.output.size()));
+    if (aux_channels) *aux_channels = r.stats.aux_channels_stored;
+    return 0;
+  } catch (...) {
+    return map_exception();
+  }
+}
+
+extern "C" int ref_compose_backward(const ref_cfg* c, int32_t route, int32_t use_cc, int64_t n,
+                                    int64_t h, int64_t w, const double* dy, const double* x,
+                                    const double* wt, double* dx, double* dwt, double* dbias) {
+  try {
+    const sccl::SccConfig cfg = to_cfg(c);
+    std::vector<double> zb(static_cast<size_t>(cfg.c_out), 0.0);
+    const sccl::SccWeights wts = make_wts(cfg, wt, zb.data());
+    const sccl::Tensor4 in = load(x, n, cfg.c_in, h, w), g = load(dy, n, cfg.c_out, h, w);
+    const sccl::SccGradients r = route == 0 ? sccl::scc_channel_stack_backward(g, in, wts, cfg, use_cc != 0)
+                                            : sccl::scc_conv_stack_backward(g, in, wts, cfg, use_cc != 0);
+    std::memcpy(dx, r.grad_input.data(), sizeof(double) * static_cast<size_t>(r.grad_input.size()));
+    std::memcpy(dwt, r.params.grad_weight.data(), sizeof(double) * r.params.grad_weight.size());
+    if (cfg.has_bias && dbias)
+      std::memcpy(dbias, r.params.grad_bias.data(), sizeof(double) * r.params.grad_bias.size());
     return 0;
   } catch (...) {
     return map_exception();
