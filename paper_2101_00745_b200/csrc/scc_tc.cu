@@ -94,6 +94,7 @@ struct TcBandArgs {
   int32_t out_cls;           // output view rows per class
   int32_t store_ok;          // TMA-store epilogue usable
   int32_t ptiles;            // pixel tiles per sample
+  int32_t spt;               // > 1: a tile packs spt = 128 / plane whole samples (planes that divide 128)
   int32_t panel_floats;      // whole panel size (resident mode)
   BandSmem sm;
   int64_t plane;
@@ -113,13 +114,24 @@ struct TileCoord {
   int n;
   int p0;
 };
+// Packed tiles (spt > 1): tile pt covers samples [pt*spt, pt*spt + spt), the
+// 128 TMEM lanes are (sample, pixel) in that order, p0 = 0.
 __device__ __forceinline__ TileCoord tile_coord(const TcBandArgs& a, int64_t t) {
   TileCoord c;
   c.rt = static_cast<int>(t % a.n_rt);
   const int64_t pt = t / a.n_rt;
+  if (a.spt > 1) {
+    c.n = static_cast<int>(pt * a.spt);
+    c.p0 = 0;
+    return c;
+  }
   c.n = static_cast<int>(pt / a.ptiles);
   c.p0 = static_cast<int>(pt - static_cast<int64_t>(c.n) * a.ptiles) * TM;
   return c;
+}
+
+__device__ __forceinline__ int64_t band_tiles(const TcBandArgs& a) {
+  return (a.spt > 1 ? (a.n + a.spt - 1) / a.spt : a.n * a.ptiles) * a.n_rt;
 }
 
 __device__ __forceinline__ int chunks_of(const TcBandArgs& a, int rt) {
@@ -186,7 +198,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   const uint32_t tmem = *tmem_slot;
   if (threadIdx.x == 0) TRACE(1);
 
-  const int64_t total = a.n * a.ptiles * a.n_rt;
+  const int64_t total = band_tiles(a);
 
   if (warp == 0) {
     // ---------------- producer: activation ring (+ streamed weight panel) ----------------
@@ -224,8 +236,12 @@ __global__ void __launch_bounds__(kTcThreads, 1)
               int pos = start8 + 32 * c + r;
               while (pos >= a.ring) pos -= a.ring;
               const int cl = pos / a.cls, j = pos - cl * a.cls;
-              tma_load_3d(a_ring + sa * kABytes + r * (TM * 4), &tmap, &a_full[sa], tc.p0,
-                          __ldg(a.class_d + cl), tc.n * a.rows_per_sample_3d + j);
+              if (a.spt > 1)  // 4-D view {P, N, rows, D}: box {P, spt, rb, 1} = [rb rows][128 px]
+                tma_load_4d(a_ring + sa * kABytes + r * (TM * 4), &tmap, &a_full[sa], 0, tc.n, j,
+                            __ldg(a.class_d + cl));
+              else
+                tma_load_3d(a_ring + sa * kABytes + r * (TM * 4), &tmap, &a_full[sa], tc.p0,
+                            __ldg(a.class_d + cl), tc.n * a.rows_per_sample_3d + j);
             }
           }
           __syncwarp();
@@ -395,8 +411,14 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       }
       mbar_wait_tag(&tfull[acc], acc_phase, 9);
       tc_fence_after();
-      const int64_t p = tc.p0 + q * 32 + lane;
-      const bool pv = p < a.plane;
+      // this lane's pixel: (sample n_l, pixel p) -- packed tiles hold spt samples
+      int n_l = tc.n;
+      int64_t p = tc.p0 + q * 32 + lane;
+      if (a.spt > 1) {
+        n_l = tc.n + static_cast<int>(p / a.plane);
+        p -= static_cast<int64_t>(n_l - tc.n) * a.plane;
+      }
+      const bool pv = p < a.plane && n_l < a.n;
       const uint32_t taddr = tmem + acc * C::kAccCols + (static_cast<uint32_t>(q * 32) << 16);
 #pragma unroll 1
       for (int c0 = 0; c0 < NT; c0 += 32) {
@@ -419,13 +441,20 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           __syncwarp();
           if (lane == 0) {
             const int cl = g0 / a.out_cls, jj = g0 - cl * a.out_cls;
-            tma_store_3d(&tout, buf, tc.p0 + 32 * q, __ldg(a.out_class_d + cl),
-                         tc.n * a.out_cls + jj);
+            if (a.spt > 1) {
+              // 4-D view {P, N, out_cls, D_out}: box {min(P,32), max(32/P,1), 32, 1}
+              const int px0 = 32 * q;
+              tma_store_4d(&tout, buf, static_cast<int>(px0 % a.plane), tc.n + static_cast<int>(px0 / a.plane), jj,
+                           __ldg(a.out_class_d + cl));
+            } else {
+              tma_store_3d(&tout, buf, tc.p0 + 32 * q, __ldg(a.out_class_d + cl),
+                           tc.n * a.out_cls + jj);
+            }
             bulk_commit();
           }
           sbuf ^= 1;
         } else if (pv) {
-          float* __restrict__ obase = a.out + static_cast<int64_t>(tc.n) * a.c_out_t * a.plane + p;
+          float* __restrict__ obase = a.out + static_cast<int64_t>(n_l) * a.c_out_t * a.plane + p;
           int32_t rr[32];
 #pragma unroll
           for (int j = 0; j < 32; ++j) rr[j] = row_s[c0 + j];
@@ -539,9 +568,30 @@ static cudaError_t launch_tc_nt(const TcBandPlan& tp, const TcDeviceTables& dt,
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
 
-  // --- activations: {P, D, N * rows_per_sample} fp32, no swizzle, box {32, 1, rb}
+  // Planes that divide the 128-pixel tile pack spt = 128 / P samples per tile
+  // (4-D views with a sample dimension); otherwise one sample per tile.
+  const int64_t P = call.plane;
+  const int32_t spt = (P < TM && TM % P == 0 && P % 4 == 0) ? static_cast<int32_t>(TM / P) : 1;
   CUtensorMap tm, tout;
-  {
+  if (spt > 1) {
+    const uint64_t C = static_cast<uint64_t>(tp.n_class) * tp.rows_per_sample_3d;
+    const uint64_t dims[4] = {static_cast<uint64_t>(P), static_cast<uint64_t>(call.n),
+                              static_cast<uint64_t>(tp.rows_per_sample_3d), static_cast<uint64_t>(tp.n_class)};
+    const uint64_t strides[3] = {C * P * 4, static_cast<uint64_t>(tp.n_class) * P * 4, static_cast<uint64_t>(P) * 4};
+    const uint32_t box[4] = {static_cast<uint32_t>(P), static_cast<uint32_t>(spt), static_cast<uint32_t>(tp.rb), 1};
+    if (!encode_f32(&tm, call.in, 4, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_NONE)) return cudaErrorInvalidValue;
+    const int32_t ocls = tp.store_ok ? tp.out_cls : call.c_out_t;
+    const int32_t ond = tp.store_ok ? tp.out_n_class : 1;
+    const uint64_t odims[4] = {static_cast<uint64_t>(P), static_cast<uint64_t>(call.n), static_cast<uint64_t>(ocls),
+                               static_cast<uint64_t>(ond)};
+    const uint64_t ostr[3] = {static_cast<uint64_t>(call.c_out_t) * P * 4, static_cast<uint64_t>(ond) * P * 4,
+                              static_cast<uint64_t>(P) * 4};
+    const uint32_t obox[4] = {static_cast<uint32_t>(std::min<int64_t>(P, 32)),
+                              static_cast<uint32_t>(std::max<int64_t>(32 / P, 1)), 32, 1};
+    if (!encode_f32(&tout, call.out, 4, odims, ostr, obox, CU_TENSOR_MAP_SWIZZLE_NONE)) return cudaErrorInvalidValue;
+  }
+  // --- activations: {P, D, N * rows_per_sample} fp32, no swizzle, box {32, 1, rb}
+  if (spt == 1) {
     const uint64_t dims[3] = {static_cast<uint64_t>(call.plane), static_cast<uint64_t>(tp.n_class),
                               static_cast<uint64_t>(call.n) * tp.rows_per_sample_3d};
     const uint64_t strides[2] = {static_cast<uint64_t>(call.plane) * 4,
@@ -551,7 +601,7 @@ static cudaError_t launch_tc_nt(const TcBandPlan& tp, const TcDeviceTables& dt,
       return cudaErrorInvalidValue;
   }
   // --- output view for TMA stores: {P, D_out, N * out_cls}, box {32, 1, 32}
-  {
+  if (spt == 1) {
     const int32_t ocls = tp.store_ok ? tp.out_cls : call.c_out_t;
     const int32_t ond = tp.store_ok ? tp.out_n_class : 1;
     const uint64_t dims[3] = {static_cast<uint64_t>(call.plane), static_cast<uint64_t>(ond),
@@ -581,9 +631,10 @@ static cudaError_t launch_tc_nt(const TcBandPlan& tp, const TcDeviceTables& dt,
   ka.store_ok = tp.store_ok && call.plane % 4 == 0;
   ka.rows_per_sample_3d = tp.rows_per_sample_3d;
   ka.ptiles = static_cast<int32_t>((call.plane + TM - 1) / TM);
+  ka.spt = spt;
   ka.plane = call.plane;
   ka.n = call.n;
-  const int64_t tiles = call.n * ka.ptiles * tp.n_rt;
+  const int64_t tiles = (spt > 1 ? (call.n + spt - 1) / spt : call.n * ka.ptiles) * tp.n_rt;
   int nsm = 148;
   {
     int dev = 0;

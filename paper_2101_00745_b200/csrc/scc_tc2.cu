@@ -643,9 +643,12 @@ __global__ void __launch_bounds__(kThreads, 1)
               float bb[32];
 #pragma unroll
               for (int j = 0; j < 32; ++j) bb[j] = bias_s[g0 + j];
-              if (a.store_mode == kStoreRows32) {
+              if (a.store_mode == kStoreRows32 && g0 + 32 <= a.c_out_t) {
                 // Stage [32 rows][32 px] (lanes own consecutive words: no
                 // conflicts) and write it with one TMA store; buffers rotate.
+                // (A group past the last channel -- a tile wider than the
+                // tensor -- takes the per-row path, which skips rows = -1;
+                // its class coordinate would be outside the store view.)
                 if (lane == 0) bulk_wait_read<kStoreBufs - 1>();
                 __syncwarp();
                 const uint32_t buf = wbuf_a + sbuf * kStoreBuf + lane * 4;
