@@ -570,7 +570,17 @@ void do_backward(Plan& p, int64_t n, int64_t h, int64_t w, const float* dy, cons
                      choose_path(p, n, h, w, 2) == SCC_PATH_TENSOR &&
                      tc_band2_supported(p.tc_bwd, plane, static_cast<int32_t>(p.cfg.c_out)) &&
                      tc_wgrad2_supported(p.tc_wgt, plane, static_cast<int32_t>(p.cfg.group_width));
-  if (!both2) {
+  // Generation-1 pair on a small (latency-bound) problem: the weight kernel
+  // is sized to half the SMs (tc_weight_small), backward-data takes the rest.
+  const bool both1 = !both2 && aligned16(dy) && aligned16(x) && aligned16(dx) &&
+                     p.path != SCC_PATH_CUDA_CORE &&
+                     tc_weight_small(n, plane, std::max(p.cfg.c_in, p.cfg.c_out)) &&
+                     choose_path(p, n, h, w, 1) == SCC_PATH_TENSOR &&
+                     choose_path(p, n, h, w, 2) == SCC_PATH_TENSOR &&
+                     tc_weight_supported(p.tc_wgt, plane) &&
+                     (p.path == SCC_PATH_TENSOR_STREAMED ||
+                      !tc_wgrad2_supported(p.tc_wgt, plane, static_cast<int32_t>(p.cfg.group_width)));
+  if (!both2 && !both1) {
     do_backward_data(p, n, h, w, dy, wt, dx, s);
     do_backward_weight(p, n, h, w, dy, x, dw, db, ws, ws_bytes, s);
     return;

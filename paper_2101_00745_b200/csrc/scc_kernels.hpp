@@ -128,6 +128,9 @@ cudaError_t launch_wgrad2(const TcWeightPlan& tw, const TcWeightCall& call, cons
                           cudaStream_t s);
 cudaError_t launch_band_tc(const TcBandPlan& tp, const TcDeviceTables& dt, const TcBandCall& call,
                            cudaStream_t s);
+// Small (latency-bound) problems: the generation-1 backward-weight kernel
+// takes half the SMs so scc_backward can run backward-data beside it.
+bool tc_weight_small(int64_t n, int64_t plane, int64_t channels);
 
 // Fused backward (scc_tc_bwd.cu): backward-data and backward-weight from one
 // pass over dy (either half can be switched off; the arithmetic of each half

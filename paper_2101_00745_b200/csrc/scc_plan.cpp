@@ -325,6 +325,8 @@ void build_tc_weight(const Plan& p, TcWeightPlan& tw) {
       break;
     }
   }
+  tw.c_in = static_cast<int32_t>(p.cfg.c_in);
+  tw.c_out = static_cast<int32_t>(p.cfg.c_out);
   tw.ok = true;
 }
 

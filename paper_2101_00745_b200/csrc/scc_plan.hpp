@@ -84,6 +84,7 @@ struct TcWeightPlan {
   bool ok = false;
   std::string why;
   int32_t n_rt = 0, n_nc = 0, nw = 0;  // row tiles, column chunks per tile, chunk width
+  int32_t c_in = 0, c_out = 0;
   int32_t cls = 0, n_class = 1;        // dy 3-D view (as backward-data)
   int32_t rba = 8, rbb = 8;            // TMA box rows for dy (per warp quarter) and x
   int32_t rbb1 = 8;                    // x box rows of the generation-1 kernel (no quarter rule)

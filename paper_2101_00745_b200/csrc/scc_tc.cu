@@ -116,11 +116,12 @@ struct TileCoord {
 };
 // Packed tiles (spt > 1): tile pt covers samples [pt*spt, pt*spt + spt), the
 // 128 TMEM lanes are (sample, pixel) in that order, p0 = 0.
+template <bool PACK>
 __device__ __forceinline__ TileCoord tile_coord(const TcBandArgs& a, int64_t t) {
   TileCoord c;
   c.rt = static_cast<int>(t % a.n_rt);
   const int64_t pt = t / a.n_rt;
-  if (a.spt > 1) {
+  if (PACK) {
     c.n = static_cast<int>(pt * a.spt);
     c.p0 = 0;
     return c;
@@ -130,15 +131,16 @@ __device__ __forceinline__ TileCoord tile_coord(const TcBandArgs& a, int64_t t) 
   return c;
 }
 
+template <bool PACK>
 __device__ __forceinline__ int64_t band_tiles(const TcBandArgs& a) {
-  return (a.spt > 1 ? (a.n + a.spt - 1) / a.spt : a.n * a.ptiles) * a.n_rt;
+  return (PACK ? (a.n + a.spt - 1) / a.spt : a.n * a.ptiles) * a.n_rt;
 }
 
 __device__ __forceinline__ int chunks_of(const TcBandArgs& a, int rt) {
   return (a.rt_info[4 * rt + 1] + 3) / 4;
 }
 
-template <int NT>
+template <int NT, bool PACK>
 __global__ void __launch_bounds__(kTcThreads, 1)
     tc_band_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap tout,
                    const TcBandArgs a) {
@@ -198,7 +200,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   const uint32_t tmem = *tmem_slot;
   if (threadIdx.x == 0) TRACE(1);
 
-  const int64_t total = band_tiles(a);
+  const int64_t total = band_tiles<PACK>(a);
 
   if (warp == 0) {
     // ---------------- producer: activation ring (+ streamed weight panel) ----------------
@@ -221,7 +223,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         }
       };
       for (int64_t t = blockIdx.x; t < total; t += gridDim.x) {
-        const TileCoord tc = tile_coord(a, t);
+        const TileCoord tc = tile_coord<PACK>(a, t);
         const int start8 = a.rt_info[4 * tc.rt], nk8 = a.rt_info[4 * tc.rt + 1];
         const int nch = (nk8 + 3) / 4;
         for (int c = 0; c < nch; ++c) {
@@ -236,7 +238,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
               int pos = start8 + 32 * c + r;
               while (pos >= a.ring) pos -= a.ring;
               const int cl = pos / a.cls, j = pos - cl * a.cls;
-              if (a.spt > 1)  // 4-D view {P, N, rows, D}: box {P, spt, rb, 1} = [rb rows][128 px]
+              if (PACK)  // 4-D view {P, N, rows, D}: box {P, spt, rb, 1} = [rb rows][128 px]
                 tma_load_4d(a_ring + sa * kABytes + r * (TM * 4), &tmap, &a_full[sa], 0, tc.n, j,
                             __ldg(a.class_d + cl));
               else
@@ -397,7 +399,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     int cur_rt = -1;
     int sbuf = 0;
     for (int64_t t = blockIdx.x; t < total; t += gridDim.x) {
-      const TileCoord tc = tile_coord(a, t);
+      const TileCoord tc = tile_coord<PACK>(a, t);
       const int rt = tc.rt;
       if (rt != cur_rt) {
         named_bar_sync(1, 128);
@@ -414,11 +416,11 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       // this lane's pixel: (sample n_l, pixel p) -- packed tiles hold spt samples
       int n_l = tc.n;
       int64_t p = tc.p0 + q * 32 + lane;
-      if (a.spt > 1) {
+      if (PACK) {
         n_l = tc.n + static_cast<int>(p / a.plane);
         p -= static_cast<int64_t>(n_l - tc.n) * a.plane;
       }
-      const bool pv = p < a.plane && n_l < a.n;
+      const bool pv = p < a.plane && (!PACK || n_l < a.n);
       const uint32_t taddr = tmem + acc * C::kAccCols + (static_cast<uint32_t>(q * 32) << 16);
 #pragma unroll 1
       for (int c0 = 0; c0 < NT; c0 += 32) {
@@ -441,7 +443,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           __syncwarp();
           if (lane == 0) {
             const int cl = g0 / a.out_cls, jj = g0 - cl * a.out_cls;
-            if (a.spt > 1) {
+            if (PACK) {
               // 4-D view {P, N, out_cls, D_out}: box {min(P,32), max(32/P,1), 32, 1}
               const int px0 = 32 * q;
               tma_store_4d(&tout, buf, static_cast<int>(px0 % a.plane), tc.n + static_cast<int>(px0 / a.plane), jj,
@@ -641,7 +643,7 @@ static cudaError_t launch_tc_nt(const TcBandPlan& tp, const TcDeviceTables& dt,
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   }
-  int64_t grid = std::min<int64_t>(tiles, nsm);
+  int64_t grid = std::min<int64_t>(tiles, call.max_ctas > 0 ? std::min(call.max_ctas, nsm) : nsm);
   // Shared memory: resident weight panel when it fits next to a >= 5-deep
   // activation ring; else, when a grid that is a multiple of n_rt gives each
   // CTA a single row tile, that row tile's panel resident; else a streamed
@@ -676,15 +678,19 @@ static cudaError_t launch_tc_nt(const TcBandPlan& tp, const TcDeviceTables& dt,
     sm.total = sm.a_stages * kABytes + b_total + C::kStoreBytes + 1024 + 512;
   }
   ka.panel_floats = static_cast<int32_t>(tc_panel_bytes(tp) / 4);
+  // packed tiles are a separate instantiation: the unpacked kernel keeps its
+  // register allocation (the sample arithmetic cost 20 registers and ~25 %
+  // at C256 cg8 56x56 when it was a runtime branch)
+  auto kern = spt > 1 ? tc_band_kernel<NT, true> : tc_band_kernel<NT, false>;
   {
-    static bool attr_set[64] = {false};  // per device, per template instance
+    static bool attr_set[2][64] = {{false}};  // per packing, device, template instance
     int dev = 0;
     cudaGetDevice(&dev);
-    if (dev < 0 || dev >= 64 || !attr_set[dev]) {
-      e = cudaFuncSetAttribute(tc_band_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               227 * 1024 - 1024);
+    const int pk = spt > 1 ? 1 : 0;
+    if (dev < 0 || dev >= 64 || !attr_set[pk][dev]) {
+      e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024 - 1024);
       if (e != cudaSuccess) return e;
-      if (dev >= 0 && dev < 64) attr_set[dev] = true;
+      if (dev >= 0 && dev < 64) attr_set[pk][dev] = true;
     }
   }
   cudaLaunchConfig_t cfg{};
@@ -697,7 +703,7 @@ static cudaError_t launch_tc_nt(const TcBandPlan& tp, const TcDeviceTables& dt,
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  e = cudaLaunchKernelEx(&cfg, tc_band_kernel<NT>, tm, tout, ka);
+  e = cudaLaunchKernelEx(&cfg, kern, tm, tout, ka);
   if (e != cudaSuccess) return e;
   note_launches(2);
   return cudaSuccess;

@@ -496,8 +496,12 @@ WGrid weight_grid(const TcWeightPlan& tw, int64_t n, int64_t plane) {
   g.total_chunks = n * g.pcs;
   const int64_t items = static_cast<int64_t>(tw.n_rt) * tw.n_nc;
   // One CTA per SM (shared memory): a grid just over 148 runs a second,
-  // nearly empty wave, so round the split count down.
-  int64_t splits = std::max<int64_t>(1, 148 / items);
+  // nearly empty wave, so round the split count down.  Small problems
+  // (latency bound) get half the SMs: scc_backward then runs backward-data
+  // beside this kernel on the other half (tc_weight_small); the rule depends
+  // on the geometry only, so every entry point sums in the same order.
+  const int64_t cap = tc_weight_small(n, plane, std::max(tw.c_in, tw.c_out)) ? 74 : 148;
+  int64_t splits = std::max<int64_t>(1, cap / items);
   splits = std::min(splits, g.total_chunks);
   g.chunks_per_split = (g.total_chunks + splits - 1) / splits;
   g.splits = static_cast<int32_t>((g.total_chunks + g.chunks_per_split - 1) / g.chunks_per_split);
@@ -509,6 +513,13 @@ WGrid weight_grid(const TcWeightPlan& tw, int64_t n, int64_t plane) {
 int tc_wtrace(unsigned long long* out, int n) {
   if (n > 32) n = 32;
   return cudaMemcpyFromSymbol(out, g_wtrace, n * sizeof(unsigned long long)) == cudaSuccess ? n : -1;
+}
+
+// latency bound: little work per SM even on half the SMs (measured on the C5
+// 14x14 rows and the SCC-ResNet-18 8x8 / 4x4 layers: a win up to ~2 M
+// pixel-channels, a loss from C=512 at 14x14 on, where the MMAs dominate)
+bool tc_weight_small(int64_t n, int64_t plane, int64_t channels) {
+  return n * plane <= 16384 && n * plane * channels <= (int64_t{1} << 21);
 }
 
 bool tc_weight_supported(const TcWeightPlan& tw, int64_t plane) {

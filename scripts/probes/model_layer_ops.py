@@ -39,9 +39,12 @@ for ci, co, hw in SHAPES:
     ws = torch.empty(max(wsb, 1), dtype=torch.uint8, device="cuda")
     fwd = lambda i, s: _lib.check(L.scc_forward_f32(cfg.handle, N, hw, hw, xs[i].data_ptr(), wts.weight.data_ptr(), wts.bias.data_ptr(), ys[i].data_ptr(), s))
     bwd = lambda i, s: _lib.check(L.scc_backward_f32(cfg.handle, N, hw, hw, dys[i].data_ptr(), xs[i].data_ptr(), wts.weight.data_ptr(), dxs[i].data_ptr(), g.data_ptr(), g.data_ptr() + 4 * co * gw, ws.data_ptr(), wsb, s))
+    bd = lambda i, s: _lib.check(L.scc_backward_data_f32(cfg.handle, N, hw, hw, dys[i].data_ptr(), wts.weight.data_ptr(), dxs[i].data_ptr(), s))
+    bw = lambda i, s: _lib.check(L.scc_backward_weight_f32(cfg.handle, N, hw, hw, dys[i].data_ptr(), xs[i].data_ptr(), g.data_ptr(), g.data_ptr() + 4 * co * gw, ws.data_ptr(), wsb, s))
     tf, tb = tg(fwd, R), tg(bwd, R)
+    tbd, tbw = tg(bd, R), tg(bw, R)
     P = hw * hw
     bf, bb = 4 * N * P * (ci + co), 4 * N * P * (2 * ci + co)
     tot += tf + tb
-    print(f"{ci:4d}->{co:4d} {hw:2d}x{hw:<2d} path {cfg.path_for(N, hw, hw)}  fwd {tf:7.2f} us ({bf / tf / 1e3:6.0f} GB/s)  bwd {tb:7.2f} us ({bb / tb / 1e3:6.0f} GB/s)", flush=True)
+    print(f"{ci:4d}->{co:4d} {hw:2d}x{hw:<2d} path {cfg.path_for(N, hw, hw)}  fwd {tf:7.2f} us ({bf / tf / 1e3:6.0f} GB/s)  bwd {tb:7.2f} us ({bb / tb / 1e3:6.0f} GB/s)  [data {tbd:6.2f}  weight {tbw:6.2f}]", flush=True)
 print(f"sum {tot:.1f} us")
