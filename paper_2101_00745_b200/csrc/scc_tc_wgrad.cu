@@ -417,6 +417,7 @@ __global__ void __launch_bounds__(256) tc_weight_finalize_wide(const FArgs a) {
     if (o < nw_out) {
       const int oc = static_cast<int>(o / a.gw);
       const int64_t base = fin_base(a, oc, static_cast<int>(o - static_cast<int64_t>(oc) * a.gw));
+#pragma unroll 8
       for (int sp = 0; sp < a.splits; ++sp) s += a.part[base + sp * stride];
       a.dweight[o] = s;
     } else {
@@ -429,13 +430,17 @@ __global__ void __launch_bounds__(256) tc_weight_finalize_wide(const FArgs a) {
   }
 }
 
-// Few outputs, many splits: block = 32 consecutive outputs x 32 warps; warp w
-// sums splits w, w+32, ... in order (each load a coalesced row piece of one
+// Few outputs, many splits: block = 32 consecutive outputs x W warps; warp w
+// sums splits w, w+W, ... in order (each load a coalesced row piece of one
 // split plane -- the former warp-per-output scheme touched 32 split planes per
-// load, ~8x the sectors), then warp 0 adds the 32 warp sums in order.
-constexpr int kFinWarps = 32;
-__global__ void __launch_bounds__(32 * kFinWarps) tc_weight_finalize(const FArgs a) {
-  __shared__ float red[kFinWarps][33];
+// load, ~8x the sectors), then warp 0 adds the W warp sums in order.  W is
+// chosen from the output count so the grid is one resident wave (round 1
+// used W = 32 everywhere: 1032 blocks of 1024 threads, one load each, at
+// C256 cg2 14x14 -- 19.8 us cold for 4.2 MB).  The order depends on W, which
+// depends on the geometry only.
+template <int W>
+__global__ void __launch_bounds__(32 * W) tc_weight_finalize(const FArgs a) {
+  __shared__ float red[W][33];
   cudaGridDependencySynchronize();
   cudaTriggerProgrammaticLaunchCompletion();
   const int64_t nw_out = static_cast<int64_t>(a.c_out) * a.gw;
@@ -447,22 +452,41 @@ __global__ void __launch_bounds__(32 * kFinWarps) tc_weight_finalize(const FArgs
     const int oc = static_cast<int>(o / a.gw);
     const int64_t base = fin_base(a, oc, static_cast<int>(o - static_cast<int64_t>(oc) * a.gw));
     const int64_t stride = static_cast<int64_t>(a.n_rt) * a.n_nc * 128 * a.nw;
-    for (int sp = w; sp < a.splits; sp += kFinWarps) s += a.part[base + sp * stride];
+#pragma unroll 8
+    for (int sp = w; sp < a.splits; sp += W) s += a.part[base + sp * stride];
   } else if (o < total) {
     const int oc = static_cast<int>(o - nw_out);
     const int pos = a.inv_perm[oc];
     const int rt = pos >> 7, row = pos & 127;
-    for (int sp = w; sp < a.splits; sp += kFinWarps) s += a.pbias[(static_cast<int64_t>(sp) * a.n_rt + rt) * 128 + row];
+#pragma unroll 8
+    for (int sp = w; sp < a.splits; sp += W) s += a.pbias[(static_cast<int64_t>(sp) * a.n_rt + rt) * 128 + row];
+  }
+  if (W == 1) {
+    if (o < total) {
+      if (o < nw_out) a.dweight[o] = s;
+      else a.dbias[o - nw_out] = s;
+    }
+    return;
   }
   red[w][l] = s;
   __syncthreads();
   if (w == 0 && o < total) {
     float t = red[0][l];
 #pragma unroll
-    for (int q = 1; q < kFinWarps; ++q) t += red[q][l];
+    for (int q = 1; q < W; ++q) t += red[q][l];
     if (o < nw_out) a.dweight[o] = t;
     else a.dbias[o - nw_out] = t;
   }
+}
+
+// Warps per finalize block: the largest W in {32, 16, 8, 4, 2, 1} whose grid
+// (one block per 32 outputs) fits in one wave of 148 SMs x 2048 threads.
+int fin_warps(int64_t outs) {
+  const int64_t blocks = (outs + 31) / 32;
+  for (int w : {32, 16, 8, 4, 2}) {
+    if (blocks * 32 * w <= 148ll * 2048) return w;
+  }
+  return 1;
 }
 
 struct WGrid {
@@ -650,9 +674,17 @@ cudaError_t launch_weight_tc(const TcWeightPlan& tw, const TcWeightCall& call, c
     fc.blockDim = dim3(256);
     e = cudaLaunchKernelEx(&fc, tc_weight_finalize_wide, f);
   } else {
+    const int wf = fin_warps(outs);
     fc.gridDim = dim3(static_cast<unsigned>((outs + 31) / 32));
-    fc.blockDim = dim3(32 * kFinWarps);
-    e = cudaLaunchKernelEx(&fc, tc_weight_finalize, f);
+    fc.blockDim = dim3(32 * wf);
+    switch (wf) {
+      case 32: e = cudaLaunchKernelEx(&fc, tc_weight_finalize<32>, f); break;
+      case 16: e = cudaLaunchKernelEx(&fc, tc_weight_finalize<16>, f); break;
+      case 8: e = cudaLaunchKernelEx(&fc, tc_weight_finalize<8>, f); break;
+      case 4: e = cudaLaunchKernelEx(&fc, tc_weight_finalize<4>, f); break;
+      case 2: e = cudaLaunchKernelEx(&fc, tc_weight_finalize<2>, f); break;
+      default: e = cudaLaunchKernelEx(&fc, tc_weight_finalize<1>, f); break;
+    }
   }
   note_launches(2);
   return e;
