@@ -1,47 +1,48 @@
-// Fused tensor-core backward (tcgen05, 3xTF32), sm_100a: backward-data and
+// Fused tensor-core backward (tcgen05, bf16x3), sm_100a: backward-data and
 // backward-weight of one SCC layer from a single pass over dy
 // (replaces scc_backward_input + scc_backward_params, kernel.cpp:100-189):
 //
 //   dx[n, ic, p]  = sum_oc  W^T[ic, oc] * dy[n, oc, p]          (W^T: window-relative W scattered)
 //   dW[oc, ic]    = sum_{n,p} dy[n, oc, p] * x[n, ic, p]        (ic in the arc of the filters)
-//   db[oc]        = sum_{n,p} dy[n, oc, p]                      (a ones row appended to x)
+//   db[oc]        = sum_{n,p} dy[n, oc, p]                      (CUDA cores, fp32)
+//
+// Precision: every operand is split into bf16 hi + lo (x = hi + lo + r, |r| <=
+// 2^-18 |x|) and the MMAs (kind::f16, fp32 accumulate) take hi*hi + hi*lo +
+// lo*hi (+ lo*lo for dx, free with the stacked W^T): ~1e-5 relative per
+// product, inside the gradients' 1e-4 bar, at twice the rate of the 3xTF32
+// kernels (K = 16 per instruction at the tf32 K = 8 cycle count).  The forward
+// (1e-5 bar) stays 3xTF32.
 //
 // Geometry: one row tile of filters (c_out <= 128, in the class-major order
 // of a single {32 px, cls, D} dy box) and c_in <= 64 input channels.  The
 // pipeline moves PAIRS of 32-pixel blocks (any two consecutive blocks of the
-// CTA's pixel slice):
-//   * dy [c_out rows][32 px] of each block lands by TMA in the
-//     SWIZZLE_128B_BASE32B layout, which is at once an MN-major B operand of
-//     the dx GEMM (D[ic][px] = W^T[ic][oc] * dy[oc][px], K = oc; the pair's two
-//     blocks are the two 32-px atoms of an N = 64 operand) and row-readable by
-//     the converter warps, which write its tf32 lo part to the lo buffers (dx
-//     B lo) and its hi / lo rows to TMEM (A of the dW GEMM, lanes = filters);
-//   * x [arc rows][32 px] (SWIZZLE_128B, K-major) plus a converted lo copy is
-//     B of the dW GEMM (D[oc][ic] = dy[oc][px] * x[ic][px], K = px).
+// CTA's pixel slice); each pair lands raw by TMA and is rewritten in place:
+//   * dy [c_out rows][64 px] -> bf16 hi | lo rows (SWIZZLE_128B, MN-major):
+//     B of the dx GEMM (D[ic][px] = W^T[ic][oc] * dy[oc][px], K = oc); the same
+//     hi | lo rows go to TMEM as A of the dW GEMM (lanes = filters, K = px);
+//   * x [arc rows][64 px] -> bf16 hi | lo rows (SWIZZLE_128B, K-major): B of
+//     the dW GEMM (D[oc][ic] = dy[oc][px] * x[ic][px]).
 // W^T stays resident in TMEM, stacked: lanes 0-63 hold W_hi, lanes 64-127
 // W_lo, so one M = 128 MMA yields W_hi*B and W_lo*B in the two lane halves
-// (the epilogue adds them); 3xTF32 for dx is then two MMAs per k-step
-// ([W_hi; W_lo] * dy and [W_hi; W_lo] * dy_lo, the lo*lo term included for
-// free).  Every GEMM runs in TS mode (A from TMEM); shared memory only feeds
-// B operands.  Per pair the MMAs that read the lo buffers go first, so the
-// converters refill them while the rest of the pair's MMAs run.
+// (the epilogue adds them).  Every GEMM runs in TS mode (A from TMEM).
 //
 // dW accumulates over the CTA's pixel slice in TMEM and is written as that
 // slice's window-relative partial (db: the dy converters sum their rows on
-// the CUDA cores, so the dW GEMM's N is exactly the x arc); a PDL-chained
-// kernel sums the slice partials in a fixed order (the slice count is fixed
-// per geometry, so the bits of dW do not depend on the grid).  dx is drained from TMEM per pair; the W_lo half of the stacked
-// accumulator is exchanged through shared memory and the W_hi half adds it
-// and stores straight to global.  The same kernel, with either GEMM switched
-// off, serves scc_backward_input / scc_backward_params alone, so the fused
-// and separate entry points agree bit for bit.
+// the CUDA cores); a PDL-chained kernel sums the slice partials in a fixed
+// order (the slice count is fixed per geometry, so the bits of dW do not
+// depend on the grid).  dx is drained from TMEM per pair (two accumulators);
+// the W_lo half of the stacked accumulator is staged in shared memory, the
+// W_hi half adds itself in place and one TMA store per block writes dx.  The same kernel,
+// with either GEMM switched off, serves scc_backward_input /
+// scc_backward_params alone, so the fused and separate entry points agree bit
+// for bit.
 //
 // Warp roles (384 threads, one CTA per SM, one slice per CTA):
 //   warp 0      TMA producer
 //   warp 1      TMEM allocator + MMA issuer
-//   warps 2-3   x lo converters (+ the constant ones / zero rows)
-//   warps 4-7   dy row converters (warp q: filter rows 32q..32q+31)
-//   warps 8-11  W^T build (prologue), dx epilogue, dW slice epilogue
+//   warps 2-3   x converters (thread = x row)
+//   warps 4-7   dy converters (thread = filter row), db, dW slice epilogue
+//   warps 8-11  W^T build (prologue), dx epilogue
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
@@ -59,7 +60,7 @@ using namespace sm100;
 // Diagnostic timeline (build with -DSCC_TRACE): CTA-0 %globaltimer slots and
 // per-CTA start / end stamps; scripts/bwd_timing.py reads them.
 #if defined(SCC_TRACE)
-__device__ unsigned long long g_trace3[64];
+__device__ unsigned long long g_trace3[128];
 __device__ unsigned long long g_cta3[2 * 256];
 #define TRACE3(slot)                                         \
   do {                                                       \
@@ -79,17 +80,20 @@ __device__ unsigned long long g_cta3[2 * 256];
 #endif
 
 constexpr int kThreads = 384;
-constexpr int kSlots = 3;             // raw TMA pair slots (dy | x per block); x_lo is written in place
-constexpr int kStages = 2;            // dy_lo pairs and TMEM dW A stages
+constexpr int kSlots = 4;             // pair slots: raw dy | x per block, overwritten in place by bf16 hi | lo
 constexpr int kSlices = 148;          // pixel slices (dW partials) per launch = CTAs (one per SM)
 constexpr int kSmemLimit = 227 * 1024;
 constexpr int kMaxGw = 32;
 constexpr int kMaxXr = 64;            // dW accumulator columns
 // TMEM columns (512 allocated)
-constexpr uint32_t kWt = 0;          // W^T: [ic lane (hi) | 64 + ic lane (lo)][oc column]
-constexpr uint32_t kDwAcc = 128;     // dW accumulator: [filter lane][x row column] (xr <= 64)
-constexpr uint32_t kDxAcc = 192;     // dx accumulator: [ic lane (+64: lo part)][64 px]
-constexpr uint32_t kDwA = 256;       // per stage: dy hi | lo of the pair's two blocks [filter lane][px]
+constexpr uint32_t kWt = 0;          // W^T bf16 pairs: [ic lane (hi) | 64 + ic lane (lo)][oc pair column]
+constexpr uint32_t kDwAcc = 64;      // dW accumulator: [filter lane][x row column] (xr <= 64)
+constexpr uint32_t kDxAcc = 128;     // dx accumulators (2): [ic lane (+64: lo part)][64 px]
+constexpr uint32_t kDwA = 256;       // per slot: dy hi | lo bf16 pairs of the pair's 64 px [filter lane][32 | 32]
+// MN-major bf16 B (the dx GEMM's dy): SWIZZLE_128B atoms of 8 K rows x 64 px,
+// SBO = 1024 between 8-row K groups, LBO = stride between 64-px atoms (one
+// atom: N = 64); verified by tests/cuda/bf16_probe.cu
+constexpr uint32_t kMnLbo = 8192;
 
 struct BArgs {
   float* part;               // [slices][c_out*gw + c_out] partial dW | db (c_out <= 128)
@@ -130,29 +134,30 @@ __device__ __forceinline__ int blk_u(const BArgs& a, int sl, int m) { return sl 
 
 
 __host__ __device__ constexpr int round1k(int b) { return (b + 1023) & ~1023; }
+__host__ __device__ constexpr int round16(int v) { return (v + 15) & ~15; }
 
-// Shared memory: kSlots raw TMA pair slots (per block: dy | x; x is turned
-// into x_lo in place once the MMAs that read raw x are done), kStages dy_lo
-// pairs (the dx GEMM's B lo), one dx exchange pair (the W_lo half of the
-// accumulator, handed to the W_hi half), the per-filter (oc*gw - start,
-// start) table.  The W staging of the prologue
-// aliases the exchange pair when it fits (its first use follows the dx MMAs,
-// which wait for W^T); the dW row dump of the epilogue aliases slot 0 (every
-// MMA has completed by then).
+// Shared memory: kSlots pair slots of two blocks (dy | x each, as TMA lands
+// them: [rows][32 px] fp32, SWIZZLE_128B); the converters overwrite a pair in
+// place with its bf16 hi (block 0) and lo (block 1) parts, [rows][64 px]
+// SWIZZLE_128B -- the same 128 B row span per row, so each converter thread
+// only rewrites the rows it read.  Then two dx staging pairs (the W_lo half
+// of the accumulator is written there, the W_hi half adds itself in place, one
+// TMA store per block reads it), the per-filter (oc*gw - start, start) table.
+// The W staging of the prologue aliases the dx staging (its first use follows
+// the dx MMAs, which wait for W^T); the dW row dump of the epilogue aliases
+// slot 0 (every MMA has completed by then).
 struct BLayout {
-  int blk, x, slot, dlo, dlob, stg, stgb, wst, kt, dump, bars, total;
+  int blk, x, slot, stg, stgb, wst, kt, dump, bars, total;
   __host__ __device__ BLayout(int c_in, int c_out, int gw, int xr) {
-    const int dyb = round1k(c_out * 128), xb = round1k(xr * 128);
+    const int dyb = round1k(round16(c_out) * 128), xb = round1k(xr * 128);
     blk = dyb + xb;                       // one block: dy | x
     x = dyb;
     slot = 2 * blk;
-    dlob = 2 * dyb;                       // one dy_lo pair
-    dlo = kSlots * slot;
     stgb = round1k(c_in * 128);           // one block's dx [c_in rows][32 px] (SWIZZLE_128B)
-    stg = dlo + kStages * dlob;
-    int end = stg + 2 * stgb;
+    stg = kSlots * slot;                  // 2 staging pairs (TMA-store sources)
+    int end = stg + 4 * stgb;
     const int wneed = c_out * gw * 4;
-    if (wneed <= 2 * stgb) {
+    if (wneed <= 4 * stgb) {
       wst = stg;
     } else {
       wst = end;
@@ -168,48 +173,54 @@ struct BLayout {
 };
 
 // Row `L` (this thread's TMEM lane) of the resident stacked W^T operand:
-// lane ic (< 64) holds W_hi, lane 64 + ic holds W_lo, class-major filter
-// columns, zero outside each filter's window; built from W and the
-// (oc*gw - start, start) table staged in shared memory.
+// lane ic (< 64) holds bf16 W_hi, lane 64 + ic bf16 W_lo, class-major filter
+// columns in bf16 pairs, zero outside each filter's window and past c_out;
+// built from W and the (oc*gw - start, start) table staged in shared memory.
 __device__ __forceinline__ void build_wt(const BArgs& a, uint32_t tmem, uint32_t lane_base, int L,
                                          const float* ws, const int2* kt) {
   const int ic = L & 63;
   const bool lo_lane = L >= 64;
   const bool live = ic < a.c_in;
-  for (int c0 = 0; c0 < a.c_out; c0 += 32) {
-    float v[32];
-    if (a.cls % 32 == 0) {
-      // the chunk is one window class: one start, filters D apart in W
-      const int2 e = kt[c0];
-      const int wrap = ic < e.y ? a.c_in : 0;
-      const bool in = live && static_cast<unsigned>(ic - e.y + wrap) < static_cast<unsigned>(a.gw);
-      const float* p = ws + (in ? e.x + ic + wrap : 0);
-      const int stride = a.n_class * a.gw;
-#pragma unroll
-      for (int t = 0; t < 32; ++t) v[t] = in ? p[t * stride] : 0.f;
-    } else {
-      int idx[32];
-#pragma unroll
-      for (int t = 0; t < 32; ++t) {
-        const int2 e = kt[min(c0 + t, a.c_out - 1)];
-        const int wrap = ic < e.y ? a.c_in : 0;
-        const bool in = live && static_cast<unsigned>(ic - e.y + wrap) < static_cast<unsigned>(a.gw) &&
-                        c0 + t < a.c_out;
-        idx[t] = in ? e.x + ic + wrap : -1;
-      }
-#pragma unroll
-      for (int t = 0; t < 32; ++t) {
-        const float w = ws[max(idx[t], 0)];
-        v[t] = idx[t] >= 0 ? w : 0.f;
-      }
-    }
+  const int cpad = round16(a.c_out);
+  for (int c0 = 0; c0 < cpad; c0 += 64) {
     uint32_t r[32];
 #pragma unroll
-    for (int t = 0; t < 32; ++t) {
-      const float h = tf32_hi(v[t]);
-      r[t] = __float_as_uint(lo_lane ? v[t] - h : h);
+    for (int h = 0; h < 2; ++h) {
+      const int cb = c0 + 32 * h;
+      float v[32];
+      if (a.cls % 32 == 0 && cb < a.c_out) {
+        // the chunk is one window class: one start, filters D apart in W
+        const int2 e = kt[cb];
+        const int wrap = ic < e.y ? a.c_in : 0;
+        const bool in = live && static_cast<unsigned>(ic - e.y + wrap) < static_cast<unsigned>(a.gw);
+        const float* p = ws + (in ? e.x + ic + wrap : 0);
+        const int stride = a.n_class * a.gw;
+#pragma unroll
+        for (int t = 0; t < 32; ++t) v[t] = in ? p[t * stride] : 0.f;
+      } else {
+        int idx[32];
+#pragma unroll
+        for (int t = 0; t < 32; ++t) {
+          const int2 e = kt[min(cb + t, a.c_out - 1)];
+          const int wrap = ic < e.y ? a.c_in : 0;
+          const bool in = live && static_cast<unsigned>(ic - e.y + wrap) < static_cast<unsigned>(a.gw) &&
+                          cb + t < a.c_out;
+          idx[t] = in ? e.x + ic + wrap : -1;
+        }
+#pragma unroll
+        for (int t = 0; t < 32; ++t) {
+          const float w = ws[max(idx[t], 0)];
+          v[t] = idx[t] >= 0 ? w : 0.f;
+        }
+      }
+#pragma unroll
+      for (int t = 0; t < 16; ++t) {
+        uint32_t hi, lo;
+        bf16x2_split(v[2 * t], v[2 * t + 1], hi, lo);
+        r[16 * h + t] = lo_lane ? lo : hi;
+      }
     }
-    tmem_st32(tmem + kWt + c0 + lane_base, r);
+    tmem_st32(tmem + kWt + c0 / 2 + lane_base, r);
   }
   tmem_st_wait();
   tc_fence_before();
@@ -218,31 +229,74 @@ __device__ __forceinline__ void build_wt(const BArgs& a, uint32_t tmem, uint32_t
 __device__ __forceinline__ float4 f4(const uint32_t* v) {
   return make_float4(__uint_as_float(v[0]), __uint_as_float(v[1]), __uint_as_float(v[2]), __uint_as_float(v[3]));
 }
+__device__ __forceinline__ void sts_u4(uint32_t addr, const uint32_t* v) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]));
+}
 
-// Pipeline (pair p: raw slot p % 3, dy_lo pair and TMEM dW A stage p % 2):
-//   MMA  dW raw (dy_hi * x, dy_lo * x)  -> commit xraw   (x converters: x -> x_lo in place)
-//        dx (W^T * dy, W^T * dy_lo)     -> commit dxfull (single accumulator; epilogue drains it)
-//        dW lo (dy_hi * x_lo)           -> commit pfree (dy_lo pair + TMEM A), sfree (raw slot)
-// so three pairs of raw data are in flight from the start (round 1 kept one
-// lo pair and one TMEM A: conversion and MMA alternated, ~2 us per pair
-// against 1.1 us of tensor work), the dy converters of pair p+1 run under the
-// MMAs of pair p, and the in-place x_lo conversion runs under the dx MMAs.
-// The first pair's dW MMAs do not need W^T, so they start while it is built.
+// One 128 B row of a pair (row r of block 0 and of block 1: 64 fp32 pixels,
+// 16 B chunk j at physical chunk j ^ (r % 8)) -> bf16 hi | lo pairs (word c =
+// pixels 2c, 2c+1), written back in place: hi over block 0's row, lo over block
+// 1's (16 B chunk j = pixels 8j..8j+7 at j ^ (r % 8)).  The 8 rows of a
+// quarter warp hit 8 distinct 16 B bank groups on every access.  Block 1 reads
+// as zeros when the pair has one block.  Returns the fp32 sum of the row.
+__device__ __forceinline__ float convert_row(uint32_t row0, uint32_t row1, int r, int nb, uint32_t (&hi)[32],
+                                             uint32_t (&lo)[32]) {
+  const int sw = r & 7;
+  float sum = 0.f;
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    float v[32];
+    if (k == 0 || nb > 1) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float4 t = lds_v4((k ? row1 : row0) + ((j ^ sw) << 4));
+        v[4 * j] = t.x, v[4 * j + 1] = t.y, v[4 * j + 2] = t.z, v[4 * j + 3] = t.w;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] = 0.f;
+    }
+    float s0 = 0.f, s1 = 0.f;
+#pragma unroll
+    for (int j = 0; j < 32; j += 2) s0 += v[j], s1 += v[j + 1];
+    sum += s0 + s1;
+#pragma unroll
+    for (int c = 0; c < 16; ++c) bf16x2_split(v[2 * c], v[2 * c + 1], hi[16 * k + c], lo[16 * k + c]);
+  }
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    sts_u4(row0 + ((j ^ sw) << 4), hi + 4 * j);
+    sts_u4(row1 + ((j ^ sw) << 4), lo + 4 * j);
+  }
+  return sum;
+}
+
+// Pipeline (pair p: slot and TMEM A stage p % kSlots, dx accumulator p % 2):
+//   producer   TMA dy | x of both blocks into the slot
+//   dy warps   rows -> bf16 hi | lo in place (dx GEMM B, MN-major) + TMEM A of
+//              the dW GEMM (lanes = filters) + db on the CUDA cores
+//   x warps    rows -> bf16 hi | lo in place (dW GEMM B, K-major)
+//   MMA        dW: dy_hi*x_hi + dy_lo*x_hi + dy_hi*x_lo      (K = pair pixels)
+//              dx: [W_hi; W_lo]*dy_hi + [W_hi; W_lo]*dy_lo   (K = filters)
+//              -> commit dxfull[p % 2], sfree[slot]
+//   epilogue   dx accumulator -> global (W_lo half added through smem)
+// All of a CTA's slots are in flight from the start at config 1 (~3.5 pairs
+// per CTA); the double-buffered dx accumulator lets the MMAs of pair p+1 run
+// while pair p drains.  The first pair's dW MMAs do not need W^T, so they
+// start while it is built.
 __global__ void __launch_bounds__(kThreads, 1)
     tc_bwd_kernel(const __grid_constant__ CUtensorMap tdy, const __grid_constant__ CUtensorMap tx,
-                  const __grid_constant__ BArgs a) {
+                  const __grid_constant__ CUtensorMap tdx, const __grid_constant__ BArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const BLayout L(a.c_in, a.c_out, a.gw, a.xr);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bars);
   uint64_t* full = bars;                       // [slot] TMA landed
-  uint64_t* sfree = full + kSlots;             // [slot] MMA commit: raw slot consumed
-  uint64_t* pfree = sfree + kSlots;            // [stage] MMA commit: dy_lo pair + TMEM A consumed
-  uint64_t* conv = pfree + kStages;            // [stage] 4 dy converter warps: dy_lo + dW A written
-  uint64_t* xraw = conv + kStages;             // [stage] MMA commit: raw x consumed
-  uint64_t* xlo = xraw + kStages;              // [stage] 2 x warps: x_lo written in place
-  uint64_t* dxfull = xlo + kStages;            // MMA commit
-  uint64_t* dxempty = dxfull + 1;              // 4 epilogue warps
-  uint64_t* accfull = dxempty + 1;             // MMA commit: the slice's dW done
+  uint64_t* sfree = full + kSlots;             // [slot] MMA commit: slot + TMEM A stage consumed
+  uint64_t* conv = sfree + kSlots;             // [slot] 4 dy converter warps: dy hi | lo + dW A written
+  uint64_t* xconv = conv + kSlots;             // [slot] 2 x warps: x hi | lo written
+  uint64_t* dxfull = xconv + kSlots;           // [2] MMA commit
+  uint64_t* dxempty = dxfull + 2;              // [2] 4 epilogue warps
+  uint64_t* accfull = dxempty + 2;             // MMA commit: the slice's dW done
   uint64_t* wt_ready = accfull + 1;            // 4 epilogue warps: W^T in TMEM
   uint64_t* w_bar = wt_ready + 1;              // W bulk copy landed
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(w_bar + 1);
@@ -260,15 +314,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int s = 0; s < kSlots; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&sfree[s], 1);
-    }
-    for (int s = 0; s < kStages; ++s) {
-      mbar_init(&pfree[s], 1);
       mbar_init(&conv[s], 4);
-      mbar_init(&xraw[s], 1);
-      mbar_init(&xlo[s], 2);
+      mbar_init(&xconv[s], 2);
     }
-    mbar_init(dxfull, 1);
-    mbar_init(dxempty, 4);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&dxfull[b], 1);
+      mbar_init(&dxempty[b], 4);
+    }
     mbar_init(accfull, 1);
     mbar_init(wt_ready, 4);
     mbar_init(w_bar, 1);
@@ -277,6 +329,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&tdy);
     if (a.do_dw) prefetch_tmap(&tx);
+    if (a.do_dx) prefetch_tmap(&tdx);
   }
   if (warp == 1) tmem_alloc<512>(tmem_slot);
   tc_fence_before();
@@ -336,181 +389,117 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer ----------------
-    const uint32_t idw = idesc_tf32(128, static_cast<uint32_t>(a.xr), 0, 0);
-    const uint32_t idx = idesc_tf32(128, 64, 0, 1);  // B = dy of the pair, MN-major (pixels contiguous)
-    const int ksteps = a.c_out >> 3;
-    const uint32_t lbo = static_cast<uint32_t>(L.blk);   // the pair's second 32-px atom (raw)
-    const uint32_t lbol = static_cast<uint32_t>(L.dlob / 2);  // ... (dy_lo)
-    uint32_t dph = 0;
+    const uint32_t idw = idesc_bf16(128, static_cast<uint32_t>(a.xr), 0, 0);
+    const uint32_t idx = idesc_bf16(128, 64, 0, 1);  // B = dy hi | lo of the pair, MN-major (pixels contiguous)
+    const int kq = round16(a.c_out) >> 4;
     for (int p = 0; p < npairs; ++p) {
-      const int s = p % kSlots, e = p & 1;
-      const uint32_t ph = (p >> 1) & 1;
+      const int s = p % kSlots, b = p & 1;
+      const uint32_t ph = (p / kSlots) & 1;
       const int nb = min(2, nblk - 2 * p);
-      mbar_wait(&conv[e], ph);
-      tc_fence_after();
       const uint32_t st = smem_u32(smem + s * L.slot);
-      const uint32_t lb = smem_u32(smem + L.dlo + e * L.dlob);
-      const uint32_t aw = tmem + kDwA + 128 * e;
+      mbar_wait(&conv[s], ph);
       if (a.do_dw) {
-        // dW with raw x (x_hi): dy_hi * x, dy_lo * x
+        mbar_wait(&xconv[s], ph);
+        tc_fence_after();
         if (elect_one()) {
-          for (int k = 0; k < nb; ++k) {
-            const uint32_t ah = aw + 64 * k, al = ah + 32;
-            for (int q = 0; q < 4; ++q) {
-              const uint64_t dbx = desc_sw128(st + k * L.blk + L.x + q * 32, 16, 1024);
-              mma_tf32_ts(tmem + kDwAcc, ah + 8 * q, dbx, idw, (p == 0 && k == 0 && q == 0) ? 0u : 1u);
-              mma_tf32_ts(tmem + kDwAcc, al + 8 * q, dbx, idw, 1);
-            }
+          const uint32_t aw = tmem + kDwA + 64 * s;
+          const uint32_t xh = st + L.x, xl = st + L.blk + L.x;
+          for (int ks = 0; ks < 2 * nb; ++ks) {
+            const uint64_t bh = desc_sw128(xh + 32 * ks, 16, 1024), bl = desc_sw128(xl + 32 * ks, 16, 1024);
+            mma_bf16_ts(tmem + kDwAcc, aw + 8 * ks, bh, idw, (p == 0 && ks == 0) ? 0u : 1u);
+            mma_bf16_ts(tmem + kDwAcc, aw + 32 + 8 * ks, bh, idw, 1);
+            mma_bf16_ts(tmem + kDwAcc, aw + 8 * ks, bl, idw, 1);
           }
-          mma_commit(&xraw[e]);
           TRACE3K(16, p);
         }
         __syncwarp();
       }
       if (a.do_dx) {
         if (p == 0) mbar_wait(wt_ready, 0);
-        mbar_wait(dxempty, dph ^ 1u);
+        if (p >= 2) mbar_wait(&dxempty[b], ((p >> 1) - 1) & 1);
         tc_fence_after();
         if (elect_one()) {
-          const uint32_t d = tmem + kDxAcc;
-          for (int q = 0; q < ksteps; ++q) {
-            mma_tf32_ts(d, tmem + kWt + 8 * q, desc_mn32(st + q * 1024, lbo, 512), idx, q == 0 ? 0u : 1u);
-            mma_tf32_ts(d, tmem + kWt + 8 * q, desc_mn32(lb + q * 1024, lbol, 512), idx, 1);
+          const uint32_t d = tmem + kDxAcc + 64 * b;
+          for (int q = 0; q < kq; ++q) {
+            mma_bf16_ts(d, tmem + kWt + 8 * q, desc_sw128(st + 2048 * q, kMnLbo, 1024), idx, q == 0 ? 0u : 1u);
+            mma_bf16_ts(d, tmem + kWt + 8 * q, desc_sw128(st + L.blk + 2048 * q, kMnLbo, 1024), idx, 1);
           }
-          mma_commit(dxfull);
+          mma_commit(&dxfull[b]);
           TRACE3K(24, p);
         }
         __syncwarp();
-        dph ^= 1u;
       }
-      if (a.do_dw) {
-        // dW with x_lo (converted in place under the dx MMAs): dy_hi * x_lo
-        mbar_wait(&xlo[e], ph);
-        tc_fence_after();
-        if (elect_one()) {
-          for (int k = 0; k < nb; ++k) {
-            const uint32_t ah = aw + 64 * k;
-            for (int q = 0; q < 4; ++q)
-              mma_tf32_ts(tmem + kDwAcc, ah + 8 * q, desc_sw128(st + k * L.blk + L.x + q * 32, 16, 1024), idw, 1);
-          }
-        }
-        __syncwarp();
-      }
-      if (elect_one()) {
-        mma_commit(&pfree[e]);
-        mma_commit(&sfree[s]);
-      }
+      if (elect_one()) mma_commit(&sfree[s]);
       __syncwarp();
     }
     // (an empty slice accumulates nothing; the epilogue writes zeros)
     if (a.do_dw && elect_one()) mma_commit(accfull);
     __syncwarp();
   } else if (warp < 4) {
-    // ---------------- x lo converters (in place) ----------------
+    // ---------------- x converters (in place) ----------------
+    // thread r: x row r of the pair (rows [nx, xr) are the MMA's zero padding)
     if (a.do_dw) {
-      const int ct = threadIdx.x - 64;  // 0..63
-      // padding rows [nx, xr) of every x block are zero (TMA never writes
-      // them; lo of zero is zero)
-      for (int b = 0; b < 2 * kSlots && a.xr > a.nx; ++b) {
-        float* xs = reinterpret_cast<float*>(smem + (b >> 1) * L.slot + (b & 1) * L.blk + L.x);
-        for (int i = ct; i < (a.xr - a.nx) * 32; i += 64) xs[a.nx * 32 + i] = 0.f;
-      }
-      fence_proxy_async_smem();
-      const int words = a.nx * 8;  // float4 per x block
+      const int r = threadIdx.x - 64;  // 0..63
       for (int p = 0; p < npairs; ++p) {
-        const int s = p % kSlots, e = p & 1;
+        const int s = p % kSlots;
         const int nb = min(2, nblk - 2 * p);
-        // the MMAs that read raw x are done (and so the data had landed)
-        mbar_wait(&xraw[e], (p >> 1) & 1);
-        for (int k = 0; k < nb; ++k) {
-          const uint32_t base = smem_u32(smem + s * L.slot + k * L.blk + L.x);
-          for (int i0 = ct; i0 < words; i0 += 64 * 4) {
-            float4 v[4];
+        mbar_wait(&full[s], (p / kSlots) & 1);
+        if (r < a.xr) {
+          const uint32_t row0 = smem_u32(smem + s * L.slot + L.x + r * 128), row1 = row0 + L.blk;
+          uint32_t hi[32], lo[32];
+          if (r < a.nx) {
+            convert_row(row0, row1, r, nb, hi, lo);
+          } else {
+            const uint32_t z[4] = {0u, 0u, 0u, 0u};
 #pragma unroll
-            for (int q = 0; q < 4; ++q) v[q] = lds_v4(base + min(i0 + 64 * q, words - 1) * 16);
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              if (i0 + 64 * q < words) {
-                float4 o;
-                o.x = v[q].x - tf32_hi(v[q].x);
-                o.y = v[q].y - tf32_hi(v[q].y);
-                o.z = v[q].z - tf32_hi(v[q].z);
-                o.w = v[q].w - tf32_hi(v[q].w);
-                sts_v4(base + (i0 + 64 * q) * 16, o);
-              }
+            for (int j = 0; j < 8; ++j) {
+              sts_u4(row0 + 16 * j, z);
+              sts_u4(row1 + 16 * j, z);
             }
           }
         }
         fence_proxy_async_smem();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&xlo[e]);
+        if (lane == 0) mbar_arrive(&xconv[s]);
+        if (r == 0 && p < 3) TRACE3(56 + p);
       }
     }
   } else if (warp < 8) {
     // ---------------- dy row converters ----------------
-    // Row `row` of a block: 128 B, 32 B chunk c at physical chunk c ^ (row % 4)
-    // (SWIZZLE_128B_BASE32B).  Writes the lo row to the stage's lo pair (dx B
-    // lo) and, for dW, the hi / lo row to TMEM lane `row`.
+    // thread = filter row `row` of the pair: bf16 hi | lo in place (rows
+    // [c_out, round16(c_out)) zero: the dx GEMM's K padding) and, for dW, the
+    // hi | lo row to TMEM lane `row`; db summed from the fp32 values.
     const int q = warp & 3;
     const int row = q * 32 + lane;
-    const int swp = (row >> 2) & 1;
     const bool live = row < a.c_out;
+    const bool pad = !live && row < round16(a.c_out);
     const bool warp_live = q * 32 < a.c_out;  // tcgen05.st is warp-collective
     const uint32_t lane_base = static_cast<uint32_t>(q * 32) << 16;
     // window start of filter row `row` (a plan table: no dependency wait)
     const int start_i = (a.do_dw && live) ? __ldg(a.starts + row_oc(a, row)) : 0;
-    float dbsum = 0.f;  // db of this filter over the slice (fixed order: blocks, then pixels)
+    float dbsum = 0.f;  // db of this filter over the slice (fixed order: pairs, then pixels)
     for (int p = 0; p < npairs; ++p) {
-      const int s = p % kSlots, e = p & 1;
+      const int s = p % kSlots;
       const int nb = min(2, nblk - 2 * p);
       mbar_wait(&full[s], (p / kSlots) & 1);
-      if (p >= kStages) mbar_wait(&pfree[e], ((p >> 1) - 1) & 1);  // dy_lo pair + TMEM A of pair p-2
       tc_fence_after();
-      for (int k = 0; k < nb; ++k) {
-        uint32_t hi[32], lo[32];
+      uint32_t hi[32], lo[32];
 #pragma unroll
-        for (int c = 0; c < 32; ++c) hi[c] = lo[c] = 0u;
-        if (live) {
-          const float4* rp = reinterpret_cast<const float4*>(smem + s * L.slot + k * L.blk + row * 128);
-          float bs = 0.f;
+      for (int c = 0; c < 32; ++c) hi[c] = lo[c] = 0u;
+      const uint32_t row0 = smem_u32(smem + s * L.slot + row * 128), row1 = row0 + L.blk;
+      if (live) {
+        dbsum += convert_row(row0, row1, row, nb, hi, lo);
+      } else if (pad) {
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            // 32 B atom j of the row sits at atom (j ^ row) & 3; rows 4 apart
-            // share that position, so they take its two 16 B halves in the
-            // opposite order: the 8 rows of a quarter warp hit 8 distinct
-            // 16 B bank groups (no 2-way conflict).
-            const int at = ((j ^ row) & 3) << 1;
-            const float4 va = rp[at | swp], vb = rp[at | (swp ^ 1)];
-            const float4 v0 = swp ? vb : va, v1 = swp ? va : vb;
-#pragma unroll
-            for (int hh = 0; hh < 2; ++hh) {
-              const float4 v = hh ? v1 : v0;
-              const int c = 2 * j + hh;
-              const float e[4] = {v.x, v.y, v.z, v.w};
-              bs += (e[0] + e[1]) + (e[2] + e[3]);
-#pragma unroll
-              for (int t = 0; t < 4; ++t) {
-                const float h = tf32_hi(e[t]);
-                hi[4 * c + t] = __float_as_uint(h);
-                lo[4 * c + t] = __float_as_uint(e[t] - h);
-              }
-            }
-          }
-          dbsum += bs;
-          const uint32_t lo_row = smem_u32(smem + L.dlo + e * L.dlob + k * (L.dlob / 2) + row * 128);
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const int at = ((j ^ row) & 3) << 1;
-            const float4 l0 = f4(lo + 8 * j), l1 = f4(lo + 8 * j + 4);
-            sts_v4(lo_row + (at | swp) * 16, swp ? l1 : l0);
-            sts_v4(lo_row + (at | (swp ^ 1)) * 16, swp ? l0 : l1);
-          }
+        for (int j = 0; j < 8; ++j) {
+          sts_u4(row0 + 16 * j, hi);
+          sts_u4(row1 + 16 * j, lo);
         }
-        if (a.do_dw && warp_live) {
-          const uint32_t col = tmem + kDwA + 128 * e + 64 * k + lane_base;
-          tmem_st32(col, hi);
-          tmem_st32(col + 32, lo);
-        }
+      }
+      if (a.do_dw && warp_live) {
+        const uint32_t col = tmem + kDwA + 64 * s + lane_base;
+        tmem_st32(col, hi);
+        tmem_st32(col + 32, lo);
       }
       fence_proxy_async_smem();
       if (a.do_dw) {
@@ -518,7 +507,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_before();
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(&conv[e]);
+      if (lane == 0) mbar_arrive(&conv[s]);
       if (row == 0) TRACE3K(8, p);
     }
     if (a.do_dw) {
@@ -570,10 +559,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else {
-    // ---------------- W^T build, dx epilogue, dW slice epilogue ----------------
+    // ---------------- W^T build, dx epilogue ----------------
     const int q = warp & 3;
     const int et = threadIdx.x - 256;  // 0..127
-    const int i = q * 32 + lane;       // TMEM lane: input channel (+64: lo part) / filter row (dW)
+    const int i = q * 32 + lane;       // TMEM lane: input channel (+64: lo part)
     const uint32_t lane_base = static_cast<uint32_t>(q * 32) << 16;
     float* wst = reinterpret_cast<float*>(smem + L.wst);
     int2* kt = reinterpret_cast<int2*>(smem + L.kt);
@@ -619,30 +608,33 @@ __global__ void __launch_bounds__(kThreads, 1)
     const bool dx_live = dx_row < a.c_in;
     const bool dx_warp = (q & 1) * 32 < a.c_in;
     const bool leader = et == 0;
-    uint32_t dph = 0;
     if (a.do_dx) {
       for (int p = 0; p < npairs; ++p) {
-        const int nb = min(2, nblk - 2 * p);
-        mbar_wait(dxfull, dph);
-        dph ^= 1u;
+        const int nb = min(2, nblk - 2 * p), b = p & 1;
+        mbar_wait(&dxfull[b], (p >> 1) & 1);
         if (et == 0) TRACE3K(32, p);
         tc_fence_after();
         uint32_t v0[32], v1[32];
         if (dx_warp) {
-          tmem_ld32_nowait(tmem + kDxAcc + lane_base, v0);
-          tmem_ld32_nowait(tmem + kDxAcc + 32 + lane_base, v1);
+          tmem_ld32_nowait(tmem + kDxAcc + 64 * b + lane_base, v0);
+          tmem_ld32_nowait(tmem + kDxAcc + 64 * b + 32 + lane_base, v1);
           tmem_ld_wait();
         }
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(dxempty);
-        // rows 64-127 (the W_lo part) -> exchange pair; rows 0-63 add theirs and
-        // store the sum straight to global (each thread one input channel,
-        // 32 contiguous pixels per block).  The first barrier orders this
-        // pair's exchange writes after the previous pair's reads (and, on the
-        // first pair, after every lane's last read of the W staging).
+        if (lane == 0) mbar_arrive(&dxempty[b]);
+        if (leader && p < 4) TRACE3(64 + p);
+        // rows 64-127 (the W_lo part) -> staging buffer p % 2; rows 0-63 add
+        // theirs in place (each thread one input channel: 32 pixels per
+        // block, the row it alone touches) and one TMA store per block writes
+        // the pair (the SWIZZLE_128B staging is the store's box).  Leader:
+        // the stores of pair p-2 have finished reading buffer p % 2 before
+        // the first barrier releases its writers.
+        if (leader) bulk_wait_read<1>();
+        if (leader && p < 4) TRACE3(68 + p);
         named_bar_sync(1, 128);
-        const uint32_t r0 = smem_u32(smem + L.stg + dx_row * 128), r1 = r0 + L.stgb;
+        if (leader && p < 4) TRACE3(72 + p);
+        const uint32_t r0 = smem_u32(smem + L.stg + b * 2 * L.stgb + dx_row * 128), r1 = r0 + L.stgb;
         if (bottom && dx_warp && dx_live) {
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
@@ -651,30 +643,44 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
         named_bar_sync(1, 128);
-        if (!bottom && dx_warp && dx_live) {
+        if (leader && p < 4) TRACE3(76 + p);
+        if (!bottom) {
+          if (dx_warp && dx_live) {
 #pragma unroll
-          for (int k = 0; k < 2; ++k) {
-            if (k < nb) {
-              const int u = blk_u(a, sl, 2 * p + k);
-              const int n = u / a.nbps, px0 = (u - n * a.nbps) * 32;
-              float* drow = a.dx + (static_cast<int64_t>(n) * a.c_in + dx_row) * a.plane + px0;
+            for (int k = 0; k < 2; ++k) {
               const uint32_t* vv = k == 0 ? v0 : v1;
               const uint32_t rk = k == 0 ? r0 : r1;
+              // all loads in flight before the first store (the shared-memory
+              // accesses are volatile: interleaving them serialises 8 round
+              // trips, ~1 us per pair under the MMA / TMA traffic)
+              float4 o[8];
+#pragma unroll
+              for (int j = 0; j < 8; ++j) o[j] = lds_v4(rk + ((j ^ (dx_row & 7)) << 4));
 #pragma unroll
               for (int j = 0; j < 8; ++j) {
-                const float4 o = lds_v4(rk + ((j ^ (dx_row & 7)) << 4));
                 const float4 m = f4(vv + 4 * j);
-                if (px0 + 4 * j < a.plane)
-                  __stcs(reinterpret_cast<float4*>(drow + 4 * j),
-                         make_float4(m.x + o.x, m.y + o.y, m.z + o.z, m.w + o.w));
+                sts_v4(rk + ((j ^ (dx_row & 7)) << 4),
+                       make_float4(m.x + o[j].x, m.y + o[j].y, m.z + o[j].z, m.w + o[j].w));
               }
             }
+          }
+          fence_proxy_async_smem();
+          if (leader && p < 4) TRACE3(80 + p);
+          named_bar_sync(2, 64);
+          if (leader) {
+            for (int k = 0; k < nb; ++k) {
+              const int u = blk_u(a, sl, 2 * p + k);
+              const int n = u / a.nbps, px0 = (u - n * a.nbps) * 32;
+              tma_store_3d(&tdx, smem + L.stg + (2 * b + k) * L.stgb, px0, 0, n);
+            }
+            bulk_commit();
           }
         }
         if (leader) TRACE3K(40, p);
       }
     }
     if (leader) {
+      bulk_wait<0>();
       TRACE3(52);
 #if defined(SCC_TRACE)
       if (blockIdx.x < 256) g_cta3[2 * blockIdx.x + 1] = globaltimer();
@@ -752,10 +758,10 @@ Geo geometry(const TcWeightPlan& tw, int32_t c_in, int32_t c_out, int32_t gw) {
 
 int tc_bwd_trace(unsigned long long* out, int n) {
 #if defined(SCC_TRACE)
-  if (n > 64 + 512) n = 64 + 512;
-  const int m = n < 64 ? n : 64;
+  if (n > 128 + 512) n = 128 + 512;
+  const int m = n < 128 ? n : 128;
   if (cudaMemcpyFromSymbol(out, g_trace3, m * sizeof(unsigned long long)) != cudaSuccess) return -1;
-  if (n > 64 && cudaMemcpyFromSymbol(out + 64, g_cta3, (n - 64) * sizeof(unsigned long long)) != cudaSuccess)
+  if (n > 128 && cudaMemcpyFromSymbol(out + 128, g_cta3, (n - 128) * sizeof(unsigned long long)) != cudaSuccess)
     return -1;
   return n;
 #else
@@ -836,7 +842,7 @@ cudaError_t launch_tc_bwd(const TcWeightPlan& tw, const TcBwdCall& call, cudaStr
                               static_cast<uint64_t>(call.n)};
     const uint64_t strides[3] = {P * 4 * tw.n_class, P * 4, P * 4 * call.c_out};
     const uint32_t box[4] = {32, static_cast<uint32_t>(tw.cls), static_cast<uint32_t>(tw.n_class), 1};
-    if (!encode_f32(&tdy, call.dy, 4, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B))
+    if (!encode_f32(&tdy, call.dy, 4, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B))
       return cudaErrorInvalidValue;
   }
   const uint64_t dimx[3] = {P, static_cast<uint64_t>(call.c_in), static_cast<uint64_t>(call.n)};
@@ -844,6 +850,12 @@ cudaError_t launch_tc_bwd(const TcWeightPlan& tw, const TcBwdCall& call, cudaStr
   if (a.do_dw) {
     const uint32_t box[3] = {32, static_cast<uint32_t>(a.xbox ? g.nx : tw.rbb), 1};
     if (!encode_f32(&tx, call.x, 3, dimx, strx, box, CU_TENSOR_MAP_SWIZZLE_128B)) return cudaErrorInvalidValue;
+  }
+  CUtensorMap tdx{};
+  if (a.do_dx) {
+    const uint64_t dimd[3] = {P, static_cast<uint64_t>(call.c_in), static_cast<uint64_t>(call.n)};
+    const uint32_t box[3] = {32, static_cast<uint32_t>(call.c_in), 1};
+    if (!encode_f32(&tdx, call.dx, 3, dimd, strx, box, CU_TENSOR_MAP_SWIZZLE_128B)) return cudaErrorInvalidValue;
   }
   if (dev < 0 || dev >= 64 || !attr_set[dev]) {
     cudaError_t e = cudaFuncSetAttribute(tc_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit);
@@ -862,7 +874,7 @@ cudaError_t launch_tc_bwd(const TcWeightPlan& tw, const TcBwdCall& call, cudaStr
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   if (grid > nsm) return cudaErrorInvalidConfiguration;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, tc_bwd_kernel, tdy, tx, a);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, tc_bwd_kernel, tdy, tx, tdx, a);
   if (e != cudaSuccess) return e;
   int launches = 1;
   if (a.do_dw) {

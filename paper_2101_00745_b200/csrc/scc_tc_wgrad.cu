@@ -315,14 +315,24 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait_tag(&b_full[st], ps, 24);
         const uint32_t src = smem_u32(b_ring + st * b_stage_bytes) + 16u * quarter * bvec_q;
         const uint32_t dst = src + NB * b_blk_bytes;
-        for (int i = lane; i < bvec_q; i += 32) {
-          const float4 v = lds_v4(src + 16u * i);
-          float4 l4;
-          l4.x = v.x - tf32_hi(v.x);
-          l4.y = v.y - tf32_hi(v.y);
-          l4.z = v.z - tf32_hi(v.z);
-          l4.w = v.w - tf32_hi(v.w);
-          sts_v4(dst + 16u * i, l4);
+        // 8 loads in flight before their stores (the shared-memory accesses
+        // are volatile: a load-store pair per iteration serialises the round
+        // trips)
+        for (int i0 = lane; i0 < bvec_q; i0 += 32 * 8) {
+          float4 v[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) v[u] = lds_v4(src + 16u * min(i0 + 32 * u, bvec_q - 1));
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            if (i0 + 32 * u < bvec_q) {
+              float4 l4;
+              l4.x = v[u].x - tf32_hi(v[u].x);
+              l4.y = v[u].y - tf32_hi(v[u].y);
+              l4.z = v[u].z - tf32_hi(v[u].z);
+              l4.w = v[u].w - tf32_hi(v[u].w);
+              sts_v4(dst + 16u * (i0 + 32 * u), l4);
+            }
+          }
         }
         fence_proxy_async_smem();
         __syncwarp();

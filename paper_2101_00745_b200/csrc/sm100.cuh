@@ -403,5 +403,40 @@ __device__ __forceinline__ float tf32_hi(float x) {
   return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
 }
 
+// ---- bf16x3 (kind::f16 with bf16 operands, fp32 accumulate) -------------------
+// x = hi + lo + r with hi = bf16_rn(x), lo = bf16_rn(x - hi), |r| <= 2^-18 |x|;
+// a product is taken as hi*hi' + hi*lo' + lo*hi' (+ lo*lo' where it comes for
+// free), ~2^-17 relative per product: the backward's 1e-4 bar with margin, at
+// twice the tf32 MMA rate (K = 16 per instruction at the tf32 K = 8 cycle
+// count, scripts/probes/bf16_probe.py).
+//
+// Instruction descriptor for kind::f16 with bf16 A / B, fp32 accumulate.
+__host__ __device__ constexpr uint32_t idesc_bf16(uint32_t m, uint32_t n, uint32_t a_mn, uint32_t b_mn) {
+  return (1u << 4)          // D format f32
+         | (1u << 7)        // A format bf16
+         | (1u << 10)       // B format bf16
+         | (a_mn << 15) | (b_mn << 16) | ((n >> 3) << 17) | ((m >> 4) << 24);
+}
+
+// D[tmem] (+)= A[tmem] * B[smem], kind::f16 (bf16 operands); A K-major in
+// TMEM: lanes = M rows, one 32-bit column per k pair (k = 2c in the low half).
+__device__ __forceinline__ void mma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                            uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+// Two fp32 values -> packed bf16x2 hi (v0 in the low half) and the packed
+// bf16x2 of their remainders.
+__device__ __forceinline__ void bf16x2_split(float v0, float v1, uint32_t& hi, uint32_t& lo) {
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(hi) : "f"(v1), "f"(v0));
+  const float h0 = __uint_as_float(hi << 16), h1 = __uint_as_float(hi & 0xFFFF0000u);
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(lo) : "f"(v1 - h1), "f"(v0 - h0));
+}
+
 }  // namespace sm100
 }  // namespace scc

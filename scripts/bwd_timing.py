@@ -44,19 +44,22 @@ for name, f in (("bwd_data", bdata), ("bwd", bwd)):
         with torch.cuda.graph(gr, stream=st):
             for k in range(4): f(k % R, st.cuda_stream)
         gr.replay(); st.synchronize()
-    n = 64 + 512
+    n = 128 + 512
     buf = (C.c_uint64 * n)()
     L.scc_debug_trace_fused(buf, n)
-    t = [buf[i] for i in range(64)]
+    t = [buf[i] for i in range(128)]
     t0 = t[48]
     print("raw", t[48:53], t[60:63])
     if t0 == 0:
         print("(no trace: build with SCC_EXTRA=-DSCC_TRACE)"); break
     lab = {48: "start", 49: "tmem", 50: "wt_ready", 51: "accfull", 52: "end", 53: "e_dep", 55: "e_bar", 60: "red_entry", 61: "red_dep", 62: "red_end", 59: "prev_red_end"}
     for k in range(8):
+        lab[k] = f"tma{k}"
+        if k < 4: lab[64 + k] = f"eld{k}"; lab[68 + k] = f"ewr{k}"; lab[72 + k] = f"eb1_{k}"; lab[76 + k] = f"eb2_{k}"; lab[80 + k] = f"eadd{k}"
+        if k < 3: lab[56 + k] = f"xconv{k}"
         lab[k] = f"tma{k}"; lab[8 + k] = f"conv{k}"; lab[16 + k] = f"mdw{k}"; lab[24 + k] = f"mdx{k}"; lab[32 + k] = f"dxfull{k}"; lab[40 + k] = f"store{k}"  # k = block pair
     print(name, " ".join(f"{lab[i]}={(t[i] - t0) / 1e3:.2f}" for i in sorted(lab) if t[i] > 0 and abs(t[i] - t0) < 1e8))
-    cs = [buf[64 + 2 * i] for i in range(148)]; ce = [buf[64 + 2 * i + 1] for i in range(148)]
+    cs = [buf[128 + 2 * i] for i in range(148)]; ce = [buf[128 + 2 * i + 1] for i in range(148)]
     m0 = min(cs)
     s_ = sorted((x - m0) / 1e3 for x in cs); e_ = sorted((x - m0) / 1e3 for x in ce)
     print(f"  CTA start min/med/max {s_[0]:.2f}/{s_[74]:.2f}/{s_[-1]:.2f}  end {e_[0]:.2f}/{e_[74]:.2f}/{e_[-1]:.2f}")
