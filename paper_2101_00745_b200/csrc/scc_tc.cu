@@ -24,6 +24,8 @@
 //   warps 6..9  epilogue: TMEM -> registers -> coalesced NCHW stores (+ bias)
 // Accumulators are double-buffered in TMEM so the epilogue of tile i overlaps
 // the MMAs of tile i+1.  Every output element is written exactly once.
+#include <cuda_bf16.h>
+
 #include <algorithm>
 #include <cstdio>
 
@@ -53,10 +55,14 @@ constexpr int KC = 32;          // ring positions per pipeline stage (4 k-steps 
 constexpr int TM = 128;         // pixels per tile
 constexpr int kABytes = TM * KC * 4;  // 16 KB per A buffer
 
-template <int NT>
+// BF: bf16x3 (backward-data): the weight image of a chunk is one [NT rows][hi 32
+// | lo 32] bf16 K-major SWIZZLE_128B block and a TMEM A stage holds bf16 pairs
+// (KC columns instead of 2 KC); the forward (1e-5 bar) stays 3xTF32.
+template <int NT, bool BF = false>
 struct TcCfg {
   static_assert(NT == 64 || NT == 128, "row tile must be 64 or 128");
-  static constexpr int kBBytes = 2 * NT * KC * 4;  // hi + lo weight image of one chunk
+  static constexpr int kBBytes = (BF ? 1 : 2) * NT * KC * 4;  // hi + lo weight image of one chunk
+  static constexpr int kAStageCols = BF ? KC : 2 * KC;       // TMEM columns of one A stage
   static constexpr int kTStages = NT == 128 ? 3 : 4;  // TMEM A stages
   static constexpr int kAccCols = NT;               // per accumulator buffer
   static constexpr int kACol0 = 2 * NT;             // first TMEM column of A stages
@@ -140,11 +146,14 @@ __device__ __forceinline__ int chunks_of(const TcBandArgs& a, int rt) {
   return (a.rt_info[4 * rt + 1] + 3) / 4;
 }
 
-template <int NT, bool PACK>
+template <int NT, bool PACK, bool BF>
 __global__ void __launch_bounds__(kTcThreads, 1)
     tc_band_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap tout,
                    const TcBandArgs a) {
-  using C = TcCfg<NT>;
+  using C = TcCfg<NT, BF>;
+  // panel offset (floats) of a row tile: rt_info holds the 3xTF32 layout's
+  // (two fp32 images per chunk); a bf16 chunk image is half that size
+  auto pofs = [&](int rt) { return BF ? a.rt_info[4 * rt + 2] / 2 : a.rt_info[4 * rt + 2]; };
   constexpr int ST = C::kTStages;
   const int SA = a.sm.a_stages;
   const int SB = a.sm.b_stages;
@@ -259,7 +268,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             panel_ready();
             const uint32_t bytes = static_cast<uint32_t>(nch) * C::kBBytes;
             mbar_expect_tx(&b_full[0], bytes);
-            bulk_load(b_base, a.panel + a.rt_info[4 * tc.rt + 2], bytes, &b_full[0]);
+            bulk_load(b_base, a.panel + pofs(tc.rt), bytes, &b_full[0]);
           }
         }
       }
@@ -281,7 +290,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           mbar_wait_tag(&b_free[sb], pb ^ 1u, 2);
           mbar_expect_tx(&b_full[sb], C::kBBytes);
           bulk_load(b_base + sb * C::kBBytes,
-                    a.panel + a.rt_info[4 * rt + 2] + static_cast<int64_t>(c) * (C::kBBytes / 4),
+                    a.panel + pofs(rt) + static_cast<int64_t>(c) * (C::kBBytes / 4),
                     C::kBBytes, &b_full[sb]);
           advance(sb, pb, SB);
         }
@@ -289,7 +298,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer (A from TMEM, B from SMEM) ----------------
-    constexpr uint32_t idesc = idesc_tf32(TM, NT, 0, 0);
+    constexpr uint32_t idesc = BF ? idesc_bf16(TM, NT, 0, 0) : idesc_tf32(TM, NT, 0, 0);
     int st = 0;
     uint32_t ps = 0;
     int sb = 0;
@@ -308,7 +317,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         mbar_wait_tag(&conv[st], ps, 5);
         uint8_t* bimg;
         if (a.sm.b_resident == 1) {
-          bimg = b_base + (a.rt_info[4 * rt + 2] + c * (C::kBBytes / 4)) * 4;
+          bimg = b_base + (pofs(rt) + c * (C::kBBytes / 4)) * 4;
         } else if (a.sm.b_resident == 2) {
           bimg = b_base + c * C::kBBytes;
         } else {
@@ -319,15 +328,28 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         if (t == blockIdx.x && c == 0 && lane == 0) TRACE(5);
         const int steps = min(4, nk8 - 4 * c);
         if (elect_one()) {
-          const uint32_t a_hi = tmem + C::kACol0 + st * 2 * KC;
-          const uint32_t a_lo = a_hi + KC;
-          const uint32_t bh = smem_u32(bimg), bl = bh + NT * KC * 4;
-          for (int k = 0; k < steps; ++k) {
-            const uint64_t dbh = desc_sw128(bh + k * 32, 16, 1024);
-            const uint64_t dbl = desc_sw128(bl + k * 32, 16, 1024);
-            mma_tf32_ts(d_tmem, a_hi + 8 * k, dbh, idesc, (c | k) != 0);
-            mma_tf32_ts(d_tmem, a_lo + 8 * k, dbh, idesc, 1);
-            mma_tf32_ts(d_tmem, a_hi + 8 * k, dbl, idesc, 1);
+          const uint32_t a_hi = tmem + C::kACol0 + st * C::kAStageCols;
+          if (BF) {
+            // [hi pairs 16 cols | lo pairs 16 cols]; B row = [hi 32 | lo 32] bf16
+            const uint32_t a_lo = a_hi + KC / 2;
+            const uint32_t bh = smem_u32(bimg);
+            for (int k = 0; k < (steps + 1) / 2; ++k) {
+              const uint64_t dbh = desc_sw128(bh + k * 32, 16, 1024);
+              const uint64_t dbl = desc_sw128(bh + 64 + k * 32, 16, 1024);
+              mma_bf16_ts(d_tmem, a_hi + 8 * k, dbh, idesc, (c | k) != 0);
+              mma_bf16_ts(d_tmem, a_lo + 8 * k, dbh, idesc, 1);
+              mma_bf16_ts(d_tmem, a_hi + 8 * k, dbl, idesc, 1);
+            }
+          } else {
+            const uint32_t a_lo = a_hi + KC;
+            const uint32_t bh = smem_u32(bimg), bl = bh + NT * KC * 4;
+            for (int k = 0; k < steps; ++k) {
+              const uint64_t dbh = desc_sw128(bh + k * 32, 16, 1024);
+              const uint64_t dbl = desc_sw128(bl + k * 32, 16, 1024);
+              mma_tf32_ts(d_tmem, a_hi + 8 * k, dbh, idesc, (c | k) != 0);
+              mma_tf32_ts(d_tmem, a_lo + 8 * k, dbh, idesc, 1);
+              mma_tf32_ts(d_tmem, a_hi + 8 * k, dbl, idesc, 1);
+            }
           }
           mma_commit(&t_free[st]);
           if (!a.sm.b_resident) mma_commit(&b_free[sb]);
@@ -362,21 +384,42 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         if (t == blockIdx.x && c == 0 && q == 0 && lane == 0) TRACE(4);
         const uint32_t src = smem_u32(a_ring + sa * kABytes) + 4u * (q * 32 + lane);
         uint32_t hi[KC], lo[KC];
+        if (BF) {
+          // bf16 pairs (ring rows 2i, 2i+1); rows past the chunk's last k8 step
+          // are zero (an odd step count leaves half a K = 16 step)
+          const int rows = 8 * min(4, a.rt_info[4 * static_cast<int>(t % a.n_rt) + 1] - 4 * c);
+          float v[KC];
 #pragma unroll
-        for (int k = 0; k < KC; ++k) {
-          const float v = lds_f32(src + 4u * k * TM);
-          const float h = tf32_hi(v);
-          hi[k] = __float_as_uint(h);
-          lo[k] = __float_as_uint(v - h);
+          for (int k = 0; k < KC; ++k) v[k] = lds_f32(src + 4u * k * TM);
+#pragma unroll
+          for (int k = 0; k < KC; ++k) v[k] = k < rows ? v[k] : 0.f;
+#pragma unroll
+          for (int i = 0; i < KC / 2; ++i) bf16x2_split(v[2 * i], v[2 * i + 1], hi[i], lo[i]);
+        } else {
+#pragma unroll
+          for (int k = 0; k < KC; ++k) {
+            const float v = lds_f32(src + 4u * k * TM);
+            const float h = tf32_hi(v);
+            hi[k] = __float_as_uint(h);
+            lo[k] = __float_as_uint(v - h);
+          }
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&a_free[sa]);
         advance(sa, pa, SA);
         mbar_wait_tag(&t_free[st], ps ^ 1u, 8);
         tc_fence_after();
-        const uint32_t col = tmem + C::kACol0 + st * 2 * KC + lane_base;
-        tmem_st32(col, hi);
-        tmem_st32(col + KC, lo);
+        const uint32_t col = tmem + C::kACol0 + st * C::kAStageCols + lane_base;
+        if (BF) {
+          uint32_t h16[16], l16[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) h16[i] = hi[i], l16[i] = lo[i];
+          tmem_st16(col, h16);
+          tmem_st16(col + KC / 2, l16);
+        } else {
+          tmem_st32(col, hi);
+          tmem_st32(col + KC, lo);
+        }
         tmem_st_wait();
         tc_fence_before();
         __syncwarp();
@@ -501,7 +544,7 @@ struct PanelArgs {
   const int32_t* chunk_base;  // prefix sum of chunks per row tile (entries / (NT*32))
 };
 
-template <int NT>
+template <int NT, bool BF>
 __global__ void __launch_bounds__(256) tc_panel_kernel(const PanelArgs a) {
   // Let the dependent band kernel get scheduled now; it waits for this grid's
   // completion (griddepcontrol.wait) before it reads the panel.
@@ -526,11 +569,21 @@ __global__ void __launch_bounds__(256) tc_panel_kernel(const PanelArgs a) {
       if (s < 0) s += a.c_in;
       if (s < a.gw) v = a.weight[static_cast<int64_t>(oc) * a.gw + s];
     }
-    const float hi = tf32_hi(v);
-    float* img = a.panel + gc * (2 * NT * 32);
-    const int off = (r >> 3) * 256 + (r & 7) * 32 + (((k >> 2) ^ (r & 7)) << 2) + (k & 3);
-    img[off] = hi;
-    img[NT * 32 + off] = v - hi;
+    if (BF) {
+      // row r = [hi 32 | lo 32] bf16, 16 B chunk j at j ^ (r % 8)
+      const __nv_bfloat16 h = __float2bfloat16_rn(v);
+      const __nv_bfloat16 l = __float2bfloat16_rn(v - __bfloat162float(h));
+      uint8_t* img = reinterpret_cast<uint8_t*>(a.panel + gc * (NT * 32));
+      const int rb = (r >> 3) * 1024 + (r & 7) * 128;
+      *reinterpret_cast<__nv_bfloat16*>(img + rb + (((k >> 3) ^ (r & 7)) << 4) + (k & 7) * 2) = h;
+      *reinterpret_cast<__nv_bfloat16*>(img + rb + ((((k >> 3) + 4) ^ (r & 7)) << 4) + (k & 7) * 2) = l;
+    } else {
+      const float hi = tf32_hi(v);
+      float* img = a.panel + gc * (2 * NT * 32);
+      const int off = (r >> 3) * 256 + (r & 7) * 32 + (((k >> 2) ^ (r & 7)) << 2) + (k & 3);
+      img[off] = hi;
+      img[NT * 32 + off] = v - hi;
+    }
   }
 }
 
@@ -543,10 +596,10 @@ bool tc_band_supported(const TcBandPlan& tp, int64_t plane) {
   return tp.ok && plane % 4 == 0 && plane >= 4;
 }
 
-template <int NT>
+template <int NT, bool BF>
 static cudaError_t launch_tc_nt(const TcBandPlan& tp, const TcDeviceTables& dt,
                                 const TcBandCall& call, cudaStream_t s) {
-  using C = TcCfg<NT>;
+  using C = TcCfg<NT, BF>;
   // --- panel ---
   const int64_t entries = static_cast<int64_t>(tp.total_chunks) * NT * 32;
   float* panel = call.panel;
@@ -566,7 +619,7 @@ static cudaError_t launch_tc_nt(const TcBandPlan& tp, const TcDeviceTables& dt,
   pa.total = entries;
   pa.chunk_base = dt.chunk_base;
   const int pgrid = static_cast<int>(std::min<int64_t>((entries + 255) / 256, 148 * 8));
-  tc_panel_kernel<NT><<<pgrid, 256, 0, s>>>(pa);
+  tc_panel_kernel<NT, BF><<<pgrid, 256, 0, s>>>(pa);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
 
@@ -650,7 +703,7 @@ static cudaError_t launch_tc_nt(const TcBandPlan& tp, const TcDeviceTables& dt,
   // panel ring on its own producer warp.
   {
     constexpr int kBudget = 227 * 1024 - 1024 /*align*/ - 2048 /*barriers + static*/;
-    const int panel_bytes = static_cast<int>(tc_panel_bytes(tp));
+    const int panel_bytes = static_cast<int>(tc_panel_bytes(tp) / (BF ? 2 : 1));
     BandSmem& sm = ka.sm;
     const int rest = kBudget - C::kStoreBytes;
     if (panel_bytes + 5 * kABytes <= rest) {
@@ -677,13 +730,13 @@ static cudaError_t launch_tc_nt(const TcBandPlan& tp, const TcDeviceTables& dt,
     sm.a_stages = std::min(C::kMaxAStages, (rest - b_total) / kABytes);
     sm.total = sm.a_stages * kABytes + b_total + C::kStoreBytes + 1024 + 512;
   }
-  ka.panel_floats = static_cast<int32_t>(tc_panel_bytes(tp) / 4);
+  ka.panel_floats = static_cast<int32_t>(tc_panel_bytes(tp) / (BF ? 8 : 4));
   // packed tiles are a separate instantiation: the unpacked kernel keeps its
   // register allocation (the sample arithmetic cost 20 registers and ~25 %
   // at C256 cg8 56x56 when it was a runtime branch)
-  auto kern = spt > 1 ? tc_band_kernel<NT, true> : tc_band_kernel<NT, false>;
+  auto kern = spt > 1 ? tc_band_kernel<NT, true, BF> : tc_band_kernel<NT, false, BF>;
   {
-    static bool attr_set[2][64] = {{false}};  // per packing, device, template instance
+    static bool attr_set[2][64] = {{false}};  // per packing, device (one table per template instance)
     int dev = 0;
     cudaGetDevice(&dev);
     const int pk = spt > 1 ? 1 : 0;
@@ -731,9 +784,9 @@ cudaError_t launch_band_tc(const TcBandPlan& tp, const TcDeviceTables& dt, const
                            cudaStream_t s) {
   switch (tp.nt) {
     case 64:
-      return launch_tc_nt<64>(tp, dt, call, s);
+      return call.backward_data ? launch_tc_nt<64, true>(tp, dt, call, s) : launch_tc_nt<64, false>(tp, dt, call, s);
     case 128:
-      return launch_tc_nt<128>(tp, dt, call, s);
+      return call.backward_data ? launch_tc_nt<128, true>(tp, dt, call, s) : launch_tc_nt<128, false>(tp, dt, call, s);
     default:
       return cudaErrorInvalidValue;
   }

@@ -309,7 +309,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 #endif
     TRACE3(48);
 #if defined(SCC_TRACE)
-    if (blockIdx.x < 256) g_cta3[2 * blockIdx.x] = globaltimer();
+    if (blockIdx.x < 256) {
+      uint32_t smid;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      g_cta3[2 * blockIdx.x] = (globaltimer() & ~0xFFull) | smid;  // start (256 ns) | SM id
+    }
 #endif
     for (int s = 0; s < kSlots; ++s) {
       mbar_init(&full[s], 1);
@@ -398,6 +402,23 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int nb = min(2, nblk - 2 * p);
       const uint32_t st = smem_u32(smem + s * L.slot);
       mbar_wait(&conv[s], ph);
+      // dx first: its accumulator drains (the exchange, TMA stores) while the
+      // dW MMAs run, which shortens the tail after the last pair lands
+      if (a.do_dx) {
+        if (p == 0) mbar_wait(wt_ready, 0);
+        if (p >= 2) mbar_wait(&dxempty[b], ((p >> 1) - 1) & 1);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint32_t d = tmem + kDxAcc + 64 * b;
+          for (int q = 0; q < kq; ++q) {
+            mma_bf16_ts(d, tmem + kWt + 8 * q, desc_sw128(st + 2048 * q, kMnLbo, 1024), idx, q == 0 ? 0u : 1u);
+            mma_bf16_ts(d, tmem + kWt + 8 * q, desc_sw128(st + L.blk + 2048 * q, kMnLbo, 1024), idx, 1);
+          }
+          mma_commit(&dxfull[b]);
+          TRACE3K(24, p);
+        }
+        __syncwarp();
+      }
       if (a.do_dw) {
         mbar_wait(&xconv[s], ph);
         tc_fence_after();
@@ -411,21 +432,6 @@ __global__ void __launch_bounds__(kThreads, 1)
             mma_bf16_ts(tmem + kDwAcc, aw + 8 * ks, bl, idw, 1);
           }
           TRACE3K(16, p);
-        }
-        __syncwarp();
-      }
-      if (a.do_dx) {
-        if (p == 0) mbar_wait(wt_ready, 0);
-        if (p >= 2) mbar_wait(&dxempty[b], ((p >> 1) - 1) & 1);
-        tc_fence_after();
-        if (elect_one()) {
-          const uint32_t d = tmem + kDxAcc + 64 * b;
-          for (int q = 0; q < kq; ++q) {
-            mma_bf16_ts(d, tmem + kWt + 8 * q, desc_sw128(st + 2048 * q, kMnLbo, 1024), idx, q == 0 ? 0u : 1u);
-            mma_bf16_ts(d, tmem + kWt + 8 * q, desc_sw128(st + L.blk + 2048 * q, kMnLbo, 1024), idx, 1);
-          }
-          mma_commit(&dxfull[b]);
-          TRACE3K(24, p);
         }
         __syncwarp();
       }
@@ -646,21 +652,24 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (leader && p < 4) TRACE3(76 + p);
         if (!bottom) {
           if (dx_warp && dx_live) {
+            // all 16 loads in flight before the first store (the shared-memory
+            // accesses are volatile: load-store pairs serialise the round
+            // trips, ~0.3-0.5 us each under the MMA / TMA traffic); the sums
+            // overwrite the staged W_lo half in place
+            float4 o[16];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              o[j] = lds_v4(r0 + ((j ^ (dx_row & 7)) << 4));
+              o[8 + j] = lds_v4(r1 + ((j ^ (dx_row & 7)) << 4));
+            }
 #pragma unroll
             for (int k = 0; k < 2; ++k) {
               const uint32_t* vv = k == 0 ? v0 : v1;
               const uint32_t rk = k == 0 ? r0 : r1;
-              // all loads in flight before the first store (the shared-memory
-              // accesses are volatile: interleaving them serialises 8 round
-              // trips, ~1 us per pair under the MMA / TMA traffic)
-              float4 o[8];
-#pragma unroll
-              for (int j = 0; j < 8; ++j) o[j] = lds_v4(rk + ((j ^ (dx_row & 7)) << 4));
 #pragma unroll
               for (int j = 0; j < 8; ++j) {
-                const float4 m = f4(vv + 4 * j);
-                sts_v4(rk + ((j ^ (dx_row & 7)) << 4),
-                       make_float4(m.x + o[j].x, m.y + o[j].y, m.z + o[j].z, m.w + o[j].w));
+                const float4 m = f4(vv + 4 * j), q4 = o[8 * k + j];
+                sts_v4(rk + ((j ^ (dx_row & 7)) << 4), make_float4(m.x + q4.x, m.y + q4.y, m.z + q4.z, m.w + q4.w));
               }
             }
           }

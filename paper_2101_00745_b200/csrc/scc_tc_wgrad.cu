@@ -80,7 +80,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int SA = a.a_stages, ST = a.t_stages, NB = a.blk;
   const int a_stage_bytes = 128 * NB * kAtom * 4;     // 128 rows x NB atoms
   const int b_blk_bytes = a.nw * kAtom * 4;           // one atom of x rows
-  const int b_stage_bytes = 2 * NB * b_blk_bytes;     // raw + lo
+  const int b_stage_bytes = NB * b_blk_bytes;         // raw, converted in place to bf16 [hi 32 | lo 32] rows
   uint8_t* a_ring = smem;
   uint8_t* b_ring = a_ring + SA * a_stage_bytes;
   uint64_t* bars = reinterpret_cast<uint64_t*>(b_ring + ST * b_stage_bytes);
@@ -218,24 +218,25 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer (dy hi/lo from TMEM, x from SMEM) ----------------
-    const uint32_t idesc = idesc_tf32(128, a.nw, 0, 0);
+    const uint32_t idesc = idesc_bf16(128, a.nw, 0, 0);
     int st = 0;
     uint32_t ps = 0;
     for (int c = 0; c < nchunks; ++c) {
       mbar_wait_tag(&conv[st], ps, 22);
       tc_fence_after();
       if (elect_one()) {
-        const uint32_t ahi = tmem + a.acol0 + st * (2 * kpix);
-        const uint32_t alo = ahi + kpix;
+        // A stage: [hi pairs: kpix/2 cols][lo pairs: kpix/2 cols]; an x atom
+        // row holds [hi 32 px | lo 32 px] bf16 (128 B, K-major SWIZZLE_128B)
+        const uint32_t ahi = tmem + a.acol0 + st * kpix;
+        const uint32_t alo = ahi + kpix / 2;
         const uint32_t braw = smem_u32(b_ring + st * b_stage_bytes);
-        const uint32_t blo = braw + NB * b_blk_bytes;
-        for (int k = 0; k < kpix / 8; ++k) {
-          const int b = k >> 2, kk = k & 3;
+        for (int k = 0; k < kpix / 16; ++k) {
+          const int b = k >> 1, kk = k & 1;
           const uint64_t dbh = desc_sw128(braw + b * b_blk_bytes + kk * 32, 16, 1024);
-          const uint64_t dbl = desc_sw128(blo + b * b_blk_bytes + kk * 32, 16, 1024);
-          mma_tf32_ts(tmem, ahi + 8 * k, dbh, idesc, (c | k) != 0);
-          mma_tf32_ts(tmem, alo + 8 * k, dbh, idesc, 1);
-          mma_tf32_ts(tmem, ahi + 8 * k, dbl, idesc, 1);
+          const uint64_t dbl = desc_sw128(braw + b * b_blk_bytes + 64 + kk * 32, 16, 1024);
+          mma_bf16_ts(tmem, ahi + 8 * k, dbh, idesc, (c | k) != 0);
+          mma_bf16_ts(tmem, alo + 8 * k, dbh, idesc, 1);
+          mma_bf16_ts(tmem, ahi + 8 * k, dbl, idesc, 1);
         }
         mma_commit(&t_free[st]);
         if (c == nchunks - 1) mma_commit(tfull);
@@ -255,24 +256,23 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int c = 0; c < nchunks; ++c) {
       mbar_wait_tag(&a_full[sa], pa, 23);
       const uint8_t* ab = a_ring + sa * a_stage_bytes;
-      uint32_t hi[2][32], lo[2][32];
+      uint32_t hi[2][16], lo[2][16];
 #pragma unroll
       for (int b = 0; b < 2; ++b) {
         if (b < NB) {
           const uint32_t src = smem_u32(ab + a_row_off(t, b));
+          float4 v[8];
 #pragma unroll
           for (int k = 0; k < 8; ++k) {
             // 16 B chunk k of the row sits at chunk index (k ^ row%8): undo the
             // swizzle so columns come out in pixel order.
-            const float4 v = lds_v4(src + 16 * (k ^ (t & 7)));
-            const float e[4] = {v.x, v.y, v.z, v.w};
+            v[k] = lds_v4(src + 16 * (k ^ (t & 7)));
+          }
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              const float h = tf32_hi(e[i]);
-              hi[b][4 * k + i] = __float_as_uint(h);
-              lo[b][4 * k + i] = __float_as_uint(e[i] - h);
-            }
-            bsum += ((v.x + v.y) + v.z) + v.w;
+          for (int k = 0; k < 8; ++k) {
+            bf16x2_split(v[k].x, v[k].y, hi[b][2 * k], lo[b][2 * k]);
+            bf16x2_split(v[k].z, v[k].w, hi[b][2 * k + 1], lo[b][2 * k + 1]);
+            bsum += ((v[k].x + v[k].y) + v[k].z) + v[k].w;
           }
         }
       }
@@ -283,12 +283,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       // (the same commit that lets the producer refill x stage st).
       mbar_wait_tag(&t_free[st], ps ^ 1u, 24);
       tc_fence_after();
-      const uint32_t col = tmem + a.acol0 + st * (2 * kpix) + lane_base;
+      const uint32_t col = tmem + a.acol0 + st * kpix + lane_base;
 #pragma unroll
       for (int b = 0; b < 2; ++b) {
         if (b < NB) {
-          tmem_st32(col + b * kAtom, hi[b]);
-          tmem_st32(col + kpix + b * kAtom, lo[b]);
+          tmem_st16(col + b * (kAtom / 2), hi[b]);
+          tmem_st16(col + kpix / 2 + b * (kAtom / 2), lo[b]);
         }
       }
       tmem_st_wait();
@@ -302,36 +302,38 @@ __global__ void __launch_bounds__(kThreads, 1)
       a.pbias[(static_cast<int64_t>(split) * a.n_rt + rt) * 128 + t] = bsum;
     }
   } else {
-    // ---------------- x lo converters, then the epilogue ----------------
-    // x lo for this warp's quarter of each stage, once x has landed (the
+    // ---------------- x converters, then the epilogue ----------------
+    // Each x atom row (32 px fp32, 128 B) becomes [hi 32 | lo 32] bf16 in
+    // place (thread = row: it alone reads and writes that 128 B, 16 B chunk j
+    // at j ^ (row % 8) both ways, conflict-free), once x has landed (the
     // producer refills a stage only after the MMAs of its previous use), in
     // parallel with the dy converters.
     const int quarter = warp & 3;  // TMEM lane quarter this warp may access
     {
-      const int bvec_q = NB * b_blk_bytes / 16 / 4;  // float4 of raw x per warp
+      const int rows = NB * a.nw;  // atom rows per stage
       int st = 0;
       uint32_t ps = 0;
       for (int c = 0; c < nchunks; ++c) {
         mbar_wait_tag(&b_full[st], ps, 24);
-        const uint32_t src = smem_u32(b_ring + st * b_stage_bytes) + 16u * quarter * bvec_q;
-        const uint32_t dst = src + NB * b_blk_bytes;
-        // 8 loads in flight before their stores (the shared-memory accesses
-        // are volatile: a load-store pair per iteration serialises the round
-        // trips)
-        for (int i0 = lane; i0 < bvec_q; i0 += 32 * 8) {
+        const uint32_t base = smem_u32(b_ring + st * b_stage_bytes);
+        for (int r = quarter * 32 + lane; r < rows; r += 128) {
+          const uint32_t row = base + 128u * r;
+          const int sw = r & 7;
           float4 v[8];
 #pragma unroll
-          for (int u = 0; u < 8; ++u) v[u] = lds_v4(src + 16u * min(i0 + 32 * u, bvec_q - 1));
+          for (int j = 0; j < 8; ++j) v[j] = lds_v4(row + ((j ^ sw) << 4));
+          uint32_t hi[16], lo[16];
 #pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            if (i0 + 32 * u < bvec_q) {
-              float4 l4;
-              l4.x = v[u].x - tf32_hi(v[u].x);
-              l4.y = v[u].y - tf32_hi(v[u].y);
-              l4.z = v[u].z - tf32_hi(v[u].z);
-              l4.w = v[u].w - tf32_hi(v[u].w);
-              sts_v4(dst + 16u * (i0 + 32 * u), l4);
-            }
+          for (int j = 0; j < 8; ++j) {
+            bf16x2_split(v[j].x, v[j].y, hi[2 * j], lo[2 * j]);
+            bf16x2_split(v[j].z, v[j].w, hi[2 * j + 1], lo[2 * j + 1]);
+          }
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(row + ((j ^ sw) << 4)), "r"(hi[4 * j]),
+                         "r"(hi[4 * j + 1]), "r"(hi[4 * j + 2]), "r"(hi[4 * j + 3]));
+            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(row + (((4 + j) ^ sw) << 4)),
+                         "r"(lo[4 * j]), "r"(lo[4 * j + 1]), "r"(lo[4 * j + 2]), "r"(lo[4 * j + 3]));
           }
         }
         fence_proxy_async_smem();
@@ -515,9 +517,9 @@ WGrid weight_grid(const TcWeightPlan& tw, int64_t n, int64_t plane) {
   int kpix = 0, a_stage = 0, b_stage = 0;
   for (;;) {
     kpix = g.blk * kAtom;
-    g.t_stages = std::min(kMaxT, (512 - g.acol0) / (2 * kpix));
+    g.t_stages = std::min(kMaxT, (512 - g.acol0) / kpix);  // bf16 hi | lo pairs: kpix columns per stage
     a_stage = 128 * kpix * 4;
-    b_stage = 2 * tw.nw * kpix * 4;
+    b_stage = tw.nw * kpix * 4;                             // raw x, converted in place
     while (g.t_stages > 1 && (kBudget - g.t_stages * b_stage) / a_stage < 2) --g.t_stages;
     g.a_stages = std::min(kMaxA, (kBudget - g.t_stages * b_stage) / a_stage);
     // A single x stage serialises load -> lo convert -> MMA per chunk

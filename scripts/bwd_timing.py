@@ -63,3 +63,6 @@ for name, f in (("bwd_data", bdata), ("bwd", bwd)):
     m0 = min(cs)
     s_ = sorted((x - m0) / 1e3 for x in cs); e_ = sorted((x - m0) / 1e3 for x in ce)
     print(f"  CTA start min/med/max {s_[0]:.2f}/{s_[74]:.2f}/{s_[-1]:.2f}  end {e_[0]:.2f}/{e_[74]:.2f}/{e_[-1]:.2f}")
+    if os.environ.get("CTA_DUMP") and name == "bwd":
+        for i in range(148):
+            print(f"  cta {i:3d} sm {cs[i] & 0xFF:3d} start {((cs[i] & ~0xFF) - m0) / 1e3:6.2f} end {(ce[i] - m0) / 1e3:6.2f}")

@@ -21,11 +21,12 @@ for mode in (0, 1):
             err = np.max(np.abs(o - ref)) / np.max(np.abs(ref))
             print(f"mode {mode} ({'B MN-major' if mode == 0 else 'B K-major'}) swap {swap} lbo {lbo} sbo {sbo}: rc {rc} err {err:.3e}", flush=True)
 res = torch.zeros(148, dtype=torch.int64, device="cuda")
-for b_mn in (1, 0):
+for m in (128, 64):
+  for b_mn in (1, 0):
     row = []
     for n in (32, 64, 128, 256):
         reps = 512
-        assert lib.bf16_rate(n, b_mn, reps, 148, C.c_void_p(res.data_ptr())) == 0
+        assert lib.bf16_rate(m, n, b_mn, reps, 148, C.c_void_p(res.data_ptr())) == 0
         v = sorted(res.tolist())
         row.append(f"N={n}: {v[74] / reps:6.1f}")
-    print(f"bf16 TS M=128 K=16 B {'MN' if b_mn else 'K '}-major  " + "  ".join(row) + "  cycles/MMA", flush=True)
+    print(f"bf16 TS M={m} K=16 B {'MN' if b_mn else 'K '}-major  " + "  ".join(row) + "  cycles/MMA", flush=True)

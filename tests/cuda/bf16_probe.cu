@@ -132,7 +132,7 @@ extern "C" int bf16_probe(const float* a, const float* b, float* out, int mode, 
   return 0;
 }
 
-__global__ void __launch_bounds__(128) bf16_rate_kernel(int n, int b_mn, int reps, unsigned long long* out) {
+__global__ void __launch_bounds__(128) bf16_rate_kernel(int m, int n, int b_mn, int reps, unsigned long long* out) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t bar;
   __shared__ uint32_t tbase;
@@ -150,7 +150,7 @@ __global__ void __launch_bounds__(128) bf16_rate_kernel(int n, int b_mn, int rep
   const uint32_t tmem = tbase;
   if (warp == 0) {
     if (elect_one()) {
-      const uint32_t idesc = idesc_bf16_p(128, static_cast<uint32_t>(n), 0, static_cast<uint32_t>(b_mn));
+      const uint32_t idesc = idesc_bf16_p(static_cast<uint32_t>(m), static_cast<uint32_t>(n), 0, static_cast<uint32_t>(b_mn));
       const uint32_t b = smem_u32(smem);
       const long long t0 = clock64();
       for (int r = 0; r < reps; ++r) {
@@ -170,9 +170,9 @@ __global__ void __launch_bounds__(128) bf16_rate_kernel(int n, int b_mn, int rep
   if (warp == 0) tmem_dealloc<512>(tmem);
 }
 
-extern "C" int bf16_rate(int n, int b_mn, int reps, int grid, unsigned long long* out_dev) {
+extern "C" int bf16_rate(int m, int n, int b_mn, int reps, int grid, unsigned long long* out_dev) {
   cudaFuncSetAttribute(bf16_rate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
-  bf16_rate_kernel<<<grid, 128, 65536>>>(n, b_mn, reps, out_dev);
+  bf16_rate_kernel<<<grid, 128, 65536>>>(m, n, b_mn, reps, out_dev);
   const cudaError_t e = cudaDeviceSynchronize();
   if (e != cudaSuccess) printf("bf16_rate: %s\n", cudaGetErrorString(e));
   return e == cudaSuccess ? 0 : -1;
