@@ -780,13 +780,29 @@ size_t tc_panel_bytes(const TcBandPlan& tp) {
   return static_cast<size_t>(tp.total_chunks) * 2 * tp.nt * 32 * sizeof(float);
 }
 
+// bf16x3 for backward-data only (1e-4 bar).  The forward stays 3xTF32: a
+// bf16x3 forward measured <= 6e-6 norm-relative on every C5 shape (within the
+// 1e-5 bar; 3xTF32: 0.9-5.8e-6) and 1.2-1.5x faster at gw >= 128, but through
+// a network its larger errors flip ReLU masks of near-zero activations: the
+// reference harness's mobilenet_like gradients moved from ~1e-5 to 5e-3
+// (scripts/probes/harness_prec.py).  -DSCC_FWD_BF16 builds that variant for
+// scripts/probes/precision_probe.py.
+static bool bf16x3_band(const TcBandCall& call) {
+#if defined(SCC_FWD_BF16)
+  (void)call;
+  return true;
+#else
+  return call.backward_data;
+#endif
+}
+
 cudaError_t launch_band_tc(const TcBandPlan& tp, const TcDeviceTables& dt, const TcBandCall& call,
                            cudaStream_t s) {
   switch (tp.nt) {
     case 64:
-      return call.backward_data ? launch_tc_nt<64, true>(tp, dt, call, s) : launch_tc_nt<64, false>(tp, dt, call, s);
+      return bf16x3_band(call) ? launch_tc_nt<64, true>(tp, dt, call, s) : launch_tc_nt<64, false>(tp, dt, call, s);
     case 128:
-      return call.backward_data ? launch_tc_nt<128, true>(tp, dt, call, s) : launch_tc_nt<128, false>(tp, dt, call, s);
+      return bf16x3_band(call) ? launch_tc_nt<128, true>(tp, dt, call, s) : launch_tc_nt<128, false>(tp, dt, call, s);
     default:
       return cudaErrorInvalidValue;
   }
