@@ -118,6 +118,39 @@ struct Band2Args {
   int64_t plane;
 };
 
+// This CTA's block range [u, u1) (see TileIter).  Not inlined: every warp
+// role builds a TileIter, and four inlined copies of the division code were
+// ~1,000 instructions of the kernel's ~3,900.
+__device__ __noinline__ int2 tile_range(const Band2Args& a) {
+  int32_t u, u1;
+  const int32_t ns = a.nbps > 0 ? a.units / a.nbps : 0;  // samples
+  if (ns > 0 && static_cast<int32_t>(gridDim.x) >= ns) {
+    const int32_t g = static_cast<int32_t>(gridDim.x), i = static_cast<int32_t>(blockIdx.x);
+    const int32_t base = g / ns, extra = g % ns;
+    int32_t smp, r, nr;
+    if (i < extra * (base + 1)) {
+      smp = i / (base + 1);
+      r = i - smp * (base + 1);
+      nr = base + 1;
+    } else {
+      const int32_t i2 = i - extra * (base + 1);
+      smp = extra + i2 / base;
+      r = i2 - (smp - extra) * base;
+      nr = base;
+    }
+    u = smp * a.nbps + (r * a.nbps) / nr;
+    u1 = smp * a.nbps + ((r + 1) * a.nbps) / nr;
+  } else if (a.units < (1 << 22)) {
+    // 32-bit division when the products fit (the 64-bit one is a slow call)
+    u = static_cast<int32_t>((blockIdx.x * static_cast<uint32_t>(a.units)) / gridDim.x);
+    u1 = static_cast<int32_t>(((blockIdx.x + 1) * static_cast<uint32_t>(a.units)) / gridDim.x);
+  } else {
+    u = static_cast<int32_t>((static_cast<int64_t>(blockIdx.x) * a.units) / gridDim.x);
+    u1 = static_cast<int32_t>((static_cast<int64_t>(blockIdx.x + 1) * a.units) / gridDim.x);
+  }
+  return make_int2(u, u1);
+}
+
 // Contiguous run of blocks owned by this CTA, cut into tiles of <= 4 blocks
 // that never straddle a sample.  A tile costs one pass of the load / convert /
 // MMA / store pipeline whatever its width, so when there are at least as many
@@ -129,31 +162,9 @@ struct TileIter {
   int32_t u, u1, nbps;
   int32_t n, b0, cnt;
   __device__ explicit TileIter(const Band2Args& a) {
-    const int32_t ns = a.nbps > 0 ? a.units / a.nbps : 0;  // samples
-    if (ns > 0 && static_cast<int32_t>(gridDim.x) >= ns) {
-      const int32_t g = static_cast<int32_t>(gridDim.x), i = static_cast<int32_t>(blockIdx.x);
-      const int32_t base = g / ns, extra = g % ns;
-      int32_t smp, r, nr;
-      if (i < extra * (base + 1)) {
-        smp = i / (base + 1);
-        r = i - smp * (base + 1);
-        nr = base + 1;
-      } else {
-        const int32_t i2 = i - extra * (base + 1);
-        smp = extra + i2 / base;
-        r = i2 - (smp - extra) * base;
-        nr = base;
-      }
-      u = smp * a.nbps + (r * a.nbps) / nr;
-      u1 = smp * a.nbps + ((r + 1) * a.nbps) / nr;
-    } else if (a.units < (1 << 22)) {
-      // 32-bit division when the products fit (the 64-bit one is a slow call)
-      u = static_cast<int32_t>((blockIdx.x * static_cast<uint32_t>(a.units)) / gridDim.x);
-      u1 = static_cast<int32_t>(((blockIdx.x + 1) * static_cast<uint32_t>(a.units)) / gridDim.x);
-    } else {
-      u = static_cast<int32_t>((static_cast<int64_t>(blockIdx.x) * a.units) / gridDim.x);
-      u1 = static_cast<int32_t>((static_cast<int64_t>(blockIdx.x + 1) * a.units) / gridDim.x);
-    }
+    const int2 r = tile_range(a);
+    u = r.x;
+    u1 = r.y;
     nbps = a.nbps;
     n = b0 = cnt = 0;
   }

@@ -178,49 +178,46 @@ struct BLayout {
 // built from W and the (oc*gw - start, start) table staged in shared memory.
 __device__ __forceinline__ void build_wt(const BArgs& a, uint32_t tmem, uint32_t lane_base, int L,
                                          const float* ws, const int2* kt) {
+  // One 32-filter group (16 TMEM columns) per iteration, the group body
+  // unrolled, the group loop not: the fully unrolled form (two code paths x
+  // 128 filters) was ~2,100 instructions -- a third of the kernel's code,
+  // fetched from L2 while the data loads; one column per store measured
+  // 6 us slower (the W^T build is on the first dx MMA's path).
   const int ic = L & 63;
   const bool lo_lane = L >= 64;
   const bool live = ic < a.c_in;
   const int cpad = round16(a.c_out);
-  for (int c0 = 0; c0 < cpad; c0 += 64) {
-    uint32_t r[32];
+#pragma unroll 1
+  for (int c0 = 0; c0 < cpad; c0 += 32) {
+    float v[32];
+    if (a.cls % 32 == 0 && c0 < a.c_out) {
+      // the group is one window class: one start, filters D apart in W
+      const int2 e = kt[c0];
+      const int wrap = ic < e.y ? a.c_in : 0;
+      const bool in = live && static_cast<unsigned>(ic - e.y + wrap) < static_cast<unsigned>(a.gw);
+      const float* p = ws + (in ? e.x + ic + wrap : 0);
+      const int stride = a.n_class * a.gw;
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int cb = c0 + 32 * h;
-      float v[32];
-      if (a.cls % 32 == 0 && cb < a.c_out) {
-        // the chunk is one window class: one start, filters D apart in W
-        const int2 e = kt[cb];
+      for (int t = 0; t < 32; ++t) v[t] = in ? p[t * stride] : 0.f;
+    } else {
+#pragma unroll
+      for (int t = 0; t < 32; ++t) {
+        const int f = c0 + t;
+        const int2 e = kt[min(f, a.c_out - 1)];
         const int wrap = ic < e.y ? a.c_in : 0;
-        const bool in = live && static_cast<unsigned>(ic - e.y + wrap) < static_cast<unsigned>(a.gw);
-        const float* p = ws + (in ? e.x + ic + wrap : 0);
-        const int stride = a.n_class * a.gw;
-#pragma unroll
-        for (int t = 0; t < 32; ++t) v[t] = in ? p[t * stride] : 0.f;
-      } else {
-        int idx[32];
-#pragma unroll
-        for (int t = 0; t < 32; ++t) {
-          const int2 e = kt[min(cb + t, a.c_out - 1)];
-          const int wrap = ic < e.y ? a.c_in : 0;
-          const bool in = live && static_cast<unsigned>(ic - e.y + wrap) < static_cast<unsigned>(a.gw) &&
-                          cb + t < a.c_out;
-          idx[t] = in ? e.x + ic + wrap : -1;
-        }
-#pragma unroll
-        for (int t = 0; t < 32; ++t) {
-          const float w = ws[max(idx[t], 0)];
-          v[t] = idx[t] >= 0 ? w : 0.f;
-        }
-      }
-#pragma unroll
-      for (int t = 0; t < 16; ++t) {
-        uint32_t hi, lo;
-        bf16x2_split(v[2 * t], v[2 * t + 1], hi, lo);
-        r[16 * h + t] = lo_lane ? lo : hi;
+        const bool in = live && f < a.c_out && static_cast<unsigned>(ic - e.y + wrap) < static_cast<unsigned>(a.gw);
+        v[t] = ws[in ? e.x + ic + wrap : 0];
+        v[t] = in ? v[t] : 0.f;
       }
     }
-    tmem_st32(tmem + kWt + c0 / 2 + lane_base, r);
+    uint32_t r[16];
+#pragma unroll
+    for (int t = 0; t < 16; ++t) {
+      uint32_t hi, lo;
+      bf16x2_split(v[2 * t], v[2 * t + 1], hi, lo);
+      r[t] = lo_lane ? lo : hi;
+    }
+    tmem_st16(tmem + kWt + static_cast<uint32_t>(c0 / 2) + lane_base, r);
   }
   tmem_st_wait();
   tc_fence_before();
@@ -543,23 +540,20 @@ __global__ void __launch_bounds__(kThreads, 1)
         j0 += j0 < 0 ? a.c_in : 0;
       }
       float* dst = a.part + static_cast<int64_t>(sl) * a.elems;
-      float wv[kMaxGw];
-#pragma unroll
-      for (int t = 0; t < kMaxGw; ++t) {
-        int j = j0 + t;
-        j -= j >= a.c_in ? a.c_in : 0;
-        wv[t] = (wlive && t < a.gw) ? prow[j] : 0.f;
-      }
       if (i < a.c_out) {
+        // (compact loop: a fully unrolled gather was ~500 instructions)
+        auto wat = [&](int t) {
+          int j = j0 + t;
+          j -= j >= a.c_in ? a.c_in : 0;
+          return wlive ? prow[j] : 0.f;
+        };
         if ((a.gw & 3) == 0) {
-#pragma unroll
-          for (int t = 0; t < kMaxGw; t += 4)
-            if (t < a.gw)
-              *reinterpret_cast<float4*>(dst + i * a.gw + t) = make_float4(wv[t], wv[t + 1], wv[t + 2], wv[t + 3]);
+#pragma unroll 1
+          for (int t = 0; t < a.gw; t += 4)
+            *reinterpret_cast<float4*>(dst + i * a.gw + t) = make_float4(wat(t), wat(t + 1), wat(t + 2), wat(t + 3));
         } else {
-#pragma unroll
-          for (int t = 0; t < kMaxGw; ++t)
-            if (t < a.gw) dst[i * a.gw + t] = wv[t];
+#pragma unroll 1
+          for (int t = 0; t < a.gw; ++t) dst[i * a.gw + t] = wat(t);
         }
         dst[a.c_out * a.gw + i] = wlive ? dbsum : 0.f;
       }

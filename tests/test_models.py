@@ -96,6 +96,10 @@ def test_training_loss_falls(name):
         pytest.skip("no CUDA device")
     from paper_2101_00745_b200.train import train_throughput
     kw = dict(image=64, num_classes=10) if name == "resnet50" else {}
-    r = train_throughput(name, batch=32, steps=15, warmup=1, **kw)
+    # ResNet-50 from scratch hovers near its first loss for ~15 steps at batch
+    # 32 (measured 2.49-2.61 vs 2.57 across runs: stock cuDNN convolutions are
+    # not bitwise reproducible); by 30 steps it is at ~2.15
+    steps = 30 if name == "resnet50" else 15
+    r = train_throughput(name, batch=32, steps=steps, warmup=1, **kw)
     assert r["images_per_s"] > 0
     assert r["loss_last"] < r["loss_first"], r
