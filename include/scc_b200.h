@@ -65,7 +65,8 @@ typedef enum { SCC_OVERLAP_CHANNELS = 0, SCC_OVERLAP_RATIO = 1 } scc_overlap_kin
 typedef enum {
   SCC_PATH_AUTO = 0,
   SCC_PATH_CUDA_CORE = 1,       /* fp32 FFMA banded kernels                                */
-  SCC_PATH_TENSOR = 2,          /* tcgen05 3xTF32 banded-GEMM kernels (AUTO's choice)        */
+  SCC_PATH_TENSOR = 2,          /* tcgen05 banded-GEMM kernels (AUTO): 3xTF32 forward, bf16x3 fused /
+                                   generation-1 backward (gradient bar 1e-4)                   */
   SCC_PATH_TENSOR_STREAMED = 3  /* tcgen05 kernels that stream the weight panel from L2: the
                                    family AUTO uses for layers whose panel does not fit in
                                    shared memory; forcing it on small layers is for tests  */
