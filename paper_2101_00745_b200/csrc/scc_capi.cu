@@ -266,9 +266,9 @@ WeightLaunch weight_args(const Plan& p, const DeviceTables& t, int64_t n, int64_
 // The fused backward kernel (scc_tc_bwd.cu) serves scc_backward and, so
 // that fused and separate calls agree bitwise, the separate backward-data and
 // backward-weight entry points too, whenever its geometry fits.
-bool fused_bwd_supported(const Plan& p, int64_t plane) {
+bool fused_bwd_supported(const Plan& p, int64_t n, int64_t plane) {
   if (p.path == SCC_PATH_TENSOR_STREAMED || p.path == SCC_PATH_CUDA_CORE) return false;
-  return tc_bwd_supported(p.tc_wgt, plane, static_cast<int32_t>(p.cfg.c_in), static_cast<int32_t>(p.cfg.c_out),
+  return tc_bwd_supported(p.tc_wgt, n, plane, static_cast<int32_t>(p.cfg.c_in), static_cast<int32_t>(p.cfg.c_out),
                           static_cast<int32_t>(p.cfg.group_width));
 }
 
@@ -282,13 +282,13 @@ size_t weight_ws_bytes(const Plan& p, int64_t n, int64_t plane) {
 size_t weight_ws_bytes_plane(const Plan& p, int64_t n, int64_t plane) {
   const size_t cc = weight_cc_workspace_bytes(p.fwd.nblk(), p.fwd.max_block_len, n, plane);
   const size_t tc = tc_weight_supported(p.tc_wgt, plane) ? tc_weight_workspace_bytes(p.tc_wgt, n, plane) : 0;
-  const size_t tc2 = tc_wgrad2_supported(p.tc_wgt, plane, static_cast<int32_t>(p.cfg.group_width))
+  const size_t tc2 = tc_wgrad2_supported(p.tc_wgt, n, plane, static_cast<int32_t>(p.cfg.group_width))
                          ? tc_wgrad2_workspace_bytes(static_cast<int32_t>(p.cfg.c_out),
                                                      static_cast<int32_t>(p.cfg.group_width), 74)
                          : 0;
   // (independent of the forced path, so a size queried before set_path stays
   // large enough after it)
-  const size_t tc3 = tc_bwd_supported(p.tc_wgt, plane, static_cast<int32_t>(p.cfg.c_in),
+  const size_t tc3 = tc_bwd_supported(p.tc_wgt, n, plane, static_cast<int32_t>(p.cfg.c_in),
                                       static_cast<int32_t>(p.cfg.c_out), static_cast<int32_t>(p.cfg.group_width))
                          ? tc_bwd_workspace_bytes(static_cast<int32_t>(p.cfg.c_out),
                                                   static_cast<int32_t>(p.cfg.group_width), n, plane)
@@ -386,7 +386,7 @@ void do_forward(Plan& p, int64_t n, int64_t h, int64_t w, const float* x, const 
 bool use_fused(Plan& p, int64_t n, int64_t h, int64_t w, std::initializer_list<const void*> ptrs) {
   for (const void* q : ptrs)
     if (q != nullptr && !aligned16(q)) return false;
-  return choose_path(p, n, h, w, 2) == SCC_PATH_TENSOR && fused_bwd_supported(p, h * w);
+  return choose_path(p, n, h, w, 2) == SCC_PATH_TENSOR && fused_bwd_supported(p, n, h * w);
 }
 
 void launch_fused(Plan& p, int64_t n, int64_t h, int64_t w, const float* dy, const float* x, const float* wt,
@@ -493,7 +493,7 @@ void do_backward_weight(Plan& p, int64_t n, int64_t h, int64_t w, const float* d
     c.rt_info = t.tcw_rt_info;
     c.class_d = t.tcw_class_d;
     c.max_ctas = max_ctas;
-    if (p.path != SCC_PATH_TENSOR_STREAMED && tc_wgrad2_supported(p.tc_wgt, h * w, c.gw)) {
+    if (p.path != SCC_PATH_TENSOR_STREAMED && tc_wgrad2_supported(p.tc_wgt, n, h * w, c.gw)) {
       cuda_check(launch_wgrad2(p.tc_wgt, c, t.perm, s), "backward-weight (tensor) launch");
       return;
     }
@@ -569,7 +569,7 @@ void do_backward(Plan& p, int64_t n, int64_t h, int64_t w, const float* dy, cons
                      choose_path(p, n, h, w, 1) == SCC_PATH_TENSOR &&
                      choose_path(p, n, h, w, 2) == SCC_PATH_TENSOR &&
                      tc_band2_supported(p.tc_bwd, plane, static_cast<int32_t>(p.cfg.c_out)) &&
-                     tc_wgrad2_supported(p.tc_wgt, plane, static_cast<int32_t>(p.cfg.group_width));
+                     tc_wgrad2_supported(p.tc_wgt, n, plane, static_cast<int32_t>(p.cfg.group_width));
   // Generation-1 pair on a small (latency-bound) problem: the weight kernel
   // is sized to half the SMs (tc_weight_small), backward-data takes the rest.
   const bool both1 = !both2 && aligned16(dy) && aligned16(x) && aligned16(dx) &&
@@ -579,7 +579,7 @@ void do_backward(Plan& p, int64_t n, int64_t h, int64_t w, const float* dy, cons
                      choose_path(p, n, h, w, 2) == SCC_PATH_TENSOR &&
                      tc_weight_supported(p.tc_wgt, plane) &&
                      (p.path == SCC_PATH_TENSOR_STREAMED ||
-                      !tc_wgrad2_supported(p.tc_wgt, plane, static_cast<int32_t>(p.cfg.group_width)));
+                      !tc_wgrad2_supported(p.tc_wgt, n, plane, static_cast<int32_t>(p.cfg.group_width)));
   if (!both2 && !both1) {
     do_backward_data(p, n, h, w, dy, wt, dx, s);
     do_backward_weight(p, n, h, w, dy, x, dw, db, ws, ws_bytes, s);

@@ -121,7 +121,7 @@ cudaError_t launch_band_tc2(const TcBandPlan& tp, const TcDeviceTables& dt, cons
 int tc2_trace(unsigned long long* out, int n);
 // Backward-weight generation 2 (scc_tc_wgrad2.cu): TS-mode MMAs, per-slice
 // partials reduced in a fixed order by a PDL-chained second kernel.
-bool tc_wgrad2_supported(const TcWeightPlan& tw, int64_t plane, int32_t gw);
+bool tc_wgrad2_supported(const TcWeightPlan& tw, int64_t n, int64_t plane, int32_t gw);
 size_t tc_wgrad2_workspace_bytes(int32_t c_out, int32_t gw, int nsm);
 int tc_w2trace(unsigned long long* out, int n);
 cudaError_t launch_wgrad2(const TcWeightPlan& tw, const TcWeightCall& call, const int32_t* perm,
@@ -150,7 +150,7 @@ struct TcBwdCall {
   bool do_dx = false, do_dw = false;
   int32_t max_ctas = 0;
 };
-bool tc_bwd_supported(const TcWeightPlan& tw, int64_t plane, int32_t c_in, int32_t c_out, int32_t gw);
+bool tc_bwd_supported(const TcWeightPlan& tw, int64_t n, int64_t plane, int32_t c_in, int32_t c_out, int32_t gw);
 size_t tc_bwd_workspace_bytes(int32_t c_out, int32_t gw, int64_t n, int64_t plane);
 cudaError_t launch_tc_bwd(const TcWeightPlan& tw, const TcBwdCall& call, cudaStream_t s);
 int tc_bwd_trace(unsigned long long* out, int n);

@@ -773,8 +773,14 @@ int tc_bwd_trace(unsigned long long* out, int n) {
 #endif
 }
 
-bool tc_bwd_supported(const TcWeightPlan& tw, int64_t plane, int32_t c_in, int32_t c_out, int32_t gw) {
+bool tc_bwd_supported(const TcWeightPlan& tw, int64_t n, int64_t plane, int32_t c_in, int32_t c_out,
+                      int32_t gw) {
   if (!tw.ok || plane % 4 != 0 || tw.n_rt != 1 || tw.rt_info.size() < 2) return false;
+  // dW accumulation chain of a slice (2 K = 16 steps per 32-pixel block, one
+  // slice per CTA): at most 768 steps, as the generation-1 weight kernel
+  // bounds its splits (each MMA rounds the running sum toward zero); larger
+  // problems take the two-kernel backward.
+  if ((n * ((plane + 31) / 32) + kSlices - 1) / kSlices * 2 > 768) return false;
   if (c_out > 128 || c_out % 8 != 0 || c_out != tw.n_class * tw.cls || tw.cls > 256 || tw.n_class > 256)
     return false;
   if (c_in > 64 || gw > kMaxGw) return false;

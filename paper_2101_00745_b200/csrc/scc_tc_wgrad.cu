@@ -538,6 +538,19 @@ WGrid weight_grid(const TcWeightPlan& tw, int64_t n, int64_t plane) {
   // on the geometry only, so every entry point sums in the same order.
   const int64_t cap = tc_weight_small(n, plane, std::max(tw.c_in, tw.c_out)) ? 74 : 148;
   int64_t splits = std::max<int64_t>(1, cap / items);
+  // Bound the accumulation chain of each split's TMEM accumulator: every MMA
+  // rounds the running fp32 sum toward zero, a bias that grows linearly with
+  // the chain (measured ~6e-8 of max|dW| per K = 16 step: 4.0e-5 at the
+  // 697-step chains of C=1024 cg=2 56x56, N=32).  At most kMaxChain steps per
+  // split keeps dW within ~4.5e-5 of the 1e-4 bar at any N * plane; extra
+  // splits come in whole waves.
+  constexpr int64_t kMaxChain = 768;
+  const int64_t steps = g.total_chunks * (kpix / 16);
+  if (steps > splits * kMaxChain) {
+    const int64_t wave = splits;
+    splits = (steps + kMaxChain - 1) / kMaxChain;
+    splits = (splits + wave - 1) / wave * wave;
+  }
   splits = std::min(splits, g.total_chunks);
   g.chunks_per_split = (g.total_chunks + splits - 1) / splits;
   g.splits = static_cast<int32_t>((g.total_chunks + g.chunks_per_split - 1) / g.chunks_per_split);

@@ -483,8 +483,13 @@ int w2_stages(int xr) {
 // Supported when the tile's arc plus the ones row fits one MMA (N <= 128, so
 // the accumulator and four TMEM A stages fit 512 columns) and the small tables
 // fit the kernel parameters.
-bool tc_wgrad2_supported(const TcWeightPlan& tw, int64_t plane, int32_t gw) {
+bool tc_wgrad2_supported(const TcWeightPlan& tw, int64_t n, int64_t plane, int32_t gw) {
   if (!tw.ok || plane % 4 != 0 || tw.n_rt > kMaxRt || tw.n_class > kMaxCls) return false;
+  // Accumulation chain of a slice's TMEM accumulator (4 K = 8 steps per
+  // 32-pixel block): each MMA rounds the running sum toward zero, a bias
+  // linear in the chain (~6e-8 of max|dW| per step, scc_tc_wgrad.cu); larger
+  // problems take the generation-1 kernel, which adds splits instead.
+  if ((n * ((plane + 31) / 32) + kSlices - 1) / kSlices * 4 > 768) return false;
   int nx = 0;
   for (int rt = 0; rt < tw.n_rt; ++rt) nx = std::max(nx, tw.rt_info[2 * rt + 1]);
   const int xr = (nx + 1 + 15) / 16 * 16;
