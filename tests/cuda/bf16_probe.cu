@@ -177,3 +177,96 @@ extern "C" int bf16_rate(int m, int n, int b_mn, int reps, int grid, unsigned lo
   if (e != cudaSuccess) printf("bf16_rate: %s\n", cudaGetErrorString(e));
   return e == cudaSuccess ? 0 : -1;
 }
+
+// M = 64 layout probe: A rows (bf16 pairs) at TMEM lanes [lb, lb + 64), D at
+// lanes [lb, lb + 64) of columns [0, 64); every lane of D's columns is first
+// filled with a sentinel so the caller sees which lanes the MMA wrote.
+// out[128][64]: all 128 lanes of the D columns.
+__global__ void __launch_bounds__(128) m64_kernel(const float* a, const float* b, float* out, int lb) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tbase;
+  const int tid = threadIdx.x;
+  const uint32_t warp = warp_id();
+  if (tid == 0) {
+    mbar_init(&bar, 1);
+    fence_mbar_init();
+  }
+  if (warp == 0) tmem_alloc<256>(&tbase);
+  for (int i = tid; i < 65536 / 4; i += 128) reinterpret_cast<uint32_t*>(smem)[i] = 0u;
+  __syncthreads();
+  // B: K-major SWIZZLE_128B, N = 64 rows, K = 128
+  for (int i = tid; i < K * N; i += 128) {
+    const int k = i / N, n = i % N;
+    const int off = (k / 64) * (N / 8 * 1024) + (n / 8) * 1024 + (n % 8) * 128 + ((((k % 64) / 8) ^ (n % 8)) * 16) + (k % 8) * 2;
+    *reinterpret_cast<__nv_bfloat16*>(smem + off) = __float2bfloat16_rn(b[k * N + n]);
+  }
+  fence_proxy_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tbase;
+  {
+    // A rows: lb < 0: row r at lane (r % 16) + 32 * (r / 16) (the M = 64
+    // datapath layout); else lane m holds row (m - lb) for m in [lb, lb + 64).
+    // D sentinel 7777.
+    const int m = tid;
+    const bool m64l = lb < 0;
+    const bool live = m64l ? (m & 31) < 16 : (m >= lb && m < lb + 64);
+    const int row = m64l ? (m & 15) + 16 * (m >> 5) : m - lb;
+    if (m64l) lb = 0;
+    for (int c0 = 0; c0 < K / 2; c0 += 32) {
+      uint32_t r[32];
+      for (int c = 0; c < 32; ++c) {
+        const int k = 2 * (c0 + c);
+        const uint32_t lo = live ? __bfloat16_as_ushort(__float2bfloat16_rn(a[row * K + k])) : 0u;
+        const uint32_t hi = live ? __bfloat16_as_ushort(__float2bfloat16_rn(a[row * K + k + 1])) : 0u;
+        r[c] = (hi << 16) | lo;
+      }
+      tmem_st32(tmem + 128 + c0 + ((warp * 32) << 16), r);
+    }
+    uint32_t s[32];
+    for (int c = 0; c < 32; ++c) s[c] = __float_as_uint(7777.f);
+    tmem_st32(tmem + ((warp * 32) << 16), s);
+    tmem_st32(tmem + 32 + ((warp * 32) << 16), s);
+    tmem_st_wait();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 0) {
+    if (elect_one()) {
+      const uint32_t idesc = idesc_bf16_p(64, N, 0, 0);
+      const uint32_t bb = smem_u32(smem);
+      for (int ks = 0; ks < K / 16; ++ks) {
+        const uint64_t bd = desc_t(bb + (ks / 4) * (N / 8 * 1024) + (ks % 4) * 32, 16, 1024, 2);
+        mma_bf16_ts_p(tmem + (static_cast<uint32_t>(lb) << 16), tmem + 128 + 8 * ks + (static_cast<uint32_t>(lb) << 16), bd,
+                      idesc, ks > 0);
+      }
+      mma_commit(&bar);
+    }
+    __syncwarp();
+  }
+  mbar_wait(&bar, 0);
+  tc_fence_after();
+  for (int c = 0; c < N; c += 16) {
+    float v[16];
+    tmem_ld16(tmem + ((warp * 32) << 16) + c, v);
+    const int r = warp * 32 + (tid & 31);
+    for (int j = 0; j < 16; ++j) out[r * N + c + j] = v[j];
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc<256>(tmem);
+}
+
+extern "C" int m64_probe(const float* a, const float* b, float* out, int lb) {
+  cudaFuncSetAttribute(m64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
+  m64_kernel<<<1, 128, 65536>>>(a, b, out, lb);
+  const cudaError_t e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) {
+    fprintf(stderr, "m64_probe: %s\n", cudaGetErrorString(e));
+    return -2;
+  }
+  return 0;
+}
