@@ -288,9 +288,13 @@ void build_tc_weight(const Plan& p, TcWeightPlan& tw) {
     tw.rt_info.insert(tw.rt_info.end(), {start8, ncols});
     max_cols = std::max(max_cols, ncols);
   }
-  // Column chunk: multiple of 32 (four 8-row quarters, M=128 MMA), <= 256.
+  // Column chunk: multiple of 32 (four 8-row quarters, M=128 MMA).  Up to 384
+  // columns stay one chunk (the kernel splits the MMA's N at 256, TMEM holds
+  // 384 accumulator columns next to its A stages): a second chunk would be a
+  // second CTA re-reading the tile's dy -- co = 25 / 75 % at gw = 256 gives
+  // 320-384-column arcs (measured 1.7x the backward-weight time of co = 50 %).
   const int32_t w32 = (max_cols + 31) / 32 * 32;
-  tw.n_nc = (w32 + 255) / 256;
+  tw.n_nc = w32 <= 384 ? 1 : (w32 + 255) / 256;
   tw.nw = ((w32 + tw.n_nc - 1) / tw.n_nc + 31) / 32 * 32;
   // dy boxes: each converter warp loads its 32 filter rows; one box when the
   // 32 rows are one contiguous class run.

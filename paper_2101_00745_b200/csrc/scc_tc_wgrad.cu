@@ -218,7 +218,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer (dy hi/lo from TMEM, x from SMEM) ----------------
-    const uint32_t idesc = idesc_bf16(128, a.nw, 0, 0);
+    // N in at most two parts: an MMA's N is <= 256 (columns [256, nw) of a
+    // 257-384-column chunk are a second MMA on the B rows past 256)
+    const int n1 = min(a.nw, 256), n2 = a.nw - n1;
+    const uint32_t idesc = idesc_bf16(128, n1, 0, 0);
+    const uint32_t idesc2 = idesc_bf16(128, n2 > 0 ? n2 : 16, 0, 0);
     int st = 0;
     uint32_t ps = 0;
     for (int c = 0; c < nchunks; ++c) {
@@ -237,6 +241,14 @@ __global__ void __launch_bounds__(kThreads, 1)
           mma_bf16_ts(tmem, ahi + 8 * k, dbh, idesc, (c | k) != 0);
           mma_bf16_ts(tmem, alo + 8 * k, dbh, idesc, 1);
           mma_bf16_ts(tmem, ahi + 8 * k, dbl, idesc, 1);
+          if (n2 > 0) {
+            const uint32_t off = static_cast<uint32_t>(n1) * 128u;  // B rows past 256 (1 KB-aligned 8-row groups)
+            const uint64_t dbh2 = desc_sw128(braw + b * b_blk_bytes + off + kk * 32, 16, 1024);
+            const uint64_t dbl2 = desc_sw128(braw + b * b_blk_bytes + off + 64 + kk * 32, 16, 1024);
+            mma_bf16_ts(tmem + n1, ahi + 8 * k, dbh2, idesc2, (c | k) != 0);
+            mma_bf16_ts(tmem + n1, alo + 8 * k, dbh2, idesc2, 1);
+            mma_bf16_ts(tmem + n1, ahi + 8 * k, dbl2, idesc2, 1);
+          }
         }
         mma_commit(&t_free[st]);
         if (c == nchunks - 1) mma_commit(tfull);
@@ -510,7 +522,7 @@ struct WGrid {
 WGrid weight_grid(const TcWeightPlan& tw, int64_t n, int64_t plane) {
   WGrid g{};
   g.blk = tw.nw <= 128 ? 2 : 1;
-  g.acol0 = tw.nw <= 128 ? 128 : 256;
+  g.acol0 = tw.nw <= 128 ? 128 : (tw.nw <= 256 ? 256 : 384);
   constexpr int kBudget = 227 * 1024 - 1024 - 1024;
   // Keep >= 2 dy stages: shed x/TMEM stages first, then halve the stage width
   // (nw = 128 with 2-atom stages needs 64 KB per x stage).
