@@ -531,6 +531,31 @@ def run_ours(args):
         except Exception as ex:  # reported, never required for the headline
             compositions = {"error": str(ex)[:200]}
 
+    # ---- BASELINE config C5 (the design-space sweep), a representative subset
+    # timed in this run: cg=4, co=50 % at every (C, H x W) -- the full 54-shape
+    # sweep is scripts/sweep.py (profiles/*_sweep_c5.json)
+    c5 = None
+    if rank == 0 and ws == 1 and not args.no_c5 and args.workload == "c1":
+        try:
+            sys.path.insert(0, os.path.join(ROOT, "scripts"))
+            import sweep as c5sweep
+            hbm_peak, _ = c5sweep.peaks()
+            rows = []
+            st5 = torch.cuda.Stream()
+            for hw in (56, 14):
+                for c in (256, 512, 1024):
+                    r = c5sweep.run_shape(c, 4, 50, hw, 32, _lib.lib(), st5)
+                    r["hbm_frac_step"] = round(r["gbs"]["step"] / hbm_peak, 4)
+                    rows.append({k: r[k] for k in ("C", "hw", "cg", "co", "gw", "us", "gbs", "hbm_frac_step")})
+                    torch.cuda.empty_cache()
+            fr = sorted(r["hbm_frac_step"] for r in rows)
+            c5 = {"subset": "C in {256,512,1024} x H=W in {56,14}, cg=4, co=50%, N=32; fwd / bwd / step "
+                            "= forward, scc_backward_f32, both (CUDA graphs of 8 calls, inputs > 3x L2)",
+                  "rows": rows, "hbm_frac_step_median": round((fr[2] + fr[3]) / 2, 4),
+                  "hbm_frac_step_min": fr[0], "hbm_frac_step_max": fr[-1]}
+        except Exception as ex:  # reported, never required for the headline
+            c5 = {"error": str(ex)[:200]}
+
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
         try:
@@ -561,6 +586,7 @@ def run_ours(args):
             "gpu_launches": int(launches),
             "models": models,
             "compositions": compositions,
+            "c5": c5,
             "clocks": clocks,
         }
         print(json.dumps(line), flush=True)
@@ -583,6 +609,7 @@ def main():
     ap.add_argument("--no-models", action="store_true", help="skip the SCC-ResNet-18/VGG16 images/sec")
     ap.add_argument("--no-compositions", action="store_true",
                     help="skip the stock-operator (paper 'Base') composition timings")
+    ap.add_argument("--no-c5", action="store_true", help="skip the C5 sweep subset")
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--no-traffic", action="store_true", help="skip the ncu DRAM-traffic pass")
     args = ap.parse_args()

@@ -4,7 +4,7 @@
 out=$1; shift
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum \
     --clock-control none -k regex:'scc|band|weight|tc_' -c 40 --csv --log-file "$out" \
-    python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu-baseline --no-models "$@" > /dev/null 2>&1
+    python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu-baseline --no-models --no-c5 "$@" > /dev/null 2>&1
 python - "$out" <<'PY'
 import csv, sys, collections
 rows = [r for r in csv.reader(open(sys.argv[1])) if len(r) > 10 and r[0].isdigit()]

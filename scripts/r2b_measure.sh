@@ -9,7 +9,7 @@ timeout 300 python bench.py --impl reference --steps 10 --warmup 3 > gpurun_out/
 scripts/ncu_launches.sh gpurun_out/launches.csv --no-graph --no-traffic --no-compositions > gpurun_out/launches.txt 2>&1; cat gpurun_out/launches.txt
 for k in tc_bwd_kernel tc_band2_kernel; do
   timeout 300 ncu --set full --clock-control none --import-source on -k regex:"$k" -s 3 -c 1 -o gpurun_out/prof_$k -f \
-    python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu-baseline --no-models --no-graph --no-traffic --no-compositions > /dev/null 2>&1
+    python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu-baseline --no-models --no-graph --no-traffic --no-compositions --no-c5 > /dev/null 2>&1
   ls gpurun_out/prof_$k.ncu-rep
 done
 S=256,256,2,50%,32,56,56
