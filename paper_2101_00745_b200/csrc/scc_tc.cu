@@ -45,10 +45,16 @@ using namespace sm100;
 // 5 MMA first stage converted, 6.. per tile (up to 8): MMA commit of tile i
 // at 6+2i, epilogue done with tile i at 7+2i, 30 end.
 __device__ unsigned long long g_trace[32];
+#if defined(SCC_TRACE)
 #define TRACE(slot)                                           \
   do {                                                        \
     if (blockIdx.x == 0) g_trace[(slot)] = globaltimer();     \
   } while (0)
+#else
+#define TRACE(slot) \
+  do {              \
+  } while (0)
+#endif
 
 constexpr int kTcThreads = 352;  // 11 warps: + a streamed-panel producer
 constexpr int KC = 32;          // ring positions per pipeline stage (4 k-steps of 8)

@@ -35,10 +35,16 @@ using namespace sm100;
 // (i<8), 10+i converter done with chunk i, 18+i MMA committed chunk i,
 // 26 epilogue done.
 __device__ unsigned long long g_wtrace[32];
+#if defined(SCC_TRACE)
 #define WTRACE(slot)                                            \
   do {                                                          \
     if (blockIdx.x == 0) g_wtrace[(slot)] = globaltimer();      \
   } while (0)
+#else
+#define WTRACE(slot) \
+  do {               \
+  } while (0)
+#endif
 
 constexpr int kThreads = 352;  // 11 warps: dy loads from warp 0, x loads from warp 10
 constexpr int kAtom = 32;              // pixels per SWIZZLE_128B atom (128 B)

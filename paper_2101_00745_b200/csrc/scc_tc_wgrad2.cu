@@ -45,10 +45,23 @@ using namespace sm100;
 
 __device__ unsigned long long g_w2trace[64];
 __device__ unsigned long long g_w2cta[3 * 256];  // per CTA: start, accfull, barrier arrival
+#if defined(SCC_TRACE)
 #define W2T(slot)                                              \
   do {                                                         \
     if (blockIdx.x == 0) g_w2trace[(slot)] = globaltimer();    \
   } while (0)
+#define W2CTA(k)                                                            \
+  do {                                                                      \
+    if (blockIdx.x < 256) g_w2cta[3 * blockIdx.x + (k)] = globaltimer();    \
+  } while (0)
+#else
+#define W2T(slot) \
+  do {            \
+  } while (0)
+#define W2CTA(k) \
+  do {           \
+  } while (0)
+#endif
 
 constexpr int kThreads = 384;
 constexpr int kDyBytes = 128 * 128;   // [128 rows][32 px]
@@ -143,7 +156,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     W2T(0);
-    if (blockIdx.x < 256) g_w2cta[3 * blockIdx.x] = globaltimer();
+    W2CTA(0);
     for (int s = 0; s < kMaxStages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&sfree[s], 5);
@@ -373,7 +386,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_after();
         if (i == 0) {
           W2T(34);
-          if (blockIdx.x < 256) g_w2cta[3 * blockIdx.x + 1] = globaltimer();
+          W2CTA(1);
         }
         // own TMEM row (lane = tile row) -> own smem dump row
         for (int c0 = 0; c0 < a.xr; c0 += 32) {
@@ -426,7 +439,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   }
 
-  if (threadIdx.x == 0 && blockIdx.x < 256) g_w2cta[3 * blockIdx.x + 2] = globaltimer();
+  if (threadIdx.x == 0) W2CTA(2);
   tc_fence_before();
   __syncthreads();
   if (warp == 1) tmem_dealloc<512>(tmem);

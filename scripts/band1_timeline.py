@@ -20,6 +20,8 @@ buf = (C.c_uint64 * 32)()
 L.scc_debug_trace(buf, 32)
 t = [buf[i] for i in range(32)]
 t0 = t[0]
+if t0 == 0:
+    sys.exit("no trace: build with make -C paper_2101_00745_b200/csrc SCC_EXTRA=-DSCC_TRACE and load it via SCC_LIB_PATH")
 lab = {0: "start", 1: "setup", 2: "p_first_tma", 3: "p_dep", 4: "conv_first_landed", 5: "mma_first_conv", 30: "end"}
 for i in range(8):
     lab[6 + 2 * i] = f"mma_commit{i}"; lab[7 + 2 * i] = f"epi_done{i}"

@@ -22,6 +22,8 @@ buf = (C.c_uint64 * 64)()
 L.scc_debug_trace(buf, 64)
 t = [buf[32 + i] for i in range(32)]
 t0 = t[0]
+if t0 == 0:
+    sys.exit("no trace: build with make -C paper_2101_00745_b200/csrc SCC_EXTRA=-DSCC_TRACE and load it via SCC_LIB_PATH")
 lab = {0: "start", 1: "setup", 26: "epi_done", 27: "p_wait_afree", 28: "p_afree_ok", 29: "p_dy_issued", 30: "p_tfree_ok", 31: "p_x_issued"}
 for i in range(8):
     lab[2 + i] = f"issued{i}"; lab[10 + i] = f"conv{i}"; lab[18 + i] = f"mma{i}"
