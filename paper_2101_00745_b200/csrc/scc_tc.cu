@@ -76,7 +76,7 @@ struct TcCfg {
   static_assert(kACol0 + kTStages * 2 * KC <= kTmemCols, "TMEM budget");
   static constexpr int kStoreBytes = 4 * 2 * 32 * 32 * 4;  // 4 warps x 2 bufs x [32 rows][32 px]
   static constexpr int kMaxAStages = 8;
-  static constexpr int kMaxBStages = 4;
+  static constexpr int kMaxBStages = 8;
 };
 
 // Shared-memory plan of one launch (host computes, kernel re-derives).
@@ -292,11 +292,12 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       for (int64_t t = blockIdx.x; t < total; t += gridDim.x) {
         const int rt = static_cast<int>(t % a.n_rt);
         const int nch = chunks_of(a, rt);
+        const float* prow = a.panel + pofs(rt);
         for (int c = 0; c < nch; ++c) {
           mbar_wait_tag(&b_free[sb], pb ^ 1u, 2);
           mbar_expect_tx(&b_full[sb], C::kBBytes);
           bulk_load(b_base + sb * C::kBBytes,
-                    a.panel + pofs(rt) + static_cast<int64_t>(c) * (C::kBBytes / 4),
+                    prow + static_cast<int64_t>(c) * (C::kBBytes / 4),
                     C::kBBytes, &b_full[sb]);
           advance(sb, pb, SB);
         }
@@ -316,6 +317,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       const int rt = static_cast<int>(t % a.n_rt);
       const int nk8 = a.rt_info[4 * rt + 1];
       const int nch = (nk8 + 3) / 4;
+      const int prt = a.sm.b_resident == 1 ? pofs(rt) : 0;  // (global loads once per tile)
       mbar_wait_tag(&tempty[acc], acc_phase ^ 1u, 4);
       tc_fence_after();
       const uint32_t d_tmem = tmem + acc * C::kAccCols;
@@ -323,7 +325,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         mbar_wait_tag(&conv[st], ps, 5);
         uint8_t* bimg;
         if (a.sm.b_resident == 1) {
-          bimg = b_base + (pofs(rt) + c * (C::kBBytes / 4)) * 4;
+          bimg = b_base + (prt + c * (C::kBBytes / 4)) * 4;
         } else if (a.sm.b_resident == 2) {
           bimg = b_base + c * C::kBBytes;
         } else {
@@ -384,7 +386,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     int st = 0;
     uint32_t ps = 0;
     for (int64_t t = blockIdx.x; t < total; t += gridDim.x) {
-      const int nch = chunks_of(a, static_cast<int>(t % a.n_rt));
+      const int nk8 = a.rt_info[4 * static_cast<int>(t % a.n_rt) + 1];  // once per tile
+      const int nch = (nk8 + 3) / 4;
       for (int c = 0; c < nch; ++c) {
         mbar_wait_tag(&a_full[sa], pa, 7);
         if (t == blockIdx.x && c == 0 && q == 0 && lane == 0) TRACE(4);
@@ -393,7 +396,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         if (BF) {
           // bf16 pairs (ring rows 2i, 2i+1); rows past the chunk's last k8 step
           // are zero (an odd step count leaves half a K = 16 step)
-          const int rows = 8 * min(4, a.rt_info[4 * static_cast<int>(t % a.n_rt) + 1] - 4 * c);
+          const int rows = 8 * min(4, nk8 - 4 * c);
           float v[KC];
 #pragma unroll
           for (int k = 0; k < KC; ++k) v[k] = lds_f32(src + 4u * k * TM);
@@ -727,9 +730,13 @@ static cudaError_t launch_tc_nt(const TcBandPlan& tp, const TcDeviceTables& dt,
         sm.b_stages = 1;
         grid = grid_rt;
       } else {
+        // Streamed panel ring: one chunk image per MMA stage from L2, so its
+        // depth x (L2 latency) bounds the MMA rate.  bf16 chunk images are
+        // half the bytes: twice the depth in the same shared memory (3 tf32
+        // stages kept the tensor pipe ~52 % busy at C=1024 cg=2 56x56).
         sm.b_resident = 0;
         sm.b_bytes = C::kBBytes;
-        sm.b_stages = 3;
+        sm.b_stages = BF ? 6 : 3;
       }
     }
     const int b_total = sm.b_resident ? sm.b_bytes : sm.b_stages * C::kBBytes;
