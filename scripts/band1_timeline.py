@@ -12,9 +12,10 @@ f = os.environ.get("SCC_SHAPE", "256,256,2,50%,32,56,56").split(",")
 CI, CO, CG, OV, N, H, W = int(f[0]), int(f[1]), int(f[2]), f[3], int(f[4]), int(f[5]), int(f[6])
 cfg = scc.scc_config_new(CI, CO, CG, OV, True)
 x = torch.randn(N, CI, H, W, device="cuda")
+dy = torch.randn(N, CO, H, W, device="cuda")
 wts = scc.scc_weights_init(cfg)
-for _ in range(3):
-    y = scc.scc_forward(x, wts, cfg)
+for _ in range(3):  # OP=bdata: backward-data (the same kernel, bf16x3)
+    y = scc.scc_backward_input(dy, wts, cfg) if os.environ.get("OP") == "bdata" else scc.scc_forward(x, wts, cfg)
 torch.cuda.synchronize()
 buf = (C.c_uint64 * 32)()
 L.scc_debug_trace(buf, 32)
