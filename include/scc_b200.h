@@ -222,6 +222,18 @@ scc_status_t scc_dsc_forward_f32(const scc_plan_t* plan, int64_t n, int64_t h, i
                                  const float* dw_bias, const float* weight, const float* bias,
                                  float* y, void* stream);
 
+/* dsc_block forward that also returns t = DW3x3(x) (the SCC stage's input,
+ * which the block's backward needs): y = SCC(t).  For stride 1 on 16- or
+ * 32-wide images (planes a multiple of 128 px) whose SCC layer is one
+ * tensor-core row tile over every input channel, one kernel computes t in
+ * its staging step (the depthwise output goes to HBM once, as t, and is
+ * never read back); otherwise the depthwise kernel then
+ * scc_forward_f32.  t: [n][c_in][h_out][w_out]. */
+scc_status_t scc_dsc_forward_t_f32(const scc_plan_t* plan, int64_t n, int64_t h, int64_t w,
+                                   int64_t stride, const float* x, const float* dw_weight,
+                                   const float* dw_bias, const float* weight, const float* bias,
+                                   float* y, float* t, void* stream);
+
 /* ---- depthwise 3x3 stage of a dsc_block (model.cpp:213-220) -------------- */
 /* groups = c, kernel 3, padding 1, stride 1 or 2 (conv_forward_impl,
  * reference.cpp:74-123).  x: [n][c][h][w]; weight: [c][3][3]; bias: [c] or

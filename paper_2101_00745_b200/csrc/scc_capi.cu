@@ -1107,6 +1107,49 @@ scc_status_t scc_dsc_forward_f32(const scc_plan_t* plan, int64_t n, int64_t h, i
   });
 }
 
+scc_status_t scc_dsc_forward_t_f32(const scc_plan_t* plan, int64_t n, int64_t h, int64_t w,
+                                   int64_t stride, const float* x, const float* dw_weight,
+                                   const float* dw_bias, const float* weight, const float* bias,
+                                   float* y, float* t, void* stream) {
+  return guard([&] {
+    scc::check_ptr(plan, "plan");
+    scc::check_extents(n, h, w);
+    scc::check_ptr(x, "x");
+    scc::check_ptr(dw_weight, "dw_weight");
+    scc::check_ptr(weight, "weight");
+    scc::check_ptr(y, "y");
+    scc::check_ptr(t, "t");
+    auto& p = *const_cast<scc_plan_t*>(plan);
+    scc::check_bias(p, bias, "bias");
+    if (stride != 1 && stride != 2) {
+      scc::fail(SCC_ERR_ARGUMENT, "depthwise stride must be 1 or 2, got " + std::to_string(stride));
+    }
+    const int64_t ho = (h - 1) / stride + 1, wo = (w - 1) / stride + 1;
+    const cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const int32_t ci = static_cast<int32_t>(p.cfg.c_in), co = static_cast<int32_t>(p.cfg.c_out);
+    // One tensor-core kernel when the geometry allows (stride 1, 16- or
+    // 32-wide images, one row tile over every channel): the depthwise stage
+    // runs in the SCC kernel's converters and t is stored on the way.
+    if (stride == 1 && p.path != SCC_PATH_CUDA_CORE && p.path != SCC_PATH_TENSOR_STREAMED &&
+        scc::aligned16(x) && scc::aligned16(y) && scc::aligned16(t) &&
+        scc::choose_path(p, n, h, w, 0) == SCC_PATH_TENSOR &&
+        scc::tc_dsc2_supported(p.tc_fwd, h * w, w, ci, co) && n * ci * h * w < (int64_t(1) << 31)) {
+      const scc::DeviceTables& tb = scc::tables(p);
+      scc::TcBandCall c = scc::tc_call(p, false, n, h * w, x, y, weight, bias);
+      c.dsc_w = dw_weight;
+      c.dsc_b = dw_bias;
+      c.dsc_t = t;
+      c.img_w = static_cast<int32_t>(w);
+      scc::cuda_check(scc::launch_band_tc2(p.tc_fwd, tb.tc_fwd, c, p.cfg.shift, co, s), "dsc forward (tensor) launch");
+      return;
+    }
+    // otherwise the pair: depthwise kernel into t, then the SCC forward on t
+    const scc_status_t st = scc_dw3x3_forward_f32(n, ci, h, w, stride, x, dw_weight, dw_bias, t, stream);
+    if (st != SCC_OK) scc::fail(st, scc::g_err);
+    scc::do_forward(p, n, ho, wo, t, weight, bias, y, s);
+  });
+}
+
 namespace scc {
 namespace {
 DwArgs dw_args(int64_t n, int64_t c, int64_t h, int64_t w, int64_t stride) {

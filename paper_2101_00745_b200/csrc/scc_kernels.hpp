@@ -71,7 +71,18 @@ struct TcBandCall {
   bool backward_data;
   float* panel;         // scratch for the band weight images (tc_panel_bytes)
   int32_t max_ctas = 0; // grid cap (0 = one CTA per SM); the concurrent backward splits the SMs
+  // fused dsc_block forward (generation-2 kernel only): `in` is the block
+  // input x, the converters compute t = DW3x3(x) (stride 1, padding 1) from a
+  // haloed stage, feed it to the SCC GEMM and (if dsc_t) store it
+  const float* dsc_w = nullptr;  // [c_in][3][3], nullptr: plain SCC forward
+  const float* dsc_b = nullptr;  // [c_in] or nullptr
+  float* dsc_t = nullptr;        // [n][c_in][plane] or nullptr
+  int32_t img_w = 0;             // image width (the plane is img_w wide)
 };
+// The fused dsc_block forward on the generation-2 kernel: stride 1, image
+// width 16 / 32 (planes a multiple of 128 px), one row tile whose arc is
+// every input channel exactly once.
+bool tc_dsc2_supported(const TcBandPlan& tp, int64_t plane, int64_t img_w, int32_t c_in, int32_t c_out);
 
 size_t tc_panel_bytes(const TcBandPlan& tp);
 

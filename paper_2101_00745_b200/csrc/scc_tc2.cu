@@ -76,6 +76,11 @@ __device__ unsigned long long g_cta2[2 * 1024];
 #endif
 
 constexpr int kThreads = 384;
+// dsc_block fusion: the depthwise stage quadruples the converters' work, so
+// a second converter set (warps 12..15, same TMEM lane quarters as 4..7)
+// takes the upper 16 rows of every stage
+constexpr int kDscThreads = 512;
+constexpr int kDwStride = 12;                  // depthwise table row: 9 taps, bias, 2 pad (3 x 16 B)
 constexpr int kBlkPx = 32;                     // pixels per block (one 128 B row)
 constexpr int kStageBytes = 32 * 128 * 4;      // [32 ring rows][128 px]
 constexpr int kMaxStages = 8;
@@ -116,6 +121,13 @@ struct Band2Args {
   int32_t total_chunks;
   int32_t units;             // n * nbps
   int64_t plane;
+  // fused dsc_block forward (DSC instantiation): stage rows carry a halo of
+  // one image row (img_w px) before and after the tile's 128 px
+  const float* dsc_w;        // [c_in][9]
+  const float* dsc_b;        // [c_in] or nullptr
+  float* dsc_t;              // [n][c_in][plane] or nullptr
+  int32_t img_w;             // image width = halo
+  int32_t stage_bytes;       // raw stage: 32 rows x (128 + 2 halo) px x 4 B
 };
 
 // This CTA's block range [u, u1) (see TileIter).  Not inlined: every warp
@@ -190,17 +202,20 @@ __device__ __forceinline__ void advance(int& stage, uint32_t& phase, int stages)
 // barriers.
 template <int NT>
 struct Layout {
-  int panel, raw, st, st_warp, rows, bias, bars, total;
-  __host__ __device__ Layout(int total_chunks, int stages, int n_rt, int mode, int tile_bufs, int scratch) {
+  int panel, raw, st, st_warp, rows, bias, dwt, bars, total;
+  // stage_bytes: one raw stage (kStageBytes, or more with the dsc halo);
+  // dw_floats: the dsc_block's depthwise table (c_in x 10) or 0
+  __host__ __device__ Layout(int total_chunks, int stages, int n_rt, int mode, int stage_bytes, int scratch,
+                             int dw_floats = 0) {
     panel = 0;
     raw = panel + total_chunks * 2 * NT * 128;
-    st = raw + stages * kStageBytes;
+    st = raw + stages * stage_bytes;
     st_warp = mode == kStoreRows32 ? kStoreBufs * kStoreBuf : 0;
-    (void)tile_bufs;
     const int stb = 4 * st_warp > scratch ? 4 * st_warp : scratch;
     rows = st + ((stb + 1023) & ~1023);
     bias = rows + 4 * n_rt * NT;
-    bars = bias + 4 * n_rt * NT;
+    dwt = bias + 4 * n_rt * NT;
+    bars = dwt + 4 * ((dw_floats + 3) & ~3);
     total = bars + (2 * kMaxStages + 2 * kTStages + 7) * 8 + 16;
   }
 };
@@ -376,8 +391,8 @@ __device__ __forceinline__ void build_panel_fwd4(const Band2Args& a, uint8_t* pa
   }
 }
 
-template <int NT, bool BWD>
-__global__ void __launch_bounds__(kThreads, 1)
+template <int NT, bool BWD, bool DSC>
+__global__ void __launch_bounds__(DSC ? kDscThreads : kThreads, 1)
     tc_band2_kernel(const __grid_constant__ CUtensorMap t1, const __grid_constant__ CUtensorMap tout,
                     const __grid_constant__ Band2Args a) {
   constexpr int kPanelChunk = 2 * NT * 128;  // hi + lo image of one 32-k chunk
@@ -385,7 +400,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   // No static shared memory in this kernel: the dynamic window starts
   // 1024-aligned and every derived pointer stays in the shared address space.
   extern __shared__ __align__(1024) uint8_t smem[];
-  const Layout<NT> L(a.total_chunks, a.stages, a.n_rt, a.store_mode, 0, a.scratch);
+  static_assert(!(BWD && DSC), "the dsc_block fusion is a forward");
+  const Layout<NT> L(a.total_chunks, a.stages, a.n_rt, a.store_mode, a.stage_bytes, a.scratch,
+                     DSC ? kDwStride * a.c_in : 0);
   uint8_t* panel = smem + L.panel;
   uint8_t* raw = smem + L.raw;
   uint8_t* stbuf = smem + L.st;
@@ -414,9 +431,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int i = threadIdx.x;
     if (i < kMaxStages) {
       mbar_init(&full[i], 1);
-      mbar_init(&afree[i], 4);
+      mbar_init(&afree[i], DSC ? 8 : 4);
     } else if (i < kMaxStages + kTStages) {
-      mbar_init(&conv[i - kMaxStages], 4);
+      mbar_init(&conv[i - kMaxStages], DSC ? 8 : 4);
       mbar_init(&tfree[i - kMaxStages], 1);
     } else if (i < kMaxStages + kTStages + 2) {
       mbar_init(&tfull[i - kMaxStages - kTStages], 1);
@@ -485,15 +502,20 @@ __global__ void __launch_bounds__(kThreads, 1)
             // One box {128 px, rb rows} per rb rows: stage = [32 rows][128 px].
             // A partial tile over-reads the neighbour's pixels (or zero-fills
             // past the end of the sample); the epilogue never stores them.
-            if (lane == 0) mbar_expect_tx(&full[s], rows * 512);
+            // (dsc: rows of 128 + 2 halo px from one image row before the
+            // tile; out-of-sample pixels are zero-filled by TMA -- the
+            // depthwise stage's top / bottom padding)
+            const int rowb = DSC ? a.stage_bytes / 32 : 512;
+            if (lane == 0) mbar_expect_tx(&full[s], rows * rowb);
             __syncwarp();
-            uint8_t* st = raw + s * kStageBytes;
+            uint8_t* st = raw + s * a.stage_bytes;
             const int r = lane * a.rb;
             if (r < rows) {
               int pos = start8 + 32 * c + r;
               while (pos >= a.ring) pos -= a.ring;
               const int cl = pos / a.cls, j = pos - cl * a.cls;
-              tma_load_4d(st + r * 512, &t1, &full[s], it.b0 * kBlkPx, j, a.class_d[cl], it.n);
+              tma_load_4d(st + r * rowb, &t1, &full[s], it.b0 * kBlkPx - (DSC ? a.img_w : 0), j, a.class_d[cl],
+                          it.n);
             }
             __syncwarp();
             if (c == 0 && lane == 0) TRACE2(2);
@@ -548,7 +570,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else {
-    if (warp < 4 || warp >= 8) {
+    if (warp < 4 || (warp >= 8 && warp < 12)) {
       // ---------------- panel build (warps 2, 3, 8..11; the converters start at once) ----------------
       const int ct = warp < 4 ? threadIdx.x - 64 : threadIdx.x - 192;  // 0..191
       cudaGridDependencySynchronize();  // W may come from the previous kernel
@@ -572,6 +594,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         else
           build_panel<NT, false>(a, panel, rows_s, a.weight, a.starts, a.perm, ct);
       }
+      if constexpr (DSC) {
+        // the dsc_block's depthwise taps and bias, [c_in][12] (converters)
+        float* dwt = reinterpret_cast<float*>(smem + L.dwt);
+        for (int i = ct; i < kDwStride * a.c_in; i += kWorkers) {
+          const int ch = i / kDwStride, k = i - kDwStride * ch;
+          dwt[i] = k < 9 ? __ldg(a.dsc_w + 9 * ch + k) : (k == 9 && a.dsc_b != nullptr ? __ldg(a.dsc_b + ch) : 0.f);
+        }
+      }
       fence_proxy_async_smem();
       named_bar_sync(1, kWorkers);
       if (ct == 0) {
@@ -579,14 +609,23 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_arrive(panel_bar);
       }
     }
-    if (warp >= 4 && warp < 8) {
+    if ((warp >= 4 && warp < 8) || warp >= 12) {
       // ---------------- converters: raw [row][px] -> TMEM [px lane][row] hi / lo ----------------
       const int q = warp & 3;  // pixel block of the tile = TMEM lane quarter
+      const int half = warp >= 12 ? 1 : 0;  // dsc: rows 16 * half .. + 15 of each stage
       const uint32_t lane_base = static_cast<uint32_t>(q * 32) << 16;
       int s = 0, st = 0;
       uint32_t ph = 0, tph = 0;
+      const float* dwt = reinterpret_cast<const float*>(smem + L.dwt);
+      if (DSC) mbar_wait(panel_bar, 0);  // the depthwise table is staged with the panel
       TileIter it(a);
       while (it.next()) {
+        // dsc: this lane's pixel and its column masks (the depthwise stage's
+        // left / right padding; rows come zero-filled from TMA)
+        const int pix = it.b0 * kBlkPx + q * 32 + lane;
+        const bool pv = q < it.cnt && pix < a.plane;
+        const int col = DSC ? (pix & (a.img_w - 1)) : 0;
+        const float vl = col > 0 ? 1.f : 0.f, vr = col < a.img_w - 1 ? 1.f : 0.f;
         for (int rt = 0; rt < a.n_rt; ++rt) {
           const int nk8 = a.rt_nk8[rt];
           const int nch = (nk8 + 3) >> 2;
@@ -595,22 +634,63 @@ __global__ void __launch_bounds__(kThreads, 1)
             // Element (row r, pixel 32q + lane) of the [32 rows][128 px] stage.
             // Rows past the chunk's k-steps hold stale data that lands in TMEM
             // columns the MMAs never read.
-            const float* src = reinterpret_cast<const float*>(raw + s * kStageBytes) + q * 32 + lane;
-            uint32_t hi[32], lo[32];
+            if constexpr (DSC) {
+              // t = DW3x3(x) for ring rows (channels, n_class == 1: channel =
+              // ring position) 32c + 16 half.., from the haloed stage; t is
+              // also the block's stored activation (the backward's SCC input)
+              uint32_t hi[16], lo[16];
+              const int W = a.img_w, SW = 128 + 2 * W;
+              const float* src = reinterpret_cast<const float*>(raw + s * a.stage_bytes) + (16 * half) * SW + W +
+                                 q * 32 + lane;
+              const int ch0 = a.rt_start8[rt] + 32 * c + 16 * half;
+              const int rows = min(4, nk8 - 4 * c) * 8 - 16 * half;
+              float* tdst = a.dsc_t != nullptr ? a.dsc_t + (static_cast<int64_t>(it.n) * a.c_in + ch0) * a.plane + pix
+                                               : nullptr;
 #pragma unroll
-            for (int r = 0; r < 32; ++r) {
-              const float v = src[r * 128];
-              const float h = tf32_hi(v);
-              hi[r] = __float_as_uint(h);
-              lo[r] = __float_as_uint(v - h);
+              for (int r = 0; r < 16; ++r) {
+                const float* x0 = src + r * SW;
+                const float4* w4 = reinterpret_cast<const float4*>(dwt + kDwStride * min(ch0 + r, a.c_in - 1));
+                const float4 wa = w4[0], wb = w4[1], wc = w4[2];
+                float v = wc.y;
+                v = fmaf(wa.x * vl, x0[-W - 1], v);
+                v = fmaf(wa.y, x0[-W], v);
+                v = fmaf(wa.z * vr, x0[-W + 1], v);
+                v = fmaf(wa.w * vl, x0[-1], v);
+                v = fmaf(wb.x, x0[0], v);
+                v = fmaf(wb.y * vr, x0[1], v);
+                v = fmaf(wb.z * vl, x0[W - 1], v);
+                v = fmaf(wb.w, x0[W], v);
+                v = fmaf(wc.x * vr, x0[W + 1], v);
+                if (tdst != nullptr && pv && r < rows) __stcs(tdst + static_cast<int64_t>(r) * a.plane, v);
+                const float h = tf32_hi(v);
+                hi[r] = __float_as_uint(h);
+                lo[r] = __float_as_uint(v - h);
+              }
+              __syncwarp();
+              if (lane == 0) mbar_arrive(&afree[s]);
+              mbar_wait(&tfree[st], tph ^ 1u);
+              tc_fence_after();
+              const uint32_t col = tmem + kACol0 + st * 64 + lane_base + 16 * half;
+              tmem_st16(col, hi);
+              tmem_st16(col + 32, lo);
+            } else {
+              uint32_t hi[32], lo[32];
+              const float* src = reinterpret_cast<const float*>(raw + s * kStageBytes) + q * 32 + lane;
+#pragma unroll
+              for (int r = 0; r < 32; ++r) {
+                const float v = src[r * 128];
+                const float h = tf32_hi(v);
+                hi[r] = __float_as_uint(h);
+                lo[r] = __float_as_uint(v - h);
+              }
+              __syncwarp();
+              if (lane == 0) mbar_arrive(&afree[s]);
+              mbar_wait(&tfree[st], tph ^ 1u);
+              tc_fence_after();
+              const uint32_t col = tmem + kACol0 + st * 64 + lane_base;
+              tmem_st32(col, hi);
+              tmem_st32(col + 32, lo);
             }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&afree[s]);
-            mbar_wait(&tfree[st], tph ^ 1u);
-            tc_fence_after();
-            const uint32_t col = tmem + kACol0 + st * 64 + lane_base;
-            tmem_st32(col, hi);
-            tmem_st32(col + 32, lo);
             tmem_st_wait();
             tc_fence_before();
             __syncwarp();
@@ -621,7 +701,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
-    if (warp >= 8) {
+    if (warp >= 8 && warp < 12) {
       // ---------------- epilogue (warps 8..11) ----------------
       const int et = threadIdx.x - 256;  // 0..127
       for (int i = et; i < a.n_rt * NT; i += 128) {
@@ -706,27 +786,29 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 template <int NT>
-int band2_stages(const TcBandPlan& tp, int mode, int tile_bufs, int scratch) {
+int band2_stages(const TcBandPlan& tp, int mode, int stage_bytes, int scratch, int dw_floats = 0) {
   int st = kMaxStages;
   while (st >= 2 &&
-         1024 + Layout<NT>(tp.total_chunks, st, tp.n_rt, mode, tile_bufs, scratch).total > kSmemLimit)
+         1024 + Layout<NT>(tp.total_chunks, st, tp.n_rt, mode, stage_bytes, scratch, dw_floats).total > kSmemLimit)
     --st;
   return st;
 }
 
-template <int NT, bool BWD>
+template <int NT, bool BWD, bool DSC>
 cudaError_t launch_tc2_nt(const TcBandPlan& tp, const TcDeviceTables& dt, const TcBandCall& call,
                           int64_t shift, int32_t c_out, cudaStream_t s) {
   const int64_t P = call.plane;
   const int32_t C = tp.cls * tp.n_class;  // channels of the activation tensor
-  // Activations {P, cls, n_class, N}, box {128 px, rb rows}, no swizzle.
+  // Activations {P, cls, n_class, N}, box {128 px (+ 2 halo rows of the
+  // image: dsc), rb rows}, no swizzle.
+  const int halo = DSC ? call.img_w : 0;
   CUtensorMap t1;
   {
     const uint64_t dims[4] = {static_cast<uint64_t>(P), static_cast<uint64_t>(tp.cls),
                               static_cast<uint64_t>(tp.n_class), static_cast<uint64_t>(call.n)};
     const uint64_t strides[3] = {static_cast<uint64_t>(tp.n_class) * P * 4, static_cast<uint64_t>(P) * 4,
                                  static_cast<uint64_t>(C) * P * 4};
-    const uint32_t box[4] = {128, static_cast<uint32_t>(tp.rb), 1, 1};
+    const uint32_t box[4] = {static_cast<uint32_t>(128 + 2 * halo), static_cast<uint32_t>(tp.rb), 1, 1};
     if (!encode_f32(&t1, call.in, 4, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_NONE))
       return cudaErrorInvalidValue;
   }
@@ -792,13 +874,20 @@ cudaError_t launch_tc2_nt(const TcBandPlan& tp, const TcDeviceTables& dt, const 
     // multiples of 4 when shift and c_in are
     a.fwd4 = (!BWD && a.w_staged && call.gw % 4 == 0 && call.c_in % 4 == 0 && shift % 4 == 0) ? 1 : 0;
   }
-  a.stages = band2_stages<NT>(tp, a.store_mode, 0, a.scratch);
+  a.stage_bytes = 32 * (128 + 2 * halo) * 4;
+  a.dsc_w = call.dsc_w;
+  a.dsc_b = call.dsc_b;
+  a.dsc_t = call.dsc_t;
+  a.img_w = call.img_w;
+  const int dw_floats = DSC ? kDwStride * call.c_in : 0;
+  a.stages = band2_stages<NT>(tp, a.store_mode, a.stage_bytes, a.scratch, dw_floats);
+  if (a.stages < 3) return cudaErrorInvalidValue;
   a.plane = P;
   const int64_t units = call.n * a.nbps;
   if (units > (1ll << 30)) return cudaErrorInvalidValue;
   a.units = static_cast<int32_t>(units);
   const int smem =
-      1024 + Layout<NT>(a.total_chunks, a.stages, a.n_rt, a.store_mode, 0, a.scratch).total;
+      1024 + Layout<NT>(a.total_chunks, a.stages, a.n_rt, a.store_mode, a.stage_bytes, a.scratch, dw_floats).total;
 
   static int nsm_cache[64] = {0};
   static bool attr_set[64] = {false};
@@ -812,7 +901,7 @@ cudaError_t launch_tc2_nt(const TcBandPlan& tp, const TcDeviceTables& dt, const 
     if (dev >= 0 && dev < 64) nsm_cache[dev] = nsm;
   }
   if (dev < 0 || dev >= 64 || !attr_set[dev]) {
-    cudaError_t e = cudaFuncSetAttribute(tc_band2_kernel<NT, BWD>,
+    cudaError_t e = cudaFuncSetAttribute(tc_band2_kernel<NT, BWD, DSC>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit);
     if (e != cudaSuccess) return e;
     if (dev >= 0 && dev < 64) attr_set[dev] = true;
@@ -820,7 +909,7 @@ cudaError_t launch_tc2_nt(const TcBandPlan& tp, const TcDeviceTables& dt, const 
   cudaLaunchConfig_t cfg{};
   const int64_t cap = call.max_ctas > 0 ? std::min(call.max_ctas, nsm) : nsm;
   cfg.gridDim = dim3(static_cast<unsigned>(std::min<int64_t>(a.units, cap)));
-  cfg.blockDim = dim3(kThreads);
+  cfg.blockDim = dim3(DSC ? kDscThreads : kThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
@@ -828,7 +917,7 @@ cudaError_t launch_tc2_nt(const TcBandPlan& tp, const TcDeviceTables& dt, const 
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, tc_band2_kernel<NT, BWD>, t1, tout, a);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, tc_band2_kernel<NT, BWD, DSC>, t1, tout, a);
   if (e != cudaSuccess) return e;
   note_launches(1);
   return cudaSuccess;
@@ -841,21 +930,43 @@ bool tc_band2_supported(const TcBandPlan& tp, int64_t plane, int32_t c_out) {
   if (!tp.ok || plane % 4 != 0 || plane < 4) return false;
   if (tp.rb % 8 != 0 || tp.n_rt > kMaxRt || tp.n_class > kMaxCls) return false;
   // The whole panel stays resident next to >= 4 raw stages.
-  const int st = tp.nt == 128 ? band2_stages<128>(tp, kStoreRows32, 0, kMaxScratch)
-                               : band2_stages<64>(tp, kStoreRows32, 0, kMaxScratch);
+  const int st = tp.nt == 128 ? band2_stages<128>(tp, kStoreRows32, kStageBytes, kMaxScratch)
+                               : band2_stages<64>(tp, kStoreRows32, kStageBytes, kMaxScratch);
   return st >= 4;
+}
+
+bool tc_dsc2_supported(const TcBandPlan& tp, int64_t plane, int64_t img_w, int32_t c_in, int32_t c_out) {
+  if (!tc_band2_supported(tp, plane, c_out)) return false;
+  // (widths 16 and 32: every tile starts at an image column 0 and ends at
+  // column w - 1, so a halo of exactly one image row covers every tap)
+  if (!(img_w == 16 || img_w == 32) || plane % 128 != 0 || plane % img_w != 0) return false;
+  // one row tile whose arc is every input channel once, ring position =
+  // channel (the converters index the depthwise table by it).  Several row
+  // tiles would each convert their own (overlapping) arc: measured slower
+  // than the depthwise kernel + SCC forward pair (128 -> 128 at 16x16,
+  // N = 128: 32.3 vs 29.0 us, the converters redoing 1.5x the depthwise work)
+  if (tp.n_rt != 1 || tp.n_class != 1 || tp.rt_info.size() < 2 || tp.rt_info[0] != 0 ||
+      tp.rt_info[1] * 8 != c_in || tp.ring != c_in)
+    return false;
+  const int halo_stage = 32 * (128 + 2 * static_cast<int>(img_w)) * 4;
+  const int st = tp.nt == 128 ? band2_stages<128>(tp, kStoreRows32, halo_stage, kMaxScratch, kDwStride * c_in)
+                               : band2_stages<64>(tp, kStoreRows32, halo_stage, kMaxScratch, kDwStride * c_in);
+  return st >= 3;
 }
 
 cudaError_t launch_band_tc2(const TcBandPlan& tp, const TcDeviceTables& dt, const TcBandCall& call,
                             int64_t shift, int32_t c_out, cudaStream_t s) {
-  const bool bwd = call.backward_data;
+  const bool bwd = call.backward_data, dsc = call.dsc_w != nullptr;
+  if (dsc && bwd) return cudaErrorInvalidValue;
   switch (tp.nt) {
     case 64:
-      return bwd ? launch_tc2_nt<64, true>(tp, dt, call, shift, c_out, s)
-                 : launch_tc2_nt<64, false>(tp, dt, call, shift, c_out, s);
+      return bwd ? launch_tc2_nt<64, true, false>(tp, dt, call, shift, c_out, s)
+                 : (dsc ? launch_tc2_nt<64, false, true>(tp, dt, call, shift, c_out, s)
+                        : launch_tc2_nt<64, false, false>(tp, dt, call, shift, c_out, s));
     case 128:
-      return bwd ? launch_tc2_nt<128, true>(tp, dt, call, shift, c_out, s)
-                 : launch_tc2_nt<128, false>(tp, dt, call, shift, c_out, s);
+      return bwd ? launch_tc2_nt<128, true, false>(tp, dt, call, shift, c_out, s)
+                 : (dsc ? launch_tc2_nt<128, false, true>(tp, dt, call, shift, c_out, s)
+                        : launch_tc2_nt<128, false, false>(tp, dt, call, shift, c_out, s));
     default:
       return cudaErrorInvalidValue;
   }

@@ -38,10 +38,13 @@ from .module import DSC2d, SCC2d
 class DSC(DSC2d):
     """dsc_block (model.cpp:213-220): depthwise 3x3 (stride s) then SCC, both
     stages on the libscc_b200 kernels (module.DSC2d; no bias on either stage,
-    BN follows)."""
+    BN follows).  fused=True: on stride-1 16- / 32-wide layers with one SCC
+    row tile the depthwise stage runs inside the SCC tensor-core forward
+    (scc_dsc_forward_t_f32), elsewhere the same pair of kernels as
+    fused=False."""
 
     def __init__(self, cin: int, cout: int, stride: int = 1, cg: int = 2, co="50%", device=None):
-        super().__init__(cin, cout, stride, cg, co, dw_bias=False, bias=False, fused=False, device=device)
+        super().__init__(cin, cout, stride, cg, co, dw_bias=False, bias=False, fused=True, device=device)
 
 
 class BasicBlock(nn.Module):

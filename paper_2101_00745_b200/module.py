@@ -83,8 +83,12 @@ class _DSCFunction(torch.autograd.Function):
     """dsc_block (model.cpp:213-220): y = SCC(DW3x3(x)), every stage on the
     B200 kernels.
 
-    fused=True : forward is scc_dsc_forward_f32 (the DW output lives only in
-                 shared memory); backward recomputes t = DW(x).
+    fused=True : forward is scc_dsc_forward_t_f32: one tensor-core kernel
+                 computes t = DW(x) in its staging step, feeds the SCC GEMM
+                 and stores t for the backward (stride 1, 16- / 32-wide
+                 images, one SCC row tile); other geometries run the
+                 depthwise kernel then the SCC forward -- never slower than
+                 fused=False.
     fused=False: forward is the depthwise kernel then the SCC tensor-core
                  forward, t kept for backward (the reference's
                  Network::backward also keeps stage inputs, model.cpp:306-380).
@@ -95,8 +99,7 @@ class _DSCFunction(torch.autograd.Function):
     def forward(ctx, x, dw_weight, dw_bias, weight, bias, cfg, stride, fused):
         wts = _scc.SccWeights(weight.reshape(-1), bias)
         if fused:
-            y = _scc.dsc_forward(x, dw_weight, dw_bias, wts, cfg, stride)
-            t = None
+            y, t = _scc.dsc_forward_t(x, dw_weight, dw_bias, wts, cfg, stride)
         else:
             t = _scc.dw3x3_forward(x, dw_weight, dw_bias, stride)
             y = _scc.scc_forward(t, wts, cfg)

@@ -319,6 +319,36 @@ def dsc_forward(input: torch.Tensor, dw_weight: torch.Tensor, dw_bias: Optional[
     return y
 
 
+def dsc_forward_t(input: torch.Tensor, dw_weight: torch.Tensor, dw_bias: Optional[torch.Tensor],
+                  wts: SccWeights, cfg: SccConfig, stride: int = 1):
+    """dsc_block forward returning (y, t) with t = DW3x3(input), the SCC
+    stage's input the block's backward needs (scc_dsc_forward_t_f32): one
+    tensor-core kernel when the geometry allows, else the depthwise kernel
+    then scc_forward."""
+    x = _dev4(input, "input")
+    if x.shape[1] != cfg.c_in:
+        raise ShapeError(f"input has {x.shape[1]} channels, config expects {cfg.c_in}")
+    if dw_weight.numel() != cfg.c_in * 9:
+        raise ShapeError(f"depthwise weight has {dw_weight.numel()} entries, needs {cfg.c_in * 9}")
+    if dw_bias is not None and dw_bias.numel() != cfg.c_in:
+        raise ShapeError(f"depthwise bias has {dw_bias.numel()} entries, needs {cfg.c_in}")
+    _check_param(dw_weight, "dw_weight", x.device)
+    _check_param(dw_bias, "dw_bias", x.device)
+    _check_weights(wts, cfg, x.device)
+    n, _, h, w = x.shape
+    ho, wo = (h - 1) // stride + 1, (w - 1) // stride + 1
+    y = torch.empty((n, cfg.c_out, ho, wo), dtype=torch.float32, device=x.device)
+    t = torch.empty((n, cfg.c_in, ho, wo), dtype=torch.float32, device=x.device)
+    dww = dw_weight.contiguous().float()
+    dwb = dw_bias.contiguous().float() if dw_bias is not None else None
+    wt = wts.weight.contiguous()
+    b = wts.bias.contiguous() if wts.bias is not None else None
+    check(lib().scc_dsc_forward_t_f32(cfg.handle, n, h, w, stride, x.data_ptr(), dww.data_ptr(),
+                                      _ptr(dwb), wt.data_ptr(), _ptr(b), y.data_ptr(), t.data_ptr(),
+                                      _stream(x)))
+    return y, t
+
+
 def _dw_out(h: int, w: int, stride: int):
     return (h - 1) // stride + 1, (w - 1) // stride + 1
 

@@ -38,6 +38,9 @@ for ci, co, hw, s in SHAPES:
          "scc_tc_us": round(t_graph(tc), 2)}
     gy = torch.randn_like(t)
     r["dw_ours_us"] = round(t_graph(lambda: scc.dw3x3_forward(x, dw, None, s)), 2)
+    # the training forward: y and t (the SCC backward's input) from one call
+    r["fused_t_us"] = round(t_graph(lambda: scc.dsc_forward_t(x, dw, None, wts, cfg, s)), 2)
+    r["pair_ours_us"] = round(t_graph(lambda: scc.scc_forward(scc.dw3x3_forward(x, dw, None, s), wts, cfg)), 2)
     r["dw_bwd_data_ours_us"] = round(t_graph(lambda: scc.dw3x3_backward_data(gy, dw, (hw, hw), s)), 2)
     r["dw_bwd_weight_ours_us"] = round(t_graph(lambda: scc.dw3x3_backward_weight(gy, x, s)), 2)
     r["dw_bwd_data_torch_us"] = round(t_graph(lambda: torch.nn.grad.conv2d_input(x.shape, dw, gy, s, 1, 1, ci)), 2)

@@ -204,3 +204,90 @@ def test_dsc2d_matches_reference_composition(ref, case, fused):
         assert norm_rel(layer.bias.grad.cpu().numpy(), rdb) <= GRAD_TOL
     if dwb:
         assert norm_rel(layer.dw_bias.grad.cpu().numpy(), rddb) <= GRAD_TOL
+
+
+TC_DSC = [  # c_in, c_out, cg, co, n, h, w, stride, dw_bias, bias, expect one fused kernel
+    (64, 64, 2, "50%", 4, 32, 32, 1, True, True, True),
+    (64, 128, 2, "50%", 3, 32, 32, 1, False, True, True),
+    (128, 128, 2, "50%", 2, 16, 16, 1, True, False, False),  # two 64-row SCC tiles: the pair
+    (128, 128, 2, "25%", 2, 32, 32, 1, True, True, False),  # co = 25 %: several window classes, the pair
+    (32, 64, 2, "25%", 3, 16, 16, 1, False, True, True),
+    (64, 128, 2, "50%", 2, 16, 16, 1, False, True, True),
+    (64, 64, 2, "50%", 2, 16, 32, 1, True, True, True),   # 16 rows of 32
+    (64, 64, 2, "50%", 2, 8, 8, 1, False, True, False),   # 8-wide: the depthwise + SCC pair
+    (64, 128, 2, "50%", 2, 32, 32, 2, True, True, False),  # stride 2: the pair
+]
+
+
+@pytest.mark.parametrize("case", TC_DSC, ids=lambda c: f"{c[0]}-{c[1]}-cg{c[2]}-{c[3]}-{c[5]}x{c[6]}-s{c[7]}")
+def test_dsc_forward_t_matches_oracle(port, case):
+    """scc_dsc_forward_t_f32: y = SCC(DW3x3(x)) and t = DW3x3(x) against the
+    oracle composition (port.dw_forward -> port.forward, fp64); on stride-1
+    16- / 32-wide images one tensor-core kernel (the depthwise stage in its
+    staging step) when the SCC layer is one row tile over every channel,
+    elsewhere the depthwise kernel + the SCC forward."""
+    import paper_2101_00745_b200 as scc
+    ci, co, cg, ov, n, h, w, s, dwb, hb, one = case
+    cfg = scc.scc_config_new(ci, co, cg, ov, hb)
+    x, dww, dwbias = _problem(case[:10], seed=7)
+    rng = np.random.default_rng(2)
+    gw = cfg.group_width
+    wt = rng.uniform(-(1 / gw) ** 0.5, (1 / gw) ** 0.5, co * gw).astype(np.float32)
+    b = rng.uniform(-0.5, 0.5, co).astype(np.float32) if hb else None
+    wts = scc.SccWeights(torch.from_numpy(wt).cuda(), torch.from_numpy(b).cuda() if hb else None)
+    xt, wd = torch.from_numpy(x).cuda(), torch.from_numpy(dww).cuda()
+    bd = torch.from_numpy(dwbias).cuda() if dwb else None
+    scc.dsc_forward_t(xt, wd, bd, wts, cfg, s)  # plan tables / scratch
+    torch.cuda.synchronize()
+    before = scc.launch_count()
+    y, t = scc.dsc_forward_t(xt, wd, bd, wts, cfg, s)
+    torch.cuda.synchronize()
+    launched = scc.launch_count() - before
+    assert (launched == 1) == one, launched
+    rt = port.dw_forward(x, dww, dwbias, 3, s)
+    o = port.config(ci, co, cg, ("ratio", float(ov[:-1]) / 100), hb)
+    ry = port.forward(o, rt, wt, b)
+    assert norm_rel(t.cpu().numpy(), rt) <= FWD_TOL
+    assert norm_rel(y.cpu().numpy(), ry) <= FWD_TOL
+    y2, t2 = scc.dsc_forward_t(xt, wd, bd, wts, cfg, s)
+    assert torch.equal(y, y2) and torch.equal(t, t2)  # deterministic
+
+
+@pytest.mark.parametrize("case", [TC_DSC[0], TC_DSC[1], TC_DSC[2], TC_DSC[3], TC_DSC[4]], ids=lambda c: f"{c[0]}-{c[1]}-{c[5]}x{c[6]}")
+def test_dsc2d_fused_tensor_core_matches_reference(ref, case):
+    """DSC2d(fused=True) on the tensor-core fused forward: forward and every
+    gradient against the reference's own stages (t from the fused kernel is
+    the SCC backward's input)."""
+    import paper_2101_00745_b200 as scc
+    ci, co, cg, ov, n, h, w, s, dwb, hb, _ = case
+    torch.manual_seed(4)
+    layer = scc.DSC2d(ci, co, s, cg, ov, dw_bias=dwb, bias=hb, fused=True, device="cuda")
+    with torch.no_grad():
+        if hb:
+            layer.bias.uniform_(-0.5, 0.5)
+        if dwb:
+            layer.dw_bias.uniform_(-0.5, 0.5)
+    x = torch.randn(n, ci, h, w, device="cuda", requires_grad=True)
+    y = layer(x)
+    gy = torch.randn_like(y)
+    y.backward(gy)
+    xn = x.detach().cpu().numpy()
+    dww = layer.dw_weight.detach().cpu().numpy().reshape(ci, 3, 3)
+    dwbn = layer.dw_bias.detach().cpu().numpy() if dwb else None
+    wn = layer.weight.detach().cpu().numpy().reshape(-1)
+    bn = layer.bias.detach().cpu().numpy() if hb else None
+    o = ref.config(ci, co, cg, ov, hb)
+    t = ref.dw_forward(xn, dww, dwbn, 3, s)
+    ry = ref.forward(o, t, wn, bn)
+    gyn = gy.cpu().numpy()
+    dt = ref.backward_input(o, gyn, wn)
+    rdw, rdb = ref.backward_params(o, gyn, t)
+    rdx, rddw, rddb = ref.dw_backward(dt, xn, dww, 3, s, dwb)
+    assert norm_rel(y.detach().cpu().numpy(), ry) <= FWD_TOL
+    assert norm_rel(x.grad.cpu().numpy(), rdx) <= GRAD_TOL
+    assert norm_rel(layer.dw_weight.grad.cpu().numpy().reshape(ci, 3, 3), rddw) <= GRAD_TOL
+    assert norm_rel(layer.weight.grad.cpu().numpy().reshape(-1), rdw) <= GRAD_TOL
+    if hb:
+        assert norm_rel(layer.bias.grad.cpu().numpy(), rdb) <= GRAD_TOL
+    if dwb:
+        assert norm_rel(layer.dw_bias.grad.cpu().numpy(), rddb) <= GRAD_TOL
