@@ -251,6 +251,13 @@ scc_status_t scc_dw3x3_backward_weight_f32(int64_t n, int64_t c, int64_t h, int6
                                            int64_t stride, const float* dy, const float* x,
                                            float* dweight, float* dbias, void* workspace,
                                            size_t workspace_bytes, void* stream);
+/* The whole depthwise backward (grouped_conv_backward, reference.cpp:155-247):
+ * dx, dweight and dbias (NULL: skipped) from one pass over dy and x at
+ * stride 1 (bitwise the two calls above); stride 2 runs those two calls. */
+scc_status_t scc_dw3x3_backward_f32(int64_t n, int64_t c, int64_t h, int64_t w, int64_t stride,
+                                    const float* dy, const float* x, const float* weight, float* dx,
+                                    float* dweight, float* dbias, void* workspace, size_t workspace_bytes,
+                                    void* stream);
 
 #ifdef __cplusplus
 }  /* extern "C" */

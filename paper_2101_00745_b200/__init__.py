@@ -23,6 +23,7 @@ from .scc import (  # noqa: F401
     covering_filters,
     dsc_forward,
     dsc_forward_t,
+    dw3x3_backward,
     dw3x3_backward_data,
     dw3x3_backward_weight,
     dw3x3_forward,

@@ -42,7 +42,7 @@ EXPORTS = (
     "scc_forward_f32", "scc_backward_data_f32", "scc_backward_weight_workspace_size",
     "scc_backward_weight_f32", "scc_backward_f32", "scc_dsc_forward_f32", "scc_dsc_forward_t_f32",
     "scc_dw3x3_forward_f32", "scc_dw3x3_backward_data_f32", "scc_dw3x3_workspace_size",
-    "scc_dw3x3_backward_weight_f32",
+    "scc_dw3x3_backward_weight_f32", "scc_dw3x3_backward_f32",
     "scc_forward_host_f32", "scc_backward_host_f32", "scc_fwd_bwd_host_f32",
     "scc_backward_data_host_f32", "scc_backward_weight_host_f32",
 )
@@ -141,6 +141,8 @@ def _declare(L):
         "scc_dw3x3_workspace_size": ([i64, P(C.c_size_t)], C.c_int),
         "scc_dw3x3_backward_weight_f32": ([i64, i64, i64, i64, i64, fp, fp, fp, fp, vp, C.c_size_t,
                                            vp], C.c_int),
+        "scc_dw3x3_backward_f32": ([i64, i64, i64, i64, i64, fp, fp, fp, fp, fp, fp, vp, C.c_size_t,
+                                    vp], C.c_int),
         "scc_backward_f32": ([vp, i64, i64, i64, fp, fp, fp, fp, fp, fp, vp, C.c_size_t, vp],
                              C.c_int),
         "scc_forward_host_f32": ([vp, i64, i64, i64, fp, fp, fp, fp], C.c_int),

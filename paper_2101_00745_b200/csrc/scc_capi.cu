@@ -1234,6 +1234,31 @@ scc_status_t scc_dw3x3_backward_weight_f32(int64_t n, int64_t c, int64_t h, int6
   });
 }
 
+scc_status_t scc_dw3x3_backward_f32(int64_t n, int64_t c, int64_t h, int64_t w, int64_t stride,
+                                    const float* dy, const float* x, const float* weight, float* dx,
+                                    float* dweight, float* dbias, void* workspace, size_t workspace_bytes,
+                                    void* stream) {
+  return guard([&] {
+    scc::DwArgs a = scc::dw_args(n, c, h, w, stride);
+    scc::check_ptr(dy, "dy");
+    scc::check_ptr(x, "x");
+    scc::check_ptr(weight, "weight");
+    scc::check_ptr(dx, "dx");
+    scc::check_ptr(dweight, "dweight");
+    if (workspace == nullptr || workspace_bytes < scc::dw_workspace_bytes(c)) {
+      scc::fail(SCC_ERR_ARGUMENT, "workspace too small: need " + std::to_string(scc::dw_workspace_bytes(c)) + " bytes");
+    }
+    a.dy = dy;
+    a.x = x;
+    a.wt = weight;
+    a.dx = dx;
+    a.dw = dweight;
+    a.db = dbias;
+    a.part = static_cast<float*>(workspace);
+    scc::cuda_check(scc::launch_dw(a, 3, static_cast<cudaStream_t>(stream)), "depthwise backward launch");
+  });
+}
+
 scc_status_t scc_forward_host_f32(scc_plan_t* plan, int64_t n, int64_t h, int64_t w,
                                   const float* x, const float* weight, const float* bias,
                                   float* y) {

@@ -121,9 +121,14 @@ class _DSCFunction(torch.autograd.Function):
         g = _scc.scc_backward(gy.contiguous(), t, wts, cfg)
         dt = g.grad_input
         dx = ddw = ddb = None
-        if ctx.needs_input_grad[0]:
+        need_w = ctx.needs_input_grad[1] or (ctx.has_dwb and ctx.needs_input_grad[2])
+        if ctx.needs_input_grad[0] and need_w:
+            # one pass over dt and x (stride 1)
+            dx, ddw, ddb = _scc.dw3x3_backward(dt, x, dw_weight, s, ctx.has_dwb)
+            ddw = ddw.view_as(dw_weight)
+        elif ctx.needs_input_grad[0]:
             dx = _scc.dw3x3_backward_data(dt, dw_weight, x.shape[2:], s)
-        if ctx.needs_input_grad[1] or (ctx.has_dwb and ctx.needs_input_grad[2]):
+        elif need_w:
             ddw, ddb = _scc.dw3x3_backward_weight(dt, x, s, ctx.has_dwb)
             ddw = ddw.view_as(dw_weight)
         dw = g.params.grad_weight.view_as(weight)

@@ -396,6 +396,28 @@ def dw3x3_backward_weight(grad_out: torch.Tensor, x: torch.Tensor, stride: int =
     return dw, db
 
 
+def dw3x3_backward(grad_out: torch.Tensor, x: torch.Tensor, weight: torch.Tensor, stride: int = 1,
+                   with_bias: bool = False):
+    """The whole depthwise backward (grouped_conv_backward, reference.cpp:
+    155-247): (dx, dweight [c,3,3], dbias or None), one pass over grad_out
+    and x at stride 1 (scc_dw3x3_backward_f32)."""
+    g, x = _dev4(grad_out, "grad_out"), _dev4(x, "input")
+    n, c, h, w = x.shape
+    if weight.numel() != c * 9:
+        raise ShapeError(f"depthwise weight has {weight.numel()} entries, needs {c * 9}")
+    dx = torch.empty_like(x)
+    dw = torch.empty((c, 3, 3), dtype=torch.float32, device=x.device)
+    db = torch.empty(c, dtype=torch.float32, device=x.device) if with_bias else None
+    nb = C.c_size_t()
+    check(lib().scc_dw3x3_workspace_size(c, C.byref(nb)))
+    ws = torch.empty(max(nb.value, 4), dtype=torch.uint8, device=x.device)
+    wt = weight.contiguous()
+    check(lib().scc_dw3x3_backward_f32(n, c, h, w, stride, g.data_ptr(), x.data_ptr(), wt.data_ptr(),
+                                       dx.data_ptr(), dw.data_ptr(), _ptr(db), ws.data_ptr(), ws.numel(),
+                                       _stream(x)))
+    return dx, dw, db
+
+
 def scc_backward_input(grad_out: torch.Tensor, wts: SccWeights, cfg: SccConfig) -> torch.Tensor:
     """scc_backward_input (kernel.hpp:56-61)."""
     g = _dev4(grad_out, "grad_out")

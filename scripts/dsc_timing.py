@@ -44,6 +44,7 @@ for ci, co, hw, s in SHAPES:
     r["dw_bwd_data_ours_us"] = round(t_graph(lambda: scc.dw3x3_backward_data(gy, dw, (hw, hw), s)), 2)
     r["dw_bwd_weight_ours_us"] = round(t_graph(lambda: scc.dw3x3_backward_weight(gy, x, s)), 2)
     r["dw_bwd_data_torch_us"] = round(t_graph(lambda: torch.nn.grad.conv2d_input(x.shape, dw, gy, s, 1, 1, ci)), 2)
+    r["dw_bwd_ours_us"] = round(t_graph(lambda: scc.dw3x3_backward(gy, x, dw, s)), 2)
     r["dw_bwd_weight_torch_us"] = round(t_graph(lambda: torch.nn.grad.conv2d_weight(x, dw.shape, gy, s, 1, 1, ci)), 2)
     cfg.set_path(1)  # SCC_PATH_CUDA_CORE
     r["scc_cc_us"] = round(t_graph(tc), 2)

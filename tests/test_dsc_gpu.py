@@ -164,6 +164,36 @@ def test_dw3x3_backward_matches_reference(ref, shape):
     assert torch.equal(dw, dw2)  # fixed-order reduction
 
 
+@pytest.mark.parametrize("shape", DW_SHAPES + [(3, 64, 32, 32, 1), (2, 16, 7, 9, 1), (2, 16, 5, 6, 1)],
+                         ids=lambda s: f"{s[1]}ch-{s[2]}x{s[3]}-s{s[4]}")
+def test_dw3x3_backward_one_pass(ref, shape):
+    """scc_dw3x3_backward_f32 (dx, dW, db from one pass over dy and x) against
+    the reference's grouped_conv_backward; dx bitwise the separate
+    backward-data kernel's (same per-element tap order), dW / db bitwise the
+    separate weight kernel's on planes under 32 rows (same per-thread order;
+    4-row blocks above that) and deterministic."""
+    import paper_2101_00745_b200 as scc
+    n, c, h, w, s = shape
+    g = torch.Generator().manual_seed(6)
+    x = torch.randn(n, c, h, w, generator=g)
+    wt = torch.rand(c, 1, 3, 3, generator=g) - 0.5
+    ho, wo = (h - 1) // s + 1, (w - 1) // s + 1
+    gy = torch.randn(n, c, ho, wo, generator=g)
+    rdx, rdw, rdb = ref.dw_backward(gy.numpy(), x.numpy(), wt.view(c, 3, 3).numpy(), 3, s, True)
+    gyc, xc, wc = gy.cuda(), x.cuda(), wt.cuda()
+    dx, dw, db = scc.dw3x3_backward(gyc, xc, wc, s, True)
+    assert norm_rel(dx.cpu().numpy(), rdx) <= GRAD_TOL
+    assert norm_rel(dw.cpu().numpy(), rdw) <= GRAD_TOL
+    assert norm_rel(db.cpu().numpy(), rdb) <= GRAD_TOL
+    sdx = scc.dw3x3_backward_data(gyc, wc, (h, w), s)
+    sdw, sdb = scc.dw3x3_backward_weight(gyc, xc, s, True)
+    assert torch.equal(dx, sdx)
+    if h < 32 or s == 2:
+        assert torch.equal(dw, sdw) and torch.equal(db, sdb)
+    _, dw_nb, db_nb = scc.dw3x3_backward(gyc, xc, wc, s, False)
+    assert db_nb is None and torch.equal(dw_nb, dw)
+
+
 @pytest.mark.parametrize("fused", [False, True], ids=["dw+scc", "fused"])
 @pytest.mark.parametrize("case", CASES, ids=lambda c: f"{c[0]}-{c[1]}-cg{c[2]}-{c[3]}-{c[5]}x{c[6]}-s{c[7]}")
 def test_dsc2d_matches_reference_composition(ref, case, fused):
