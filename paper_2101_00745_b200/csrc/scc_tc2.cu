@@ -401,7 +401,8 @@ __global__ void __launch_bounds__(DSC ? kDscThreads : kThreads, 1)
   // 1024-aligned and every derived pointer stays in the shared address space.
   extern __shared__ __align__(1024) uint8_t smem[];
   static_assert(!(BWD && DSC), "the dsc_block fusion is a forward");
-  const Layout<NT> L(a.total_chunks, a.stages, a.n_rt, a.store_mode, a.stage_bytes, a.scratch,
+  const int stage_bytes = DSC ? a.stage_bytes : kStageBytes;  // compile-time unless fused
+  const Layout<NT> L(a.total_chunks, a.stages, a.n_rt, a.store_mode, stage_bytes, a.scratch,
                      DSC ? kDwStride * a.c_in : 0);
   uint8_t* panel = smem + L.panel;
   uint8_t* raw = smem + L.raw;
@@ -505,10 +506,10 @@ __global__ void __launch_bounds__(DSC ? kDscThreads : kThreads, 1)
             // (dsc: rows of 128 + 2 halo px from one image row before the
             // tile; out-of-sample pixels are zero-filled by TMA -- the
             // depthwise stage's top / bottom padding)
-            const int rowb = DSC ? a.stage_bytes / 32 : 512;
+            const int rowb = stage_bytes / 32;
             if (lane == 0) mbar_expect_tx(&full[s], rows * rowb);
             __syncwarp();
-            uint8_t* st = raw + s * a.stage_bytes;
+            uint8_t* st = raw + s * stage_bytes;
             const int r = lane * a.rb;
             if (r < rows) {
               int pos = start8 + 32 * c + r;
@@ -570,7 +571,7 @@ __global__ void __launch_bounds__(DSC ? kDscThreads : kThreads, 1)
       }
     }
   } else {
-    if (warp < 4 || (warp >= 8 && warp < 12)) {
+    if (warp < 4 || (warp >= 8 && (!DSC || warp < 12))) {
       // ---------------- panel build (warps 2, 3, 8..11; the converters start at once) ----------------
       const int ct = warp < 4 ? threadIdx.x - 64 : threadIdx.x - 192;  // 0..191
       cudaGridDependencySynchronize();  // W may come from the previous kernel
@@ -609,10 +610,10 @@ __global__ void __launch_bounds__(DSC ? kDscThreads : kThreads, 1)
         mbar_arrive(panel_bar);
       }
     }
-    if ((warp >= 4 && warp < 8) || warp >= 12) {
+    if ((warp >= 4 && warp < 8) || (DSC && warp >= 12)) {
       // ---------------- converters: raw [row][px] -> TMEM [px lane][row] hi / lo ----------------
       const int q = warp & 3;  // pixel block of the tile = TMEM lane quarter
-      const int half = warp >= 12 ? 1 : 0;  // dsc: rows 16 * half .. + 15 of each stage
+      const int half = DSC && warp >= 12 ? 1 : 0;  // dsc: rows 16 * half .. + 15 of each stage
       const uint32_t lane_base = static_cast<uint32_t>(q * 32) << 16;
       int s = 0, st = 0;
       uint32_t ph = 0, tph = 0;
@@ -701,7 +702,7 @@ __global__ void __launch_bounds__(DSC ? kDscThreads : kThreads, 1)
         }
       }
     }
-    if (warp >= 8 && warp < 12) {
+    if (warp >= 8 && (!DSC || warp < 12)) {
       // ---------------- epilogue (warps 8..11) ----------------
       const int et = threadIdx.x - 256;  // 0..127
       for (int i = et; i < a.n_rt * NT; i += 128) {
