@@ -134,42 +134,34 @@ struct Band2Args {
 // role builds a TileIter, and four inlined copies of the division code were
 // ~1,000 instructions of the kernel's ~3,900.
 __device__ __noinline__ int2 tile_range(const Band2Args& a) {
-  int32_t u, u1;
-  const int32_t ns = a.nbps > 0 ? a.units / a.nbps : 0;  // samples
-  if (ns > 0 && static_cast<int32_t>(gridDim.x) >= ns) {
-    const int32_t g = static_cast<int32_t>(gridDim.x), i = static_cast<int32_t>(blockIdx.x);
-    const int32_t base = g / ns, extra = g % ns;
-    int32_t smp, r, nr;
-    if (i < extra * (base + 1)) {
-      smp = i / (base + 1);
-      r = i - smp * (base + 1);
-      nr = base + 1;
-    } else {
-      const int32_t i2 = i - extra * (base + 1);
-      smp = extra + i2 / base;
-      r = i2 - (smp - extra) * base;
-      nr = base;
-    }
-    u = smp * a.nbps + (r * a.nbps) / nr;
-    u1 = smp * a.nbps + ((r + 1) * a.nbps) / nr;
-  } else if (a.units < (1 << 22)) {
+  // Whole tiles, evenly: tile t = (sample t / tps, blocks 4 (t % tps) ..);
+  // a CTA's run [t0, t1) maps to the block run TileIter cuts back into
+  // exactly those tiles (tiles never straddle a sample).
+  const int32_t tps = (a.nbps + 3) >> 2;  // tiles per sample
+  const int32_t ns = a.nbps > 0 ? a.units / a.nbps : 0;
+  const int64_t tiles = static_cast<int64_t>(ns) * tps;
+  int64_t t0, t1;
+  if (tiles < (1 << 22)) {
     // 32-bit division when the products fit (the 64-bit one is a slow call)
-    u = static_cast<int32_t>((blockIdx.x * static_cast<uint32_t>(a.units)) / gridDim.x);
-    u1 = static_cast<int32_t>(((blockIdx.x + 1) * static_cast<uint32_t>(a.units)) / gridDim.x);
+    t0 = (blockIdx.x * static_cast<uint32_t>(tiles)) / gridDim.x;
+    t1 = ((blockIdx.x + 1) * static_cast<uint32_t>(tiles)) / gridDim.x;
   } else {
-    u = static_cast<int32_t>((static_cast<int64_t>(blockIdx.x) * a.units) / gridDim.x);
-    u1 = static_cast<int32_t>((static_cast<int64_t>(blockIdx.x + 1) * a.units) / gridDim.x);
+    t0 = (static_cast<int64_t>(blockIdx.x) * tiles) / gridDim.x;
+    t1 = (static_cast<int64_t>(blockIdx.x + 1) * tiles) / gridDim.x;
   }
-  return make_int2(u, u1);
+  const int32_t s0 = static_cast<int32_t>(t0 / tps), s1 = static_cast<int32_t>(t1 / tps);
+  const int32_t j0 = static_cast<int32_t>(t0 - static_cast<int64_t>(s0) * tps);
+  const int32_t j1 = static_cast<int32_t>(t1 - static_cast<int64_t>(s1) * tps);
+  return make_int2(s0 * a.nbps + min(4 * j0, a.nbps), s1 * a.nbps + min(4 * j1, a.nbps));
 }
 
 // Contiguous run of blocks owned by this CTA, cut into tiles of <= 4 blocks
 // that never straddle a sample.  A tile costs one pass of the load / convert /
-// MMA / store pipeline whatever its width, so when there are at least as many
-// CTAs as samples the runs are cut inside samples (each sample gets
-// floor(grid / n) or one more runs): on config 1 every CTA then has <= 2
-// tiles (7-8 blocks), where an even split of the flat block range gave 22 % of
-// the CTAs a run across a sample boundary and 3 tiles.
+// MMA / store pipeline whatever its width, so the runs are whole tiles,
+// ceil(tiles / grid) at most per CTA: on config 1 every CTA has <= 2 tiles
+// (an even split of the flat block range gave 22 % of the CTAs a run across a
+// sample boundary and 3 tiles); at 64 -> 64, 32x32, N = 128, 7 (cutting runs
+// inside samples, floor(grid / n) or one more per sample, gave 8).
 struct TileIter {
   int32_t u, u1, nbps;
   int32_t n, b0, cnt;
