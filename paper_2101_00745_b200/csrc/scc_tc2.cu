@@ -618,7 +618,9 @@ __global__ void __launch_bounds__(DSC ? kDscThreads : kThreads, 1)
         const int pix = it.b0 * kBlkPx + q * 32 + lane;
         const bool pv = q < it.cnt && pix < a.plane;
         const int col = DSC ? (pix & (a.img_w - 1)) : 0;
-        const float vl = col > 0 ? 1.f : 0.f, vr = col < a.img_w - 1 ? 1.f : 0.f;
+        // (selects, not weight x 0: the corner taps of the stage's first and
+        // last pixel read outside the stage, and 0 x NaN is NaN)
+        const bool ml = col > 0, mr = col < a.img_w - 1;
         for (int rt = 0; rt < a.n_rt; ++rt) {
           const int nk8 = a.rt_nk8[rt];
           const int nch = (nk8 + 3) >> 2;
@@ -645,15 +647,15 @@ __global__ void __launch_bounds__(DSC ? kDscThreads : kThreads, 1)
                 const float4* w4 = reinterpret_cast<const float4*>(dwt + kDwStride * min(ch0 + r, a.c_in - 1));
                 const float4 wa = w4[0], wb = w4[1], wc = w4[2];
                 float v = wc.y;
-                v = fmaf(wa.x * vl, x0[-W - 1], v);
+                v = fmaf(wa.x, ml ? x0[-W - 1] : 0.f, v);
                 v = fmaf(wa.y, x0[-W], v);
-                v = fmaf(wa.z * vr, x0[-W + 1], v);
-                v = fmaf(wa.w * vl, x0[-1], v);
+                v = fmaf(wa.z, mr ? x0[-W + 1] : 0.f, v);
+                v = fmaf(wa.w, ml ? x0[-1] : 0.f, v);
                 v = fmaf(wb.x, x0[0], v);
-                v = fmaf(wb.y * vr, x0[1], v);
-                v = fmaf(wb.z * vl, x0[W - 1], v);
+                v = fmaf(wb.y, mr ? x0[1] : 0.f, v);
+                v = fmaf(wb.z, ml ? x0[W - 1] : 0.f, v);
                 v = fmaf(wb.w, x0[W], v);
-                v = fmaf(wc.x * vr, x0[W + 1], v);
+                v = fmaf(wc.x, mr ? x0[W + 1] : 0.f, v);
                 if (tdst != nullptr && pv && r < rows) __stcs(tdst + static_cast<int64_t>(r) * a.plane, v);
                 const float h = tf32_hi(v);
                 hi[r] = __float_as_uint(h);

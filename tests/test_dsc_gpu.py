@@ -321,3 +321,24 @@ def test_dsc2d_fused_tensor_core_matches_reference(ref, case):
         assert norm_rel(layer.bias.grad.cpu().numpy(), rdb) <= GRAD_TOL
     if dwb:
         assert norm_rel(layer.dw_bias.grad.cpu().numpy(), rddb) <= GRAD_TOL
+
+
+def test_dsc_forward_t_ignores_stale_memory():
+    """The fused forward's corner taps of a stage's first / last pixel read
+    outside the stage; their padding must come from selects, not from a zero
+    weight (0 x NaN is NaN).  Shared and global memory left full of NaN by
+    earlier work must not reach y or t."""
+    import paper_2101_00745_b200 as scc
+    cfg = scc.scc_config_new(64, 64, 2, "50%", False)
+    wts = scc.scc_weights_init(cfg, device="cuda")
+    g = torch.Generator(device="cuda").manual_seed(9)
+    x = torch.randn(32, 64, 32, 32, device="cuda", generator=g)
+    dw = (torch.rand(64, 1, 3, 3, device="cuda", generator=g) - 0.5) / 3
+    y0, t0 = scc.dsc_forward_t(x, dw, None, wts, cfg, 1)
+    for _ in range(3):
+        junk = torch.full((1 << 26,), float("nan"), device="cuda")
+        scc.scc_forward(junk[: x.numel()].view_as(x), wts, cfg)  # NaN through the kernels' shared memory
+        del junk
+        y, t = scc.dsc_forward_t(x, dw, None, wts, cfg, 1)
+        assert torch.isfinite(y).all() and torch.isfinite(t).all()
+        assert torch.equal(y, y0) and torch.equal(t, t0)
