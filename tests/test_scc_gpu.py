@@ -608,3 +608,43 @@ def test_weight_gradient_accumulation_chain_bounded(c_in, c_out, cg, hw, n):
     assert e_w <= 0.5 * GRAD_TOL and e_b <= GRAD_TOL, (e_w, e_b)
     del x, dy, g, rdw, rdb
     torch.cuda.empty_cache()
+
+
+STALE_SHAPES = [  # c_in, c_out, cg, co, n, h, w: every kernel family at least once
+    (64, 128, 2, "50%", 32, 32, 32),    # gen-2 band + fused backward (config 1)
+    (256, 256, 2, "50%", 4, 14, 14),    # gen-1 band (P = 196, partial tiles) + weight kernels
+    (256, 256, 4, "25%", 2, 56, 56),    # gen-1, several window classes
+    (128, 128, 2, "50%", 8, 4, 4),      # packed small planes
+    (512, 512, 2, "50%", 4, 7, 7),      # padded planes (P = 49)
+    (48, 80, 3, 1, 2, 7, 5),            # ragged: the CUDA-core kernels
+]
+
+
+@pytest.mark.parametrize("path", PATHS, ids=lambda p: PATH_IDS[p])
+@pytest.mark.parametrize("shape", STALE_SHAPES, ids=lambda s: f"{s[0]}-{s[1]}-cg{s[2]}-{s[4]}x{s[5]}x{s[6]}")
+def test_results_ignore_stale_memory(path, shape):
+    """No kernel may let memory it did not write this call reach its outputs
+    (masked-out operands must be selected away, never multiplied by zero:
+    0 x NaN is NaN).  Global memory handed out by the caching allocator and
+    the kernels' shared memory are left full of NaN by a run on NaN inputs,
+    then a finite run must be bitwise the clean one."""
+    import paper_2101_00745_b200 as scc
+    ci, co, cg, ov, n, h, w = shape
+    cfg = make_cfg(ci, co, cg, ov, True, path)
+    wts = scc.scc_weights_init(cfg, device="cuda")
+    g = torch.Generator(device="cuda").manual_seed(11)
+    x = torch.randn(n, ci, h, w, device="cuda", generator=g)
+    dy = torch.randn(n, co, h, w, device="cuda", generator=g)
+    y0 = scc.scc_forward(x, wts, cfg)
+    g0 = scc.scc_backward(dy, x, wts, cfg)
+    for _ in range(2):
+        junk = torch.full((1 << 26,), float("nan"), device="cuda")
+        scc.scc_forward(junk[: x.numel()].view_as(x), wts, cfg)
+        scc.scc_backward(junk[: dy.numel()].view_as(dy), junk[: x.numel()].view_as(x), wts, cfg)
+        del junk
+        y = scc.scc_forward(x, wts, cfg)
+        gr = scc.scc_backward(dy, x, wts, cfg)
+        assert torch.equal(y, y0)
+        assert torch.equal(gr.grad_input, g0.grad_input)
+        assert torch.equal(gr.params.grad_weight, g0.params.grad_weight)
+        assert torch.equal(gr.params.grad_bias, g0.params.grad_bias)
