@@ -342,3 +342,38 @@ def test_dsc_forward_t_ignores_stale_memory():
         y, t = scc.dsc_forward_t(x, dw, None, wts, cfg, 1)
         assert torch.isfinite(y).all() and torch.isfinite(t).all()
         assert torch.equal(y, y0) and torch.equal(t, t0)
+
+
+@pytest.mark.parametrize("shape", [(8, 64, 32, 32, 1), (8, 64, 32, 32, 2), (16, 128, 16, 16, 1), (4, 32, 7, 9, 1)],
+                         ids=lambda s: f"{s[1]}ch-{s[2]}x{s[3]}-s{s[4]}")
+def test_depthwise_and_dsc_ignore_stale_memory(shape):
+    """The depthwise kernels and the CUDA-core fused dsc forward are bitwise
+    unchanged after global and shared memory were left full of NaN."""
+    import paper_2101_00745_b200 as scc
+    n, c, h, w, s = shape
+    g = torch.Generator(device="cuda").manual_seed(12)
+    x = torch.randn(n, c, h, w, device="cuda", generator=g)
+    wt = (torch.rand(c, 1, 3, 3, device="cuda", generator=g) - 0.5) / 3
+    b = torch.rand(c, device="cuda", generator=g) - 0.5
+    cfg = scc.scc_config_new(c, 2 * c, 2, "50%", True)
+    wts = scc.scc_weights_init(cfg, device="cuda")
+
+    def run():
+        y = scc.dw3x3_forward(x, wt, b, s)
+        gy = torch.ones_like(y) * 0.25 + y
+        dx, dw, db = scc.dw3x3_backward(gy, x, wt, s, True)
+        dx2 = scc.dw3x3_backward_data(gy, wt, (h, w), s)
+        dw2, db2 = scc.dw3x3_backward_weight(gy, x, s, True)
+        yd = scc.dsc_forward(x, wt, b, wts, cfg, s)
+        yt, t = scc.dsc_forward_t(x, wt, b, wts, cfg, s)
+        return [y, dx, dw, db, dx2, dw2, db2, yd, yt, t]
+
+    ref = run()
+    for _ in range(2):
+        junk = torch.full((1 << 26,), float("nan"), device="cuda")
+        v = junk[: x.numel()].view_as(x)
+        scc.dw3x3_forward(v, wt, b, s)
+        scc.dsc_forward(v, wt, b, wts, cfg, s)
+        del junk, v
+        for a, r in zip(run(), ref):
+            assert torch.equal(a, r)
