@@ -648,3 +648,27 @@ def test_results_ignore_stale_memory(path, shape):
         assert torch.equal(gr.grad_input, g0.grad_input)
         assert torch.equal(gr.params.grad_weight, g0.params.grad_weight)
         assert torch.equal(gr.params.grad_bias, g0.params.grad_bias)
+
+
+def test_host_entry_points_ignore_stale_memory():
+    """The host-buffer pipeline's plan-owned device buffers hold the previous
+    call's data; a call on NaN inputs must not leak into the next call."""
+    import ctypes as C
+    import paper_2101_00745_b200 as scc
+    from paper_2101_00745_b200 import _lib
+    rng = np.random.default_rng(4)
+    cfg = scc.scc_config_new(64, 128, 2, "50%", True)
+    n, h, w = 32, 32, 32
+    x, wt, b, dy = rand_problem(rng, 64, 128, 32, n, h, w, True)
+    p = lambda a: a.ctypes.data_as(C.c_void_p)  # noqa: E731
+
+    def call(xx, dyy):
+        outs = [np.empty((n, 128, h, w), np.float32), np.empty_like(x), np.empty_like(wt), np.empty_like(b)]
+        _lib.check(_lib.lib().scc_fwd_bwd_host_f32(cfg.handle, n, h, w, p(xx), p(wt), p(b), p(dyy),
+                                                   *[p(o) for o in outs]))
+        return outs
+
+    ref = call(x, dy)
+    call(np.full_like(x, np.nan), np.full_like(dy, np.nan))
+    for a, r in zip(call(x, dy), ref):
+        assert np.array_equal(a, r)
